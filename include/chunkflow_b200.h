@@ -1,0 +1,239 @@
+/* chunkflow_b200.h — C-ABI of the B200-native ChunkFlow training path.
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API
+ * (namespace chunkflow, /root/reference/proj/include/chunkflow/).  Every
+ * entry point below names the reference interface it replaces.  No torch or
+ * C++ types cross this boundary: plain pointers, sizes and POD records only.
+ * Errors are status codes (never exceptions); cf_last_error() returns the
+ * thread-local message of the last failing call.
+ *
+ * Ownership: opaque handles own all device memory; host buffers are
+ * caller-owned.  Threading: one host thread per cf_ctx (per GPU); a context is
+ * not re-entrant.  Each call runs on the context's stream.
+ */
+#ifndef CHUNKFLOW_B200_H_
+#define CHUNKFLOW_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: mirror the reference exception taxonomy
+ *      (common.hpp:15-30) and the CLI exit codes (chunkflow_main.cpp:29-32) */
+#define CF_OK 0
+#define CF_EVALIDATION 1 /* chunkflow::ValidationError */
+#define CF_EVERIFY 2     /* verification failure (kExitVerification) */
+#define CF_EIO 3         /* chunkflow::IoError */
+#define CF_ECUDA 4       /* CUDA runtime / driver error */
+#define CF_ENCCL 5       /* NCCL error */
+#define CF_EPARSE 6      /* chunkflow::ParseError */
+#define CF_EINTERNAL 7   /* std::logic_error and anything else */
+
+/* ---- flat plan records (exact field-for-field images of the reference
+ *      structs, so layouts can be diffed bit-exactly) */
+
+/* ChunkKind (chunker.hpp:16) */
+#define CF_CHUNK_STANDALONE 0
+#define CF_CHUNK_DEPENDENT 1
+/* ExecKind (scheduler.hpp:17) */
+#define CF_EXEC_FORWARD_DISCARD 0
+#define CF_EXEC_FORWARD_RETAIN 1
+#define CF_EXEC_BACKWARD 2
+
+/* Chunk (chunker.hpp:25-32); segments live in a separate array at
+ * [seg_offset, seg_offset + seg_count). */
+typedef struct cf_chunk_rec {
+  int64_t chunk_id;
+  int64_t kind;
+  int64_t group_id;       /* -1 for standalone */
+  int64_t index_in_group; /* -1 for standalone */
+  int64_t total_tokens;
+  int64_t seg_offset;
+  int64_t seg_count;
+} cf_chunk_rec;
+
+/* ChunkSegment (chunker.hpp:19-23) */
+typedef struct cf_segment_rec {
+  int64_t sequence_id;
+  int64_t start_token;
+  int64_t length;
+} cf_segment_rec;
+
+/* ExecEvent + KvActions (scheduler.hpp:20-34) */
+typedef struct cf_event_rec {
+  int64_t kind;
+  int64_t chunk_id;
+  int64_t group_id;
+  int64_t index_in_group;
+  int64_t is_recompute;
+  int64_t save_kv;
+  int64_t read_kv_prefix;
+  int64_t accumulate_kv_grad;
+} cf_event_rec;
+
+/* PlanDiagnostics (scheduler.hpp:173-177); violations are counted here and
+ * their text is available through cf_plan_violation(). */
+typedef struct cf_plan_diag {
+  int64_t peak_retained_tokens;
+  int64_t recompute_token_count;
+  int64_t num_violations;
+} cf_plan_diag;
+
+/* ---- model configuration (ToyModelConfig, toy_model.hpp:20-46, extended
+ *      with the Llama/Qwen layer shape the north star asks for) */
+#define CF_ARCH_TOY 0   /* reference toy: norm-free, no RoPE, tanh FFN (2d) */
+#define CF_ARCH_LLAMA 1 /* RMSNorm + RoPE + SwiGLU, GQA, untied head */
+
+typedef struct cf_model_cfg {
+  int32_t arch;
+  int32_t reserved;
+  int64_t vocab_size;
+  int64_t d_model;
+  int64_t num_heads;
+  int64_t num_kv_heads;
+  int64_t num_layers;
+  int64_t ffn_width; /* 0 => 2*d_model (toy); required for llama */
+  uint64_t seed;
+  double rope_theta; /* llama only */
+  double rms_eps;    /* llama only */
+} cf_model_cfg;
+
+/* RunPlanOptions (plan_runner.hpp:49-54) */
+typedef struct cf_run_opts {
+  int32_t corrupt_kv_grads;   /* fault-injection hook: scale incoming dK/dV */
+  int32_t accumulate_grads;   /* 0: zero grads first (reference semantics) */
+  double normalizer_override; /* > 0 replaces the global target count */
+} cf_run_opts;
+
+/* RunPlanResult + RunInstrumentation (plan_runner.hpp:36-60), plus the
+ * device-side numbers the B200 runtime adds. */
+typedef struct cf_run_result {
+  double loss;
+  int64_t peak_retained_tokens;
+  int64_t recompute_forward_count;
+  int64_t recompute_loss_mismatches;
+  int64_t kv_completeness_violations;
+  int64_t tokens;            /* real tokens processed */
+  int64_t gpu_launches;      /* kernels this call launched */
+  int64_t peak_hbm_bytes;    /* arena high-water mark incl. static */
+  int64_t static_hbm_bytes;  /* params + grads */
+  int64_t act_hbm_bytes;     /* retained-activation arena high-water */
+  int64_t kv_hbm_bytes;      /* per-sequence KV-state high-water */
+  double model_flops;        /* algorithmic FLOPs (no recompute) */
+  double hw_flops;           /* incl. recompute */
+} cf_run_result;
+
+typedef struct cf_ctx cf_ctx;
+typedef struct cf_model cf_model;
+typedef struct cf_plan cf_plan;
+
+/* ---- errors ---- */
+const char* cf_last_error(void);
+const char* cf_version(void);
+
+/* ---- planning (host, integer; bit-exact with the reference) ---- */
+
+/* construct_chunks (chunker.hpp:177) + schedule_step (scheduler.hpp:132) +
+ * validate_plan (scheduler.hpp:182).  seq_ids/lengths describe the batch
+ * (Batch::sequences, dataset.hpp:75-82) in batch order. */
+int cf_plan_build(const int64_t* seq_ids, const int64_t* lengths, int64_t n,
+                  int64_t chunk_size, int64_t k, cf_plan** out);
+/* schedule_group (scheduler.hpp:106): one abstract dependent group. */
+int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out);
+int cf_plan_counts(const cf_plan* plan, int64_t* n_chunks, int64_t* n_segments,
+                   int64_t* n_events, int64_t* n_groups);
+int cf_plan_export(const cf_plan* plan, cf_chunk_rec* chunks,
+                   cf_segment_rec* segments, cf_event_rec* events,
+                   cf_plan_diag* diag);
+/* ExecutionPlan.groups (scheduler.hpp:41): group ids ascending, members in
+ * index order; offsets has n_groups+1 entries. */
+int cf_plan_export_groups(const cf_plan* plan, int64_t* group_ids,
+                          int64_t* offsets, int64_t* members);
+/* text of violation i (validate_plan messages). */
+int cf_plan_violation(const cf_plan* plan, int64_t i, char* buf, size_t cap);
+/* execution_plan_listing (scheduler.hpp:284): writes up to cap bytes,
+ * returns the full length via *len. */
+int cf_plan_listing(const cf_plan* plan, char* buf, size_t cap, size_t* len);
+/* Data-parallel partition (new): split the global plan's units
+ * (standalone chunks and whole dependent groups) across world ranks by
+ * deterministic LPT on attention+GEMM cost, then re-schedule rank's units
+ * with schedule_step semantics (global chunk ids preserved). */
+int cf_plan_partition(const cf_plan* global, int64_t world, int64_t rank,
+                      cf_plan** out);
+/* Per-unit costs used by the partitioner (for tests / reporting). */
+int cf_plan_rank_tokens(const cf_plan* global, int64_t world, int64_t* tokens);
+void cf_plan_destroy(cf_plan* plan);
+
+/* SplitMix64 token payload exactly as chunkflow_main.cpp:427-443: one
+ * stream over all sequences in order, next_below(vocab) per token. */
+int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab,
+                  uint64_t seed, int32_t* tokens_out);
+
+/* ---- device context / model ---- */
+int cf_ctx_create(int device, cf_ctx** out);
+void cf_ctx_destroy(cf_ctx* ctx);
+/* Stream the context runs on (cudaStream_t as an opaque pointer). */
+void* cf_ctx_stream(cf_ctx* ctx);
+/* NCCL data-parallel group: nccl_unique_id is the 128-byte ncclUniqueId
+ * produced by cf_nccl_unique_id on rank 0 and broadcast by the launcher. */
+int cf_nccl_unique_id(uint8_t* out128);
+int cf_ctx_init_dp(cf_ctx* ctx, int rank, int world, const uint8_t* id128);
+
+/* init_model (toy_model.hpp:110): parameters drawn on the device by a
+ * counter-based SplitMix64 identical to the reference's sequential stream. */
+int cf_model_create(cf_ctx* ctx, const cf_model_cfg* cfg, cf_model** out);
+void cf_model_destroy(cf_model* model);
+int64_t cf_model_num_tensors(const cf_model* model);
+/* ToyModelParams::tensors order and [rows, cols] row-major shapes. */
+int cf_model_tensor_info(const cf_model* model, int64_t idx, char* name,
+                         size_t cap, int64_t* rows, int64_t* cols);
+int cf_model_get_param(cf_model* model, int64_t idx, double* host);
+int cf_model_set_param(cf_model* model, int64_t idx, const double* host);
+int cf_model_get_grad(cf_model* model, int64_t idx, double* host);
+int cf_model_zero_grads(cf_model* model);
+/* Flat fp32 gradient buffer (device pointer + element count), for callers
+ * that reduce gradients themselves. */
+int cf_model_grad_buffer(cf_model* model, void** dev_ptr, int64_t* numel);
+int64_t cf_model_num_params(const cf_model* model);
+
+/* ---- execution ---- */
+
+/* run_plan (plan_runner.hpp:67): executes the plan's events on the GPU.
+ * seq_ids/lengths/tokens: the batch, tokens concatenated in batch order
+ * (host pointer).  If ctx has a DP group the gradients (and loss) are
+ * all-reduced after the last event. */
+int cf_run_plan(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
+                const int64_t* seq_ids, const int64_t* lengths,
+                const int32_t* tokens, int64_t n, const cf_run_opts* opts,
+                cf_run_result* result);
+/* Same with the token payload already resident in device memory
+ * (tokens_dev: int32, concatenated in batch order). */
+int cf_run_plan_device(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
+                       const int64_t* seq_ids, const int64_t* lengths,
+                       const int32_t* tokens_host, const void* tokens_dev,
+                       int64_t n, const cf_run_opts* opts,
+                       cf_run_result* result);
+/* backward_full (toy_model.hpp:575): every sequence alone, unchunked. */
+int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids,
+                     const int64_t* lengths, const int32_t* tokens, int64_t n,
+                     double normalizer_override, cf_run_result* result);
+int cf_ctx_synchronize(cf_ctx* ctx);
+
+/* ---- operator level (kernel unit tests); all pointers are device ---- */
+
+/* C[M,N] (+)= sum_k A(m,k) B(n,k).  a_kmajor: A stored [M,K] (else [K,M]);
+ * b_kmajor: B stored [N,K] (else [K,N]).  epi: 0 store bf16, 1 store fp32,
+ * 2 accumulate into fp32, 3 bf16 store of acc + residual(bf16). */
+int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
+               const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
+               int64_t m, int64_t n, int64_t k, int epi, const void* residual,
+               int64_t ld_res);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHUNKFLOW_B200_H_ */
