@@ -21,6 +21,11 @@
 extern "C" {
 #endif
 
+/* Exported even when the library is built with -fvisibility=hidden. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
 /* ---- status codes: mirror the reference exception taxonomy
  *      (common.hpp:15-30) and the CLI exit codes (chunkflow_main.cpp:29-32) */
 #define CF_OK 0
@@ -209,13 +214,17 @@ int cf_run_plan(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
                 const int64_t* seq_ids, const int64_t* lengths,
                 const int32_t* tokens, int64_t n, const cf_run_opts* opts,
                 cf_run_result* result);
-/* Same with the token payload already resident in device memory
- * (tokens_dev: int32, concatenated in batch order). */
-int cf_run_plan_device(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
-                       const int64_t* seq_ids, const int64_t* lengths,
-                       const int32_t* tokens_host, const void* tokens_dev,
-                       int64_t n, const cf_run_opts* opts,
-                       cf_run_result* result);
+/* Split form of cf_run_plan for callers that keep a step's inputs resident:
+ * cf_step_prepare uploads the batch (tokens + per-chunk index metadata:
+ * targets, positions, cu_seqlens-style segment tables, attention tiles) once;
+ * cf_step_run executes the plan's events from HBM-resident inputs. */
+typedef struct cf_step cf_step;
+int cf_step_prepare(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
+                    const int64_t* seq_ids, const int64_t* lengths,
+                    const int32_t* tokens, int64_t n, cf_step** out);
+int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step,
+                const cf_run_opts* opts, cf_run_result* result);
+void cf_step_destroy(cf_step* step);
 /* backward_full (toy_model.hpp:575): every sequence alone, unchunked. */
 int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids,
                      const int64_t* lengths, const int32_t* tokens, int64_t n,
@@ -231,6 +240,10 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
                const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
                int64_t m, int64_t n, int64_t k, int epi, const void* residual,
                int64_t ld_res);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 
 #ifdef __cplusplus
 }

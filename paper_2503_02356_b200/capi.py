@@ -1,0 +1,330 @@
+"""ctypes binding of libchunkflow_b200.so (include/chunkflow_b200.h).
+
+The shared library is the product: every compute call below goes to the
+sm_100a kernels inside it.  There is no fallback — if the library is missing
+the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libchunkflow_b200.so")
+
+CHUNK_DT = np.dtype([(k, np.int64) for k in
+                     ("chunk_id", "kind", "group_id", "index_in_group",
+                      "total_tokens", "seg_offset", "seg_count")])
+SEG_DT = np.dtype([(k, np.int64) for k in ("sequence_id", "start_token", "length")])
+EVENT_DT = np.dtype([(k, np.int64) for k in
+                     ("kind", "chunk_id", "group_id", "index_in_group",
+                      "is_recompute", "save_kv", "read_kv_prefix",
+                      "accumulate_kv_grad")])
+DIAG_DT = np.dtype([(k, np.int64) for k in
+                    ("peak_retained_tokens", "recompute_token_count",
+                     "num_violations")])
+
+ARCH_TOY, ARCH_LLAMA = 0, 1
+EPI_BF16, EPI_F32, EPI_F32_ACC, EPI_F32_RES, EPI_BF16_TANH, EPI_BF16_TANHGRAD = range(6)
+
+
+class ModelCfg(C.Structure):
+    _fields_ = [("arch", C.c_int32), ("reserved", C.c_int32),
+                ("vocab_size", C.c_int64), ("d_model", C.c_int64),
+                ("num_heads", C.c_int64), ("num_kv_heads", C.c_int64),
+                ("num_layers", C.c_int64), ("ffn_width", C.c_int64),
+                ("seed", C.c_uint64), ("rope_theta", C.c_double),
+                ("rms_eps", C.c_double)]
+
+
+class RunOpts(C.Structure):
+    _fields_ = [("corrupt_kv_grads", C.c_int32), ("accumulate_grads", C.c_int32),
+                ("normalizer_override", C.c_double)]
+
+
+class RunResult(C.Structure):
+    _fields_ = [("loss", C.c_double), ("peak_retained_tokens", C.c_int64),
+                ("recompute_forward_count", C.c_int64),
+                ("recompute_loss_mismatches", C.c_int64),
+                ("kv_completeness_violations", C.c_int64), ("tokens", C.c_int64),
+                ("gpu_launches", C.c_int64), ("peak_hbm_bytes", C.c_int64),
+                ("static_hbm_bytes", C.c_int64), ("act_hbm_bytes", C.c_int64),
+                ("kv_hbm_bytes", C.c_int64), ("model_flops", C.c_double),
+                ("hw_flops", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+# Every symbol include/chunkflow_b200.h declares (checked by the CPU tests).
+EXPORTS = [
+    "cf_last_error", "cf_version", "cf_plan_build", "cf_plan_build_group",
+    "cf_plan_counts", "cf_plan_export", "cf_plan_export_groups",
+    "cf_plan_violation", "cf_plan_listing", "cf_plan_partition",
+    "cf_plan_rank_tokens", "cf_plan_destroy", "cf_gen_tokens", "cf_ctx_create",
+    "cf_ctx_destroy", "cf_ctx_stream", "cf_nccl_unique_id", "cf_ctx_init_dp",
+    "cf_model_create", "cf_model_destroy", "cf_model_num_tensors",
+    "cf_model_tensor_info", "cf_model_get_param", "cf_model_set_param",
+    "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
+    "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
+    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm",
+]
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.cf_last_error.restype = C.c_char_p
+        L.cf_version.restype = C.c_char_p
+        L.cf_ctx_stream.restype = C.c_void_p
+        L.cf_model_num_tensors.restype = C.c_int64
+        L.cf_model_num_params.restype = C.c_int64
+        vp = C.c_void_p
+        for name in ("cf_plan_destroy", "cf_ctx_destroy", "cf_model_destroy", "cf_step_destroy"):
+            getattr(L, name).argtypes = [vp]
+            getattr(L, name).restype = None
+        L.cf_model_num_tensors.argtypes = [vp]
+        L.cf_model_num_params.argtypes = [vp]
+        L.cf_ctx_stream.argtypes = [vp]
+        L.cf_op_gemm.argtypes = [vp, vp, C.c_int, C.c_int64, vp, C.c_int, C.c_int64, vp, C.c_int64,
+                                 C.c_int64, C.c_int64, C.c_int64, C.c_int, vp, C.c_int64]
+        _lib = L
+    return _lib
+
+
+class CfError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"[cf {code}] {msg}")
+        self.code = code
+
+
+def check(rc):
+    if rc != 0:
+        raise CfError(rc, lib().cf_last_error().decode())
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+class Plan:
+    """A chunk plan + execution schedule (construct_chunks + schedule_step)."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle) if not isinstance(handle, C.c_void_p) else handle
+
+    @classmethod
+    def build(cls, lengths, chunk_size, k, ids=None):
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        h = C.c_void_p()
+        check(lib().cf_plan_build(_p(ids), _p(lengths), C.c_int64(len(lengths)),
+                                  C.c_int64(chunk_size), C.c_int64(k), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def group(cls, n, k, chunk_size=1):
+        h = C.c_void_p()
+        check(lib().cf_plan_build_group(C.c_int64(n), C.c_int64(k), C.c_int64(chunk_size), C.byref(h)))
+        return cls(h)
+
+    def counts(self):
+        v = [C.c_int64() for _ in range(4)]
+        check(lib().cf_plan_counts(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def export(self):
+        nc, ns, ne, ng = self.counts()
+        ch = np.zeros(nc, CHUNK_DT)
+        sg = np.zeros(ns, SEG_DT)
+        ev = np.zeros(ne, EVENT_DT)
+        dg = np.zeros(1, DIAG_DT)
+        check(lib().cf_plan_export(self.h, _p(ch), _p(sg), _p(ev), _p(dg)))
+        return ch, sg, ev, dg[0]
+
+    def groups(self):
+        nc, ns, ne, ng = self.counts()
+        gid = np.zeros(max(ng, 1), np.int64)
+        off = np.zeros(ng + 1, np.int64)
+        mem = np.zeros(max(nc, 1), np.int64)
+        check(lib().cf_plan_export_groups(self.h, _p(gid), _p(off), _p(mem)))
+        return {int(gid[i]): [int(x) for x in mem[off[i]:off[i + 1]]] for i in range(ng)}
+
+    def violations(self):
+        n = int(self.export()[3]["num_violations"])
+        out = []
+        for i in range(n):
+            buf = C.create_string_buffer(256)
+            check(lib().cf_plan_violation(self.h, C.c_int64(i), buf, C.c_size_t(256)))
+            out.append(buf.value.decode())
+        return out
+
+    def listing(self):
+        n = C.c_size_t()
+        check(lib().cf_plan_listing(self.h, None, C.c_size_t(0), C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().cf_plan_listing(self.h, buf, C.c_size_t(n.value + 1), None))
+        return buf.value.decode()
+
+    def partition(self, world, rank):
+        h = C.c_void_p()
+        check(lib().cf_plan_partition(self.h, C.c_int64(world), C.c_int64(rank), C.byref(h)))
+        return Plan(h)
+
+    def rank_tokens(self, world):
+        out = np.zeros(world, np.int64)
+        check(lib().cf_plan_rank_tokens(self.h, C.c_int64(world), _p(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value and _lib is not None:
+            _lib.cf_plan_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def gen_tokens(lengths, vocab, seed):
+    lengths = np.ascontiguousarray(lengths, np.int64)
+    out = np.zeros(int(lengths.sum()), np.int32)
+    check(lib().cf_gen_tokens(_p(lengths), C.c_int64(len(lengths)), C.c_int64(vocab),
+                              C.c_uint64(seed), _p(out)))
+    return out
+
+
+class Context:
+    """One device context (stream + memory pool) on one GPU."""
+
+    def __init__(self, device=0):
+        self.h = C.c_void_p()
+        check(lib().cf_ctx_create(C.c_int(device), C.byref(self.h)))
+
+    @property
+    def stream(self):
+        return lib().cf_ctx_stream(self.h)
+
+    def synchronize(self):
+        check(lib().cf_ctx_synchronize(self.h))
+
+    def init_dp(self, rank, world, uid: bytes | None):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid else None
+        check(lib().cf_ctx_init_dp(self.h, C.c_int(rank), C.c_int(world), buf))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().cf_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def gemm(self, a, a_kmajor, lda, b, b_kmajor, ldb, c, ldc, m, n, k, epi, r=0, ldr=0):
+        check(lib().cf_op_gemm(self.h, C.c_void_p(a), a_kmajor, lda, C.c_void_p(b), b_kmajor, ldb,
+                               C.c_void_p(c), ldc, m, n, k, epi, C.c_void_p(r), ldr))
+
+    def close(self):
+        if self.h and self.h.value:
+            lib().cf_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+class Model:
+    """Device model (ToyModelParams / Llama-shaped) with fp32 gradients."""
+
+    def __init__(self, ctx: Context, cfg: ModelCfg):
+        self.ctx = ctx
+        self.cfg = cfg
+        self.h = C.c_void_p()
+        check(lib().cf_model_create(ctx.h, C.byref(cfg), C.byref(self.h)))
+
+    def num_tensors(self):
+        return lib().cf_model_num_tensors(self.h)
+
+    def num_params(self):
+        return lib().cf_model_num_params(self.h)
+
+    def tensor_info(self, i):
+        name = C.create_string_buffer(128)
+        r, c = C.c_int64(), C.c_int64()
+        check(lib().cf_model_tensor_info(self.h, C.c_int64(i), name, C.c_size_t(128), C.byref(r), C.byref(c)))
+        return name.value.decode(), r.value, c.value
+
+    def get_param(self, i):
+        _, r, c = self.tensor_info(i)
+        out = np.zeros((r, c), np.float64)
+        check(lib().cf_model_get_param(self.h, C.c_int64(i), _p(out)))
+        return out
+
+    def set_param(self, i, value):
+        v = np.ascontiguousarray(value, np.float64)
+        check(lib().cf_model_set_param(self.h, C.c_int64(i), _p(v)))
+
+    def get_grad(self, i):
+        _, r, c = self.tensor_info(i)
+        out = np.zeros((r, c), np.float64)
+        check(lib().cf_model_get_grad(self.h, C.c_int64(i), _p(out)))
+        return out
+
+    def params_flat(self):
+        return np.concatenate([self.get_param(i).ravel() for i in range(self.num_tensors())])
+
+    def grads_flat(self):
+        return np.concatenate([self.get_grad(i).ravel() for i in range(self.num_tensors())])
+
+    def grad_buffer(self):
+        p, n = C.c_void_p(), C.c_int64()
+        check(lib().cf_model_grad_buffer(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def run_plan(self, plan: Plan, lengths, tokens, ids=None, corrupt=False, normalizer=0.0,
+                 accumulate=False) -> RunResult:
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        r = RunResult()
+        check(lib().cf_run_plan(self.ctx.h, self.h, plan.h, _p(ids), _p(lengths), _p(tokens),
+                                C.c_int64(len(lengths)), C.byref(o), C.byref(r)))
+        return r
+
+    def backward_full(self, lengths, tokens, ids=None, normalizer=0.0) -> RunResult:
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        r = RunResult()
+        check(lib().cf_backward_full(self.ctx.h, self.h, _p(ids), _p(lengths), _p(tokens),
+                                     C.c_int64(len(lengths)), C.c_double(normalizer), C.byref(r)))
+        return r
+
+    def close(self):
+        if self.h and self.h.value:
+            lib().cf_model_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+class Step:
+    """Prepared step (cf_step_prepare): inputs resident in HBM."""
+
+    def __init__(self, model: Model, plan: Plan, lengths, tokens, ids=None):
+        self.model = model
+        self.plan = plan
+        self.lengths = np.ascontiguousarray(lengths, np.int64)
+        self.ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        self.tokens = np.ascontiguousarray(tokens, np.int32)
+        self.h = C.c_void_p()
+        check(lib().cf_step_prepare(model.ctx.h, model.h, plan.h, _p(self.ids), _p(self.lengths),
+                                    _p(self.tokens), C.c_int64(len(self.lengths)), C.byref(self.h)))
+
+    def run(self, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
+        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        r = RunResult()
+        check(lib().cf_step_run(self.model.ctx.h, self.model.h, self.h, C.byref(o), C.byref(r)))
+        return r
+
+    def close(self):
+        if self.h and self.h.value:
+            lib().cf_step_destroy(self.h)
+            self.h = C.c_void_p()

@@ -1,0 +1,232 @@
+// C-ABI: device context, model, execution and operator-level entry points.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+
+#include "../../../include/chunkflow_b200.h"
+#include "../kernels/gemm.h"
+#include "../runtime/engine.hpp"
+#include "capi_util.hpp"
+
+struct cf_ctx {
+  cfb::Ctx c;
+};
+struct cf_model {
+  cfb::Model* m = nullptr;
+  cf_ctx* ctx = nullptr;
+};
+namespace {
+void need(const void* p, const char* what) {
+  if (!p) throw cfb::ValidationError(std::string(what) + " is null");
+}
+}  // namespace
+
+extern "C" {
+
+int cf_ctx_create(int device, cf_ctx** out) {
+  return cfb::guard([&] {
+    need(out, "out");
+    int n = 0;
+    cfb::cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (device < 0 || device >= n) throw cfb::ValidationError("no CUDA device " + std::to_string(device));
+    cfb::cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    cfb::cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10) throw cfb::ValidationError("chunkflow_b200 requires an sm_100 (B200) device");
+    auto h = std::make_unique<cf_ctx>();
+    h->c.device = device;
+    h->c.num_sms = prop.multiProcessorCount;
+    cfb::cuda_check(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cfb::cuda_check(cudaDeviceGetDefaultMemPool(&h->c.pool, device), "cudaDeviceGetDefaultMemPool");
+    uint64_t keep = UINT64_MAX;  // keep freed blocks cached across chunks/steps
+    cfb::cuda_check(cudaMemPoolSetAttribute(h->c.pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool attr");
+    *out = h.release();
+  });
+}
+
+void cf_ctx_destroy(cf_ctx* ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->c.stream);
+  cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+void* cf_ctx_stream(cf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+
+int cf_ctx_synchronize(cf_ctx* ctx) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    cfb::cuda_check(cudaStreamSynchronize(ctx->c.stream), "cudaStreamSynchronize");
+  });
+}
+
+int cf_nccl_unique_id(uint8_t* out128) {
+  return cfb::guard([&] {
+    need(out128, "out");
+    cfb::dp_unique_id(out128);
+  });
+}
+
+int cf_ctx_init_dp(cf_ctx* ctx, int rank, int world, const uint8_t* id128) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    if (world < 1 || rank < 0 || rank >= world) throw cfb::ValidationError("bad rank/world");
+    if (world > 1) need(id128, "nccl id");
+    cfb::dp_init(&ctx->c, rank, world, id128);
+  });
+}
+
+int cf_model_create(cf_ctx* ctx, const cf_model_cfg* cfg, cf_model** out) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(cfg, "cfg");
+    auto h = std::make_unique<cf_model>();
+    h->ctx = ctx;
+    h->m = cfb::model_create(&ctx->c, *cfg);
+    *out = h.release();
+  });
+}
+
+void cf_model_destroy(cf_model* model) {
+  if (!model) return;
+  cfb::model_destroy(model->m);
+  delete model;
+}
+
+int64_t cf_model_num_tensors(const cf_model* model) {
+  return model ? static_cast<int64_t>(model->m->slots.size()) : -1;
+}
+int64_t cf_model_num_params(const cf_model* model) { return model ? model->m->num_params : -1; }
+
+int cf_model_tensor_info(const cf_model* model, int64_t idx, char* name, size_t cap, int64_t* rows, int64_t* cols) {
+  return cfb::guard([&] {
+    need(model, "model");
+    if (idx < 0 || idx >= static_cast<int64_t>(model->m->slots.size()))
+      throw cfb::ValidationError("tensor index out of range");
+    const cfb::Slot& s = model->m->slots[static_cast<size_t>(idx)];
+    if (rows) *rows = s.rows;
+    if (cols) *cols = s.cols;
+    if (name && cap) {
+      const size_t n = std::min(cap - 1, s.name.size());
+      std::memcpy(name, s.name.data(), n);
+      name[n] = 0;
+    }
+  });
+}
+
+int cf_model_get_param(cf_model* model, int64_t idx, double* host) {
+  return cfb::guard([&] {
+    need(model, "model");
+    need(host, "host");
+    cfb::model_get_param(model->m, idx, host);
+  });
+}
+int cf_model_set_param(cf_model* model, int64_t idx, const double* host) {
+  return cfb::guard([&] {
+    need(model, "model");
+    need(host, "host");
+    cfb::model_set_param(model->m, idx, host);
+  });
+}
+int cf_model_get_grad(cf_model* model, int64_t idx, double* host) {
+  return cfb::guard([&] {
+    need(model, "model");
+    need(host, "host");
+    cfb::model_get_grad(model->m, idx, host);
+  });
+}
+int cf_model_zero_grads(cf_model* model) {
+  return cfb::guard([&] {
+    need(model, "model");
+    cfb::cuda_check(cudaMemsetAsync(model->m->grads, 0, static_cast<size_t>(model->m->grad_numel) * 4,
+                                    model->ctx->c.stream),
+                    "memset");
+  });
+}
+int cf_model_grad_buffer(cf_model* model, void** dev_ptr, int64_t* numel) {
+  return cfb::guard([&] {
+    need(model, "model");
+    if (dev_ptr) *dev_ptr = model->m->grads;
+    if (numel) *numel = model->m->grad_numel;
+  });
+}
+
+int cf_run_plan(cf_ctx* ctx, cf_model* model, const cf_plan* plan, const int64_t* seq_ids, const int64_t* lengths,
+                const int32_t* tokens, int64_t n, const cf_run_opts* opts, cf_run_result* result) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    need(plan, "plan");
+    cf_run_opts o{};
+    if (opts) o = *opts;
+    cfb::Batch b{seq_ids, lengths, tokens, nullptr, n};
+    cfb::run_plan(&ctx->c, model->m, plan->p, b, o, result);
+  });
+}
+
+int cf_step_prepare(cf_ctx* ctx, cf_model* model, const cf_plan* plan, const int64_t* seq_ids,
+                    const int64_t* lengths, const int32_t* tokens, int64_t n, cf_step** out) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    need(plan, "plan");
+    cfb::Batch b{seq_ids, lengths, tokens, nullptr, n};
+    *out = cfb::step_prepare(&ctx->c, model->m, plan->p, b);
+  });
+}
+
+int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, const cf_run_opts* opts, cf_run_result* result) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    need(step, "step");
+    cf_run_opts o{};
+    if (opts) o = *opts;
+    cfb::step_run(&ctx->c, model->m, step, o, result);
+  });
+}
+
+void cf_step_destroy(cf_step* step) { cfb::step_destroy(step); }
+
+int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids, const int64_t* lengths,
+                     const int32_t* tokens, int64_t n, double normalizer_override, cf_run_result* result) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    // backward_full: each sequence is its own standalone chunk of one
+    // segment (no packing, no prefix), forward then backward.
+    cfb::Plan p;
+    p.chunk_size = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      cfb::Chunk c;
+      c.id = i;
+      c.kind = cfb::kStandalone;
+      c.total = lengths[i];
+      c.seg_off = i;
+      c.seg_cnt = 1;
+      p.segments.push_back({seq_ids[i], 0, lengths[i]});
+      p.index_of[i] = i;
+      p.chunk_tokens[i] = lengths[i];
+      p.chunk_size = std::max(p.chunk_size, lengths[i]);
+      p.chunks.push_back(c);
+    }
+    cfb::schedule_step(p, 1);
+    cf_run_opts o{};
+    o.normalizer_override = normalizer_override;
+    cfb::Batch b{seq_ids, lengths, tokens, nullptr, n};
+    cfb::run_plan(&ctx->c, model->m, p, b, o, result);
+  });
+}
+
+int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda, const void* b, int b_kmajor, int64_t ldb,
+               void* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int epi, const void* residual, int64_t ld_res) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    cfk::GemmDesc d{a, lda, a_kmajor, b, ldb, b_kmajor, c, ldc, residual, ld_res, m, n, k, epi};
+    cfb::cuda_check(cfk::gemm(d, ctx->c.stream), "gemm");
+    ctx->c.launches += 1;
+  });
+}
+
+}  // extern "C"

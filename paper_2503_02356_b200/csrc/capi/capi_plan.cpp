@@ -1,0 +1,147 @@
+// C-ABI: errors + planning entry points (include/chunkflow_b200.h).
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../../include/chunkflow_b200.h"
+#include "../host/plan.hpp"
+#include "capi_util.hpp"
+
+namespace cfb {
+thread_local std::string g_last_error;
+}
+
+extern "C" {
+
+const char* cf_last_error(void) { return cfb::g_last_error.c_str(); }
+const char* cf_version(void) { return "chunkflow_b200 0.1 (sm_100a)"; }
+
+int cf_plan_build(const int64_t* seq_ids, const int64_t* lengths, int64_t n, int64_t chunk_size, int64_t k,
+                  cf_plan** out) {
+  return cfb::guard([&] {
+    if (n < 0 || (n > 0 && (!seq_ids || !lengths))) throw cfb::ValidationError("bad batch arrays");
+    for (int64_t i = 0; i < n; ++i)
+      if (lengths[i] < 1) throw cfb::ValidationError("sequence lengths must be positive");
+    auto h = std::make_unique<cf_plan>();
+    h->p = cfb::construct_chunks(seq_ids, lengths, n, chunk_size);
+    cfb::schedule_step(h->p, k);
+    *out = h.release();
+  });
+}
+
+int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out) {
+  return cfb::guard([&] {
+    auto h = std::make_unique<cf_plan>();
+    h->p = cfb::schedule_group(n, k, chunk_size);
+    *out = h.release();
+  });
+}
+
+int cf_plan_counts(const cf_plan* plan, int64_t* n_chunks, int64_t* n_segments, int64_t* n_events,
+                   int64_t* n_groups) {
+  return cfb::guard([&] {
+    if (n_chunks) *n_chunks = static_cast<int64_t>(plan->p.chunks.size());
+    if (n_segments) *n_segments = static_cast<int64_t>(plan->p.segments.size());
+    if (n_events) *n_events = static_cast<int64_t>(plan->p.events.size());
+    if (n_groups) *n_groups = static_cast<int64_t>(plan->p.groups.size());
+  });
+}
+
+int cf_plan_export(const cf_plan* plan, cf_chunk_rec* chunks, cf_segment_rec* segments, cf_event_rec* events,
+                   cf_plan_diag* diag) {
+  return cfb::guard([&] {
+    const cfb::Plan& p = plan->p;
+    if (chunks)
+      for (size_t i = 0; i < p.chunks.size(); ++i) {
+        const cfb::Chunk& c = p.chunks[i];
+        chunks[i] = {c.id, c.kind, c.group, c.index, c.total, c.seg_off, c.seg_cnt};
+      }
+    if (segments)
+      for (size_t i = 0; i < p.segments.size(); ++i)
+        segments[i] = {p.segments[i].seq, p.segments[i].start, p.segments[i].len};
+    if (events)
+      for (size_t i = 0; i < p.events.size(); ++i) {
+        const cfb::Event& e = p.events[i];
+        events[i] = {e.kind, e.chunk, e.group, e.index, e.recompute, e.save_kv, e.read_prefix, e.acc_grad};
+      }
+    if (diag) *diag = {p.peak_retained, p.recompute_tokens, static_cast<int64_t>(p.violations.size())};
+  });
+}
+
+int cf_plan_export_groups(const cf_plan* plan, int64_t* group_ids, int64_t* offsets, int64_t* members) {
+  return cfb::guard([&] {
+    int64_t g = 0, m = 0;
+    offsets[0] = 0;
+    for (const auto& [gid, mem] : plan->p.groups) {
+      group_ids[g] = gid;
+      for (int64_t c : mem) members[m++] = c;
+      offsets[++g] = m;
+    }
+  });
+}
+
+int cf_plan_violation(const cf_plan* plan, int64_t i, char* buf, size_t cap) {
+  return cfb::guard([&] {
+    if (i < 0 || i >= static_cast<int64_t>(plan->p.violations.size())) throw cfb::ValidationError("violation index");
+    const std::string& s = plan->p.violations[static_cast<size_t>(i)];
+    if (cap == 0) return;
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  });
+}
+
+int cf_plan_listing(const cf_plan* plan, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] {
+    const std::string s = cfb::listing(plan->p);
+    if (len) *len = s.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int cf_plan_partition(const cf_plan* global, int64_t world, int64_t rank, cf_plan** out) {
+  return cfb::guard([&] {
+    if (rank < 0 || rank >= world) throw cfb::ValidationError("rank out of range");
+    const auto units = cfb::plan_units(global->p, 1.0, cfb::kPairWeight);
+    const auto assign = cfb::lpt_assign(units, world);
+    auto h = std::make_unique<cf_plan>();
+    h->p = cfb::sub_plan(global->p, units, assign[static_cast<size_t>(rank)], global->p.k);
+    *out = h.release();
+  });
+}
+
+int cf_plan_rank_tokens(const cf_plan* global, int64_t world, int64_t* tokens) {
+  return cfb::guard([&] {
+    const auto units = cfb::plan_units(global->p, 1.0, cfb::kPairWeight);
+    const auto assign = cfb::lpt_assign(units, world);
+    for (int64_t r = 0; r < world; ++r) {
+      tokens[r] = 0;
+      for (int64_t u : assign[static_cast<size_t>(r)]) tokens[r] += units[static_cast<size_t>(u)].tokens;
+    }
+  });
+}
+
+void cf_plan_destroy(cf_plan* plan) { delete plan; }
+
+int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab, uint64_t seed, int32_t* tokens_out) {
+  return cfb::guard([&] {
+    if (vocab < 1) throw cfb::ValidationError("vocab must be positive");
+    uint64_t s = seed;
+    int64_t o = 0;
+    const uint64_t v = static_cast<uint64_t>(vocab);
+    const uint64_t thr = (0 - v) % v;  // next_below rejection (common.hpp:52-58)
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t t = 0; t < lengths[i]; ++t) {
+        uint64_t r;
+        do r = cfb::splitmix_next(s);
+        while (r < thr);
+        tokens_out[o++] = static_cast<int32_t>(r % v);
+      }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,465 @@
+// Bandwidth-bound kernels (see ops.h): coalesced, vectorised where the row
+// pitch allows, warp-shuffle reductions, and fixed reduction orders so every
+// result is bitwise reproducible run to run (needed for the reference's
+// recompute-loss check, plan_runner.hpp:232-241).
+#include "common.cuh"
+#include "ops.h"
+
+namespace cfk {
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned blocks_for(int64_t n, int per = kThreads) {
+  int64_t b = (n + per - 1) / per;
+  if (b > 148 * 64) b = 148 * 64;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+
+__global__ void init_uniform_kernel(bf16* dst, int64_t ld, int64_t rows, int64_t cols, uint64_t base, uint64_t seed,
+                                    double scale) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // state after (base + i + 1) increments of the golden gamma
+    uint64_t z = seed + (base + static_cast<uint64_t>(i) + 1ull) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+    const int64_t r = i / cols, c = i % cols;
+    dst[r * ld + c] = __double2bfloat16((u * 2.0 - 1.0) * scale);
+  }
+}
+
+__global__ void fill_kernel(float* d, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[i] = v;
+}
+
+// One warp per row.
+__global__ void embed_kernel(const int32_t* tok, const bf16* E, int64_t d, int64_t T, float* x) {
+  const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const bf16* e = E + static_cast<int64_t>(tok[row]) * d;
+  float* o = x + row * d;
+  if ((d & 7) == 0) {
+    for (int64_t c = lane * 8; c < d; c += 256) {
+      const uint4 v = *reinterpret_cast<const uint4*>(e + c);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+      float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]), f2 = __bfloat1622float2(h[2]),
+             f3 = __bfloat1622float2(h[3]);
+      *reinterpret_cast<float4*>(o + c) = make_float4(f0.x, f0.y, f1.x, f1.y);
+      *reinterpret_cast<float4*>(o + c + 4) = make_float4(f2.x, f2.y, f3.x, f3.y);
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) o[c] = __bfloat162float(e[c]);
+  }
+}
+
+__global__ void rmsnorm_fwd_kernel(const float* x, const float* gain, int64_t T, int64_t d, float eps, bf16* y) {
+  const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const float* xr = x + row * d;
+  bf16* yr = y + row * d;
+  float ss = 0.f;
+  const bool vec = (d & 3) == 0;
+  if (vec) {
+    for (int64_t c = lane * 4; c < d; c += 128) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + c);
+      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) ss += xr[c] * xr[c];
+  }
+  ss = warp_sum(ss);
+  const float r = rsqrtf(ss / static_cast<float>(d) + eps);
+  if (vec) {
+    for (int64_t c = lane * 4; c < d; c += 128) {
+      const float4 v = *reinterpret_cast<const float4*>(xr + c);
+      const float4 g = *reinterpret_cast<const float4*>(gain + c);
+      uint2 o;
+      o.x = pack_bf16(v.x * r * g.x, v.y * r * g.y);
+      o.y = pack_bf16(v.z * r * g.z, v.w * r * g.w);
+      *reinterpret_cast<uint2*>(yr + c) = o;
+    }
+  } else {
+    for (int64_t c = lane; c < d; c += 32) yr[c] = __float2bfloat16_rn(xr[c] * r * gain[c]);
+  }
+}
+
+__global__ void to_bf16_kernel(const float* x, bf16* y, int64_t n) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(x)[i];
+    uint2 o;
+    o.x = pack_bf16(v.x, v.y);
+    o.y = pack_bf16(v.z, v.w);
+    reinterpret_cast<uint2*>(y)[i] = o;
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
+__global__ void rope_table_kernel(const int32_t* pos, int64_t T, int half, int dh, double theta, float2* tab) {
+  const int64_t n = T * half;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / half;
+    const int j = static_cast<int>(i % half);
+    const double f = pow(theta, -2.0 * static_cast<double>(j) / static_cast<double>(dh));
+    double s, c;
+    sincos(static_cast<double>(pos[t]) * f, &s, &c);
+    tab[i] = make_float2(static_cast<float>(c), static_cast<float>(s));
+  }
+}
+
+// grid-stride over (t, head, j) with j < half; heads [0,H) are q, [H, H+KVH) are k.
+__global__ void rope_qk_kernel(bf16* qkv, int64_t ld, int64_t T, int H, int KVH, int dh, int64_t col_k,
+                               const float2* tab, int inverse_q_only) {
+  const int half = dh / 2;
+  const int heads = inverse_q_only ? H : H + KVH;
+  const int64_t n = T * heads * half;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % half);
+    const int64_t th = i / half;
+    const int hh = static_cast<int>(th % heads);
+    const int64_t t = th / heads;
+    bf16* p = qkv + t * ld + (hh < H ? static_cast<int64_t>(hh) * dh : col_k + static_cast<int64_t>(hh - H) * dh);
+    const float2 cs = tab[t * half + j];
+    const float sn = inverse_q_only ? -cs.y : cs.y;
+    const float x0 = __bfloat162float(p[j]), x1 = __bfloat162float(p[j + half]);
+    p[j] = __float2bfloat16_rn(x0 * cs.x - x1 * sn);
+    p[j + half] = __float2bfloat16_rn(x1 * cs.x + x0 * sn);
+  }
+}
+
+__global__ void kv_store_kernel(const bf16* qkv, int64_t ld, int64_t T, int64_t kvw, int64_t col_k, int64_t col_v,
+                                bf16* kc, bf16* vc, int64_t cache_ld) {
+  const int64_t n = T * kvw;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / kvw, c = i % kvw;
+    kc[t * cache_ld + c] = qkv[t * ld + col_k + c];
+    vc[t * cache_ld + c] = qkv[t * ld + col_v + c];
+  }
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
+
+__global__ void swiglu_fwd_kernel(const bf16* gu, int64_t T, int64_t ffn, bf16* h) {
+  const int64_t n = T * ffn;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / ffn, j = i % ffn;
+    const float g = __bfloat162float(gu[t * 2 * ffn + j]);
+    const float u = __bfloat162float(gu[t * 2 * ffn + ffn + j]);
+    h[i] = __float2bfloat16_rn(g * sigmoidf_(g) * u);
+  }
+}
+
+__global__ void swiglu_bwd_kernel(const bf16* gu, const bf16* dh, int64_t T, int64_t ffn, bf16* dgu) {
+  const int64_t n = T * ffn;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / ffn, j = i % ffn;
+    const float g = __bfloat162float(gu[t * 2 * ffn + j]);
+    const float u = __bfloat162float(gu[t * 2 * ffn + ffn + j]);
+    const float d = __bfloat162float(dh[i]);
+    const float s = sigmoidf_(g);
+    dgu[t * 2 * ffn + j] = __float2bfloat16_rn(d * u * s * (1.f + g * (1.f - s)));
+    dgu[t * 2 * ffn + ffn + j] = __float2bfloat16_rn(d * g * s);
+  }
+}
+
+// One 256-thread block per row.
+__global__ void ce_kernel(const float* logits, int64_t V, int64_t ld, const int32_t* targets, float inv_norm, float* row_loss,
+                          bf16* dlogits) {
+  const int64_t row = blockIdx.x;
+  const int32_t tgt = targets[row];
+  const float* l = logits + row * ld;
+  __shared__ float red_m[8], red_s[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (tgt < 0) {
+    if (threadIdx.x == 0) row_loss[row] = 0.f;
+    if (dlogits)
+      for (int64_t c = threadIdx.x; c < V; c += blockDim.x) dlogits[row * ld + c] = __float2bfloat16(0.f);
+    return;
+  }
+  float m = -INFINITY, s = 0.f;
+  for (int64_t c = threadIdx.x; c < V; c += blockDim.x) {
+    const float x = l[c];
+    if (x > m) {
+      s = s * __expf(m - x) + 1.f;
+      m = x;
+    } else {
+      s += __expf(x - m);
+    }
+  }
+  // combine (m, s) across the warp then the block
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  if (lane == 0) {
+    red_m[warp] = m;
+    red_s[warp] = s;
+  }
+  __syncthreads();
+  float M = red_m[0];
+  for (int w = 1; w < 8; ++w) M = fmaxf(M, red_m[w]);
+  float S = 0.f;
+  for (int w = 0; w < 8; ++w) S += red_s[w] * __expf(red_m[w] - M);
+  const float lse = M + logf(S);
+  if (threadIdx.x == 0) row_loss[row] = lse - l[tgt];
+  if (dlogits) {
+    const float invS = 1.f / S;
+    for (int64_t c = threadIdx.x; c < V; c += blockDim.x) {
+      const float p = __expf(l[c] - M) * invS - (c == tgt ? 1.f : 0.f);
+      dlogits[row * ld + c] = __float2bfloat16_rn(p * inv_norm);
+    }
+  }
+}
+
+__global__ void sum_f64_kernel(const float* v, int64_t n, double* out) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += static_cast<double>(v[i]);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+// One warp per row.
+__global__ void rmsnorm_bwd_kernel(const float* x, const float* gain, const float* dy, const float* dres, int64_t T,
+                                   int64_t d, float eps, float* dx, float* rstd) {
+  const int64_t row = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const float* xr = x + row * d;
+  const float* gr = dy + row * d;
+  float ss = 0.f, dot = 0.f;
+  for (int64_t c = lane; c < d; c += 32) {
+    const float xv = xr[c];
+    ss += xv * xv;
+    dot += gr[c] * gain[c] * xv;
+  }
+  ss = warp_sum(ss);
+  dot = warp_sum(dot);
+  const float r = rsqrtf(ss / static_cast<float>(d) + eps);
+  const float k = r * r * r * dot / static_cast<float>(d);
+  for (int64_t c = lane; c < d; c += 32) {
+    const float base = dres ? dres[row * d + c] : 0.f;
+    dx[row * d + c] = base + r * gr[c] * gain[c] - xr[c] * k;
+  }
+  if (lane == 0 && rstd) rstd[row] = r;
+}
+
+// Block = 32 columns x 8 row-groups; fixed order over rows.
+__global__ void gain_grad_kernel(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d,
+                                 float* dgain) {
+  __shared__ float part[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < d)
+    for (int64_t t = w; t < T; t += 8) s += dy[t * d + c] * x[t * d + c] * rstd[t];
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < d) {
+    float tot = 0.f;
+    for (int i = 0; i < 8; ++i) tot += part[i][lane];
+    dgain[c] += tot;
+  }
+}
+
+__global__ void dkv_to_dqkv_kernel(const float* dk, const float* dv, int64_t acc_ld, int64_t T, int KVH, int dh,
+                                   const float2* tab, bf16* dqkv, int64_t ld, int64_t col_k, int64_t col_v) {
+  const int64_t kvw = static_cast<int64_t>(KVH) * dh;
+  const int64_t n = T * kvw;
+  const int half = dh / 2;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / kvw, c = i % kvw;
+    dqkv[t * ld + col_v + c] = __float2bfloat16_rn(dv[t * acc_ld + c]);
+    float val = dk[t * acc_ld + c];
+    if (tab) {
+      const int j = static_cast<int>(c % dh);
+      const int64_t hb = c - j;
+      const int jj = j < half ? j : j - half;
+      const float2 cs = tab[t * half + jj];
+      if (j < half) {  // dx0 = dy0 c + dy1 s
+        val = val * cs.x + dk[t * acc_ld + hb + j + half] * cs.y;
+      } else {  // dx1 = -dy0 s + dy1 c
+        val = val * cs.x - dk[t * acc_ld + hb + jj] * cs.y;
+      }
+    }
+    dqkv[t * ld + col_k + c] = __float2bfloat16_rn(val);
+  }
+}
+
+__global__ void scale_rows_kernel(float* x, int64_t rows, int64_t cols, int64_t ld, float s) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[(i / cols) * ld + i % cols] *= s;
+}
+
+__global__ void embed_bwd_kernel(const float* dx, int64_t d, const int32_t* order, const int32_t* uniq,
+                                 const int32_t* off, float* dE) {
+  const int u = blockIdx.x;
+  const int32_t b = off[u], e = off[u + 1];
+  float* dst = dE + static_cast<int64_t>(uniq[u]) * d;
+  for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int32_t i = b; i < e; ++i) s += dx[static_cast<int64_t>(order[i]) * d + c];
+    dst[c] += s;
+  }
+}
+
+__global__ void bf16_to_f64_kernel(const bf16* src, int64_t ld, int64_t rows, int64_t cols, double* dst) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<double>(__bfloat162float(src[(i / cols) * ld + i % cols]));
+}
+__global__ void f64_to_bf16_kernel(const double* src, int64_t rows, int64_t cols, bf16* dst, int64_t ld) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[(i / cols) * ld + i % cols] = __double2bfloat16(src[i]);
+}
+__global__ void f32_to_f64_kernel(const float* src, int64_t ld, int64_t rows, int64_t cols, double* dst) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = static_cast<double>(src[(i / cols) * ld + i % cols]);
+}
+__global__ void f64_to_f32_kernel(const double* src, int64_t rows, int64_t cols, float* dst, int64_t ld) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[(i / cols) * ld + i % cols] = static_cast<float>(src[i]);
+}
+
+}  // namespace
+
+cudaError_t init_uniform_bf16(bf16* dst, int64_t ld, int64_t rows, int64_t cols, uint64_t draw_base, uint64_t seed,
+                              double scale, cudaStream_t st) {
+  init_uniform_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(dst, ld, rows, cols, draw_base, seed, scale);
+  return cudaGetLastError();
+}
+cudaError_t fill_f32(float* dst, int64_t n, float v, cudaStream_t st) {
+  fill_kernel<<<blocks_for(n), kThreads, 0, st>>>(dst, n, v);
+  return cudaGetLastError();
+}
+cudaError_t embed_fwd(const int32_t* tok, const bf16* E, int64_t d, int64_t T, float* x, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  embed_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(tok, E, d, T, x);
+  return cudaGetLastError();
+}
+cudaError_t rmsnorm_fwd(const float* x, const float* gain, int64_t T, int64_t d, float eps, bf16* y,
+                        cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  rmsnorm_fwd_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(x, gain, T, d, eps, y);
+  return cudaGetLastError();
+}
+cudaError_t to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st) {
+  to_bf16_kernel<<<blocks_for(n / 4 + 1), kThreads, 0, st>>>(x, y, n);
+  return cudaGetLastError();
+}
+cudaError_t rope_table(const int32_t* pos, int64_t T, int dh, double theta, float2* tab, cudaStream_t st) {
+  rope_table_kernel<<<blocks_for(T * (dh / 2)), kThreads, 0, st>>>(pos, T, dh / 2, dh, theta, tab);
+  return cudaGetLastError();
+}
+cudaError_t rope_qk(bf16* qkv, int64_t ld, int64_t T, int H, int KVH, int dh, int64_t col_k, const float2* tab,
+                    cudaStream_t st) {
+  rope_qk_kernel<<<blocks_for(T * (H + KVH) * (dh / 2)), kThreads, 0, st>>>(qkv, ld, T, H, KVH, dh, col_k, tab, 0);
+  return cudaGetLastError();
+}
+cudaError_t rope_bwd_q(bf16* dqkv, int64_t ld, int64_t T, int H, int dh, const float2* tab, cudaStream_t st) {
+  rope_qk_kernel<<<blocks_for(T * H * (dh / 2)), kThreads, 0, st>>>(dqkv, ld, T, H, 0, dh, 0, tab, 1);
+  return cudaGetLastError();
+}
+cudaError_t kv_store(const bf16* qkv, int64_t ld, int64_t T, int64_t kvw, int64_t col_k, int64_t col_v, bf16* kc,
+                     bf16* vc, int64_t cache_ld, cudaStream_t st) {
+  kv_store_kernel<<<blocks_for(T * kvw), kThreads, 0, st>>>(qkv, ld, T, kvw, col_k, col_v, kc, vc, cache_ld);
+  return cudaGetLastError();
+}
+cudaError_t swiglu_fwd(const bf16* gu, int64_t T, int64_t ffn, bf16* h, cudaStream_t st) {
+  swiglu_fwd_kernel<<<blocks_for(T * ffn), kThreads, 0, st>>>(gu, T, ffn, h);
+  return cudaGetLastError();
+}
+cudaError_t swiglu_bwd(const bf16* gu, const bf16* dh, int64_t T, int64_t ffn, bf16* dgu, cudaStream_t st) {
+  swiglu_bwd_kernel<<<blocks_for(T * ffn), kThreads, 0, st>>>(gu, dh, T, ffn, dgu);
+  return cudaGetLastError();
+}
+cudaError_t ce_fwd_bwd(const float* logits, int64_t T, int64_t V, int64_t ld, const int32_t* targets, float inv_norm,
+                       float* row_loss, bf16* dlogits, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  ce_kernel<<<static_cast<unsigned>(T), 256, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  return cudaGetLastError();
+}
+cudaError_t sum_f64(const float* v, int64_t n, double* out, cudaStream_t st) {
+  sum_f64_kernel<<<1, 1024, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t rmsnorm_bwd(const float* x, const float* gain, const float* dy, const float* dres, int64_t T, int64_t d,
+                        float eps, float* dx, float* rstd, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  rmsnorm_bwd_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(x, gain, dy, dres, T, d, eps, dx,
+                                                                                    rstd);
+  return cudaGetLastError();
+}
+cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d, float* dgain,
+                      cudaStream_t st) {
+  gain_grad_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(x, dy, rstd, T, d, dgain);
+  return cudaGetLastError();
+}
+cudaError_t dkv_to_dqkv(const float* dk, const float* dv, int64_t acc_ld, int64_t T, int KVH, int dh,
+                        const float2* tab, bf16* dqkv, int64_t ld, int64_t col_k, int64_t col_v, cudaStream_t st) {
+  dkv_to_dqkv_kernel<<<blocks_for(T * KVH * dh), kThreads, 0, st>>>(dk, dv, acc_ld, T, KVH, dh, tab, dqkv, ld, col_k,
+                                                                   col_v);
+  return cudaGetLastError();
+}
+cudaError_t scale_rows_f32(float* x, int64_t rows, int64_t cols, int64_t ld, float s, cudaStream_t st) {
+  scale_rows_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(x, rows, cols, ld, s);
+  return cudaGetLastError();
+}
+cudaError_t embed_bwd(const float* dx, int64_t d, const int32_t* order, const int32_t* uniq, const int32_t* off,
+                      int64_t nuniq, float* dE, cudaStream_t st) {
+  if (nuniq == 0) return cudaSuccess;
+  embed_bwd_kernel<<<static_cast<unsigned>(nuniq), 256, 0, st>>>(dx, d, order, uniq, off, dE);
+  return cudaGetLastError();
+}
+cudaError_t bf16_to_f64(const bf16* src, int64_t ld, int64_t rows, int64_t cols, double* dst, cudaStream_t st) {
+  bf16_to_f64_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(src, ld, rows, cols, dst);
+  return cudaGetLastError();
+}
+cudaError_t f64_to_bf16(const double* src, int64_t rows, int64_t cols, bf16* dst, int64_t ld, cudaStream_t st) {
+  f64_to_bf16_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(src, rows, cols, dst, ld);
+  return cudaGetLastError();
+}
+cudaError_t f32_to_f64(const float* src, int64_t ld, int64_t rows, int64_t cols, double* dst, cudaStream_t st) {
+  f32_to_f64_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(src, ld, rows, cols, dst);
+  return cudaGetLastError();
+}
+cudaError_t f64_to_f32(const double* src, int64_t rows, int64_t cols, float* dst, int64_t ld, cudaStream_t st) {
+  f64_to_f32_kernel<<<blocks_for(rows * cols), kThreads, 0, st>>>(src, rows, cols, dst, ld);
+  return cudaGetLastError();
+}
+
+}  // namespace cfk

@@ -1,0 +1,365 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a.
+//
+//   C[M,N] (op)= sum_k A(m,k) * B(n,k)          bf16 x bf16 -> fp32 in TMEM
+//
+// A is K-major ([M,K] row-major, activations) or M-major ([K,M] row-major,
+// i.e. a transposed view of activations for weight gradients); B is K-major
+// ([N,K]) or N-major ([K,N], the reference's [in,out] weight layout).  Both
+// majors are fed by TMA with 128B swizzle straight into the UMMA canonical
+// layouts, so no transpose kernels exist anywhere on the path.
+//
+// Roles (256 threads, 1 CTA/SM, grid = min(tiles, #SM)):
+//   warp 0      TMA producer  (one lane)   smem ring of kStages A/B stages
+//   warp 1      MMA issuer    (one lane)   tcgen05.mma 128xBNx16, fp32 accum
+//   warp 2      TMEM allocator             2 accumulator buffers (2*BN cols)
+//   warps 4-7   epilogue                   tcgen05.ld -> fused op -> global
+// The epilogue of tile i overlaps the main loop of tile i+1 through the two
+// TMEM accumulators (tmem_full / tmem_empty mbarriers).
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace cfk {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr uint32_t kSlab = 64 * BK * 2;  // one 64-wide MN slab x BK rows = 8 KiB
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kABytes = BM * BK * 2;
+  static constexpr uint32_t kBBytes = BN * BK * 2;
+  static constexpr uint32_t kTmemCols = 2 * BN;
+  static constexpr size_t kSmem = 1024 + kStages * (kABytes + kBBytes) + 256;
+};
+
+struct Args {
+  int M, N, K;
+  int num_m, num_n, num_k;
+  void* C;
+  int64_t ldc;
+  const void* R;  // fp32 residual (EPI_F32_RES) or bf16 aux (EPI_BF16_TANHGRAD)
+  int64_t ldr;
+};
+
+template <int EPI>
+__device__ __forceinline__ void store_row32(const Args& g, int row, int col0, const uint32_t (&r)[32]) {
+  if (row >= g.M) return;
+  const bool full = col0 + 32 <= g.N;
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_TANH || EPI == EPI_BF16_TANHGRAD) {
+    __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+    const __nv_bfloat16* aux = nullptr;
+    if constexpr (EPI == EPI_BF16_TANHGRAD)
+      aux = reinterpret_cast<const __nv_bfloat16*>(g.R) + static_cast<int64_t>(row) * g.ldr + col0;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float x = __uint_as_float(r[j]);
+      if constexpr (EPI == EPI_BF16_TANH) x = tanhf(x);
+      if constexpr (EPI == EPI_BF16_TANHGRAD) {
+        if (full || col0 + j < g.N) {
+          const float h = __bfloat162float(aux[j]);
+          x = x * (1.0f - h * h);
+        }
+      }
+      v[j] = x;
+    }
+    if (full) {
+      uint4* dst = reinterpret_cast<uint4*>(c);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                            pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < g.N) c[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* c = reinterpret_cast<float*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+    const float* res = nullptr;
+    if constexpr (EPI == EPI_F32_RES) res = reinterpret_cast<const float*>(g.R) + static_cast<int64_t>(row) * g.ldr + col0;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        if constexpr (EPI == EPI_F32_ACC) {
+          const float4 o = reinterpret_cast<const float4*>(c)[q];
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        if constexpr (EPI == EPI_F32_RES) {
+          const float4 o = reinterpret_cast<const float4*>(res)[q];
+          v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+        }
+        reinterpret_cast<float4*>(c)[q] = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (col0 + j >= g.N) continue;
+        float x = __uint_as_float(r[j]);
+        if constexpr (EPI == EPI_F32_ACC) x += c[j];
+        if constexpr (EPI == EPI_F32_RES) x += res[j];
+        c[j] = x;
+      }
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args g) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = g.num_m * g.num_n;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % g.num_m, nb = tile / g.num_m;
+        for (int kb = 0; kb < g.num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * C::kABytes;
+          uint8_t* b = sB + stage * C::kBBytes;
+          mbar_expect_tx(&full[stage], C::kABytes + C::kBBytes);
+          if constexpr (!A_MN) {
+            tma_load_2d(a, &tmA, &full[stage], kb * BK, mb * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * kSlab, &tmA, &full[stage], mb * BM + j * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(b, &tmB, &full[stage], kb * BK, nb * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * kSlab, &tmB, &full[stage], nb * BN + j * 64, kb * BK);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < g.num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, kSlab, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, kSlab, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
+            umma_bf16(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mb = tile % g.num_m, nb = tile / g.num_m;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (c == BN / 32 - 1) {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+        const int col0 = nb * BN + c * 32;
+        if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<C::kTmemCols>(tmem_base);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map, dim0 = contiguous.
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+              uint32_t box_outer) {
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  bool ok = A_MN ? make_map(&ta, d.a, d.M, d.K, d.lda, 64, 64) : make_map(&ta, d.a, d.K, d.M, d.lda, BK, BM);
+  ok = ok && (B_MN ? make_map(&tb, d.b, d.N, d.K, d.ldb, 64, 64) : make_map(&tb, d.b, d.K, d.N, d.ldb, BK, BN));
+  if (!ok) return cudaErrorInvalidValue;
+  Args g;
+  g.M = static_cast<int>(d.M);
+  g.N = static_cast<int>(d.N);
+  g.K = static_cast<int>(d.K);
+  g.num_m = static_cast<int>((d.M + BM - 1) / BM);
+  g.num_n = static_cast<int>((d.N + BN - 1) / BN);
+  g.num_k = static_cast<int>((d.K + BK - 1) / BK);
+  g.C = d.c;
+  g.ldc = d.ldc;
+  g.R = d.r;
+  g.ldr = d.ldr;
+  auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int tiles = g.num_m * g.num_n;
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  kern<<<grid, 256, C::kSmem, st>>>(ta, tb, g);
+  return cudaGetLastError();
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t by_epi(const GemmDesc& d, cudaStream_t st) {
+  switch (d.epi) {
+    case EPI_BF16: return launch_t<BN, A_MN, B_MN, EPI_BF16>(d, st);
+    case EPI_F32: return launch_t<BN, A_MN, B_MN, EPI_F32>(d, st);
+    case EPI_F32_ACC: return launch_t<BN, A_MN, B_MN, EPI_F32_ACC>(d, st);
+    case EPI_F32_RES: return launch_t<BN, A_MN, B_MN, EPI_F32_RES>(d, st);
+    case EPI_BF16_TANH: return launch_t<BN, A_MN, B_MN, EPI_BF16_TANH>(d, st);
+    case EPI_BF16_TANHGRAD: return launch_t<BN, A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int BN>
+cudaError_t by_major(const GemmDesc& d, cudaStream_t st) {
+  if (d.a_kmajor && d.b_kmajor) return by_epi<BN, false, false>(d, st);
+  if (d.a_kmajor && !d.b_kmajor) return by_epi<BN, false, true>(d, st);
+  if (!d.a_kmajor && !d.b_kmajor) return by_epi<BN, true, true>(d, st);
+  return by_epi<BN, true, false>(d, st);
+}
+
+}  // namespace
+
+int gemm_num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0) return cudaSuccess;
+  // TMA: 16-byte aligned bases and row pitches.
+  if ((reinterpret_cast<uintptr_t>(d.a) & 15) || (reinterpret_cast<uintptr_t>(d.b) & 15) || (d.lda % 8) ||
+      (d.ldb % 8) || (reinterpret_cast<uintptr_t>(d.c) & 15) || (d.ldc % 8))
+    return cudaErrorMisalignedAddress;
+  const int64_t sms = gemm_num_sms();
+  const int64_t tiles256 = ((d.M + BM - 1) / BM) * ((d.N + 255) / 256);
+  const bool wide = d.N > 128 && tiles256 >= sms;
+  return wide ? by_major<256>(d, st) : by_major<128>(d, st);
+}
+
+}  // namespace cfk

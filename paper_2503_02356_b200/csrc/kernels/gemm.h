@@ -1,0 +1,36 @@
+// tcgen05 GEMM launcher (see gemm.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cfk {
+
+enum GemmEpi : int {
+  EPI_BF16 = 0,          // C(bf16)  = acc
+  EPI_F32 = 1,           // C(fp32)  = acc
+  EPI_F32_ACC = 2,       // C(fp32) += acc              (weight-gradient accumulation)
+  EPI_F32_RES = 3,       // C(fp32)  = acc + R(fp32)    (residual; R may alias C)
+  EPI_BF16_TANH = 4,     // C(bf16)  = tanh(acc)        (toy FFN)
+  EPI_BF16_TANHGRAD = 5  // C(bf16)  = acc * (1 - R^2)  (toy FFN backward, R = h bf16)
+};
+
+struct GemmDesc {
+  const void* a;  // bf16
+  int64_t lda;
+  int a_kmajor;   // 1: A[M,K] row-major; 0: A stored [K,M]
+  const void* b;  // bf16
+  int64_t ldb;
+  int b_kmajor;   // 1: B[N,K] row-major; 0: B stored [K,N]
+  void* c;
+  int64_t ldc;
+  const void* r;
+  int64_t ldr;
+  int64_t M, N, K;
+  int epi;
+};
+
+cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
+int gemm_num_sms();
+
+}  // namespace cfk

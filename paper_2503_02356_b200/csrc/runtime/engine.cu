@@ -1,0 +1,945 @@
+// Device runtime: model storage + the chunk event executor.
+//
+// Mirrors run_plan (reference plan_runner.hpp:67-339) event by event, but
+// with B200 data structures instead of the reference's StateStore copies:
+//  * per dependent group, one contiguous KV cache [L][S][kvw] (bf16 K, V)
+//    and one fp32 KV-gradient store [L][S][2*kvw] (dK | dV) for the whole
+//    sequence.  A forward writes its own K/V rows in place (replaces
+//    save_kv + assemble_prefix, plan_runner.hpp:128-156/206-217); attention
+//    reads the prefix straight from the cache; a backward adds dK/dV for
+//    every key row [0, start+T) in place (replaces the dKV scatter,
+//    :306-321) and then consumes its own rows (incoming from later chunks +
+//    its own contribution, :488-495).
+//  * retained activations ("tapes") live in stream-ordered pool memory from a
+//    retain-forward until the chunk's backward, so at most K chunks' tapes
+//    are resident (Alg. 2).
+//  * losses are reduced on the device in a fixed order into per-event slots,
+//    read back once per step; recompute-loss equality is checked bitwise.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <dlfcn.h>
+#include <memory>
+#include <numeric>
+#include <set>
+
+#include "../capi/capi_util.hpp"
+#include "../kernels/gemm.h"
+#include "engine.hpp"
+
+namespace cfb {
+
+using cfk::AttnParams;
+using cfk::AttnSeg;
+using cfk::AttnTile;
+using cfk::bf16;
+
+#define CK(expr) cuda_check((expr), #expr)
+
+namespace {
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Bump allocator over one pool allocation.
+struct Arena {
+  char* base = nullptr;
+  int64_t off = 0;
+  template <class T>
+  T* take(int64_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * static_cast<int64_t>(sizeof(T));
+    return p;
+  }
+};
+
+void* pool_alloc(Ctx* c, int64_t bytes) {
+  void* p = nullptr;
+  CK(cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(bytes, 256)), c->stream));
+  return p;
+}
+void pool_free(Ctx* c, void* p) {
+  if (p) CK(cudaFreeAsync(p, c->stream));
+}
+
+// --------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  void* h = nullptr;
+  int (*get_id)(void*) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*err)(int) = nullptr;
+  void* init_rank = nullptr;
+};
+struct Id128 {
+  char b[128];
+};
+Nccl& nccl() {
+  static Nccl n;
+  if (!n.h) {
+    n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!n.h) throw NcclError("libnccl.so.2 not loadable");
+    n.get_id = reinterpret_cast<int (*)(void*)>(dlsym(n.h, "ncclGetUniqueId"));
+    n.all_reduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(n.h, "ncclAllReduce"));
+    n.err = reinterpret_cast<const char* (*)(int)>(dlsym(n.h, "ncclGetErrorString"));
+    n.init_rank = dlsym(n.h, "ncclCommInitRank");
+    if (!n.get_id || !n.all_reduce || !n.init_rank) throw NcclError("NCCL symbols missing");
+  }
+  return n;
+}
+void nccl_check(int r, const char* what) {
+  if (r != 0) throw NcclError(std::string(what) + ": " + (nccl().err ? nccl().err(r) : "error"));
+}
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0;
+
+}  // namespace
+
+void dp_unique_id(uint8_t* out) { nccl_check(nccl().get_id(out), "ncclGetUniqueId"); }
+
+void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id) {
+  if (world <= 1) return;
+  Id128 u;
+  std::memcpy(u.b, id, 128);
+  auto init = reinterpret_cast<int (*)(void**, int, Id128, int)>(nccl().init_rank);
+  CK(cudaSetDevice(ctx->device));
+  nccl_check(init(&ctx->nccl_comm, world, u, rank), "ncclCommInitRank");
+  ctx->rank = rank;
+  ctx->world = world;
+}
+
+// ------------------------------------------------------------------ model
+Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
+  auto m = std::make_unique<Model>();
+  m->ctx = ctx;
+  m->cfg = cfg;
+  m->llama = cfg.arch == CF_ARCH_LLAMA;
+  if (cfg.arch != CF_ARCH_TOY && cfg.arch != CF_ARCH_LLAMA) throw ValidationError("unknown arch");
+  if (cfg.vocab_size < 1 || cfg.d_model < 1 || cfg.num_heads < 1 || cfg.num_kv_heads < 1 || cfg.num_layers < 1)
+    throw ValidationError("model dimensions must be positive");
+  if (cfg.d_model % cfg.num_heads) throw ValidationError("d_model must be divisible by num_heads");
+  if (cfg.num_heads % cfg.num_kv_heads) throw ValidationError("num_heads must be divisible by num_kv_heads");
+  m->V = cfg.vocab_size;
+  m->d = cfg.d_model;
+  m->H = cfg.num_heads;
+  m->KVH = cfg.num_kv_heads;
+  m->dh = m->d / m->H;
+  m->kvw = m->KVH * m->dh;
+  m->L = cfg.num_layers;
+  m->ffn = m->llama ? cfg.ffn_width : 2 * m->d;
+  if (m->ffn < 1) throw ValidationError("llama arch needs ffn_width");
+  if (m->llama && (m->dh % 2)) throw ValidationError("RoPE needs an even head dim");
+  if (m->dh > 128) throw ValidationError("head_dim > 128 not supported");
+  if (m->d % 8 || m->kvw % 8 || m->ffn % 8)
+    throw ValidationError("d_model, kv width and ffn width must be multiples of 8 (16-byte TMA rows)");
+  m->qkv_w = m->d + 2 * m->kvw;
+  m->gu_w = m->llama ? 2 * m->ffn : m->ffn;
+  const int64_t Vp = align_up(m->V, 8);
+
+  // Storage plan: weights (bf16) then gains (fp32), each 256-byte aligned;
+  // gradients (fp32) mirror the weight layout in one flat buffer.
+  struct Piece {
+    int64_t elems;
+    bool f32;
+  };
+  std::vector<Piece> pieces;
+  pieces.push_back({m->V * m->d, false});  // emb
+  for (int64_t l = 0; l < m->L; ++l) {
+    pieces.push_back({m->d * m->qkv_w, false});
+    pieces.push_back({m->d * m->d, false});
+    pieces.push_back({m->d * m->gu_w, false});
+    pieces.push_back({m->ffn * m->d, false});
+    if (m->llama) {
+      pieces.push_back({m->d, true});
+      pieces.push_back({m->d, true});
+    }
+  }
+  if (m->llama) pieces.push_back({m->d, true});
+  pieces.push_back({m->d * Vp, false});  // head [d, Vp]
+  int64_t wbytes = 0, gelems = 0;
+  std::vector<int64_t> woff, goff;
+  for (const Piece& p : pieces) {
+    wbytes = align_up(wbytes, 256);
+    woff.push_back(wbytes);
+    wbytes += p.elems * (p.f32 ? 4 : 2);
+    gelems = align_up(gelems, 64);
+    goff.push_back(gelems);
+    gelems += p.elems;
+  }
+  CK(cudaMalloc(&m->wbuf, static_cast<size_t>(wbytes)));
+  CK(cudaMalloc(&m->grads, static_cast<size_t>(gelems) * 4));
+  CK(cudaMemsetAsync(m->grads, 0, static_cast<size_t>(gelems) * 4, ctx->stream));
+  m->wbytes = wbytes;
+  m->grad_numel = gelems;
+  char* wb = static_cast<char*>(m->wbuf);
+  size_t pi = 0;
+  auto wptr = [&](size_t i) { return wb + woff[i]; };
+  auto gptr = [&](size_t i) { return m->grads + goff[i]; };
+  m->emb = reinterpret_cast<bf16*>(wptr(pi));
+  m->d_emb = gptr(pi++);
+  m->layers.resize(static_cast<size_t>(m->L));
+  for (auto& ly : m->layers) {
+    ly.wqkv = reinterpret_cast<bf16*>(wptr(pi));
+    ly.d_wqkv = gptr(pi++);
+    ly.wo = reinterpret_cast<bf16*>(wptr(pi));
+    ly.d_wo = gptr(pi++);
+    ly.w1 = reinterpret_cast<bf16*>(wptr(pi));
+    ly.d_w1 = gptr(pi++);
+    ly.w2 = reinterpret_cast<bf16*>(wptr(pi));
+    ly.d_w2 = gptr(pi++);
+    ly.g1 = ly.g2 = ly.d_g1 = ly.d_g2 = nullptr;
+    if (m->llama) {
+      ly.g1 = reinterpret_cast<float*>(wptr(pi));
+      ly.d_g1 = gptr(pi++);
+      ly.g2 = reinterpret_cast<float*>(wptr(pi));
+      ly.d_g2 = gptr(pi++);
+    }
+  }
+  if (m->llama) {
+    m->gf = reinterpret_cast<float*>(wptr(pi));
+    m->d_gf = gptr(pi++);
+  }
+  m->head = reinterpret_cast<bf16*>(wptr(pi));
+  m->d_head = gptr(pi++);
+
+  // Reference tensor order (toy_model.hpp:116-126; llama extension).
+  auto add = [&](std::string name, int64_t r, int64_t c, void* w, float* g, int64_t ld, bool gain) {
+    Slot s;
+    s.name = std::move(name);
+    s.rows = r;
+    s.cols = c;
+    s.w = w;
+    s.g = g;
+    s.ld = ld;
+    s.is_gain = gain;
+    m->slots.push_back(s);
+  };
+  add("embedding", m->V, m->d, m->emb, m->d_emb, m->d, false);
+  for (int64_t l = 0; l < m->L; ++l) {
+    Layer& ly = m->layers[static_cast<size_t>(l)];
+    const std::string p = "layer" + std::to_string(l) + ".";
+    if (m->llama) add(p + "attn_norm", 1, m->d, ly.g1, ly.d_g1, m->d, true);
+    add(p + "wq", m->d, m->d, ly.wqkv, ly.d_wqkv, m->qkv_w, false);
+    add(p + "wk", m->d, m->kvw, ly.wqkv + m->d, ly.d_wqkv + m->d, m->qkv_w, false);
+    add(p + "wv", m->d, m->kvw, ly.wqkv + m->d + m->kvw, ly.d_wqkv + m->d + m->kvw, m->qkv_w, false);
+    add(p + "wo", m->d, m->d, ly.wo, ly.d_wo, m->d, false);
+    if (m->llama) {
+      add(p + "ffn_norm", 1, m->d, ly.g2, ly.d_g2, m->d, true);
+      add(p + "w_gate", m->d, m->ffn, ly.w1, ly.d_w1, m->gu_w, false);
+      add(p + "w_up", m->d, m->ffn, ly.w1 + m->ffn, ly.d_w1 + m->ffn, m->gu_w, false);
+      add(p + "w_down", m->ffn, m->d, ly.w2, ly.d_w2, m->d, false);
+    } else {
+      add(p + "w1", m->d, m->ffn, ly.w1, ly.d_w1, m->gu_w, false);
+      add(p + "w2", m->ffn, m->d, ly.w2, ly.d_w2, m->d, false);
+    }
+  }
+  if (m->llama) add("final_norm", 1, m->d, m->gf, m->d_gf, m->d, true);
+  add("head", m->d, m->V, m->head, m->d_head, Vp, false);
+
+  // init_model (toy_model.hpp:128-132): one SplitMix64 stream in tensor
+  // order, regenerated per element on the device (every rank identical).
+  const double scale = 1.0 / std::sqrt(static_cast<double>(m->d));
+  int64_t draw = 0;
+  for (Slot& s : m->slots) {
+    m->num_params += s.rows * s.cols;
+    if (s.is_gain) {
+      CK(cfk::fill_f32(static_cast<float*>(s.w), s.cols, 1.0f, ctx->stream));
+      continue;
+    }
+    s.draw_base = draw;
+    CK(cfk::init_uniform_bf16(static_cast<bf16*>(s.w), s.ld, s.rows, s.cols, static_cast<uint64_t>(draw), cfg.seed,
+                              scale, ctx->stream));
+    draw += s.rows * s.cols;
+  }
+  if (Vp != m->V)  // zero the head's pad columns
+    CK(cudaMemset2DAsync(m->head + m->V, static_cast<size_t>(Vp) * 2, 0, static_cast<size_t>(Vp - m->V) * 2,
+                         static_cast<size_t>(m->d), ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return m.release();
+}
+
+void model_destroy(Model* m) {
+  if (!m) return;
+  cudaFree(m->wbuf);
+  cudaFree(m->grads);
+  delete m;
+}
+
+static const Slot& slot_at(Model* m, int64_t idx) {
+  if (idx < 0 || idx >= static_cast<int64_t>(m->slots.size())) throw ValidationError("tensor index out of range");
+  return m->slots[static_cast<size_t>(idx)];
+}
+
+void model_get_param(Model* m, int64_t idx, double* host) {
+  const Slot& s = slot_at(m, idx);
+  cudaStream_t st = m->ctx->stream;
+  double* tmp = static_cast<double*>(pool_alloc(m->ctx, s.rows * s.cols * 8));
+  if (s.is_gain)
+    CK(cfk::f32_to_f64(static_cast<float*>(s.w), s.ld, s.rows, s.cols, tmp, st));
+  else
+    CK(cfk::bf16_to_f64(static_cast<bf16*>(s.w), s.ld, s.rows, s.cols, tmp, st));
+  CK(cudaMemcpyAsync(host, tmp, static_cast<size_t>(s.rows * s.cols) * 8, cudaMemcpyDeviceToHost, st));
+  pool_free(m->ctx, tmp);
+  CK(cudaStreamSynchronize(st));
+}
+
+void model_set_param(Model* m, int64_t idx, const double* host) {
+  const Slot& s = slot_at(m, idx);
+  cudaStream_t st = m->ctx->stream;
+  double* tmp = static_cast<double*>(pool_alloc(m->ctx, s.rows * s.cols * 8));
+  CK(cudaMemcpyAsync(tmp, host, static_cast<size_t>(s.rows * s.cols) * 8, cudaMemcpyHostToDevice, st));
+  if (s.is_gain)
+    CK(cfk::f64_to_f32(tmp, s.rows, s.cols, static_cast<float*>(s.w), s.ld, st));
+  else
+    CK(cfk::f64_to_bf16(tmp, s.rows, s.cols, static_cast<bf16*>(s.w), s.ld, st));
+  pool_free(m->ctx, tmp);
+  CK(cudaStreamSynchronize(st));
+}
+
+void model_get_grad(Model* m, int64_t idx, double* host) {
+  const Slot& s = slot_at(m, idx);
+  cudaStream_t st = m->ctx->stream;
+  double* tmp = static_cast<double*>(pool_alloc(m->ctx, s.rows * s.cols * 8));
+  CK(cfk::f32_to_f64(s.g, s.ld, s.rows, s.cols, tmp, st));
+  CK(cudaMemcpyAsync(host, tmp, static_cast<size_t>(s.rows * s.cols) * 8, cudaMemcpyDeviceToHost, st));
+  pool_free(m->ctx, tmp);
+  CK(cudaStreamSynchronize(st));
+}
+
+// ---------------------------------------------------------------- executor
+namespace {
+
+// Per-chunk index metadata (built on the host from the plan + token payload;
+// uploaded once per step).  Offsets are in int32 units into the meta buffer.
+struct ChunkMeta {
+  int64_t id = 0, T = 0;
+  bool dependent = false;
+  int64_t seq = -1, start = 0, seq_len = 0, group = -1, index = -1;
+  int64_t o_tok = 0, o_tgt = 0, o_pos = 0, o_segs = 0, nsegs = 0, o_qt = 0, nqt = 0, o_kt = 0, nkt = 0;
+  int64_t o_order = 0, o_uniq = 0, o_uoff = 0, nuniq = 0;
+  double pairs = 0;
+};
+
+struct GroupState {
+  int64_t S = 0;
+  bf16* kc = nullptr;   // [L][S][kvw]
+  bf16* vc = nullptr;
+  float* dkv = nullptr; // [L][S][2kvw]
+  void* mem = nullptr;
+  std::vector<int64_t> contributions;  // per chunk index
+  std::vector<bool> saved;
+};
+
+struct Tape {
+  void* mem = nullptr;
+  int64_t T = 0;
+  float* x_in = nullptr;  // (L+1) x T x d
+  bf16* qkv = nullptr;    // L x T x qkv_w
+  bf16* o = nullptr;      // L x T x d
+  float* lse = nullptr;   // L x H x T
+  float* x_mid = nullptr; // L x T x d
+  bf16* act = nullptr;    // L x T x gu_w
+  bf16* dlogits = nullptr;// T x Vp
+  float2* tab = nullptr;  // T x dh/2
+  int64_t bytes = 0;
+};
+
+}  // namespace
+}  // namespace cfb
+
+struct cf_step {
+  std::vector<cfb::ChunkMeta> chunks;  // indexed by plan position
+  std::map<int64_t, int64_t> pos_of;   // chunk id -> position
+  const cfb::Plan* plan = nullptr;
+  int32_t* meta_dev = nullptr;
+  int32_t* meta_host = nullptr;  // pinned
+  int64_t meta_len = 0;
+  double normalizer = 0;
+  int64_t tokens = 0;
+  double model_flops = 0, hw_flops = 0;
+  std::map<int64_t, int64_t> group_len;  // group -> sequence length
+  cfb::Plan plan_copy;
+};
+
+namespace cfb {
+
+// Builds metadata for every chunk of the plan.
+cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
+  auto st = std::make_unique<cf_step>();
+  st->plan_copy = plan;
+  st->plan = &st->plan_copy;
+  std::map<int64_t, int64_t> idx_of;
+  std::vector<int64_t> tok_off(static_cast<size_t>(b.n) + 1, 0);
+  for (int64_t i = 0; i < b.n; ++i) {
+    if (!idx_of.emplace(b.ids[i], i).second) throw ValidationError("duplicate sequence id " + std::to_string(b.ids[i]));
+    tok_off[i + 1] = tok_off[i] + b.lengths[i];
+  }
+  // normalizer: global target count (toy_model.hpp:533-541)
+  int64_t targets = 0;
+  for (int64_t i = 0; i < b.n; ++i) {
+    if (b.lengths[i] < 2) throw ValidationError("sequence " + std::to_string(b.ids[i]) + " must have length >= 2");
+    targets += b.lengths[i] - 1;
+  }
+  if (targets <= 0) throw ValidationError("batch has no prediction targets");
+  st->normalizer = static_cast<double>(targets);
+  if (!b.tokens_host) throw ValidationError("token payload required");
+  for (int64_t i = 0; i < tok_off[b.n]; ++i)
+    if (b.tokens_host[i] < 0 || b.tokens_host[i] >= m->V)
+      throw ValidationError("token id " + std::to_string(b.tokens_host[i]) + " out of vocabulary range");
+
+  const double Nmm = static_cast<double>(m->L * (m->d * m->qkv_w + m->d * m->d + m->d * m->gu_w + m->ffn * m->d) +
+                                         m->d * m->V);
+  const double attn_unit = static_cast<double>(m->L * m->H * m->dh);
+  std::vector<int32_t> meta;
+  auto put = [&](int32_t v) { meta.push_back(v); };
+  auto here = [&]() { return static_cast<int64_t>(meta.size()); };
+  for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
+    const Chunk& c = plan.chunks[ci];
+    ChunkMeta cm;
+    cm.id = c.id;
+    cm.T = c.total;
+    cm.dependent = c.kind == kDependent;
+    cm.group = c.group;
+    cm.index = c.index;
+    st->pos_of[c.id] = static_cast<int64_t>(ci);
+    // tokens / targets / positions (plan_runner.hpp:112-122)
+    cm.o_tok = here();
+    std::vector<int32_t> tg, ps;
+    std::vector<std::pair<int32_t, int32_t>> tok_rows;
+    int32_t row = 0;
+    for (int64_t s = 0; s < c.seg_cnt; ++s) {
+      const Segment& sg = plan.segments[static_cast<size_t>(c.seg_off + s)];
+      auto it = idx_of.find(sg.seq);
+      if (it == idx_of.end()) throw ValidationError("chunk references unknown sequence " + std::to_string(sg.seq));
+      const int64_t len = b.lengths[it->second];
+      if (sg.start < 0 || sg.len < 1 || sg.start + sg.len > len)
+        throw ValidationError("chunk segment exceeds sequence " + std::to_string(sg.seq));
+      const int32_t* tk = b.tokens_host + tok_off[it->second];
+      for (int64_t t = 0; t < sg.len; ++t) {
+        const int64_t p = sg.start + t;
+        put(tk[p]);
+        tok_rows.emplace_back(tk[p], row++);
+        tg.push_back(p + 1 < len ? tk[p + 1] : -1);
+        ps.push_back(static_cast<int32_t>(p));
+      }
+      if (cm.dependent) {
+        cm.seq = sg.seq;
+        cm.start = sg.start;
+        cm.seq_len = len;
+        st->group_len[c.group] = len;
+      }
+      const double L_ = static_cast<double>(sg.len), P_ = static_cast<double>(sg.start);
+      cm.pairs += L_ * P_ + L_ * (L_ + 1) / 2;
+    }
+    cm.o_tgt = here();
+    for (int32_t v : tg) put(v);
+    cm.o_pos = here();
+    for (int32_t v : ps) put(v);
+    // attention segments and tiles
+    while (meta.size() % 4) put(0);
+    cm.o_segs = here();
+    std::vector<AttnSeg> segs;
+    int32_t qs = 0;
+    for (int64_t s = 0; s < c.seg_cnt; ++s) {
+      const Segment& sg = plan.segments[static_cast<size_t>(c.seg_off + s)];
+      AttnSeg a;
+      a.q_start = qs;
+      a.len = static_cast<int32_t>(sg.len);
+      a.prefix = static_cast<int32_t>(cm.dependent ? sg.start : 0);
+      a.kv_row0 = cm.dependent ? 0 : qs;
+      segs.push_back(a);
+      qs += a.len;
+    }
+    for (const AttnSeg& a : segs) {
+      put(a.q_start);
+      put(a.len);
+      put(a.kv_row0);
+      put(a.prefix);
+    }
+    cm.nsegs = static_cast<int64_t>(segs.size());
+    cm.o_qt = here();
+    for (size_t s = 0; s < segs.size(); ++s)
+      for (int32_t f = 0; f < segs[s].len; f += 64) {
+        put(static_cast<int32_t>(s));
+        put(f);
+        put(std::min(64, segs[s].len - f));
+        put(0);
+        ++cm.nqt;
+      }
+    cm.o_kt = here();
+    for (size_t s = 0; s < segs.size(); ++s) {
+      const int32_t nk = segs[s].prefix + segs[s].len;
+      for (int32_t f = 0; f < nk; f += 64) {
+        put(static_cast<int32_t>(s));
+        put(f);
+        put(std::min(64, nk - f));
+        put(0);
+        ++cm.nkt;
+      }
+    }
+    // embedding-backward CSR: rows grouped by token id, ascending rows
+    std::sort(tok_rows.begin(), tok_rows.end());
+    cm.o_order = here();
+    for (const auto& tr : tok_rows) put(tr.second);
+    std::vector<int32_t> uniq, uoff;
+    for (size_t i = 0; i < tok_rows.size(); ++i) {
+      if (i == 0 || tok_rows[i].first != tok_rows[i - 1].first) {
+        uniq.push_back(tok_rows[i].first);
+        uoff.push_back(static_cast<int32_t>(i));
+      }
+    }
+    uoff.push_back(static_cast<int32_t>(tok_rows.size()));
+    cm.o_uniq = here();
+    for (int32_t v : uniq) put(v);
+    cm.o_uoff = here();
+    for (int32_t v : uoff) put(v);
+    cm.nuniq = static_cast<int64_t>(uniq.size());
+    while (meta.size() % 4) put(0);
+    st->tokens += cm.T;
+    st->model_flops += 6.0 * Nmm * static_cast<double>(cm.T) + 12.0 * attn_unit * cm.pairs;
+    st->chunks.push_back(cm);
+  }
+  st->hw_flops = st->model_flops;
+  for (const Event& e : plan.events)
+    if (e.recompute) {
+      const ChunkMeta& cm = st->chunks[static_cast<size_t>(st->pos_of.at(e.chunk))];
+      st->hw_flops += 2.0 * Nmm * static_cast<double>(cm.T) + 4.0 * attn_unit * cm.pairs;
+    }
+  st->meta_len = static_cast<int64_t>(meta.size());
+  CK(cudaMallocHost(&st->meta_host, static_cast<size_t>(st->meta_len + 4) * 4));
+  std::memcpy(st->meta_host, meta.data(), meta.size() * 4);
+  CK(cudaMalloc(&st->meta_dev, static_cast<size_t>(st->meta_len + 4) * 4));
+  CK(cudaMemcpyAsync(st->meta_dev, st->meta_host, static_cast<size_t>(st->meta_len) * 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return st.release();
+}
+
+void step_destroy(cf_step* st) {
+  if (!st) return;
+  cudaFree(st->meta_dev);
+  cudaFreeHost(st->meta_host);
+  delete st;
+}
+
+namespace {
+
+struct Exec {
+  Ctx* ctx;
+  Model* m;
+  cf_step* st;
+  cudaStream_t s;
+  bool corrupt = false;
+  float inv_norm = 0;
+  double* loss_slots = nullptr;  // device, one per event
+  int64_t launches = 0;
+  int64_t act_bytes = 0, act_peak = 0, kv_bytes = 0, kv_peak = 0;
+
+  template <class T>
+  T* meta(int64_t off) const {
+    return reinterpret_cast<T*>(st->meta_dev + off);
+  }
+  void L(cudaError_t e, const char* what, int n = 1) {
+    cuda_check(e, what);
+    launches += n;
+  }
+  void gemm(const void* a, int a_k, int64_t lda, const void* b, int b_k, int64_t ldb, void* c, int64_t ldc, int64_t M,
+            int64_t N, int64_t K, int epi, const void* r = nullptr, int64_t ldr = 0) {
+    cfk::GemmDesc d{a, lda, a_k, b, ldb, b_k, c, ldc, r, ldr, M, N, K, epi};
+    L(cfk::gemm(d, s), "gemm");
+  }
+
+  Tape alloc_tape(int64_t T, bool retain) {
+    Tape t;
+    t.T = T;
+    const int64_t L_ = m->L, d = m->d;
+    const int64_t Vp = align_up(m->V, 8);
+    auto carve = [&](Arena& a) {
+      t.x_in = a.take<float>((L_ + 1) * T * d);
+      t.qkv = a.take<bf16>(L_ * T * m->qkv_w);
+      t.o = a.take<bf16>(L_ * T * d);
+      t.lse = a.take<float>(L_ * m->H * T);
+      t.x_mid = a.take<float>(L_ * T * d);
+      t.act = a.take<bf16>(L_ * T * m->gu_w);
+      if (retain) t.dlogits = a.take<bf16>(T * Vp);
+      t.tab = a.take<float2>(T * std::max<int64_t>(1, m->dh / 2));
+    };
+    Arena measure{nullptr, 0};
+    carve(measure);
+    const int64_t bytes = measure.off + 256;
+    t.mem = pool_alloc(ctx, bytes);
+    t.bytes = bytes;
+    Arena a{static_cast<char*>(t.mem), 0};
+    carve(a);
+    act_bytes += bytes;
+    act_peak = std::max(act_peak, act_bytes);
+    return t;
+  }
+  void free_tape(Tape& t) {
+    pool_free(ctx, t.mem);
+    act_bytes -= t.bytes;
+    t.mem = nullptr;
+  }
+
+  AttnParams attn_params(const ChunkMeta& cm, const Tape& t, int64_t l, GroupState* gs) {
+    AttnParams p{};
+    const int64_t T = cm.T;
+    p.q = t.qkv + l * T * m->qkv_w;
+    p.q_stride = m->qkv_w;
+    if (cm.dependent) {
+      p.k = gs->kc + l * gs->S * m->kvw;
+      p.v = gs->vc + l * gs->S * m->kvw;
+      p.kv_stride = m->kvw;
+      p.dk_acc = gs->dkv + l * gs->S * 2 * m->kvw;
+      p.dv_acc = p.dk_acc + m->kvw;
+    } else {
+      p.k = p.q + m->d;
+      p.v = p.q + m->d + m->kvw;
+      p.kv_stride = m->qkv_w;
+    }
+    p.acc_stride = 2 * m->kvw;
+    p.o = t.o + l * T * m->d;
+    p.o_stride = m->d;
+    p.lse = t.lse + l * m->H * T;
+    p.segs = meta<const AttnSeg>(cm.o_segs);
+    p.tiles = meta<const AttnTile>(cm.o_qt);
+    p.num_tiles = static_cast<int32_t>(cm.nqt);
+    p.T = static_cast<int32_t>(T);
+    p.H = static_cast<int32_t>(m->H);
+    p.KVH = static_cast<int32_t>(m->KVH);
+    p.dh = static_cast<int32_t>(m->dh);
+    p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(m->dh)));
+    return p;
+  }
+
+  // Forward of one chunk (segment_forward per segment, toy_model.hpp:206-334).
+  void forward(const ChunkMeta& cm, Tape& t, GroupState* gs, int64_t slot, bool retain) {
+    const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8);
+    const int32_t* tok = meta<const int32_t>(cm.o_tok);
+    const int32_t* tgt = meta<const int32_t>(cm.o_tgt);
+    bf16* A = static_cast<bf16*>(pool_alloc(ctx, T * std::max(d, m->ffn) * 2));
+    float* logits = static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4));
+    float* row_loss = logits + T * Vp;
+    L(cfk::embed_fwd(tok, m->emb, d, T, t.x_in, s), "embed");
+    if (m->llama)
+      L(cfk::rope_table(meta<const int32_t>(cm.o_pos), T, static_cast<int>(m->dh), m->cfg.rope_theta, t.tab, s),
+        "rope_table");
+    for (int64_t l = 0; l < m->L; ++l) {
+      const Layer& ly = m->layers[static_cast<size_t>(l)];
+      float* x = t.x_in + l * T * d;
+      float* xm = t.x_mid + l * T * d;
+      bf16* qkv = t.qkv + l * T * m->qkv_w;
+      bf16* act = t.act + l * T * m->gu_w;
+      if (m->llama)
+        L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+      else
+        L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
+      gemm(A, 1, d, ly.wqkv, 0, m->qkv_w, qkv, m->qkv_w, T, m->qkv_w, d, cfk::EPI_BF16);
+      if (m->llama)
+        L(cfk::rope_qk(qkv, m->qkv_w, T, static_cast<int>(m->H), static_cast<int>(m->KVH), static_cast<int>(m->dh),
+                       d, t.tab, s),
+          "rope");
+      if (cm.dependent)
+        L(cfk::kv_store(qkv, m->qkv_w, T, m->kvw, d, d + m->kvw, gs->kc + l * gs->S * m->kvw + cm.start * m->kvw,
+                        gs->vc + l * gs->S * m->kvw + cm.start * m->kvw, m->kvw, s),
+          "kv_store");
+      AttnParams p = attn_params(cm, t, l, gs);
+      L(cfk::attn_forward(p, s), "attn_fwd");
+      gemm(t.o + l * T * d, 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
+      float* xn = t.x_in + (l + 1) * T * d;
+      if (m->llama) {
+        L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+        gemm(A, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
+        L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");
+        gemm(A, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
+      } else {
+        L(cfk::to_bf16(xm, A, T * d, s), "to_bf16");
+        gemm(A, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->ffn, d, cfk::EPI_BF16_TANH);
+        gemm(act, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
+      }
+    }
+    const float* xL = t.x_in + m->L * T * d;
+    if (m->llama)
+      L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+    else
+      L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+    gemm(A, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
+    L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, tgt, inv_norm, row_loss, retain ? t.dlogits : nullptr, s), "ce");
+    L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
+    pool_free(ctx, A);
+    pool_free(ctx, logits);
+  }
+
+  // Backward of one chunk (segment_backward, toy_model.hpp:341-520).
+  void backward(const ChunkMeta& cm, Tape& t, GroupState* gs) {
+    const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8), qw = m->qkv_w, kvw = m->kvw;
+    const float eps = static_cast<float>(m->cfg.rms_eps);
+    float *dx, *dmid, *da, *dsum, *rstd, *dkv_local = nullptr;
+    bf16 *A, *xb, *dh, *dgu, *dqkv;
+    auto carve = [&](Arena& a) {
+      dx = a.take<float>(T * d);
+      dmid = a.take<float>(T * d);
+      da = a.take<float>(T * d);
+      A = a.take<bf16>(T * std::max(d, m->ffn));  // bf16 activations (recomputed)
+      xb = a.take<bf16>(T * d);                    // bf16 of a gradient
+      dh = a.take<bf16>(T * m->ffn);
+      dgu = a.take<bf16>(T * m->gu_w);
+      dqkv = a.take<bf16>(T * qw);
+      dsum = a.take<float>(m->H * T);
+      rstd = a.take<float>(T);
+      if (!cm.dependent) dkv_local = a.take<float>(T * 2 * kvw);
+    };
+    Arena measure{nullptr, 0};
+    carve(measure);
+    Arena a{static_cast<char*>(pool_alloc(ctx, measure.off + 256)), 0};
+    carve(a);
+    void* scratch = a.base;
+
+    // Output head + CE (toy_model.hpp:369-388): dHead += xf^T dlogits, dxf = dlogits head^T.
+    const float* xL = t.x_in + m->L * T * d;
+    if (m->llama)
+      L(cfk::rmsnorm_fwd(xL, m->gf, T, d, eps, A, s), "rmsnorm");
+    else
+      L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+    gemm(A, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
+    if (m->llama) {
+      gemm(t.dlogits, 1, Vp, m->head, 1, Vp, da, d, T, d, m->V, cfk::EPI_F32);
+      L(cfk::rmsnorm_bwd(xL, m->gf, da, nullptr, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
+      L(cfk::gain_grad(xL, da, rstd, T, d, m->d_gf, s), "gain_grad");
+    } else {
+      gemm(t.dlogits, 1, Vp, m->head, 1, Vp, dx, d, T, d, m->V, cfk::EPI_F32);
+    }
+
+    for (int64_t l = m->L - 1; l >= 0; --l) {
+      const Layer& ly = m->layers[static_cast<size_t>(l)];
+      const float* x = t.x_in + l * T * d;
+      const float* xm = t.x_mid + l * T * d;
+      const bf16* act = t.act + l * T * m->gu_w;
+      const bf16* O = t.o + l * T * d;
+      // FFN (toy_model.hpp:409-425)
+      L(cfk::to_bf16(dx, xb, T * d, s), "to_bf16");
+      if (m->llama) {
+        gemm(xb, 1, d, ly.w2, 1, d, dh, m->ffn, T, m->ffn, d, cfk::EPI_BF16);
+        L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");  // recompute h
+        gemm(A, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
+        L(cfk::swiglu_bwd(act, dh, T, m->ffn, dgu, s), "swiglu_bwd");
+        L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, eps, A, s), "rmsnorm");  // recompute xn2
+        gemm(A, 0, d, dgu, 0, m->gu_w, ly.d_w1, m->gu_w, d, m->gu_w, T, cfk::EPI_F32_ACC);
+        gemm(dgu, 1, m->gu_w, ly.w1, 1, m->gu_w, da, d, T, d, m->gu_w, cfk::EPI_F32);
+        L(cfk::rmsnorm_bwd(xm, ly.g2, da, dx, T, d, eps, dmid, rstd, s), "rmsnorm_bwd");
+        L(cfk::gain_grad(xm, da, rstd, T, d, ly.d_g2, s), "gain_grad");
+      } else {
+        gemm(xb, 1, d, ly.w2, 1, d, dgu, m->ffn, T, m->ffn, d, cfk::EPI_BF16_TANHGRAD, act, m->ffn);
+        gemm(act, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
+        gemm(dgu, 1, m->ffn, ly.w1, 1, m->ffn, dmid, d, T, d, m->ffn, cfk::EPI_F32_RES, dx, d);
+        L(cfk::to_bf16(xm, A, T * d, s), "to_bf16");
+        gemm(A, 0, d, dgu, 0, m->ffn, ly.d_w1, m->gu_w, d, m->ffn, T, cfk::EPI_F32_ACC);
+      }
+      // Attention output projection (toy_model.hpp:427-434)
+      L(cfk::to_bf16(dmid, xb, T * d, s), "to_bf16");
+      bf16* dO = A;  // reuse
+      gemm(xb, 1, d, ly.wo, 1, d, dO, d, T, d, d, cfk::EPI_BF16);
+      gemm(O, 0, d, xb, 0, d, ly.d_wo, d, d, d, T, cfk::EPI_F32_ACC);
+      // Attention (toy_model.hpp:436-495)
+      AttnParams p = attn_params(cm, t, l, gs);
+      p.dout = dO;
+      p.dout_stride = d;
+      p.dsum = dsum;
+      p.dq = dqkv;
+      p.dq_stride = qw;
+      const float* own_dk;
+      if (cm.dependent) {
+        float* own = p.dk_acc + cm.start * 2 * kvw;
+        if (corrupt) L(cfk::scale_rows_f32(own, T, 2 * kvw, 2 * kvw, 1.0000001f, s), "corrupt");
+        own_dk = own;
+      } else {
+        CK(cudaMemsetAsync(dkv_local, 0, static_cast<size_t>(T * 2 * kvw) * 4, s));
+        p.dk_acc = dkv_local;
+        p.dv_acc = dkv_local + kvw;
+        own_dk = dkv_local;
+      }
+      L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
+      L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
+                         m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
+        "dkv_to_dqkv");
+      if (m->llama)
+        L(cfk::rope_bwd_q(dqkv, qw, T, static_cast<int>(m->H), static_cast<int>(m->dh), t.tab, s), "rope_bwd");
+      // Projections (toy_model.hpp:497-511)
+      if (m->llama)
+        L(cfk::rmsnorm_fwd(x, ly.g1, T, d, eps, A, s), "rmsnorm");  // recompute xn
+      else
+        L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
+      gemm(A, 0, d, dqkv, 0, qw, ly.d_wqkv, qw, d, qw, T, cfk::EPI_F32_ACC);
+      if (m->llama) {
+        gemm(dqkv, 1, qw, ly.wqkv, 1, qw, da, d, T, d, qw, cfk::EPI_F32);
+        L(cfk::rmsnorm_bwd(x, ly.g1, da, dmid, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
+        L(cfk::gain_grad(x, da, rstd, T, d, ly.d_g1, s), "gain_grad");
+      } else {
+        gemm(dqkv, 1, qw, ly.wqkv, 1, qw, dx, d, T, d, qw, cfk::EPI_F32_RES, dmid, d);
+      }
+    }
+    // Embedding (toy_model.hpp:514-519), deterministic per-token sums.
+    L(cfk::embed_bwd(dx, d, meta<const int32_t>(cm.o_order), meta<const int32_t>(cm.o_uniq),
+                     meta<const int32_t>(cm.o_uoff), cm.nuniq, m->d_emb, s),
+      "embed_bwd");
+    pool_free(ctx, scratch);
+  }
+};
+
+}  // namespace
+
+void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res) {
+  const Plan& plan = *st->plan;
+  if (!plan.violations.empty()) throw ValidationError("execution plan is invalid: " + plan.violations.front());
+  Exec ex;
+  ex.ctx = ctx;
+  ex.m = m;
+  ex.st = st;
+  ex.s = ctx->stream;
+  ex.corrupt = opts.corrupt_kv_grads != 0;
+  const double norm = opts.normalizer_override > 0 ? opts.normalizer_override : st->normalizer;
+  ex.inv_norm = static_cast<float>(1.0 / norm);
+  const int64_t nev = static_cast<int64_t>(plan.events.size());
+  if (ctx->pool) {
+    uint64_t zero = 0;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &zero);
+  }
+  ex.loss_slots = static_cast<double*>(pool_alloc(ctx, (nev + 1) * 8));
+  CK(cudaMemsetAsync(ex.loss_slots, 0, static_cast<size_t>(nev + 1) * 8, ex.s));
+  if (!opts.accumulate_grads) CK(cudaMemsetAsync(m->grads, 0, static_cast<size_t>(m->grad_numel) * 4, ex.s));
+
+  std::map<int64_t, Tape> live;
+  std::map<int64_t, GroupState> groups;
+  std::map<int64_t, int64_t> first_slot;
+  std::vector<std::pair<int64_t, int64_t>> recompute_pairs;  // (slot, first slot)
+  std::vector<int64_t> first_pass_slots;
+  int64_t held = 0, peak = 0, violations = 0, recomputes = 0;
+
+  for (int64_t ei = 0; ei < nev; ++ei) {
+    const Event& e = plan.events[static_cast<size_t>(ei)];
+    auto pit = st->pos_of.find(e.chunk);
+    if (pit == st->pos_of.end()) throw ValidationError("plan references unknown chunk " + std::to_string(e.chunk));
+    const ChunkMeta& cm = st->chunks[static_cast<size_t>(pit->second)];
+    GroupState* gs = nullptr;
+    if (cm.dependent) {
+      auto git = groups.find(cm.group);
+      if (git == groups.end()) {
+        GroupState g;
+        g.S = cm.seq_len;
+        const int64_t n = static_cast<int64_t>(plan.groups.at(cm.group).size());
+        g.contributions.assign(static_cast<size_t>(n), 0);
+        g.saved.assign(static_cast<size_t>(n), false);
+        const int64_t kvb = m->L * g.S * m->kvw * 2;
+        const int64_t bytes = 3 * 256 + 2 * kvb + m->L * g.S * 2 * m->kvw * 4;
+        g.mem = pool_alloc(ctx, bytes);
+        Arena a{static_cast<char*>(g.mem), 0};
+        g.kc = a.take<bf16>(m->L * g.S * m->kvw);
+        g.vc = a.take<bf16>(m->L * g.S * m->kvw);
+        g.dkv = a.take<float>(m->L * g.S * 2 * m->kvw);
+        CK(cudaMemsetAsync(g.dkv, 0, static_cast<size_t>(m->L * g.S * 2 * m->kvw) * 4, ex.s));
+        ex.kv_bytes += bytes;
+        ex.kv_peak = std::max(ex.kv_peak, ex.kv_bytes);
+        git = groups.emplace(cm.group, std::move(g)).first;
+      }
+      gs = &git->second;
+    }
+    if (e.kind != kBackward) {
+      const bool retain = e.kind == kFwdRetain;
+      Tape t = ex.alloc_tape(cm.T, retain);
+      ex.forward(cm, t, gs, ei, retain);
+      if (gs && e.save_kv) gs->saved[static_cast<size_t>(cm.index)] = true;
+      if (!e.recompute) {
+        first_slot[e.chunk] = ei;
+        first_pass_slots.push_back(ei);
+      } else {
+        ++recomputes;
+        auto f = first_slot.find(e.chunk);
+        recompute_pairs.emplace_back(ei, f == first_slot.end() ? -1 : f->second);
+      }
+      if (retain) {
+        if (live.count(e.chunk)) ex.free_tape(live[e.chunk]);
+        live[e.chunk] = t;
+        held += cm.T;
+        peak = std::max(peak, held);
+      } else {
+        ex.free_tape(t);
+      }
+      continue;
+    }
+    auto lit = live.find(e.chunk);
+    if (lit == live.end())
+      throw ValidationError("backward of chunk " + std::to_string(e.chunk) + " without retained activations");
+    if (gs) {
+      const int64_t n = static_cast<int64_t>(gs->contributions.size());
+      if (gs->saved[static_cast<size_t>(cm.index)] &&
+          gs->contributions[static_cast<size_t>(cm.index)] != n - 1 - cm.index)
+        ++violations;
+    }
+    ex.backward(cm, lit->second, gs);
+    if (gs) {
+      for (int64_t i = 0; i < cm.index; ++i) ++gs->contributions[static_cast<size_t>(i)];
+      if (cm.index == 0) {  // group complete: release its KV state
+        const int64_t bytes = 3 * 256 + 2 * m->L * gs->S * m->kvw * 2 + m->L * gs->S * 2 * m->kvw * 4;
+        pool_free(ctx, gs->mem);
+        ex.kv_bytes -= bytes;
+        groups.erase(cm.group);
+      }
+    }
+    ex.free_tape(lit->second);
+    live.erase(lit);
+    held -= cm.T;
+  }
+  for (auto& kv : live) ex.free_tape(kv.second);
+  for (auto& kv : groups) pool_free(ctx, kv.second.mem);
+
+  std::vector<double> slots(static_cast<size_t>(nev + 1));
+  CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nev + 1) * 8, cudaMemcpyDeviceToHost, ex.s));
+  CK(cudaStreamSynchronize(ex.s));
+  double total = 0;
+  for (int64_t sl : first_pass_slots) total += slots[static_cast<size_t>(sl)];
+  int64_t mism = 0;
+  for (const auto& [sl, f] : recompute_pairs)
+    if (f < 0 || slots[static_cast<size_t>(sl)] != slots[static_cast<size_t>(f)]) ++mism;
+  double loss = total / norm;
+  if (ctx->world > 1) {
+    // DP: gradients and loss are sums of per-rank partials (global normalizer)
+    double* dl = ex.loss_slots + nev;
+    CK(cudaMemcpyAsync(dl, &loss, 8, cudaMemcpyHostToDevice, ex.s));
+    nccl_check(nccl().all_reduce(m->grads, m->grads, static_cast<size_t>(m->grad_numel), kNcclFloat32, kNcclSum,
+                                 ctx->nccl_comm, ex.s),
+               "ncclAllReduce(grads)");
+    nccl_check(nccl().all_reduce(dl, dl, 1, kNcclFloat64, kNcclSum, ctx->nccl_comm, ex.s), "ncclAllReduce(loss)");
+    CK(cudaMemcpyAsync(&loss, dl, 8, cudaMemcpyDeviceToHost, ex.s));
+    CK(cudaStreamSynchronize(ex.s));
+  }
+  pool_free(ctx, ex.loss_slots);
+  ctx->launches += ex.launches;
+  if (res) {
+    res->loss = loss;
+    res->peak_retained_tokens = peak;
+    res->recompute_forward_count = recomputes;
+    res->recompute_loss_mismatches = mism;
+    res->kv_completeness_violations = violations;
+    res->tokens = st->tokens;
+    res->gpu_launches = ex.launches;
+    res->static_hbm_bytes = m->wbytes + m->grad_numel * 4;
+    res->act_hbm_bytes = ex.act_peak;
+    res->kv_hbm_bytes = ex.kv_peak;
+    uint64_t high = 0;
+    if (ctx->pool) cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &high);
+    res->peak_hbm_bytes = res->static_hbm_bytes + static_cast<int64_t>(high);
+    res->model_flops = st->model_flops;
+    res->hw_flops = st->hw_flops;
+  }
+}
+
+void run_plan(Ctx* ctx, Model* m, const Plan& plan, const Batch& b, const cf_run_opts& opts, cf_run_result* res) {
+  cf_step* st = step_prepare(ctx, m, plan, b);
+  try {
+    step_run(ctx, m, st, opts, res);
+  } catch (...) {
+    step_destroy(st);
+    throw;
+  }
+  step_destroy(st);
+}
+
+}  // namespace cfb

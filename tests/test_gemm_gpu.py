@@ -1,0 +1,71 @@
+"""tcgen05 GEMM (csrc/kernels/gemm.cu) vs a plain PyTorch fp32 reference of
+the same op, over every operand-major combination and epilogue."""
+import pytest
+import torch
+
+import paper_2503_02356_b200.capi as capi
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(128, 256, 64), (296, 520, 200), (1024, 1536, 1024), (24, 40, 16), (256, 2000, 512)]
+
+
+def _mk(rows, cols, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(rows, cols, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("a_k", [1, 0])
+@pytest.mark.parametrize("b_k", [1, 0])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_majors(ctx, a_k, b_k, shape):
+    M, N, K = shape
+    A = _mk(M, K, 1) if a_k else _mk(K, M, 1)   # stored [M,K] or [K,M]
+    B = _mk(N, K, 2) if b_k else _mk(K, N, 2)   # stored [N,K] or [K,N]
+    Am = A.float() if a_k else A.float().t()
+    Bm = B.float() if b_k else B.float().t()
+    ref = Am @ Bm.t()
+    ldc = (N + 7) // 8 * 8
+    C = torch.zeros(M, ldc, device="cuda", dtype=torch.float32)
+    torch.cuda.synchronize()
+    ctx.gemm(A.data_ptr(), a_k, A.shape[1], B.data_ptr(), b_k, B.shape[1], C.data_ptr(), ldc, M, N, K, capi.EPI_F32)
+    ctx.synchronize()
+    err = (C[:, :N] - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-5, err   # fp32 accumulation of exact bf16 products
+
+
+@pytest.mark.parametrize("epi", [capi.EPI_BF16, capi.EPI_F32_ACC, capi.EPI_F32_RES, capi.EPI_BF16_TANH,
+                                 capi.EPI_BF16_TANHGRAD])
+def test_gemm_epilogues(ctx, epi):
+    M, N, K = 384, 768, 320
+    A = _mk(M, K, 3)
+    B = _mk(K, N, 4)  # reference [in,out] weight layout (N-major B)
+    ref = A.float() @ B.float()
+    R32 = torch.randn(M, N, device="cuda")
+    Rbf = (torch.rand(M, N, device="cuda") * 0.9).to(torch.bfloat16)
+    if epi in (capi.EPI_BF16, capi.EPI_BF16_TANH, capi.EPI_BF16_TANHGRAD):
+        C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    else:
+        C = R32.clone() if epi == capi.EPI_F32_ACC else torch.zeros(M, N, device="cuda")
+    r_ptr = R32.data_ptr() if epi == capi.EPI_F32_RES else (Rbf.data_ptr() if epi == capi.EPI_BF16_TANHGRAD else 0)
+    torch.cuda.synchronize()
+    ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, C.data_ptr(), N, M, N, K, epi, r_ptr, N)
+    ctx.synchronize()
+    expect = {capi.EPI_BF16: ref, capi.EPI_F32_ACC: ref + R32, capi.EPI_F32_RES: ref + R32,
+              capi.EPI_BF16_TANH: torch.tanh(ref),
+              capi.EPI_BF16_TANHGRAD: ref * (1 - Rbf.float() ** 2)}[epi]
+    err = (C.float() - expect).abs().max().item() / expect.abs().max().item()
+    assert err < (1e-2 if C.dtype == torch.bfloat16 else 1e-5), err
+
+
+def test_gemm_residual_aliases_output(ctx):
+    """x += O @ Wo with the residual read and written in place (EPI_F32_RES)."""
+    M, N, K = 257, 512, 512
+    A = _mk(M, K, 5)
+    B = _mk(K, N, 6)
+    X = torch.randn(M, N, device="cuda")
+    ref = X + A.float() @ B.float()
+    torch.cuda.synchronize()
+    ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, X.data_ptr(), N, M, N, K, capi.EPI_F32_RES, X.data_ptr(), N)
+    ctx.synchronize()
+    assert (X - ref).abs().max().item() / ref.abs().max().item() < 1e-5
