@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""ChunkFlow B200 benchmark (BASELINE.json metric: tokens/sec on a long-tail
+SFT batch at chunk 8K; peak HBM GB).
+
+Workload (config C2): Llama-7B-shaped layer stack (d 4096, 32
+layers, 32 heads, GQA-8, SwiGLU ffn 11008, vocab 32000, RMSNorm, RoPE),
+random SplitMix64 init in bf16 (fp32 gradients), one step = the full chunked
+forward+backward of one 1,000-sequence long-tail block per GPU: 999 sequences
+log-uniform in [16,1024) + one 37,888-token sequence = 265,592 tokens, chunk
+size 8192, K=1 (33 chunks, 70 events, 4 recomputed forwards), loss and fp32
+parameter gradients (NCCL all-reduce across ranks for N>1).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One JSON line on rank 0.  `value` is device-timed (CUDA events on the
+library's stream, max over ranks) with the step's inputs resident in HBM;
+`e2e` goes through the public C-ABI call (cf_plan_build + cf_run_plan) with
+host token buffers, host->device copies and the loss read-back inside the
+timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODEL = dict(vocab=32000, d=4096, heads=32, kv_heads=8, layers=32, ffn=11008, seed=1, rope_theta=10000.0,
+             rms_eps=1e-5)
+CHUNK, K_RETAIN = 8192, 1
+METRIC = "tokens/sec on long-tail SFT batch (chunk 8K) at 1/2/4/8 B200; peak HBM GB"
+
+
+def block_lengths(seed):
+    import paper_2503_02356_b200 as cf
+    short = cf.capi.synthesize(999, seed, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
+    return np.concatenate([short, [37888]]).astype(np.int64)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+# ----------------------------------------------------------- CPU baseline
+def toy_flops(lengths, cfg, cs):
+    """Algorithmic FLOPs of the reference toy run_plan (6NT + 12*L*d*pairs)."""
+    d, L, V, kvw = cfg.d_model, cfg.num_layers, cfg.vocab_size, cfg.d_model // cfg.num_heads * cfg.num_kv_heads
+    N = L * (2 * d * d + 2 * d * kvw + 4 * d * d) + d * V
+    pairs = 0.0
+    for n in lengths:
+        pairs += n * (n + 1) / 2
+    return 6.0 * N * float(sum(lengths)) + 12.0 * L * d * pairs
+
+
+def cpu_reference_sample(target_s=15.0, procs=1):
+    """Times the UNMODIFIED reference run_plan (oracle/_ref/libcfref.so,
+    compiled from /root/reference in the build container) on a bounded slice
+    of the C1 toy batch on `procs` host processes (disjoint sequences), and
+    extrapolates to the C2 workload by algorithmic FLOPs/token."""
+    from oracle.oracle import Oracle, Reference, c1_batch, c1_cfg
+    try:
+        lib, kind = Reference(), "reference"
+    except FileNotFoundError:
+        lib, kind = Oracle(), "port"
+    o = Oracle()
+    lengths, tokens = c1_batch(o)
+    cfg = c1_cfg()
+    # bounded sample: leading short sequences of the C1 batch (~1/3 of it)
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    take = 11
+    sl, st = lengths[:take], tokens[:offs[take]]
+    flops = toy_flops(sl, cfg, 512)
+    t0 = time.perf_counter()
+    if procs == 1:
+        lib.run_plan(cfg, sl, st, 512, 2)
+        dt = time.perf_counter() - t0
+        agg_flops = flops
+    else:
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            t0 = time.perf_counter()
+            pool.starmap(_ref_worker, [(kind, sl.tolist(), st.tolist()) for _ in range(procs)])
+            dt = time.perf_counter() - t0
+        agg_flops = flops * procs
+    fps = agg_flops / dt
+    c2_flops_per_token = c2_flops_per_token_est()
+    return {"kind": kind, "cpu_flops_per_s": fps, "seconds": dt, "sample_tokens": int(sl.sum()),
+            "sample": f"reference run_plan (toy C1 model, chunk 512, K=2) on the first {take} C1 sequences "
+                      f"({int(sl.sum())} tokens) x {procs} process(es); tokens/s extrapolated to C2 by "
+                      f"algorithmic FLOPs ({c2_flops_per_token / 1e9:.1f} GFLOP/token)",
+            "tokens_per_s": fps / c2_flops_per_token, "cores": procs}
+
+
+def _ref_worker(kind, sl, st):
+    from oracle.oracle import Oracle, Reference, c1_cfg
+    lib = Reference() if kind == "reference" else Oracle()
+    lib.run_plan(c1_cfg(), np.array(sl), np.array(st, np.int32), 512, 2)
+
+
+def c2_flops_per_token_est():
+    """Algorithmic FLOPs/token of the C2 block: 6N + 12*L*H*dh*pairs/tokens
+    (pairs = sum len(len+1)/2 — chunking with KV state preserves the pairs)."""
+    from oracle.oracle import Oracle
+    d, L, H, dh, kvw, ffn, V = 4096, 32, 32, 128, 1024, 11008, 32000
+    N = L * (d * (d + 2 * kvw) + d * d + d * 2 * ffn + ffn * d) + d * V
+    lens = np.concatenate([Oracle().synthesize(999, 1, preset=0, bounds=[1024], fracs=[1.0], max_length=1024),
+                           [37888]]).astype(np.float64)
+    pairs = float((lens * (lens + 1) / 2).sum())
+    return 6.0 * N + 12.0 * L * H * dh * pairs / float(lens.sum())
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_sample(procs=procs)
+    for _ in range(args.steps):
+        vals.append(cpu_reference_sample(procs=procs))
+    tps = statistics.median(v["tokens_per_s"] for v in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 Llama-7B-shaped long-tail block, chunk 8192, K=1 (CPU: reference toy "
+                                   "run_plan, FLOP-extrapolated)", "global_batch": 1000 * args.gpus},
+            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": procs, "kind": vals[0]["kind"],
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ B200 arm
+def run_b200(args):
+    import torch
+    import paper_2503_02356_b200 as cf
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = cf.Context(local)
+    if world > 1:
+        uid = [cf.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.init_dp(rank, world, uid[0])
+    cfg = cf.model_cfg(arch=cf.ARCH_LLAMA, **{k: v for k, v in MODEL.items()})
+    model = cf.Model(ctx, cfg)
+
+    # global batch: one 1,000-sequence block per rank (weak scaling)
+    blocks = [block_lengths(b + 1) for b in range(world)]
+    lengths = np.concatenate(blocks)
+    ids = np.arange(len(lengths), dtype=np.int64)
+    tokens = np.concatenate([cf.gen_tokens(bl, MODEL["vocab"], b + 1) for b, bl in enumerate(blocks)])
+    gplan = cf.Plan.build(lengths, CHUNK, K_RETAIN, ids)
+    plan = gplan.partition(world, rank) if world > 1 else gplan
+    step = cf.Step(model, plan, lengths, tokens, ids)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+
+    def barrier():
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r = step.run()
+    barrier()
+    ctx.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res.append(step.run())
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    ctx.set_profiling(False)
+    ms = ev0.elapsed_time(ev1)
+    my_tokens = sum(r.tokens for r in res) / args.steps
+    # e2e through the public call: plan build + H2D of the batch + loss D2H
+    pinned_tok = torch.from_numpy(tokens).pin_memory().numpy()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(max(1, args.steps)):
+        gp = cf.Plan.build(lengths, CHUNK, K_RETAIN, ids)
+        p = gp.partition(world, rank) if world > 1 else gp
+        re = model.run_plan(p, lengths, pinned_tok, ids)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    h2d = int(step_meta_bytes(p, lengths))
+    d2h = 8 * (p.counts()[2] + 1)
+
+    stats = torch.tensor([ms, e2e_ms, my_tokens], dtype=torch.float64, device="cuda")
+    if dist:
+        t = stats.clone()
+        dist.all_reduce(t[:2], op=dist.ReduceOp.MAX)
+        tok = stats[2:].clone()
+        dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+        stats = torch.cat([t[:2], tok])
+    ms_max, e2e_max, tokens_all = stats.tolist()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    pk = peaks()
+    r0 = res[-1]
+    gemm_tf = sum(r.gemm_flops for r in res) / (sum(r.gemm_ms for r in res) / 1e3) / 1e12
+    attn_tf = sum(r.attn_flops for r in res) / max(1e-9, sum(r.attn_ms for r in res) / 1e3) / 1e12
+    gemm_share = sum(r.gemm_ms for r in res) / ms
+    attn_share = sum(r.attn_ms for r in res) / ms
+    step_ms = ms_max / args.steps
+    value = tokens_all / (step_ms / 1e3)  # tokens of one step over all ranks / slowest rank's step time
+    mfu = r0.model_flops * world / (step_ms / 1e3) / 1e12
+    cpu = cpu_reference_sample() if world == 1 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (SplitMix64 long-tail lengths + tokens, "
+                                                      "random-init weights)",
+        "config": {"workload": "C2: Llama-7B-shaped (GQA-8) layer stack, 1,000-seq long-tail block per GPU "
+                               "(999 log-uniform [16,1024) + 1 x 37,888), chunk 8192, K=1",
+                   "global_batch": 1000 * world, "tokens_per_gpu": int(r0.tokens), "chunk_size": CHUNK,
+                   "k": K_RETAIN, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (12 GB weights + 25 GB activations per chunk stream through)"},
+        "peak_hbm_gb": {"peak": r0.peak_hbm_bytes / 1e9, "static_params_grads": r0.static_hbm_bytes / 1e9,
+                        "activations": r0.act_hbm_bytes / 1e9, "kv_state": r0.kv_hbm_bytes / 1e9},
+        "mfu": {"model_tflops": mfu, "frac_of_2250": mfu / 2250.0,
+                "frac_of_measured_sustained": mfu / pk["bf16_tflops_sustained"]},
+        "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all projection/MLP/head GEMMs)",
+                     "achieved": gemm_tf, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                     "frac": gemm_tf / pk["bf16_tflops_sustained"], "traffic": None,
+                     "share_of_step": gemm_share, "peak_kind": "measured sustained (MEASURED_PEAKS.json)",
+                     "attention": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s"}},
+        "e2e": {"value": tokens_all / (e2e_max / 1e3 / max(1, args.steps)), "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(sum(r.gpu_launches for r in res)),
+        "clocks": clk.summary(),
+        "loss": r0.loss,
+    }
+    if cpu:
+        line["cpu_baseline"] = {"value": cpu["tokens_per_s"], "unit": "tokens/s", "cores": cpu["cores"],
+                                "kind": cpu["kind"], "sample": cpu["sample"]}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def step_meta_bytes(plan, lengths):
+    # tokens/targets/positions + segment tables + tiles + embedding CSR: about 5 int32 per token
+    return 4 * 5 * int(sum(c["total_tokens"] for c in plan.export()[0]))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

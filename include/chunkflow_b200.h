@@ -129,6 +129,14 @@ typedef struct cf_run_result {
   int64_t kv_hbm_bytes;      /* per-sequence KV-state high-water */
   double model_flops;        /* algorithmic FLOPs (no recompute) */
   double hw_flops;           /* incl. recompute */
+  /* per-kernel-class device time, filled when cf_ctx_set_profiling(ctx,1):
+   * CUDA events on the context stream around every launch of the class */
+  double gemm_ms, gemm_flops;
+  int64_t gemm_launches;
+  double attn_ms, attn_flops;
+  int64_t attn_launches;
+  double other_ms;
+  int64_t other_launches;
 } cf_run_result;
 
 typedef struct cf_ctx cf_ctx;
@@ -176,12 +184,25 @@ void cf_plan_destroy(cf_plan* plan);
  * stream over all sequences in order, next_below(vocab) per token. */
 int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab,
                   uint64_t seed, int32_t* tokens_out);
+/* synthesize (dataset.hpp:207): `count` lengths from a long-tail CDF spec
+ * (bounds strictly increasing, cumulative fractions in (0,1]); preset 1 =
+ * eval_table5_spec (dataset.hpp:88-97), preset 2 = lmsys_table2_spec. */
+int cf_synthesize(const int64_t* bounds, const double* fracs, int64_t nb,
+                  int64_t max_length, int64_t preset, int64_t count,
+                  uint64_t seed, int64_t* lengths_out);
+/* sample_batch (dataset.hpp:242): indices of step's global batch under a
+ * seed-keyed epoch shuffle of n records; *count_out = 0 past the epoch. */
+int cf_sample_batch(int64_t n, int64_t global_batch, int64_t step,
+                    uint64_t seed, int64_t* idx_out, int64_t* count_out);
 
 /* ---- device context / model ---- */
 int cf_ctx_create(int device, cf_ctx** out);
 void cf_ctx_destroy(cf_ctx* ctx);
 /* Stream the context runs on (cudaStream_t as an opaque pointer). */
 void* cf_ctx_stream(cf_ctx* ctx);
+/* 1: bracket every kernel launch with CUDA events and report per-class
+ * device time in cf_run_result (roofline evidence); 0: off (default). */
+int cf_ctx_set_profiling(cf_ctx* ctx, int on);
 /* NCCL data-parallel group: nccl_unique_id is the 128-byte ncclUniqueId
  * produced by cf_nccl_unique_id on rank 0 and broadcast by the launcher. */
 int cf_nccl_unique_id(uint8_t* out128);

@@ -52,7 +52,9 @@ class RunResult(C.Structure):
                 ("gpu_launches", C.c_int64), ("peak_hbm_bytes", C.c_int64),
                 ("static_hbm_bytes", C.c_int64), ("act_hbm_bytes", C.c_int64),
                 ("kv_hbm_bytes", C.c_int64), ("model_flops", C.c_double),
-                ("hw_flops", C.c_double)]
+                ("hw_flops", C.c_double), ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
+                ("gemm_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
+                ("attn_launches", C.c_int64), ("other_ms", C.c_double), ("other_launches", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -63,8 +65,9 @@ EXPORTS = [
     "cf_last_error", "cf_version", "cf_plan_build", "cf_plan_build_group",
     "cf_plan_counts", "cf_plan_export", "cf_plan_export_groups",
     "cf_plan_violation", "cf_plan_listing", "cf_plan_partition",
-    "cf_plan_rank_tokens", "cf_plan_destroy", "cf_gen_tokens", "cf_ctx_create",
-    "cf_ctx_destroy", "cf_ctx_stream", "cf_nccl_unique_id", "cf_ctx_init_dp",
+    "cf_plan_rank_tokens", "cf_plan_destroy", "cf_gen_tokens", "cf_synthesize", "cf_sample_batch",
+    "cf_ctx_create",
+    "cf_ctx_destroy", "cf_ctx_stream", "cf_ctx_set_profiling", "cf_nccl_unique_id", "cf_ctx_init_dp",
     "cf_model_create", "cf_model_destroy", "cf_model_num_tensors",
     "cf_model_tensor_info", "cf_model_get_param", "cf_model_set_param",
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
@@ -189,6 +192,23 @@ class Plan:
             self.h = C.c_void_p()
 
 
+def synthesize(count, seed, preset=1, bounds=(), fracs=(), max_length=0):
+    b = np.ascontiguousarray(bounds, np.int64)
+    f = np.ascontiguousarray(fracs, np.float64)
+    out = np.zeros(count, np.int64)
+    check(lib().cf_synthesize(_p(b), _p(f), C.c_int64(len(b)), C.c_int64(max_length), C.c_int64(preset),
+                              C.c_int64(count), C.c_uint64(seed), _p(out)))
+    return out
+
+
+def sample_batch(n, global_batch, step, seed):
+    out = np.zeros(global_batch, np.int64)
+    cnt = C.c_int64()
+    check(lib().cf_sample_batch(C.c_int64(n), C.c_int64(global_batch), C.c_int64(step), C.c_uint64(seed),
+                                _p(out), C.byref(cnt)))
+    return out[:cnt.value]
+
+
 def gen_tokens(lengths, vocab, seed):
     lengths = np.ascontiguousarray(lengths, np.int64)
     out = np.zeros(int(lengths.sum()), np.int32)
@@ -210,6 +230,9 @@ class Context:
 
     def synchronize(self):
         check(lib().cf_ctx_synchronize(self.h))
+
+    def set_profiling(self, on: bool):
+        check(lib().cf_ctx_set_profiling(self.h, C.c_int(int(on))))
 
     def init_dp(self, rank, world, uid: bytes | None):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid else None

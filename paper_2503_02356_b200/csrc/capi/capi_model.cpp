@@ -54,6 +54,13 @@ void cf_ctx_destroy(cf_ctx* ctx) {
 
 void* cf_ctx_stream(cf_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
 
+int cf_ctx_set_profiling(cf_ctx* ctx, int on) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    ctx->c.profile = on != 0;
+  });
+}
+
 int cf_ctx_synchronize(cf_ctx* ctx) {
   return cfb::guard([&] {
     need(ctx, "ctx");

@@ -127,6 +127,38 @@ int cf_plan_rank_tokens(const cf_plan* global, int64_t world, int64_t* tokens) {
 
 void cf_plan_destroy(cf_plan* plan) { delete plan; }
 
+int cf_synthesize(const int64_t* bounds, const double* fracs, int64_t nb, int64_t max_length, int64_t preset,
+                  int64_t count, uint64_t seed, int64_t* lengths_out) {
+  return cfb::guard([&] {
+    std::vector<int64_t> b;
+    std::vector<double> f;
+    int64_t mx = max_length;
+    if (preset == 1) {
+      b = {1024, 4096, 8192, 32768, 131072};
+      f = {0.9817, 0.9972, 0.9983, 0.9992, 0.9998};
+      mx = 262144;
+    } else if (preset == 2) {
+      b = {1024, 4096, 8192, 32768, 131072};
+      f = {0.90499, 0.99539, 0.99908, 0.99987, 0.99996};
+      mx = 303 * 1024;
+    } else {
+      b.assign(bounds, bounds + nb);
+      f.assign(fracs, fracs + nb);
+    }
+    const auto v = cfb::synthesize(b, f, mx, count, seed);
+    std::copy(v.begin(), v.end(), lengths_out);
+  });
+}
+
+int cf_sample_batch(int64_t n, int64_t global_batch, int64_t step, uint64_t seed, int64_t* idx_out,
+                    int64_t* count_out) {
+  return cfb::guard([&] {
+    const auto v = cfb::sample_batch(n, global_batch, step, seed);
+    std::copy(v.begin(), v.end(), idx_out);
+    *count_out = static_cast<int64_t>(v.size());
+  });
+}
+
 int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab, uint64_t seed, int32_t* tokens_out) {
   return cfb::guard([&] {
     if (vocab < 1) throw cfb::ValidationError("vocab must be positive");

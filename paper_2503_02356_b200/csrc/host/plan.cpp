@@ -7,6 +7,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <set>
 #include <tuple>
 
@@ -18,6 +19,62 @@ uint64_t splitmix_next(uint64_t& s) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
+}
+
+namespace {
+double next_unit(uint64_t& s) { return static_cast<double>(splitmix_next(s) >> 11) * 0x1.0p-53; }
+uint64_t next_below(uint64_t& s, uint64_t n) {
+  const uint64_t thr = (0 - n) % n;
+  while (true) {
+    const uint64_t r = splitmix_next(s);
+    if (r >= thr) return r % n;
+  }
+}
+}  // namespace
+
+std::vector<int64_t> synthesize(const std::vector<int64_t>& bounds, const std::vector<double>& fracs,
+                                int64_t max_length, int64_t count, uint64_t seed) {
+  if (bounds.empty() || bounds.size() != fracs.size()) throw ValidationError("distribution spec has no buckets");
+  for (size_t i = 0; i < bounds.size(); ++i) {
+    if (bounds[i] < 2) throw ValidationError("bucket upper bound must be at least 2");
+    if (i > 0 && bounds[i] <= bounds[i - 1]) throw ValidationError("bucket upper bounds must be strictly increasing");
+    if (fracs[i] <= 0.0 || fracs[i] > 1.0) throw ValidationError("cumulative fractions must lie in (0, 1]");
+    if (i > 0 && fracs[i] <= fracs[i - 1]) throw ValidationError("cumulative fractions must be strictly increasing");
+  }
+  if (max_length < bounds.back()) throw ValidationError("max_length must be at least the last bucket bound");
+  if (count < 1) throw ValidationError("count must be at least 1");
+  uint64_t s = seed;
+  std::vector<int64_t> out;
+  out.reserve(static_cast<size_t>(count));
+  for (int64_t i = 0; i < count; ++i) {
+    const double u = next_unit(s);
+    int64_t lo = bounds.back(), hi = max_length + 1;
+    for (size_t b = 0; b < bounds.size(); ++b) {
+      if (u < fracs[b]) {
+        lo = b == 0 ? std::max<int64_t>(1, std::min<int64_t>(16, bounds[0] - 1)) : bounds[b - 1];
+        hi = bounds[b];
+        break;
+      }
+    }
+    const double a = std::log(static_cast<double>(lo)), z = std::log(static_cast<double>(hi));
+    const double x = std::exp(a + next_unit(s) * (z - a));
+    out.push_back(std::clamp<int64_t>(static_cast<int64_t>(std::floor(x)), lo, hi - 1));
+  }
+  return out;
+}
+
+std::vector<int64_t> sample_batch(int64_t n, int64_t global_batch, int64_t step, uint64_t seed) {
+  if (n < 1) throw ValidationError("cannot sample from an empty sequence set");
+  if (global_batch < 1) throw ValidationError("global batch size must be at least 1");
+  if (step < 0) throw ValidationError("step must be non-negative");
+  const int64_t begin = step * global_batch;
+  if (begin >= n) return {};
+  std::vector<int64_t> order(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) order[static_cast<size_t>(i)] = i;
+  uint64_t s = seed;
+  for (int64_t i = n; i > 1; --i) std::swap(order[static_cast<size_t>(i - 1)], order[next_below(s, static_cast<uint64_t>(i))]);
+  const int64_t end = std::min(begin + global_batch, n);
+  return std::vector<int64_t>(order.begin() + begin, order.begin() + end);
 }
 
 const Chunk& Plan::chunk(int64_t id) const {

@@ -77,4 +77,13 @@ Plan sub_plan(const Plan& global, const std::vector<Unit>& units,
 
 uint64_t splitmix_next(uint64_t& state);
 
+// synthesize (dataset.hpp:207-237): bucket by CDF inversion, then
+// log-uniform within the bucket; bucket_low (:183-189).  Pure function of
+// (spec, count, seed); bit-exact with the reference.
+std::vector<int64_t> synthesize(const std::vector<int64_t>& bounds, const std::vector<double>& fracs,
+                                int64_t max_length, int64_t count, uint64_t seed);
+// sample_batch (dataset.hpp:242-268): seed-keyed Fisher-Yates permutation
+// of [0, n) sliced into consecutive global batches; returns indices.
+std::vector<int64_t> sample_batch(int64_t n, int64_t global_batch, int64_t step, uint64_t seed);
+
 }  // namespace cfb

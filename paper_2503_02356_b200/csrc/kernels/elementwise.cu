@@ -2,6 +2,8 @@
 // pitch allows, warp-shuffle reductions, and fixed reduction orders so every
 // result is bitwise reproducible run to run (needed for the reference's
 // recompute-loss check, plan_runner.hpp:232-241).
+#include <algorithm>
+
 #include "common.cuh"
 #include "ops.h"
 
@@ -153,28 +155,51 @@ __global__ void kv_store_kernel(const bf16* qkv, int64_t ld, int64_t T, int64_t 
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
+// 8 elements (16 bytes) per thread; ffn % 8 == 0 is validated at model creation.
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 p = __bfloat1622float2(h[i]);
+    f[2 * i] = p.x;
+    f[2 * i + 1] = p.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  return make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
 __global__ void swiglu_fwd_kernel(const bf16* gu, int64_t T, int64_t ffn, bf16* h) {
-  const int64_t n = T * ffn;
+  const int64_t f8 = ffn / 8, n = T * f8;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / ffn, j = i % ffn;
-    const float g = __bfloat162float(gu[t * 2 * ffn + j]);
-    const float u = __bfloat162float(gu[t * 2 * ffn + ffn + j]);
-    h[i] = __float2bfloat16_rn(g * sigmoidf_(g) * u);
+    const int64_t t = i / f8, j = (i % f8) * 8;
+    float g[8], u[8], o[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + t * 2 * ffn + j), g);
+    unpack8(*reinterpret_cast<const uint4*>(gu + t * 2 * ffn + ffn + j), u);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = g[e] * sigmoidf_(g[e]) * u[e];
+    *reinterpret_cast<uint4*>(h + t * ffn + j) = pack8(o);
   }
 }
 
 __global__ void swiglu_bwd_kernel(const bf16* gu, const bf16* dh, int64_t T, int64_t ffn, bf16* dgu) {
-  const int64_t n = T * ffn;
+  const int64_t f8 = ffn / 8, n = T * f8;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t t = i / ffn, j = i % ffn;
-    const float g = __bfloat162float(gu[t * 2 * ffn + j]);
-    const float u = __bfloat162float(gu[t * 2 * ffn + ffn + j]);
-    const float d = __bfloat162float(dh[i]);
-    const float s = sigmoidf_(g);
-    dgu[t * 2 * ffn + j] = __float2bfloat16_rn(d * u * s * (1.f + g * (1.f - s)));
-    dgu[t * 2 * ffn + ffn + j] = __float2bfloat16_rn(d * g * s);
+    const int64_t t = i / f8, j = (i % f8) * 8;
+    float g[8], u[8], d[8], og[8], ou[8];
+    unpack8(*reinterpret_cast<const uint4*>(gu + t * 2 * ffn + j), g);
+    unpack8(*reinterpret_cast<const uint4*>(gu + t * 2 * ffn + ffn + j), u);
+    unpack8(*reinterpret_cast<const uint4*>(dh + t * ffn + j), d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float s = sigmoidf_(g[e]);
+      og[e] = d[e] * u[e] * s * (1.f + g[e] * (1.f - s));
+      ou[e] = d[e] * g[e] * s;
+    }
+    *reinterpret_cast<uint4*>(dgu + t * 2 * ffn + j) = pack8(og);
+    *reinterpret_cast<uint4*>(dgu + t * 2 * ffn + ffn + j) = pack8(ou);
   }
 }
 
@@ -252,38 +277,73 @@ __global__ void rmsnorm_bwd_kernel(const float* x, const float* gain, const floa
   const float* xr = x + row * d;
   const float* gr = dy + row * d;
   float ss = 0.f, dot = 0.f;
-  for (int64_t c = lane; c < d; c += 32) {
-    const float xv = xr[c];
-    ss += xv * xv;
-    dot += gr[c] * gain[c] * xv;
+  // d % 8 == 0 (validated at model creation): float4 path
+  for (int64_t c = lane * 4; c < d; c += 128) {
+    const float4 xv = *reinterpret_cast<const float4*>(xr + c);
+    const float4 gv = *reinterpret_cast<const float4*>(gr + c);
+    const float4 w = *reinterpret_cast<const float4*>(gain + c);
+    ss += xv.x * xv.x + xv.y * xv.y + xv.z * xv.z + xv.w * xv.w;
+    dot += gv.x * w.x * xv.x + gv.y * w.y * xv.y + gv.z * w.z * xv.z + gv.w * w.w * xv.w;
   }
   ss = warp_sum(ss);
   dot = warp_sum(dot);
   const float r = rsqrtf(ss / static_cast<float>(d) + eps);
   const float k = r * r * r * dot / static_cast<float>(d);
-  for (int64_t c = lane; c < d; c += 32) {
-    const float base = dres ? dres[row * d + c] : 0.f;
-    dx[row * d + c] = base + r * gr[c] * gain[c] - xr[c] * k;
+  for (int64_t c = lane * 4; c < d; c += 128) {
+    const float4 xv = *reinterpret_cast<const float4*>(xr + c);
+    const float4 gv = *reinterpret_cast<const float4*>(gr + c);
+    const float4 w = *reinterpret_cast<const float4*>(gain + c);
+    float4 o = dres ? *reinterpret_cast<const float4*>(dres + row * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    o.x += r * gv.x * w.x - xv.x * k;
+    o.y += r * gv.y * w.y - xv.y * k;
+    o.z += r * gv.z * w.z - xv.z * k;
+    o.w += r * gv.w * w.w - xv.w * k;
+    *reinterpret_cast<float4*>(dx + row * d + c) = o;
   }
   if (lane == 0 && rstd) rstd[row] = r;
 }
 
-// Block = 32 columns x 8 row-groups; fixed order over rows.
-__global__ void gain_grad_kernel(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d,
-                                 float* dgain) {
-  __shared__ float part[8][33];
+// Stage 1: block (blockIdx.x: 128 columns, blockIdx.y: a contiguous row
+// slice); each thread owns 4 adjacent columns (float4), warps stride rows.
+// Partials [gridDim.y][d] are reduced in fixed order by stage 2.
+constexpr int kGainSplit = 64;
+__global__ void gain_grad_partial_kernel(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d,
+                                         float* part) {
+  __shared__ float4 red[8][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t c = blockIdx.x * 32 + lane;
-  float s = 0.f;
+  const int64_t c = (blockIdx.x * 32 + lane) * 4;
+  const int64_t rows = (T + gridDim.y - 1) / gridDim.y;
+  const int64_t r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (c < d)
-    for (int64_t t = w; t < T; t += 8) s += dy[t * d + c] * x[t * d + c] * rstd[t];
-  part[w][lane] = s;
+    for (int64_t t = r0 + w; t < r1; t += 8) {
+      const float4 a = *reinterpret_cast<const float4*>(dy + t * d + c);
+      const float4 b = *reinterpret_cast<const float4*>(x + t * d + c);
+      const float r = rstd[t];
+      s.x += a.x * b.x * r;
+      s.y += a.y * b.y * r;
+      s.z += a.z * b.z * r;
+      s.w += a.w * b.w * r;
+    }
+  red[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < d) {
-    float tot = 0.f;
-    for (int i = 0; i < 8; ++i) tot += part[i][lane];
-    dgain[c] += tot;
+    float4 tot = red[0][lane];
+    for (int i = 1; i < 8; ++i) {
+      tot.x += red[i][lane].x;
+      tot.y += red[i][lane].y;
+      tot.z += red[i][lane].z;
+      tot.w += red[i][lane].w;
+    }
+    *reinterpret_cast<float4*>(part + blockIdx.y * d + c) = tot;
   }
+}
+__global__ void gain_grad_reduce_kernel(const float* part, int splits, int64_t d, float* dgain) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c >= d) return;
+  float s = 0.f;
+  for (int i = 0; i < splits; ++i) s += part[i * d + c];
+  dgain[c] += s;
 }
 
 __global__ void dkv_to_dqkv_kernel(const float* dk, const float* dv, int64_t acc_ld, int64_t T, int KVH, int dh,
@@ -400,11 +460,11 @@ cudaError_t kv_store(const bf16* qkv, int64_t ld, int64_t T, int64_t kvw, int64_
   return cudaGetLastError();
 }
 cudaError_t swiglu_fwd(const bf16* gu, int64_t T, int64_t ffn, bf16* h, cudaStream_t st) {
-  swiglu_fwd_kernel<<<blocks_for(T * ffn), kThreads, 0, st>>>(gu, T, ffn, h);
+  swiglu_fwd_kernel<<<blocks_for(T * ffn / 8), kThreads, 0, st>>>(gu, T, ffn, h);
   return cudaGetLastError();
 }
 cudaError_t swiglu_bwd(const bf16* gu, const bf16* dh, int64_t T, int64_t ffn, bf16* dgu, cudaStream_t st) {
-  swiglu_bwd_kernel<<<blocks_for(T * ffn), kThreads, 0, st>>>(gu, dh, T, ffn, dgu);
+  swiglu_bwd_kernel<<<blocks_for(T * ffn / 8), kThreads, 0, st>>>(gu, dh, T, ffn, dgu);
   return cudaGetLastError();
 }
 cudaError_t ce_fwd_bwd(const float* logits, int64_t T, int64_t V, int64_t ld, const int32_t* targets, float inv_norm,
@@ -426,8 +486,17 @@ cudaError_t rmsnorm_bwd(const float* x, const float* gain, const float* dy, cons
 }
 cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d, float* dgain,
                       cudaStream_t st) {
-  gain_grad_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(x, dy, rstd, T, d, dgain);
-  return cudaGetLastError();
+  if (T == 0) return cudaSuccess;
+  const int splits = static_cast<int>(std::min<int64_t>(kGainSplit, (T + 7) / 8));
+  float* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, static_cast<size_t>(splits) * d * 4, st);
+  if (e != cudaSuccess) return e;
+  gain_grad_partial_kernel<<<dim3(static_cast<unsigned>((d / 4 + 31) / 32), splits), 256, 0, st>>>(x, dy, rstd, T,
+                                                                                                     d, part);
+  gain_grad_reduce_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, st>>>(part, splits, d, dgain);
+  e = cudaGetLastError();
+  cudaFreeAsync(part, st);
+  return e;
 }
 cudaError_t dkv_to_dqkv(const float* dk, const float* dv, int64_t acc_ld, int64_t T, int KVH, int dh,
                         const float2* tab, bf16* dqkv, int64_t ld, int64_t col_k, int64_t col_v, cudaStream_t st) {

@@ -541,10 +541,41 @@ struct Exec {
     cuda_check(e, what);
     launches += n;
   }
+  // --- optional per-launch timing (cf_ctx_set_profiling)
+  struct Rec {
+    cudaEvent_t a, b;
+    int cls;  // 0 gemm, 1 attention
+    double flops;
+    int n;
+  };
+  std::vector<Rec> recs;
+  size_t ev_used = 0;
+  cudaEvent_t ev() {
+    if (ev_used == ctx->event_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ctx->event_pool.push_back(e);
+    }
+    return ctx->event_pool[ev_used++];
+  }
+  cudaEvent_t mark() {
+    if (!ctx->profile) return nullptr;
+    cudaEvent_t a = ev();
+    CK(cudaEventRecord(a, s));
+    return a;
+  }
+  void close(cudaEvent_t a, int cls, double flops, int n) {
+    if (!ctx->profile) return;
+    cudaEvent_t b = ev();
+    CK(cudaEventRecord(b, s));
+    recs.push_back({a, b, cls, flops, n});
+  }
   void gemm(const void* a, int a_k, int64_t lda, const void* b, int b_k, int64_t ldb, void* c, int64_t ldc, int64_t M,
             int64_t N, int64_t K, int epi, const void* r = nullptr, int64_t ldr = 0) {
     cfk::GemmDesc d{a, lda, a_k, b, ldb, b_k, c, ldc, r, ldr, M, N, K, epi};
+    cudaEvent_t t0 = mark();
     L(cfk::gemm(d, s), "gemm");
+    close(t0, 0, 2.0 * static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K), 1);
   }
 
   Tape alloc_tape(int64_t T, bool retain) {
@@ -642,7 +673,9 @@ struct Exec {
                         gs->vc + l * gs->S * m->kvw + cm.start * m->kvw, m->kvw, s),
           "kv_store");
       AttnParams p = attn_params(cm, t, l, gs);
+      cudaEvent_t t0 = mark();
       L(cfk::attn_forward(p, s), "attn_fwd");
+      close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1);
       gemm(t.o + l * T * d, 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
       float* xn = t.x_in + (l + 1) * T * d;
       if (m->llama) {
@@ -756,7 +789,9 @@ struct Exec {
         p.dv_acc = dkv_local + kvw;
         own_dk = dkv_local;
       }
+      cudaEvent_t t0 = mark();
       L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
+      close(t0, 1, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
       L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
                          m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
         "dkv_to_dqkv");
@@ -893,6 +928,15 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
   std::vector<double> slots(static_cast<size_t>(nev + 1));
   CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nev + 1) * 8, cudaMemcpyDeviceToHost, ex.s));
   CK(cudaStreamSynchronize(ex.s));
+  double cls_ms[2] = {0, 0}, cls_flops[2] = {0, 0};
+  int64_t cls_n[2] = {0, 0};
+  for (const auto& r : ex.recs) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    cls_ms[r.cls] += ms;
+    cls_flops[r.cls] += r.flops;
+    cls_n[r.cls] += r.n;
+  }
   double total = 0;
   for (int64_t sl : first_pass_slots) total += slots[static_cast<size_t>(sl)];
   int64_t mism = 0;
@@ -928,6 +972,14 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
     res->peak_hbm_bytes = res->static_hbm_bytes + static_cast<int64_t>(high);
     res->model_flops = st->model_flops;
     res->hw_flops = st->hw_flops;
+    res->gemm_ms = cls_ms[0];
+    res->gemm_flops = cls_flops[0];
+    res->gemm_launches = cls_n[0];
+    res->attn_ms = cls_ms[1];
+    res->attn_flops = cls_flops[1];
+    res->attn_launches = cls_n[1];
+    res->other_ms = 0;
+    res->other_launches = ex.launches - cls_n[0] - cls_n[1];
   }
 }
 

@@ -28,6 +28,9 @@ struct Ctx {
   // data-parallel group (NCCL loaded at runtime)
   void* nccl_comm = nullptr;
   int rank = 0, world = 1;
+  // per-launch CUDA-event timing (cf_ctx_set_profiling)
+  bool profile = false;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 // One reference tensor (ToyModelParams::tensors order) and where it lives on
