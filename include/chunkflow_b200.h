@@ -257,6 +257,16 @@ int cf_ctx_synchronize(cf_ctx* ctx);
 /* C[M,N] (+)= sum_k A(m,k) B(n,k).  a_kmajor: A stored [M,K] (else [K,M]);
  * b_kmajor: B stored [N,K] (else [K,N]).  epi: 0 store bf16, 1 store fp32,
  * 2 accumulate into fp32, 3 bf16 store of acc + residual(bf16). */
+/* Chunked causal attention over packed segments (toy_model.hpp:263-302
+ * forward, :436-486 backward).  segs: host int32 [nseg][4] = {q_start, len,
+ * kv_row0, prefix}.  impl 0 = warp-MMA kernels, 1 = tcgen05 (head_dim 128).
+ * Backward writes dq and ADDS dK/dV into the fp32 accumulators. */
+int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q,
+                    int64_t q_stride, const void* k, const void* v,
+                    int64_t kv_stride, int64_t kv_rows, void* o, float* lse,
+                    const void* dout, void* dq, float* dk_acc, float* dv_acc,
+                    int64_t acc_stride, const int32_t* segs, int64_t nseg,
+                    int64_t T, int64_t H, int64_t KVH, int64_t dh);
 int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
                const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
                int64_t m, int64_t n, int64_t k, int epi, const void* residual,

@@ -72,7 +72,7 @@ EXPORTS = [
     "cf_model_tensor_info", "cf_model_get_param", "cf_model_set_param",
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
-    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm",
+    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention",
 ]
 
 _lib = None
@@ -247,6 +247,17 @@ class Context:
     def gemm(self, a, a_kmajor, lda, b, b_kmajor, ldb, c, ldc, m, n, k, epi, r=0, ldr=0):
         check(lib().cf_op_gemm(self.h, C.c_void_p(a), a_kmajor, lda, C.c_void_p(b), b_kmajor, ldb,
                                C.c_void_p(c), ldc, m, n, k, epi, C.c_void_p(r), ldr))
+
+    def attention(self, impl, backward, q, q_stride, k, v, kv_stride, kv_rows, o, lse, dout, dq, dk, dv,
+                  acc_stride, segs, T, H, KVH, dh):
+        """Operator-level attention on device pointers; segs = [[q_start, len, kv_row0, prefix], ...]."""
+        s = np.ascontiguousarray(np.asarray(segs, np.int32).reshape(-1, 4))
+        vp = C.c_void_p
+        check(lib().cf_op_attention(self.h, C.c_int(impl), C.c_int(int(backward)), vp(q), C.c_int64(q_stride),
+                                    vp(k), vp(v), C.c_int64(kv_stride), C.c_int64(kv_rows), vp(o), vp(lse),
+                                    vp(dout), vp(dq), vp(dk), vp(dv), C.c_int64(acc_stride), _p(s),
+                                    C.c_int64(len(s)), C.c_int64(T), C.c_int64(H), C.c_int64(KVH),
+                                    C.c_int64(dh)))
 
     def close(self):
         if self.h and self.h.value:

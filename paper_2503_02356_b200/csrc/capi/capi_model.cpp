@@ -1,10 +1,13 @@
 // C-ABI: device context, model, execution and operator-level entry points.
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
 #include <memory>
+#include <vector>
 
 #include "../../../include/chunkflow_b200.h"
+#include "../kernels/attention_tc.h"
 #include "../kernels/gemm.h"
 #include "../runtime/engine.hpp"
 #include "capi_util.hpp"
@@ -223,6 +226,78 @@ int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids, const
     o.normalizer_override = normalizer_override;
     cfb::Batch b{seq_ids, lengths, tokens, nullptr, n};
     cfb::run_plan(&ctx->c, model->m, p, b, o, result);
+  });
+}
+
+int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t q_stride, const void* k,
+                    const void* v, int64_t kv_stride, int64_t kv_rows, void* o, float* lse, const void* dout,
+                    void* dq, float* dk_acc, float* dv_acc, int64_t acc_stride, const int32_t* segs, int64_t nseg,
+                    int64_t T, int64_t H, int64_t KVH, int64_t dh) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    std::vector<int32_t> meta(segs, segs + 4 * nseg);
+    auto tiles = [&](int rows, bool keys) {
+      const int64_t off = static_cast<int64_t>(meta.size());
+      int64_t n = 0;
+      for (int64_t s = 0; s < nseg; ++s) {
+        const int32_t len = segs[4 * s + 1], prefix = segs[4 * s + 3];
+        const int32_t total = keys ? prefix + len : len;
+        for (int32_t f = 0; f < total; f += rows) {
+          meta.insert(meta.end(), {static_cast<int32_t>(s), f, std::min(rows, total - f), 0});
+          ++n;
+        }
+      }
+      return std::make_pair(off, n);
+    };
+    const auto q64 = tiles(64, false), k64 = tiles(64, true), q128 = tiles(128, false);
+    int32_t* dmeta = nullptr;
+    cudaStream_t st = ctx->c.stream;
+    cfb::cuda_check(cudaMallocAsync(&dmeta, meta.size() * 4, st), "malloc");
+    cfb::cuda_check(cudaMemcpyAsync(dmeta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, st), "h2d");
+    cfk::AttnParams p{};
+    p.q = static_cast<const cfk::bf16*>(q);
+    p.q_stride = q_stride;
+    p.k = static_cast<const cfk::bf16*>(k);
+    p.v = static_cast<const cfk::bf16*>(v);
+    p.kv_stride = kv_stride;
+    p.o = static_cast<cfk::bf16*>(o);
+    p.o_stride = H * dh;
+    p.lse = lse;
+    p.dout = static_cast<const cfk::bf16*>(dout);
+    p.dout_stride = H * dh;
+    p.dq = static_cast<cfk::bf16*>(dq);
+    p.dq_stride = H * dh;
+    p.dk_acc = dk_acc;
+    p.dv_acc = dv_acc;
+    p.acc_stride = acc_stride;
+    p.segs = reinterpret_cast<const cfk::AttnSeg*>(dmeta);
+    p.tiles = reinterpret_cast<const cfk::AttnTile*>(dmeta + q64.first);
+    p.num_tiles = static_cast<int32_t>(q64.second);
+    p.T = static_cast<int32_t>(T);
+    p.H = static_cast<int32_t>(H);
+    p.KVH = static_cast<int32_t>(KVH);
+    p.dh = static_cast<int32_t>(dh);
+    p.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dh)));
+    float* dsum = nullptr;
+    cfb::cuda_check(cudaMallocAsync(&dsum, static_cast<size_t>(T * H) * 4, st), "malloc");
+    p.dsum = dsum;
+    cudaError_t e;
+    if (!backward) {
+      if (impl == 1) {
+        if (!cfk::attn_tc_supported(p)) throw cfb::ValidationError("tcgen05 attention needs head_dim 128");
+        e = cfk::attn_forward_tc(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),
+                                 static_cast<int32_t>(q128.second), kv_rows, st);
+      } else {
+        e = cfk::attn_forward(p, st);
+      }
+    } else {
+      e = cfk::attn_backward(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + k64.first),
+                             static_cast<int32_t>(k64.second), st);
+    }
+    cfb::cuda_check(e, "attention");
+    cudaFreeAsync(dsum, st);
+    cudaFreeAsync(dmeta, st);
+    cfb::cuda_check(cudaStreamSynchronize(st), "sync");
   });
 }
 

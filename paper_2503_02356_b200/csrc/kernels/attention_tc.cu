@@ -1,0 +1,334 @@
+// tcgen05 chunked causal attention forward for head_dim 128 (sm_100a).
+//
+// One CTA = 128 queries of one q head of one packed segment; loops over
+// 128-key tiles of the segment's keys [0, prefix + last query] (bottom-right
+// causal mask, KV prefix read straight from the per-sequence cache).
+//
+//   warps 0-3  softmax: thread = query row; tcgen05.ld its S row from TMEM,
+//              online softmax (exp2, lazy O rescale when the running max grows
+//              by > 2^8), P -> bf16 -> 128B-swizzled smem (UMMA A operand)
+//   warp  4    TMA producer: Q once, K/V tiles into a 2-stage ring
+//   warp  5    MMA issuer (one lane): S = Q K^T (M128 N128 K128, K-major x2),
+//              O += P V (A = P K-major in smem, B = V N-major view of the same
+//              TMA tile), accumulators in TMEM: S0 | S1 | O (384 of 512 cols)
+// Reference semantics: toy_model.hpp:263-302 (scale 1/sqrt(dh), max-
+// subtracted softmax, PV, GQA head map hq / per_kv).
+#include <cfloat>
+
+#include "attention.h"
+#include "attention_tc.h"
+#include "common.cuh"
+
+namespace cfk {
+namespace {
+
+constexpr int TQ = 128, TK = 128, DH = 128;
+constexpr uint32_t kBox = 128 * 64 * 2;  // [128 rows][64 cols] bf16 = 16 KiB
+constexpr uint32_t kTile = 2 * kBox;     // 128 rows x 128 cols
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescale = 8.0f;  // log2 threshold for lazy O rescaling
+
+struct TcArgs {
+  const AttnSeg* segs;
+  const AttnTile* tiles;  // 128-row query tiles
+  __nv_bfloat16* o;
+  int64_t o_stride;
+  float* lse;
+  int32_t T, H, KVH;
+  float sl2;  // scale * log2(e)
+};
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16-byte chunk c (0..15 over 128 columns) of row r in a K-major SW128 tile
+// made of two [128 rows][64 cols] boxes.
+__device__ __forceinline__ uint32_t sw128_off(int r, int c) {
+  return static_cast<uint32_t>((c >> 3) * kBox + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+
+// K-major operand descriptor at k-step ks (16 elements) of a 2-box tile.
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + (ks >> 2) * kBox + (ks & 3) * 32, 16, 1024);
+}
+// MN-major view (N = the 128 tile columns, K = the 128 tile rows) at k-step ks.
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + ks * 2048, kBox, 1024);
+}
+
+__global__ void __launch_bounds__(192, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, TcArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sK = sQ + kTile;      // 2 stages
+  uint8_t* sV = sK + 2 * kTile;  // 2 stages
+  uint8_t* sP = sV + 2 * kTile;  // 1 buffer
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kTile);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;   // [2]
+  uint64_t* k_empty = bar + 3;  // [2]
+  uint64_t* v_full = bar + 5;   // [2]
+  uint64_t* v_empty = bar + 7;  // [2]
+  uint64_t* s_full = bar + 9;   // [2]
+  uint64_t* s_free = bar + 11;  // [2]
+  uint64_t* p_full = bar + 13;
+  uint64_t* p_free = bar + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int h = blockIdx.y, g = h / (a.H / a.KVH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q_row0 = sg.q_start + tl.first;
+  const int kv_len = sg.prefix + tl.first + tl.count;  // keys needed by this tile
+  const int nkt = (kv_len + TK - 1) / TK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(p_free, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 128};
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kTile);
+      tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
+      tma_load_2d(sQ + kBox, &tmQ, q_full, h * DH + 64, q_row0);
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        const int krow = sg.kv_row0 + j * TK;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], kTile);
+        tma_load_2d(sK + st * kTile, &tmK, &k_full[st], g * DH, krow);
+        tma_load_2d(sK + st * kTile + kBox, &tmK, &k_full[st], g * DH + 64, krow);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], kTile);
+        tma_load_2d(sV + st * kTile, &tmV, &v_full[st], g * DH, krow);
+        tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], g * DH + 64, krow);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
+      const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
+      auto issue_s = [&](int j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_full[st], ph);
+        mbar_wait(&s_free[st], ph ^ 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(sK + st * kTile);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tS[st], kdesc(q0, ks), kdesc(k0, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[st]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nkt; ++j) {
+        if (j + 1 < nkt) issue_s(j + 1);
+        const int st = j & 1;
+        mbar_wait(p_full, j & 1);
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t v0 = smem_u32(sV + st * kTile);
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks)
+          umma_bf16(tO, kdesc(p0, ks), mndesc(v0, ks), idO, (j > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&v_empty[st]);
+        umma_commit(p_free);
+      }
+    }
+  } else {
+    // softmax warps 0..3: TMEM lane quarter = warp, row = warp*32 + lane
+    const int row = warp * 32 + lane;
+    const int qi = tl.first + row;                      // query index in segment
+    const int lim = sg.prefix + min(qi, sg.len - 1);    // last visible key
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    float m = -FLT_MAX, l = 0.f;
+    for (int j = 0; j < nkt; ++j) {
+      const int st = j & 1;
+      mbar_wait(&s_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tS[st] + lane_off + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
+      }
+      tc_fence_before();
+      mbar_arrive(&s_free[st]);
+      const int key0 = j * TK;
+      float tmax = -FLT_MAX;
+#pragma unroll
+      for (int e = 0; e < 128; ++e) {
+        s[e] = (key0 + e <= lim) ? s[e] * a.sl2 : -FLT_MAX;
+        tmax = fmaxf(tmax, s[e]);
+      }
+      bool rescale = false;
+      float alpha = 1.f;
+      if (tmax > m + kRescale || j == 0) {
+        const float mn = fmaxf(m, tmax);
+        alpha = exp2f(m - mn);
+        rescale = j > 0;
+        m = mn;
+      }
+      l *= alpha;
+      uint32_t pk[64];
+#pragma unroll
+      for (int e = 0; e < 64; ++e) {
+        const float p0 = s[2 * e] == -FLT_MAX ? 0.f : exp2f(s[2 * e] - m);
+        const float p1 = s[2 * e + 1] == -FLT_MAX ? 0.f : exp2f(s[2 * e + 1] - m);
+        l += p0 + p1;
+        pk[e] = pack_bf16(p0, p1);
+      }
+      if (j > 0) {
+        mbar_wait(p_free, (j - 1) & 1);  // PV_{j-1} done: O stable, P buffer free
+        tc_fence_after();
+      }
+      if (rescale) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tmem_st32(tO + lane_off + c * 32, r);
+        }
+        tmem_st_wait();
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        *reinterpret_cast<uint4*>(sP + sw128_off(row, c)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(p_free, (nkt - 1) & 1);
+    tc_fence_after();
+    const bool ok = qi < sg.len && row < tl.count;
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + h * DH;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tO + lane_off + c * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * inv, __uint_as_float(r[8 * q + 1]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv));
+      }
+    }
+    if (ok) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld) {
+  EncodeFn enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool attn_tc_supported(const AttnParams& p) {
+  return p.dh == 128 && (p.q_stride % 8) == 0 && (p.kv_stride % 8) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.q) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.k) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.v) & 15) == 0;
+}
+
+cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32_t ntiles, int64_t kv_rows,
+                            cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  CUtensorMap mq, mk, mv;
+  if (!map_rows(&mq, p.q, static_cast<uint64_t>(p.H) * DH, static_cast<uint64_t>(p.T), p.q_stride) ||
+      !map_rows(&mk, p.k, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride) ||
+      !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
+    return cudaErrorInvalidValue;
+  TcArgs a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
+  const size_t smem = 1024 + 6 * kTile + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_fwd_tc_kernel<<<dim3(ntiles, p.H), 192, smem, st>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+}  // namespace cfk

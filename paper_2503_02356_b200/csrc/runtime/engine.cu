@@ -16,6 +16,7 @@
 //  * losses are reduced on the device in a fixed order into per-event slots,
 //    read back once per step; recompute-loss equality is checked bitwise.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <dlfcn.h>
@@ -24,6 +25,7 @@
 #include <set>
 
 #include "../capi/capi_util.hpp"
+#include "../kernels/attention_tc.h"
 #include "../kernels/gemm.h"
 #include "engine.hpp"
 
@@ -315,6 +317,7 @@ struct ChunkMeta {
   bool dependent = false;
   int64_t seq = -1, start = 0, seq_len = 0, group = -1, index = -1;
   int64_t o_tok = 0, o_tgt = 0, o_pos = 0, o_segs = 0, nsegs = 0, o_qt = 0, nqt = 0, o_kt = 0, nkt = 0;
+  int64_t o_qt128 = 0, nqt128 = 0, o_kt128 = 0, nkt128 = 0;  // 128-row tiles (tcgen05 kernels)
   int64_t o_order = 0, o_uniq = 0, o_uoff = 0, nuniq = 0;
   double pairs = 0;
 };
@@ -475,6 +478,38 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
         put(0);
         ++cm.nkt;
       }
+    }
+    // 128-query tiles, heaviest (most visible keys) first so the causal tail
+    // of the grid is short; 128-key tiles likewise by number of queries.
+    {
+      std::vector<std::array<int32_t, 4>> qt, kt;
+      for (size_t s = 0; s < segs.size(); ++s) {
+        for (int32_t f = 0; f < segs[s].len; f += 128)
+          qt.push_back({static_cast<int32_t>(s), f, std::min(128, segs[s].len - f), segs[s].prefix + f});
+        const int32_t nk = segs[s].prefix + segs[s].len;
+        for (int32_t f = 0; f < nk; f += 128)
+          kt.push_back({static_cast<int32_t>(s), f, std::min(128, nk - f),
+                        segs[s].len - std::max(0, f - segs[s].prefix)});
+      }
+      auto by_work = [](const std::array<int32_t, 4>& x, const std::array<int32_t, 4>& y) { return x[3] > y[3]; };
+      std::stable_sort(qt.begin(), qt.end(), by_work);
+      std::stable_sort(kt.begin(), kt.end(), by_work);
+      cm.o_qt128 = here();
+      for (auto& x : qt) {
+        put(x[0]);
+        put(x[1]);
+        put(x[2]);
+        put(0);
+      }
+      cm.nqt128 = static_cast<int64_t>(qt.size());
+      cm.o_kt128 = here();
+      for (auto& x : kt) {
+        put(x[0]);
+        put(x[1]);
+        put(x[2]);
+        put(0);
+      }
+      cm.nkt128 = static_cast<int64_t>(kt.size());
     }
     // embedding-backward CSR: rows grouped by token id, ascending rows
     std::sort(tok_rows.begin(), tok_rows.end());
@@ -674,7 +709,12 @@ struct Exec {
           "kv_store");
       AttnParams p = attn_params(cm, t, l, gs);
       cudaEvent_t t0 = mark();
-      L(cfk::attn_forward(p, s), "attn_fwd");
+      if (cfk::attn_tc_supported(p))
+        L(cfk::attn_forward_tc(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
+                               cm.dependent ? gs->S : T, s),
+          "attn_fwd_tc");
+      else
+        L(cfk::attn_forward(p, s), "attn_fwd");
       close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1);
       gemm(t.o + l * T * d, 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
       float* xn = t.x_in + (l + 1) * T * d;
