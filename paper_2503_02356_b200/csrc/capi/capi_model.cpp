@@ -249,7 +249,7 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t 
       }
       return std::make_pair(off, n);
     };
-    const auto q64 = tiles(64, false), k64 = tiles(64, true), q128 = tiles(128, false);
+    const auto q64 = tiles(64, false), k64 = tiles(64, true), q128 = tiles(128, false), k128 = tiles(128, true);
     int32_t* dmeta = nullptr;
     cudaStream_t st = ctx->c.stream;
     cfb::cuda_check(cudaMallocAsync(&dmeta, meta.size() * 4, st), "malloc");
@@ -290,6 +290,12 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t 
       } else {
         e = cfk::attn_forward(p, st);
       }
+    } else if (impl == 1) {
+      if (!cfk::attn_tc_supported(p)) throw cfb::ValidationError("tcgen05 attention needs head_dim 128");
+      e = cfk::attn_backward_tc(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),
+                                static_cast<int32_t>(q128.second),
+                                reinterpret_cast<const cfk::AttnTile*>(dmeta + k128.first),
+                                static_cast<int32_t>(k128.second), kv_rows, st);
     } else {
       e = cfk::attn_backward(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + k64.first),
                              static_cast<int32_t>(k64.second), st);

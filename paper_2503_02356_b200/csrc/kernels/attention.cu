@@ -551,6 +551,12 @@ cudaError_t attn_forward(const AttnParams& p, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+cudaError_t attn_dsum(const AttnParams& p, cudaStream_t st) {
+  const int64_t warps = static_cast<int64_t>(p.T) * p.H;
+  attn_dsum_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t attn_backward(const AttnParams& p, const AttnTile* key_tiles, int32_t nkt, cudaStream_t st) {
   if (p.num_tiles == 0) return cudaSuccess;
   if (p.dh <= 64) return bwd_t<64>(p, key_tiles, nkt, st);

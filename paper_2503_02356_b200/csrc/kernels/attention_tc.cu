@@ -274,6 +274,392 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ------------------------------------------------------------------ backward
+struct TcBwdArgs {
+  const AttnSeg* segs;
+  const AttnTile* tiles;  // 128-row tiles (queries for dQ, keys for dK/dV)
+  const float* lse;       // [H, T] natural log
+  const float* dsum;      // [H, T]
+  __nv_bfloat16* dq;
+  int64_t dq_stride;
+  float* dk_acc;
+  float* dv_acc;
+  int64_t acc_stride;
+  int32_t T, H, KVH;
+  float sl2, scale;
+};
+
+__device__ __forceinline__ void named_sync_128() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// dQ: CTA = 128 queries of one q head; per 128-key tile
+//   S = Q K^T, dP = dO V^T (TMEM) -> dS = P (dP - D) (bf16, smem) -> dQ += dS K.
+__global__ void __launch_bounds__(192, 1)
+    attn_dq_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+                      const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, TcBwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;
+  uint8_t* sdO = sQ + kTile;
+  uint8_t* sK = sdO + kTile;     // 2 stages
+  uint8_t* sV = sK + 2 * kTile;  // 2 stages
+  uint8_t* sS = sV + 2 * kTile;  // dS
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + kTile);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;
+  uint64_t* k_empty = bar + 3;
+  uint64_t* v_full = bar + 5;
+  uint64_t* v_empty = bar + 7;
+  uint64_t* s_full = bar + 9;
+  uint64_t* s_free = bar + 10;
+  uint64_t* ds_full = bar + 11;
+  uint64_t* ds_free = bar + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int h = blockIdx.y, g = h / (a.H / a.KVH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q_row0 = sg.q_start + tl.first;
+  const int kv_len = sg.prefix + tl.first + tl.count;
+  const int nkt = (kv_len + TK - 1) / TK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 128);
+    mbar_init(ds_full, 128);
+    mbar_init(ds_free, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * kTile);
+      tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
+      tma_load_2d(sQ + kBox, &tmQ, q_full, h * DH + 64, q_row0);
+      tma_load_2d(sdO, &tmO, q_full, h * DH, q_row0);
+      tma_load_2d(sdO + kBox, &tmO, q_full, h * DH + 64, q_row0);
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        const int krow = sg.kv_row0 + j * TK;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], kTile);
+        tma_load_2d(sK + st * kTile, &tmK, &k_full[st], g * DH, krow);
+        tma_load_2d(sK + st * kTile + kBox, &tmK, &k_full[st], g * DH + 64, krow);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], kTile);
+        tma_load_2d(sV + st * kTile, &tmV, &v_full[st], g * DH, krow);
+        tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], g * DH + 64, krow);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idKN = umma_idesc_bf16(128, 128, 0, 1);
+      const uint32_t q0 = smem_u32(sQ), o0 = smem_u32(sdO), s0 = smem_u32(sS);
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&k_full[st], ph);
+        mbar_wait(&v_full[st], ph);
+        mbar_wait(s_free, (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(sK + st * kTile), v0 = smem_u32(sV + st * kTile);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tS, kdesc(q0, ks), kdesc(k0, ks), idKK, ks > 0 ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tP, kdesc(o0, ks), kdesc(v0, ks), idKK, ks > 0 ? 1u : 0u);
+        umma_commit(&v_empty[st]);
+        umma_commit(s_full);
+        mbar_wait(ds_full, j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < TK / 16; ++ks)
+          umma_bf16(tQ, kdesc(s0, ks), mndesc(k0, ks), idKN, (j > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&k_empty[st]);
+        umma_commit(ds_free);
+      }
+    }
+  } else {
+    const int row = warp * 32 + lane;
+    const int qi = tl.first + row;
+    const bool ok = qi < sg.len && row < tl.count;
+    const int lim = sg.prefix + min(qi, sg.len - 1);
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
+    const float D = ok ? a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] : 0.f;
+    for (int j = 0; j < nkt; ++j) {
+      // s_full(j) is committed after dQ_{j-1}: the dS buffer is free too.
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const int key0 = j * TK;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tS + lane_off + c * 32, rs);
+        tmem_ld32(tP + lane_off + c * 32, rp);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int k0 = key0 + c * 32 + 2 * e;
+          const float p0 = (ok && k0 <= lim) ? exp2f(__uint_as_float(rs[2 * e]) * a.sl2 - lse2) : 0.f;
+          const float p1 = (ok && k0 + 1 <= lim) ? exp2f(__uint_as_float(rs[2 * e + 1]) * a.sl2 - lse2) : 0.f;
+          pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(sS + sw128_off(row, 4 * c + q)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+      tc_fence_before();
+      mbar_arrive(s_free);
+      fence_async_smem();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(ds_free, (nkt - 1) & 1);
+    tc_fence_after();
+    __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tQ + lane_off + c * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* dst = reinterpret_cast<uint4*>(out + c * 32);
+        const float sc = a.scale;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * sc, __uint_as_float(r[8 * q + 1]) * sc),
+                              pack_bf16(__uint_as_float(r[8 * q + 2]) * sc, __uint_as_float(r[8 * q + 3]) * sc),
+                              pack_bf16(__uint_as_float(r[8 * q + 4]) * sc, __uint_as_float(r[8 * q + 5]) * sc),
+                              pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// dK/dV: CTA = 128 keys of one kv head (owner of those rows -> deterministic);
+// loops over every q head of the GQA group and every 128-query tile that
+// sees the keys: S^T = K Q^T, dP^T = V dO^T -> P^T, dS^T (bf16, smem) ->
+// dV += P^T dO, dK += dS^T Q.  Q / dO tiles are used both K-major (first two
+// MMAs) and as N-major views (last two) of the same TMA tile.
+__global__ void __launch_bounds__(192, 1)
+    attn_dkv_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                       TcBwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + kTile;
+  uint8_t* sQ = sV + kTile;
+  uint8_t* sdO = sQ + kTile;
+  uint8_t* sP = sdO + kTile;  // P^T
+  uint8_t* sS = sP + kTile;   // dS^T
+  float* sL = reinterpret_cast<float*>(sS + kTile);  // [2][128] lse*log2e (INF = invalid query)
+  float* sD = sL + 256;                              // [2][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 256);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;
+  uint64_t* q_empty = bar + 2;
+  uint64_t* s_full = bar + 3;
+  uint64_t* s_free = bar + 4;
+  uint64_t* pds_full = bar + 5;
+  uint64_t* pds_free = bar + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int g = blockIdx.y, per = a.H / a.KVH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int key_first = tl.first;
+  const int kv_len = sg.prefix + sg.len;
+  const int i0 = max(0, key_first - sg.prefix);
+  const int nqt = (sg.len - i0 + TQ - 1) / TQ;
+  const int iters = per * nqt;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(kv_full, 1);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 128);
+    mbar_init(pds_full, 128);
+    mbar_init(pds_free, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      const int krow = sg.kv_row0 + key_first;
+      mbar_expect_tx(kv_full, 2 * kTile);
+      tma_load_2d(sK, &tmK, kv_full, g * DH, krow);
+      tma_load_2d(sK + kBox, &tmK, kv_full, g * DH + 64, krow);
+      tma_load_2d(sV, &tmV, kv_full, g * DH, krow);
+      tma_load_2d(sV + kBox, &tmV, kv_full, g * DH + 64, krow);
+      for (int it = 0; it < iters; ++it) {
+        const int hq = g * per + it / nqt;
+        const int qrow = sg.q_start + i0 + (it % nqt) * TQ;
+        mbar_wait(q_empty, (it & 1) ^ 1);
+        mbar_expect_tx(q_full, 2 * kTile);
+        tma_load_2d(sQ, &tmQ, q_full, hq * DH, qrow);
+        tma_load_2d(sQ + kBox, &tmQ, q_full, hq * DH + 64, qrow);
+        tma_load_2d(sdO, &tmO, q_full, hq * DH, qrow);
+        tma_load_2d(sdO + kBox, &tmO, q_full, hq * DH + 64, qrow);
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idKK = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idKN = umma_idesc_bf16(128, 128, 0, 1);
+      const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV), q0 = smem_u32(sQ), o0 = smem_u32(sdO);
+      const uint32_t p0 = smem_u32(sP), s0 = smem_u32(sS);
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < iters; ++it) {
+        mbar_wait(q_full, it & 1);
+        mbar_wait(s_free, (it & 1) ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tS, kdesc(k0, ks), kdesc(q0, ks), idKK, ks > 0 ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tP, kdesc(v0, ks), kdesc(o0, ks), idKK, ks > 0 ? 1u : 0u);
+        umma_commit(s_full);
+        mbar_wait(pds_full, it & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < TQ / 16; ++ks)
+          umma_bf16(tdV, kdesc(p0, ks), mndesc(o0, ks), idKN, (it > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < TQ / 16; ++ks)
+          umma_bf16(tdK, kdesc(s0, ks), mndesc(q0, ks), idKN, (it > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(q_empty);
+        umma_commit(pds_free);
+      }
+    }
+  } else {
+    const int row = warp * 32 + lane;  // key row within the tile
+    const int key = key_first + row;
+    const bool kok = row < tl.count && key < kv_len;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    for (int it = 0; it < iters; ++it) {
+      const int hq = g * per + it / nqt;
+      const int qt0 = i0 + (it % nqt) * TQ;  // first query of the tile (segment index)
+      float* L_ = sL + (it & 1) * 128;
+      float* D_ = sD + (it & 1) * 128;
+      {
+        const int qi = qt0 + row;
+        const bool qok = qi < sg.len;
+        const int64_t idx = static_cast<int64_t>(hq) * a.T + sg.q_start + qi;
+        L_[row] = qok ? a.lse[idx] * kLog2e : INFINITY;
+        D_[row] = qok ? a.dsum[idx] : 0.f;
+      }
+      named_sync_128();
+      // s_full(it) is committed after dV/dK of it-1: P^T / dS^T buffers free.
+      mbar_wait(s_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tS + lane_off + c * 32, rs);
+        tmem_ld32(tP + lane_off + c * 32, rp);
+        tmem_ld_wait();
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int ql = c * 32 + 2 * e;
+          const int qi = qt0 + ql;
+          const bool v0 = kok && key <= sg.prefix + qi;
+          const bool v1 = kok && key <= sg.prefix + qi + 1;
+          const float p0 = v0 ? exp2f(__uint_as_float(rs[2 * e]) * a.sl2 - L_[ql]) : 0.f;
+          const float p1 = v1 ? exp2f(__uint_as_float(rs[2 * e + 1]) * a.sl2 - L_[ql + 1]) : 0.f;
+          pp[e] = pack_bf16(p0, p1);
+          pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D_[ql]),
+                            p1 * (__uint_as_float(rp[2 * e + 1]) - D_[ql + 1]));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          *reinterpret_cast<uint4*>(sP + sw128_off(row, 4 * c + q)) =
+              make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]);
+          *reinterpret_cast<uint4*>(sS + sw128_off(row, 4 * c + q)) =
+              make_uint4(pd[4 * q], pd[4 * q + 1], pd[4 * q + 2], pd[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(s_free);
+      fence_async_smem();
+      mbar_arrive(pds_full);
+    }
+    mbar_wait(pds_free, (iters - 1) & 1);
+    tc_fence_after();
+    float* dkr = a.dk_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
+    float* dvr = a.dv_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tdK + lane_off + c * 32, rk);
+      tmem_ld32(tdV + lane_off + c * 32, rv);
+      tmem_ld_wait();
+      if (kok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 ok4 = reinterpret_cast<float4*>(dkr + c * 32)[q];
+          ok4.x += __uint_as_float(rk[4 * q]) * a.scale;
+          ok4.y += __uint_as_float(rk[4 * q + 1]) * a.scale;
+          ok4.z += __uint_as_float(rk[4 * q + 2]) * a.scale;
+          ok4.w += __uint_as_float(rk[4 * q + 3]) * a.scale;
+          reinterpret_cast<float4*>(dkr + c * 32)[q] = ok4;
+          float4 ov = reinterpret_cast<float4*>(dvr + c * 32)[q];
+          ov.x += __uint_as_float(rv[4 * q]);
+          ov.y += __uint_as_float(rv[4 * q + 1]);
+          ov.z += __uint_as_float(rv[4 * q + 2]);
+          ov.w += __uint_as_float(rv[4 * q + 3]);
+          reinterpret_cast<float4*>(dvr + c * 32)[q] = ov;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -328,6 +714,36 @@ cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32
     attr = true;
   }
   attn_fwd_tc_kernel<<<dim3(ntiles, p.H), 192, smem, st>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
+                             int32_t nk, int64_t kv_rows, cudaStream_t st) {
+  if (nq == 0) return cudaSuccess;
+  CUtensorMap mq, mo, mk, mv;
+  if (!map_rows(&mq, p.q, static_cast<uint64_t>(p.H) * DH, static_cast<uint64_t>(p.T), p.q_stride) ||
+      !map_rows(&mo, p.dout, static_cast<uint64_t>(p.H) * DH, static_cast<uint64_t>(p.T), p.dout_stride) ||
+      !map_rows(&mk, p.k, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride) ||
+      !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
+    return cudaErrorInvalidValue;
+  TcBwdArgs a{p.segs, qtiles128, p.lse, p.dsum, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride,
+              p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
+  const size_t smem_dq = 1024 + 7 * kTile + 256;
+  const size_t smem_dkv = 1024 + 6 * kTile + 4 * 256 * 4 + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_dq));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(attn_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem_dkv));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_dsum(p, st);
+  attn_dq_tc_kernel<<<dim3(nq, p.H), 192, smem_dq, st>>>(mq, mo, mk, mv, a);
+  a.tiles = ktiles128;
+  if (nk > 0) attn_dkv_tc_kernel<<<dim3(nk, p.KVH), 192, smem_dkv, st>>>(mq, mo, mk, mv, a);
   return cudaGetLastError();
 }
 

@@ -9,5 +9,10 @@ bool attn_tc_supported(const AttnParams& p);
 // tiles128: 128-query tiles per segment; kv_rows: rows addressable in p.k/p.v.
 cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32_t ntiles, int64_t kv_rows,
                             cudaStream_t st);
+// dsum, then dQ (written) and dK/dV (added into the fp32 accumulators).
+cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
+                             int32_t nk, int64_t kv_rows, cudaStream_t st);
+// D = rowsum(dO * O) (shared with the warp-MMA path, attention.cu)
+cudaError_t attn_dsum(const AttnParams& p, cudaStream_t st);
 
 }  // namespace cfk

@@ -830,7 +830,13 @@ struct Exec {
         own_dk = dkv_local;
       }
       cudaEvent_t t0 = mark();
-      L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
+      if (cfk::attn_tc_supported(p))
+        L(cfk::attn_backward_tc(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
+                                meta<const AttnTile>(cm.o_kt128), static_cast<int32_t>(cm.nkt128),
+                                cm.dependent ? gs->S : T, s),
+          "attn_bwd_tc", 3);
+      else
+        L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
       close(t0, 1, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
       L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
                          m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),

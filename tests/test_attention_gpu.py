@@ -71,9 +71,12 @@ def test_attention_forward(ctx, name, impl):
     assert (lse - L)[:, covered].abs().max().item() < 2e-3
 
 
-@pytest.mark.parametrize("name", ["dependent-prefix", "packed-standalone", "dh64"])
-def test_attention_backward(ctx, name):
+@pytest.mark.parametrize("name", ["dependent-prefix", "packed-standalone", "long-prefix", "dh64"])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_attention_backward(ctx, name, impl):
     c = CASES[name]
+    if impl == 1 and c["dh"] != 128:
+        pytest.skip("tcgen05 path is head_dim 128")
     H, KVH, dh, T, R = c["H"], c["KVH"], c["dh"], c["T"], c["R"]
     q, k, v = _inputs(c, 1)
     g = torch.Generator(device="cuda").manual_seed(7)
@@ -86,7 +89,7 @@ def test_attention_backward(ctx, name):
     torch.cuda.synchronize()
     ctx.attention(0, False, q.data_ptr(), H * dh, k.data_ptr(), v.data_ptr(), KVH * dh, R, o.data_ptr(),
                   lse.data_ptr(), 0, 0, 0, 0, 0, c["segs"], T, H, KVH, dh)
-    ctx.attention(0, True, q.data_ptr(), H * dh, k.data_ptr(), v.data_ptr(), KVH * dh, R, o.data_ptr(),
+    ctx.attention(impl, True, q.data_ptr(), H * dh, k.data_ptr(), v.data_ptr(), KVH * dh, R, o.data_ptr(),
                   lse.data_ptr(), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), KVH * dh,
                   c["segs"], T, H, KVH, dh)
     qf, kf, vf = (x.float().requires_grad_(True) for x in (q, k, v))
