@@ -40,9 +40,16 @@ CHUNK, K_RETAIN = 8192, 1
 METRIC = "tokens/sec on long-tail SFT batch (chunk 8K) at 1/2/4/8 B200; peak HBM GB"
 
 
+WORKLOAD = "c2"  # c2 (the metric's workload) | long | short (profiling slices of it)
+
+
 def block_lengths(seed):
     import paper_2503_02356_b200 as cf
     short = cf.capi.synthesize(999, seed, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
+    if WORKLOAD == "long":
+        return np.array([37888], np.int64)
+    if WORKLOAD == "short":
+        return short.astype(np.int64)
     return np.concatenate([short, [37888]]).astype(np.int64)
 
 
@@ -279,12 +286,14 @@ def run_b200(args):
     r0 = res[-1]
     gemm_tf = sum(r.gemm_flops for r in res) / (sum(r.gemm_ms for r in res) / 1e3) / 1e12
     attn_tf = sum(r.attn_flops for r in res) / max(1e-9, sum(r.attn_ms for r in res) / 1e3) / 1e12
+    attnb_tf = sum(r.attn_bwd_flops for r in res) / max(1e-9, sum(r.attn_bwd_ms for r in res) / 1e3) / 1e12
     gemm_share = sum(r.gemm_ms for r in res) / ms
     attn_share = sum(r.attn_ms for r in res) / ms
+    attnb_share = sum(r.attn_bwd_ms for r in res) / ms
     step_ms = ms_max / args.steps
     value = tokens_all / (step_ms / 1e3)  # tokens of one step over all ranks / slowest rank's step time
     mfu = r0.model_flops * world / (step_ms / 1e3) / 1e12
-    cpu = cpu_reference_sample() if world == 1 else None
+    cpu = cpu_reference_sample() if (world == 1 and not args.no_cpu_baseline) else None
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -303,7 +312,10 @@ def run_b200(args):
                      "achieved": gemm_tf, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
                      "frac": gemm_tf / pk["bf16_tflops_sustained"], "traffic": None,
                      "share_of_step": gemm_share, "peak_kind": "measured sustained (MEASURED_PEAKS.json)",
-                     "attention": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s"}},
+                     "attention_fwd": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s"},
+                     "attention_bwd": {"achieved": attnb_tf, "share_of_step": attnb_share, "unit": "TFLOP/s",
+                                       "note": "algorithmic 8*H*dh FLOP/pair"},
+                     "other_share_of_step": max(0.0, 1 - gemm_share - attn_share - attnb_share)},
         "e2e": {"value": tokens_all / (e2e_max / 1e3 / max(1, args.steps)), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(sum(r.gpu_launches for r in res)),
@@ -329,7 +341,12 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "long", "short"],
+                    help="c2 = the metric's workload; long/short = slices of it for profiling only")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    global WORKLOAD
+    WORKLOAD = args.workload
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -133,9 +133,10 @@ typedef struct cf_run_result {
    * CUDA events on the context stream around every launch of the class */
   double gemm_ms, gemm_flops;
   int64_t gemm_launches;
-  double attn_ms, attn_flops;
+  double attn_ms, attn_flops; /* attention forward */
   int64_t attn_launches;
-  double other_ms;
+  double attn_bwd_ms, attn_bwd_flops; /* attention backward (algorithmic FLOPs) */
+  int64_t attn_bwd_launches;
   int64_t other_launches;
 } cf_run_result;
 

@@ -1,0 +1,247 @@
+// chunkflow_b200.hpp — header-only C++ facade with the reference's API shape
+// (namespace chunkflow, /root/reference/proj/include/chunkflow/) over the
+// C-ABI in chunkflow_b200.h.  A caller of the reference swaps
+//   #include <chunkflow/plan_runner.hpp>   for   #include <chunkflow_b200.hpp>
+// and keeps construct_chunks / schedule_step / validate_plan / run_plan /
+// verify_equivalence call sites; errors are rethrown as the same exception
+// types (ValidationError, ParseError, IoError), CUDA/NCCL failures as
+// std::runtime_error.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "chunkflow_b200.h"
+
+namespace chunkflow_b200 {
+
+class ValidationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ParseError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class IoError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == CF_OK) return;
+  const std::string msg = cf_last_error();
+  if (rc == CF_EVALIDATION) throw ValidationError(msg);
+  if (rc == CF_EPARSE) throw ParseError(msg);
+  if (rc == CF_EIO) throw IoError(msg);
+  throw std::runtime_error(msg);
+}
+
+// --- chunker.hpp:16-37 / scheduler.hpp:17-43 types
+enum class ChunkKind { kStandalone, kDependent };
+enum class ExecKind { kForwardDiscard, kForwardRetain, kBackward };
+
+struct SequenceRecord {  // dataset.hpp:20-27
+  int64_t id = 0;
+  int64_t length = 0;
+  std::vector<int32_t> tokens;
+};
+using SequenceSet = std::vector<SequenceRecord>;
+struct Batch {  // dataset.hpp:75-82
+  int64_t step = 0;
+  std::vector<SequenceRecord> sequences;
+  int64_t global_batch_size = 0;
+};
+
+struct ChunkSegment {
+  int64_t sequence_id = 0, start_token = 0, length = 0;
+};
+struct Chunk {
+  int64_t chunk_id = 0;
+  ChunkKind kind = ChunkKind::kStandalone;
+  std::vector<ChunkSegment> segments;
+  int64_t group_id = -1, index_in_group = -1, total_tokens = 0;
+};
+struct KvActions {
+  bool save_kv = false, read_kv_prefix = false, accumulate_kv_grad = false;
+};
+struct ExecEvent {
+  ExecKind kind = ExecKind::kForwardRetain;
+  int64_t chunk_id = 0, group_id = -1, index_in_group = -1;
+  bool is_recompute = false;
+  KvActions notes;
+};
+struct PlanDiagnostics {
+  int64_t peak_retained_tokens = 0, recompute_token_count = 0;
+  std::vector<std::string> violations;
+};
+
+// Owns the library-side plan handle (chunk plan + its schedule).
+class PlanHandle {
+ public:
+  explicit PlanHandle(cf_plan* p) : p_(p, &cf_plan_destroy) {}
+  cf_plan* get() const { return p_.get(); }
+
+ private:
+  std::shared_ptr<cf_plan> p_;
+};
+
+struct ChunkPlan {
+  int64_t chunk_size = 0;
+  std::vector<Chunk> chunks;
+  std::map<int64_t, std::vector<int64_t>> groups;
+  std::vector<int64_t> ids, lengths;  // the batch it was built from
+};
+struct ExecutionPlan {
+  std::vector<ExecEvent> events;
+  int64_t k = 1, chunk_size = 0;
+  std::map<int64_t, std::vector<int64_t>> groups;
+  std::shared_ptr<PlanHandle> handle;
+};
+
+namespace detail {
+inline std::shared_ptr<PlanHandle> build(const std::vector<int64_t>& ids, const std::vector<int64_t>& lengths,
+                                         int64_t cs, int64_t k) {
+  cf_plan* p = nullptr;
+  check(cf_plan_build(ids.data(), lengths.data(), static_cast<int64_t>(ids.size()), cs, k, &p));
+  return std::make_shared<PlanHandle>(p);
+}
+inline std::map<int64_t, std::vector<int64_t>> groups_of(cf_plan* p) {
+  int64_t nc = 0, ns = 0, ne = 0, ng = 0;
+  check(cf_plan_counts(p, &nc, &ns, &ne, &ng));
+  std::vector<int64_t> gid(static_cast<size_t>(ng) + 1), off(static_cast<size_t>(ng) + 1),
+      mem(static_cast<size_t>(nc) + 1);
+  check(cf_plan_export_groups(p, gid.data(), off.data(), mem.data()));
+  std::map<int64_t, std::vector<int64_t>> out;
+  for (int64_t g = 0; g < ng; ++g) out[gid[g]] = std::vector<int64_t>(mem.begin() + off[g], mem.begin() + off[g + 1]);
+  return out;
+}
+}  // namespace detail
+
+// construct_chunks (chunker.hpp:177)
+inline ChunkPlan construct_chunks(const Batch& batch, int64_t chunk_size) {
+  ChunkPlan plan;
+  plan.chunk_size = chunk_size;
+  for (const SequenceRecord& s : batch.sequences) {
+    plan.ids.push_back(s.id);
+    plan.lengths.push_back(s.length);
+  }
+  auto h = detail::build(plan.ids, plan.lengths, chunk_size, 1);
+  int64_t nc = 0, ns = 0, ne = 0, ng = 0;
+  check(cf_plan_counts(h->get(), &nc, &ns, &ne, &ng));
+  std::vector<cf_chunk_rec> ch(static_cast<size_t>(nc));
+  std::vector<cf_segment_rec> sg(static_cast<size_t>(ns));
+  check(cf_plan_export(h->get(), ch.data(), sg.data(), nullptr, nullptr));
+  for (const cf_chunk_rec& c : ch) {
+    Chunk out;
+    out.chunk_id = c.chunk_id;
+    out.kind = c.kind == CF_CHUNK_STANDALONE ? ChunkKind::kStandalone : ChunkKind::kDependent;
+    out.group_id = c.group_id;
+    out.index_in_group = c.index_in_group;
+    out.total_tokens = c.total_tokens;
+    for (int64_t i = 0; i < c.seg_count; ++i) {
+      const cf_segment_rec& s = sg[static_cast<size_t>(c.seg_offset + i)];
+      out.segments.push_back({s.sequence_id, s.start_token, s.length});
+    }
+    plan.chunks.push_back(std::move(out));
+  }
+  plan.groups = detail::groups_of(h->get());
+  return plan;
+}
+
+// schedule_step (scheduler.hpp:132)
+inline ExecutionPlan schedule_step(const ChunkPlan& chunk_plan, int64_t k) {
+  ExecutionPlan plan;
+  plan.k = k;
+  plan.chunk_size = chunk_plan.chunk_size;
+  plan.handle = detail::build(chunk_plan.ids, chunk_plan.lengths, chunk_plan.chunk_size, k);
+  int64_t nc = 0, ns = 0, ne = 0, ng = 0;
+  check(cf_plan_counts(plan.handle->get(), &nc, &ns, &ne, &ng));
+  std::vector<cf_event_rec> ev(static_cast<size_t>(ne));
+  check(cf_plan_export(plan.handle->get(), nullptr, nullptr, ev.data(), nullptr));
+  for (const cf_event_rec& e : ev) {
+    ExecEvent x;
+    x.kind = static_cast<ExecKind>(e.kind);
+    x.chunk_id = e.chunk_id;
+    x.group_id = e.group_id;
+    x.index_in_group = e.index_in_group;
+    x.is_recompute = e.is_recompute != 0;
+    x.notes = {e.save_kv != 0, e.read_kv_prefix != 0, e.accumulate_kv_grad != 0};
+    plan.events.push_back(x);
+  }
+  plan.groups = chunk_plan.groups;
+  return plan;
+}
+
+// validate_plan (scheduler.hpp:182)
+inline PlanDiagnostics validate_plan(const ExecutionPlan& plan) {
+  cf_plan_diag d{};
+  check(cf_plan_export(plan.handle->get(), nullptr, nullptr, nullptr, &d));
+  PlanDiagnostics out{d.peak_retained_tokens, d.recompute_token_count, {}};
+  for (int64_t i = 0; i < d.num_violations; ++i) {
+    char buf[256];
+    check(cf_plan_violation(plan.handle->get(), i, buf, sizeof(buf)));
+    out.violations.emplace_back(buf);
+  }
+  return out;
+}
+
+// RAII device context + model (ToyModelParams on the GPU).
+class Device {
+ public:
+  explicit Device(int device = 0) {
+    cf_ctx* c = nullptr;
+    check(cf_ctx_create(device, &c));
+    ctx_.reset(c, &cf_ctx_destroy);
+  }
+  cf_ctx* get() const { return ctx_.get(); }
+
+ private:
+  std::shared_ptr<cf_ctx> ctx_;
+};
+
+class Model {
+ public:
+  Model(const Device& dev, const cf_model_cfg& cfg) : dev_(dev) {
+    cf_model* m = nullptr;
+    check(cf_model_create(dev.get(), &cfg, &m));
+    m_.reset(m, &cf_model_destroy);
+  }
+  cf_model* get() const { return m_.get(); }
+  const Device& device() const { return dev_; }
+
+ private:
+  Device dev_;
+  std::shared_ptr<cf_model> m_;
+};
+
+struct RunPlanOptions {  // plan_runner.hpp:49-54
+  bool corrupt_kv_grads = false;
+  double normalizer_override = 0.0;
+};
+
+// run_plan (plan_runner.hpp:67): loss + gradients stay on the device
+// (cf_model_get_grad reads them back in the reference tensor order).
+inline cf_run_result run_plan(const Model& model, const ChunkPlan& /*chunk_plan*/, const ExecutionPlan& exec_plan,
+                              const SequenceSet& batch, const RunPlanOptions& options = {}) {
+  std::vector<int64_t> ids, lengths;
+  std::vector<int32_t> tokens;
+  for (const SequenceRecord& s : batch) {
+    ids.push_back(s.id);
+    lengths.push_back(s.length);
+    if (static_cast<int64_t>(s.tokens.size()) != s.length)
+      throw ValidationError("sequence " + std::to_string(s.id) + " has no token payload");
+    tokens.insert(tokens.end(), s.tokens.begin(), s.tokens.end());
+  }
+  cf_run_opts o{options.corrupt_kv_grads ? 1 : 0, 0, options.normalizer_override};
+  cf_run_result r{};
+  check(cf_run_plan(model.device().get(), model.get(), exec_plan.handle->get(), ids.data(), lengths.data(),
+                    tokens.data(), static_cast<int64_t>(ids.size()), &o, &r));
+  return r;
+}
+
+}  // namespace chunkflow_b200

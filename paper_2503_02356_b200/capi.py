@@ -54,7 +54,8 @@ class RunResult(C.Structure):
                 ("kv_hbm_bytes", C.c_int64), ("model_flops", C.c_double),
                 ("hw_flops", C.c_double), ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
                 ("gemm_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
-                ("attn_launches", C.c_int64), ("other_ms", C.c_double), ("other_launches", C.c_int64)]
+                ("attn_launches", C.c_int64), ("attn_bwd_ms", C.c_double), ("attn_bwd_flops", C.c_double),
+                ("attn_bwd_launches", C.c_int64), ("other_launches", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -197,12 +197,20 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_before();
       mbar_arrive(&s_free[st]);
       const int key0 = j * TK;
+      // tiles entirely below the diagonal of every row of the CTA need no mask
+      const bool full = key0 + TK - 1 <= sg.prefix + tl.first;
       float tmax = -FLT_MAX;
+      if (full) {
 #pragma unroll
-      for (int e = 0; e < 128; ++e) {
-        s[e] = (key0 + e <= lim) ? s[e] * a.sl2 : -FLT_MAX;
-        tmax = fmaxf(tmax, s[e]);
+        for (int e = 0; e < 128; ++e) tmax = fmaxf(tmax, s[e]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 128; ++e) {
+          s[e] = (key0 + e <= lim) ? s[e] : -FLT_MAX;  // exp2 of the masked scores underflows to 0
+          tmax = fmaxf(tmax, s[e]);
+        }
       }
+      tmax *= a.sl2;  // max in the scaled log2 domain (sl2 > 0)
       bool rescale = false;
       float alpha = 1.f;
       if (tmax > m + kRescale || j == 0) {
@@ -215,8 +223,8 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t pk[64];
 #pragma unroll
       for (int e = 0; e < 64; ++e) {
-        const float p0 = s[2 * e] == -FLT_MAX ? 0.f : exp2f(s[2 * e] - m);
-        const float p1 = s[2 * e + 1] == -FLT_MAX ? 0.f : exp2f(s[2 * e + 1] - m);
+        const float p0 = exp2f(fmaf(s[2 * e], a.sl2, -m));
+        const float p1 = exp2f(fmaf(s[2 * e + 1], a.sl2, -m));
         l += p0 + p1;
         pk[e] = pack_bf16(p0, p1);
       }
@@ -411,6 +419,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(s_full, j & 1);
       tc_fence_after();
       const int key0 = j * TK;
+      const bool full = ok && key0 + TK - 1 <= sg.prefix + tl.first;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t rs[32], rp[32];
@@ -421,8 +430,12 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int k0 = key0 + c * 32 + 2 * e;
-          const float p0 = (ok && k0 <= lim) ? exp2f(__uint_as_float(rs[2 * e]) * a.sl2 - lse2) : 0.f;
-          const float p1 = (ok && k0 + 1 <= lim) ? exp2f(__uint_as_float(rs[2 * e + 1]) * a.sl2 - lse2) : 0.f;
+          float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
+          float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
+          if (!full) {
+            p0 = (ok && k0 <= lim) ? p0 : 0.f;
+            p1 = (ok && k0 + 1 <= lim) ? p1 : 0.f;
+          }
           pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
         }
 #pragma unroll
@@ -591,6 +604,8 @@ __global__ void __launch_bounds__(192, 1)
       // s_full(it) is committed after dV/dK of it-1: P^T / dS^T buffers free.
       mbar_wait(s_full, it & 1);
       tc_fence_after();
+      // every (key, query) pair of the tile visible and valid -> no masking
+      const bool full = key_first + TQ - 1 < kv_len && key_first + TQ - 1 <= sg.prefix + qt0 && qt0 + TQ <= sg.len;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t rs[32], rp[32];
@@ -602,10 +617,12 @@ __global__ void __launch_bounds__(192, 1)
         for (int e = 0; e < 16; ++e) {
           const int ql = c * 32 + 2 * e;
           const int qi = qt0 + ql;
-          const bool v0 = kok && key <= sg.prefix + qi;
-          const bool v1 = kok && key <= sg.prefix + qi + 1;
-          const float p0 = v0 ? exp2f(__uint_as_float(rs[2 * e]) * a.sl2 - L_[ql]) : 0.f;
-          const float p1 = v1 ? exp2f(__uint_as_float(rs[2 * e + 1]) * a.sl2 - L_[ql + 1]) : 0.f;
+          float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -L_[ql]));
+          float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -L_[ql + 1]));
+          if (!full) {
+            p0 = (kok && key <= sg.prefix + qi) ? p0 : 0.f;
+            p1 = (kok && key <= sg.prefix + qi + 1) ? p1 : 0.f;
+          }
           pp[e] = pack_bf16(p0, p1);
           pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D_[ql]),
                             p1 * (__uint_as_float(rp[2 * e + 1]) - D_[ql + 1]));

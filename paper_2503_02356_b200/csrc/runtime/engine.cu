@@ -837,7 +837,7 @@ struct Exec {
           "attn_bwd_tc", 3);
       else
         L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
-      close(t0, 1, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
+      close(t0, 2, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
       L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
                          m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
         "dkv_to_dqkv");
@@ -974,8 +974,8 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
   std::vector<double> slots(static_cast<size_t>(nev + 1));
   CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nev + 1) * 8, cudaMemcpyDeviceToHost, ex.s));
   CK(cudaStreamSynchronize(ex.s));
-  double cls_ms[2] = {0, 0}, cls_flops[2] = {0, 0};
-  int64_t cls_n[2] = {0, 0};
+  double cls_ms[3] = {0, 0, 0}, cls_flops[3] = {0, 0, 0};
+  int64_t cls_n[3] = {0, 0, 0};
   for (const auto& r : ex.recs) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, r.a, r.b));
@@ -1024,8 +1024,10 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
     res->attn_ms = cls_ms[1];
     res->attn_flops = cls_flops[1];
     res->attn_launches = cls_n[1];
-    res->other_ms = 0;
-    res->other_launches = ex.launches - cls_n[0] - cls_n[1];
+    res->attn_bwd_ms = cls_ms[2];
+    res->attn_bwd_flops = cls_flops[2];
+    res->attn_bwd_launches = cls_n[2];
+    res->other_launches = ex.launches - cls_n[0] - cls_n[1] - cls_n[2];
   }
 }
 
