@@ -290,12 +290,12 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t 
       } else {
         e = cfk::attn_forward(p, st);
       }
-    } else if (impl == 1) {
+    } else if (impl == 1 || impl == 2) {
       if (!cfk::attn_tc_supported(p)) throw cfb::ValidationError("tcgen05 attention needs head_dim 128");
-      e = cfk::attn_backward_tc(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),
-                                static_cast<int32_t>(q128.second),
-                                reinterpret_cast<const cfk::AttnTile*>(dmeta + k128.first),
-                                static_cast<int32_t>(k128.second), kv_rows, st);
+      auto fn = impl == 1 ? cfk::attn_backward_tc : cfk::attn_backward_tc_v1;
+      e = fn(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first), static_cast<int32_t>(q128.second),
+             reinterpret_cast<const cfk::AttnTile*>(dmeta + k128.first), static_cast<int32_t>(k128.second), kv_rows,
+             st);
     } else {
       e = cfk::attn_backward(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + k64.first),
                              static_cast<int32_t>(k64.second), st);

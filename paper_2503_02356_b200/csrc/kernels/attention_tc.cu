@@ -4,11 +4,14 @@
 // 128-key tiles of the segment's keys [0, prefix + last query] (bottom-right
 // causal mask, KV prefix read straight from the per-sequence cache).
 //
-//   warps 0-3  softmax: thread = query row; tcgen05.ld its S row from TMEM,
-//              online softmax (exp2, lazy O rescale when the running max grows
-//              by > 2^8), P -> bf16 -> 128B-swizzled smem (UMMA A operand)
-//   warp  4    TMA producer: Q once, K/V tiles into a 2-stage ring
-//   warp  5    MMA issuer (one lane): S = Q K^T (M128 N128 K128, K-major x2),
+//   warps 0-7  softmax: thread = (query row, 64-column half of the tile);
+//              tcgen05.ld of its half-row of S from TMEM, row max exchanged
+//              with the partner warp through smem, online softmax (exp2, lazy
+//              O rescale when the running max grows by > 2^8), P -> bf16 ->
+//              128B-swizzled smem (UMMA A operand).  Two softmax warps per SM
+//              sub-partition hide each other's MUFU / TMEM-load latency.
+//   warp  8    TMA producer: Q once, K/V tiles into a 2-stage ring
+//   warp  9    MMA issuer (one lane): S = Q K^T (M128 N128 K128, K-major x2),
 //              O += P V (A = P K-major in smem, B = V N-major view of the same
 //              TMA tile), accumulators in TMEM: S0 | S1 | O (384 of 512 cols)
 // Reference semantics: toy_model.hpp:263-302 (scale 1/sqrt(dh), max-
@@ -68,7 +71,9 @@ __device__ __forceinline__ uint64_t mndesc(uint32_t base, int ks) {
   return umma_desc_sw128(base + ks * 2048, kBox, 1024);
 }
 
-__global__ void __launch_bounds__(192, 1)
+constexpr int kFwdThreads = 320;
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -77,7 +82,8 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sK = sQ + kTile;      // 2 stages
   uint8_t* sV = sK + 2 * kTile;  // 2 stages
   uint8_t* sP = sV + 2 * kTile;  // 1 buffer
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kTile);
+  float* sRed = reinterpret_cast<float*>(sP + kTile);  // [2 parity][2 half][128 rows] row-max / row-sum exchange
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 512);
   uint64_t* q_full = bar;
   uint64_t* k_full = bar + 1;   // [2]
   uint64_t* k_empty = bar + 3;  // [2]
@@ -108,9 +114,9 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
+      mbar_init(&s_free[i], 256);
     }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(p_free, 1);
     fence_mbar_init();
   }
@@ -122,7 +128,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tS[2] = {tmem, tmem + 128};
   const uint32_t tO = tmem + 256;
 
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0) {
       mbar_expect_tx(q_full, kTile);
       tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
@@ -141,7 +147,7 @@ __global__ void __launch_bounds__(192, 1)
         tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], g * DH + 64, krow);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
@@ -175,42 +181,48 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // softmax warps 0..3: TMEM lane quarter = warp, row = warp*32 + lane
-    const int row = warp * 32 + lane;
+    // softmax warps 0..7: TMEM lane quarter = warp & 3, half = warp >> 2
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
     const int qi = tl.first + row;                      // query index in segment
     const int lim = sg.prefix + min(qi, sg.len - 1);    // last visible key
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t col0 = static_cast<uint32_t>(half * 64);
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < nkt; ++j) {
       const int st = j & 1;
       mbar_wait(&s_full[st], (j >> 1) & 1);
       tc_fence_after();
-      float s[128];
+      float s[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t r[32];
-        tmem_ld32(tS[st] + lane_off + c * 32, r);
+        tmem_ld32(tS[st] + lane_off + col0 + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
       }
       tc_fence_before();
       mbar_arrive(&s_free[st]);
-      const int key0 = j * TK;
+      const int key0 = j * TK + half * 64;
       // tiles entirely below the diagonal of every row of the CTA need no mask
-      const bool full = key0 + TK - 1 <= sg.prefix + tl.first;
+      const bool full = j * TK + TK - 1 <= sg.prefix + tl.first;
       float tmax = -FLT_MAX;
       if (full) {
 #pragma unroll
-        for (int e = 0; e < 128; ++e) tmax = fmaxf(tmax, s[e]);
+        for (int e = 0; e < 64; ++e) tmax = fmaxf(tmax, s[e]);
       } else {
 #pragma unroll
-        for (int e = 0; e < 128; ++e) {
+        for (int e = 0; e < 64; ++e) {
           s[e] = (key0 + e <= lim) ? s[e] : -FLT_MAX;  // exp2 of the masked scores underflows to 0
           tmax = fmaxf(tmax, s[e]);
         }
       }
-      tmax *= a.sl2;  // max in the scaled log2 domain (sl2 > 0)
+      // exchange the half-row maxima with the partner warp (same rows)
+      float* red = sRed + (j & 1) * 256;
+      red[half * 128 + row] = tmax;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
+      tmax = fmaxf(tmax, red[(half ^ 1) * 128 + row]) * a.sl2;  // scaled log2 domain (sl2 > 0)
       bool rescale = false;
       float alpha = 1.f;
       if (tmax > m + kRescale || j == 0) {
@@ -220,9 +232,9 @@ __global__ void __launch_bounds__(192, 1)
         m = mn;
       }
       l *= alpha;
-      uint32_t pk[64];
+      uint32_t pk[32];
 #pragma unroll
-      for (int e = 0; e < 64; ++e) {
+      for (int e = 0; e < 32; ++e) {
         const float p0 = exp2f(fmaf(s[2 * e], a.sl2, -m));
         const float p1 = exp2f(fmaf(s[2 * e + 1], a.sl2, -m));
         l += p0 + p1;
@@ -234,33 +246,38 @@ __global__ void __launch_bounds__(192, 1)
       }
       if (rescale) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
-          tmem_ld32(tO + lane_off + c * 32, r);
+          tmem_ld32(tO + lane_off + col0 + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(tO + lane_off + c * 32, r);
+          tmem_st32(tO + lane_off + col0 + c * 32, r);
         }
         tmem_st_wait();
       }
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        *reinterpret_cast<uint4*>(sP + sw128_off(row, c)) =
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sP + sw128_off(row, half * 8 + c)) =
             make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
     }
+    // combine the two half-row sums
+    float* red = sRed + (nkt & 1) * 256;
+    red[half * 128 + row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
+    l += red[(half ^ 1) * 128 + row];
     mbar_wait(p_free, (nkt - 1) & 1);
     tc_fence_after();
     const bool ok = qi < sg.len && row < tl.count;
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + h * DH;
+    __nv_bfloat16* orow = a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + h * DH + half * 64;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
-      tmem_ld32(tO + lane_off + c * 32, r);
+      tmem_ld32(tO + lane_off + col0 + c * 32, r);
       tmem_ld_wait();
       if (ok) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -272,7 +289,7 @@ __global__ void __launch_bounds__(192, 1)
                               pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv));
       }
     }
-    if (ok) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
+    if (ok && half == 0) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -722,7 +739,7 @@ cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32
       !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
     return cudaErrorInvalidValue;
   TcArgs a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
-  const size_t smem = 1024 + 6 * kTile + 256;
+  const size_t smem = 1024 + 6 * kTile + 512 * 4 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -730,11 +747,11 @@ cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  attn_fwd_tc_kernel<<<dim3(ntiles, p.H), 192, smem, st>>>(mq, mk, mv, a);
+  attn_fwd_tc_kernel<<<dim3(ntiles, p.H), kFwdThreads, smem, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
 }
 
-cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
+cudaError_t attn_backward_tc_v1(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
                              int32_t nk, int64_t kv_rows, cudaStream_t st) {
   if (nq == 0) return cudaSuccess;
   CUtensorMap mq, mo, mk, mv;

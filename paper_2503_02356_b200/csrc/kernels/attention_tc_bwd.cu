@@ -1,0 +1,520 @@
+// Pipelined tcgen05 attention backward for head_dim 128 (sm_100a).
+//
+// Same math as the first version (attention_tc.cu: dQ kernel + dK/dV-owner
+// kernel, deterministic, reference toy_model.hpp:436-486), restructured so
+// the tensor core never waits for the softmax warps: the streamed dimension
+// is cut into 64-wide sub-tiles, S/dP live in double-buffered TMEM
+// (2 x 64 columns each), and the MMA issuer runs one sub-tile ahead:
+//
+//   MMA:     S/dP(i+1)  |  [P/dS(i) ready] dQ or dV,dK(i)  |  S/dP(i+2) ...
+//   softmax:      P/dS(i) from TMEM -> bf16 -> swizzled smem  |  P/dS(i+1)
+//
+// TMEM: S0 S1 dP0 dP1 (4 x 64 cols) + accumulators (dQ: 128; dV + dK: 256).
+#include <cfloat>
+
+#include "attention.h"
+#include "attention_tc.h"
+#include "common.cuh"
+
+namespace cfk {
+namespace {
+
+constexpr int DH = 128;
+constexpr int SUB = 64;                     // streamed sub-tile (keys for dQ, queries for dK/dV)
+constexpr uint32_t kBox128 = 128 * 64 * 2;  // [128 rows][64 cols] bf16
+constexpr uint32_t kBox64 = 64 * 64 * 2;    // [64 rows][64 cols]
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct Args {
+  const AttnSeg* segs;
+  const AttnTile* tiles;  // 128-row tiles (queries for dQ, keys for dK/dV)
+  const float* lse;
+  const float* dsum;
+  __nv_bfloat16* dq;
+  int64_t dq_stride;
+  float* dk_acc;
+  float* dv_acc;
+  int64_t acc_stride;
+  int32_t T, H, KVH;
+  float sl2, scale;
+};
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_sync_256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+constexpr int kThreads = 320;
+
+// 16-byte chunk c (0..7) of row r in a [rows][64] SW128 box
+__device__ __forceinline__ uint32_t sw_off(int r, int c) {
+  return static_cast<uint32_t>(r * 128 + ((c ^ (r & 7)) << 4));
+}
+// K-major operand made of boxes of `box` bytes along K (64 elements each)
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, uint32_t box, int ks) {
+  return umma_desc_sw128(base + (ks >> 2) * box + (ks & 3) * 32, 16, 1024);
+}
+// MN-major view: N = 128 (two 64-col slabs `box` bytes apart), K = rows
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, uint32_t box, int ks) {
+  return umma_desc_sw128(base + ks * 2048, box, 1024);
+}
+
+// ------------------------------------------------------------------ dQ
+// CTA = 128 queries x one q head; keys streamed in 64-key sub-tiles.
+__global__ void __launch_bounds__(kThreads, 1)
+    dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+              const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                   // 2 x [128][64]
+  uint8_t* sdO = sQ + 2 * kBox128;    // 2 x [128][64]
+  uint8_t* sK = sdO + 2 * kBox128;    // 3 stages x 2 x [64][64]
+  uint8_t* sV = sK + 3 * 2 * kBox64;  // 3 stages
+  uint8_t* sS = sV + 3 * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * kBox128);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;    // [3]
+  uint64_t* k_empty = bar + 4;   // [3]
+  uint64_t* v_full = bar + 7;    // [3]
+  uint64_t* v_empty = bar + 10;  // [3]
+  uint64_t* s_full = bar + 13;   // [2]
+  uint64_t* s_free = bar + 15;   // [2]
+  uint64_t* ds_full = bar + 17;  // [2]
+  uint64_t* ds_free = bar + 19;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int h = blockIdx.y, g = h / (a.H / a.KVH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q_row0 = sg.q_start + tl.first;
+  const int kv_len = sg.prefix + tl.first + tl.count;
+  const int nkt = (kv_len + SUB - 1) / SUB;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 256);
+      mbar_init(&ds_full[i], 256);
+      mbar_init(&ds_free[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 64};
+  const uint32_t tP[2] = {tmem + 128, tmem + 192};
+  const uint32_t tQ = tmem + 256;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 4 * kBox128);
+      tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
+      tma_load_2d(sQ + kBox128, &tmQ, q_full, h * DH + 64, q_row0);
+      tma_load_2d(sdO, &tmO, q_full, h * DH, q_row0);
+      tma_load_2d(sdO + kBox128, &tmO, q_full, h * DH + 64, q_row0);
+      for (int j = 0; j < nkt; ++j) {
+        const int st = j % 3;
+        const uint32_t ph = (j / 3) & 1;
+        const int krow = sg.kv_row0 + j * SUB;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_expect_tx(&k_full[st], 2 * kBox64);
+        tma_load_2d(sK + st * 2 * kBox64, &tmK, &k_full[st], g * DH, krow);
+        tma_load_2d(sK + st * 2 * kBox64 + kBox64, &tmK, &k_full[st], g * DH + 64, krow);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_expect_tx(&v_full[st], 2 * kBox64);
+        tma_load_2d(sV + st * 2 * kBox64, &tmV, &v_full[st], g * DH, krow);
+        tma_load_2d(sV + st * 2 * kBox64 + kBox64, &tmV, &v_full[st], g * DH + 64, krow);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S, dP: N = 64 keys
+      constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);  // dQ: N = dh, B = K (MN-major view)
+      const uint32_t q0 = smem_u32(sQ), o0 = smem_u32(sdO);
+      auto issue_s = [&](int j) {
+        const int st = j % 3, b = j & 1;
+        const uint32_t ph = (j / 3) & 1;
+        mbar_wait(&k_full[st], ph);
+        mbar_wait(&v_full[st], ph);
+        mbar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(sK + st * 2 * kBox64), v0 = smem_u32(sV + st * 2 * kBox64);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16(tS[b], kdesc(q0, kBox128, ks), kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16(tP[b], kdesc(o0, kBox128, ks), kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(&v_empty[st]);
+        umma_commit(&s_full[b]);
+      };
+      mbar_wait(q_full, 0);
+      issue_s(0);
+      for (int j = 0; j < nkt; ++j) {
+        if (j + 1 < nkt) issue_s(j + 1);
+        const int st = j % 3, b = j & 1;
+        mbar_wait(&ds_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s0 = smem_u32(sS + b * kBox128), k0 = smem_u32(sK + st * 2 * kBox64);
+#pragma unroll
+        for (int ks = 0; ks < SUB / 16; ++ks)
+          umma_bf16(tQ, kdesc(s0, kBox128, ks), mndesc(k0, kBox64, ks), idQ, (j > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&k_empty[st]);
+        umma_commit(&ds_free[b]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3, half = warp >> 2;  // half: which 32 of the 64 key columns
+    const int row = quarter * 32 + lane;
+    const int qi = tl.first + row;
+    const bool ok = qi < sg.len && row < tl.count;
+    const int lim = sg.prefix + min(qi, sg.len - 1);
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
+    const float D = ok ? a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] : 0.f;
+    for (int j = 0; j < nkt; ++j) {
+      const int b = j & 1;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32(tS[b] + lane_off + half * 32, rs);
+      tmem_ld32(tP[b] + lane_off + half * 32, rp);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[b]);
+      const int key0 = j * SUB + half * 32;
+      const bool full = ok && j * SUB + SUB - 1 <= sg.prefix + tl.first;
+      uint32_t pk[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int k0 = key0 + 2 * e;
+        float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
+        float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
+        if (!full) {
+          p0 = (ok && k0 <= lim) ? p0 : 0.f;
+          p1 = (ok && k0 + 1 <= lim) ? p1 : 0.f;
+        }
+        pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
+      }
+      if (j >= 2) mbar_wait(&ds_free[b], ((j >> 1) & 1) ^ 1);
+      uint8_t* dst = sS + b * kBox128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(dst + sw_off(row, half * 4 + c)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_async_smem();
+      mbar_arrive(&ds_full[b]);
+    }
+    const int last = nkt - 1;
+    mbar_wait(&ds_free[last & 1], (last >> 1) & 1);
+    tc_fence_after();
+    __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int c = half * 2 + cc;  // 32-column chunk of dQ
+      uint32_t r[32];
+      tmem_ld32(tQ + lane_off + c * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(out + c * 32);
+        const float sc = a.scale;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          d4[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * sc, __uint_as_float(r[8 * q + 1]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 2]) * sc, __uint_as_float(r[8 * q + 3]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 4]) * sc, __uint_as_float(r[8 * q + 5]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------- dK / dV
+// CTA = 128 keys x one kv head (sole owner of those rows); queries streamed
+// in 64-query sub-tiles over every q head of the GQA group.
+__global__ void __launch_bounds__(kThreads, 1)
+    dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;                     // 2 x [128][64]
+  uint8_t* sV = sK + 2 * kBox128;       // 2 x [128][64]
+  uint8_t* sQ = sV + 2 * kBox128;       // 2 stages x 2 x [64][64]
+  uint8_t* sdO = sQ + 2 * 2 * kBox64;   // 2 stages x 2 x [64][64]
+  uint8_t* sP = sdO + 2 * 2 * kBox64;   // 2 x [128 keys][64 q]
+  uint8_t* sS = sP + 2 * kBox128;       // 2 x [128 keys][64 q]
+  float* sL = reinterpret_cast<float*>(sS + 2 * kBox128);  // [2][64]
+  float* sD = sL + 128;                                    // [2][64]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 128);
+  uint64_t* kv_full = bar;
+  uint64_t* q_full = bar + 1;     // [2]
+  uint64_t* q_empty = bar + 3;    // [2]
+  uint64_t* s_full = bar + 5;     // [2]
+  uint64_t* s_free = bar + 7;     // [2]
+  uint64_t* pds_full = bar + 9;   // [2]
+  uint64_t* pds_free = bar + 11;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int g = blockIdx.y, per = a.H / a.KVH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int key_first = tl.first;
+  const int kv_len = sg.prefix + sg.len;
+  const int i0 = max(0, key_first - sg.prefix);
+  const int nqt = (sg.len - i0 + SUB - 1) / SUB;
+  const int iters = per * nqt;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 256);
+      mbar_init(&pds_full[i], 256);
+      mbar_init(&pds_free[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 64};
+  const uint32_t tP[2] = {tmem + 128, tmem + 192};
+  const uint32_t tdV = tmem + 256, tdK = tmem + 384;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      const int krow = sg.kv_row0 + key_first;
+      mbar_expect_tx(kv_full, 4 * kBox128);
+      tma_load_2d(sK, &tmK, kv_full, g * DH, krow);
+      tma_load_2d(sK + kBox128, &tmK, kv_full, g * DH + 64, krow);
+      tma_load_2d(sV, &tmV, kv_full, g * DH, krow);
+      tma_load_2d(sV + kBox128, &tmV, kv_full, g * DH + 64, krow);
+      for (int it = 0; it < iters; ++it) {
+        const int b = it & 1;
+        const int hq = g * per + it / nqt;
+        const int qrow = sg.q_start + i0 + (it % nqt) * SUB;
+        mbar_wait(&q_empty[b], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[b], 4 * kBox64);
+        uint8_t* q = sQ + b * 2 * kBox64;
+        uint8_t* o = sdO + b * 2 * kBox64;
+        tma_load_2d(q, &tmQ, &q_full[b], hq * DH, qrow);
+        tma_load_2d(q + kBox64, &tmQ, &q_full[b], hq * DH + 64, qrow);
+        tma_load_2d(o, &tmO, &q_full[b], hq * DH, qrow);
+        tma_load_2d(o + kBox64, &tmO, &q_full[b], hq * DH + 64, qrow);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S^T, dP^T: N = 64 queries
+      constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);  // dV, dK: N = dh, B MN-major view
+      const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV);
+      auto issue_s = [&](int it) {
+        const int b = it & 1;
+        mbar_wait(&q_full[b], (it >> 1) & 1);
+        mbar_wait(&s_free[b], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q0 = smem_u32(sQ + b * 2 * kBox64), o0 = smem_u32(sdO + b * 2 * kBox64);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16(tS[b], kdesc(k0, kBox128, ks), kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16(tP[b], kdesc(v0, kBox128, ks), kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(&s_full[b]);
+      };
+      mbar_wait(kv_full, 0);
+      issue_s(0);
+      for (int it = 0; it < iters; ++it) {
+        if (it + 1 < iters) issue_s(it + 1);
+        const int b = it & 1;
+        mbar_wait(&pds_full[b], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q0 = smem_u32(sQ + b * 2 * kBox64), o0 = smem_u32(sdO + b * 2 * kBox64);
+        const uint32_t p0 = smem_u32(sP + b * kBox128), s0 = smem_u32(sS + b * kBox128);
+#pragma unroll
+        for (int ks = 0; ks < SUB / 16; ++ks)
+          umma_bf16(tdV, kdesc(p0, kBox128, ks), mndesc(o0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < SUB / 16; ++ks)
+          umma_bf16(tdK, kdesc(s0, kBox128, ks), mndesc(q0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+        umma_commit(&q_empty[b]);
+        umma_commit(&pds_free[b]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3, half = warp >> 2;  // half: which 32 of the 64 query columns
+    const int row = quarter * 32 + lane;                // key row within the tile
+    const int key = key_first + row;
+    const bool kok = row < tl.count && key < kv_len;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    for (int it = 0; it < iters; ++it) {
+      const int b = it & 1;
+      const int hq = g * per + it / nqt;
+      const int qt0 = i0 + (it % nqt) * SUB;
+      float* L_ = sL + b * 64;
+      float* D_ = sD + b * 64;
+      if (half == 0 && row < SUB) {
+        const int qi = qt0 + row;
+        const bool qok = qi < sg.len;
+        const int64_t idx = static_cast<int64_t>(hq) * a.T + sg.q_start + qi;
+        L_[row] = qok ? a.lse[idx] * kLog2e : INFINITY;
+        D_[row] = qok ? a.dsum[idx] : 0.f;
+      }
+      named_sync_256();
+      mbar_wait(&s_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32(tS[b] + lane_off + half * 32, rs);
+      tmem_ld32(tP[b] + lane_off + half * 32, rp);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_free[b]);
+      const bool full = key_first + 127 < kv_len && key_first + 127 <= sg.prefix + qt0 && qt0 + SUB <= sg.len;
+      uint32_t pp[16], pd[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int ql = half * 32 + 2 * e;
+        const int qi = qt0 + ql;
+        float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -L_[ql]));
+        float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -L_[ql + 1]));
+        if (!full) {
+          p0 = (kok && key <= sg.prefix + qi) ? p0 : 0.f;
+          p1 = (kok && key <= sg.prefix + qi + 1) ? p1 : 0.f;
+        }
+        pp[e] = pack_bf16(p0, p1);
+        pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D_[ql]), p1 * (__uint_as_float(rp[2 * e + 1]) - D_[ql + 1]));
+      }
+      if (it >= 2) mbar_wait(&pds_free[b], ((it >> 1) & 1) ^ 1);
+      uint8_t* dP_ = sP + b * kBox128;
+      uint8_t* dS_ = sS + b * kBox128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        *reinterpret_cast<uint4*>(dP_ + sw_off(row, half * 4 + c)) = make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
+        *reinterpret_cast<uint4*>(dS_ + sw_off(row, half * 4 + c)) = make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&pds_full[b]);
+    }
+    const int last = iters - 1;
+    mbar_wait(&pds_free[last & 1], (last >> 1) & 1);
+    tc_fence_after();
+    float* dkr = a.dk_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
+    float* dvr = a.dv_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+      const int c = half * 2 + cc;
+      uint32_t rk[32], rv[32];
+      tmem_ld32(tdK + lane_off + c * 32, rk);
+      tmem_ld32(tdV + lane_off + c * 32, rv);
+      tmem_ld_wait();
+      if (kok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 k4 = reinterpret_cast<float4*>(dkr + c * 32)[q];
+          k4.x += __uint_as_float(rk[4 * q]) * a.scale;
+          k4.y += __uint_as_float(rk[4 * q + 1]) * a.scale;
+          k4.z += __uint_as_float(rk[4 * q + 2]) * a.scale;
+          k4.w += __uint_as_float(rk[4 * q + 3]) * a.scale;
+          reinterpret_cast<float4*>(dkr + c * 32)[q] = k4;
+          float4 v4 = reinterpret_cast<float4*>(dvr + c * 32)[q];
+          v4.x += __uint_as_float(rv[4 * q]);
+          v4.y += __uint_as_float(rv[4 * q + 1]);
+          v4.z += __uint_as_float(rv[4 * q + 2]);
+          v4.w += __uint_as_float(rv[4 * q + 3]);
+          reinterpret_cast<float4*>(dvr + c * 32)[q] = v4;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<EncodeFn>(p);
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {64, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
+                             int32_t nk, int64_t kv_rows, cudaStream_t st) {
+  if (nq == 0) return cudaSuccess;
+  const uint64_t qc = static_cast<uint64_t>(p.H) * DH, kc = static_cast<uint64_t>(p.KVH) * DH;
+  CUtensorMap q128, o128, k64, v64, q64, o64, k128, v128;
+  if (!map_rows(&q128, p.q, qc, p.T, p.q_stride, 128) || !map_rows(&o128, p.dout, qc, p.T, p.dout_stride, 128) ||
+      !map_rows(&k64, p.k, kc, kv_rows, p.kv_stride, 64) || !map_rows(&v64, p.v, kc, kv_rows, p.kv_stride, 64) ||
+      !map_rows(&q64, p.q, qc, p.T, p.q_stride, 64) || !map_rows(&o64, p.dout, qc, p.T, p.dout_stride, 64) ||
+      !map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
+    return cudaErrorInvalidValue;
+  Args a{p.segs, qtiles128, p.lse, p.dsum, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride,
+         p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
+  const size_t smem_dq = 1024 + 4 * kBox128 + 12 * kBox64 + 2 * kBox128 + 256;
+  const size_t smem_dkv = 1024 + 4 * kBox128 + 8 * kBox64 + 4 * kBox128 + 4 * 128 * 4 + 128;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem_dq));
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dkv));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaError_t e = attn_dsum(p, st);
+  if (e != cudaSuccess) return e;
+  dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
+  a.tiles = ktiles128;
+  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kThreads, smem_dkv, st>>>(q64, o64, k128, v128, a);
+  return cudaGetLastError();
+}
+
+}  // namespace cfk

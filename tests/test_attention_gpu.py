@@ -72,10 +72,10 @@ def test_attention_forward(ctx, name, impl):
 
 
 @pytest.mark.parametrize("name", ["dependent-prefix", "packed-standalone", "long-prefix", "dh64"])
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 def test_attention_backward(ctx, name, impl):
     c = CASES[name]
-    if impl == 1 and c["dh"] != 128:
+    if impl in (1, 2) and c["dh"] != 128:
         pytest.skip("tcgen05 path is head_dim 128")
     H, KVH, dh, T, R = c["H"], c["KVH"], c["dh"], c["T"], c["R"]
     q, k, v = _inputs(c, 1)
