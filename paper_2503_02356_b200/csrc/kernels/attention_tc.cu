@@ -219,15 +219,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
       }
       // exchange the half-row maxima with the partner warp (same rows)
-      float* red = sRed + (j & 1) * 256;
-      red[half * 128 + row] = tmax;
+      const uint32_t red = smem_u32(sRed) + (j & 1) * 1024;
+      sts_f32(red + (half * 128 + row) * 4, tmax);
       asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
-      tmax = fmaxf(tmax, red[(half ^ 1) * 128 + row]) * a.sl2;  // scaled log2 domain (sl2 > 0)
+      tmax = fmaxf(tmax, lds_f32(red + ((half ^ 1) * 128 + row) * 4)) * a.sl2;  // scaled log2 domain (sl2 > 0)
       bool rescale = false;
       float alpha = 1.f;
       if (tmax > m + kRescale || j == 0) {
         const float mn = fmaxf(m, tmax);
-        alpha = exp2f(m - mn);
+        alpha = ex2(m - mn);
         rescale = j > 0;
         m = mn;
       }
@@ -235,8 +235,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       uint32_t pk[32];
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        const float p0 = exp2f(fmaf(s[2 * e], a.sl2, -m));
-        const float p1 = exp2f(fmaf(s[2 * e + 1], a.sl2, -m));
+        const float p0 = ex2(fmaf(s[2 * e], a.sl2, -m));
+        const float p1 = ex2(fmaf(s[2 * e + 1], a.sl2, -m));
         l += p0 + p1;
         pk[e] = pack_bf16(p0, p1);
       }
@@ -256,19 +256,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         tmem_st_wait();
       }
+      const uint32_t p_s = smem_u32(sP);
 #pragma unroll
       for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(sP + sw128_off(row, half * 8 + c)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        sts128(p_s + sw128_off(row, half * 8 + c), make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
     }
     // combine the two half-row sums
-    float* red = sRed + (nkt & 1) * 256;
-    red[half * 128 + row] = l;
+    const uint32_t red = smem_u32(sRed) + (nkt & 1) * 1024;
+    sts_f32(red + (half * 128 + row) * 4, l);
     asm volatile("bar.sync %0, 64;" ::"r"(2 + quarter) : "memory");
-    l += red[(half ^ 1) * 128 + row];
+    l += lds_f32(red + ((half ^ 1) * 128 + row) * 4);
     mbar_wait(p_free, (nkt - 1) & 1);
     tc_fence_after();
     const bool ok = qi < sg.len && row < tl.count;

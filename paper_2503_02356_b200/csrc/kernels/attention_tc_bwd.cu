@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int k0 = key0 + 2 * e;
-        float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
-        float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
+        float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
+        float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
         if (!full) {
           p0 = (ok && k0 <= lim) ? p0 : 0.f;
           p1 = (ok && k0 + 1 <= lim) ? p1 : 0.f;
@@ -209,11 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
       }
       if (j >= 2) mbar_wait(&ds_free[b], ((j >> 1) & 1) ^ 1);
-      uint8_t* dst = sS + b * kBox128;
+      const uint32_t dst = smem_u32(sS) + b * kBox128;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        *reinterpret_cast<uint4*>(dst + sw_off(row, half * 4 + c)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        sts128(dst + sw_off(row, half * 4 + c), make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
       fence_async_smem();
       mbar_arrive(&ds_full[b]);
     }
@@ -378,14 +377,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int b = it & 1;
       const int hq = g * per + it / nqt;
       const int qt0 = i0 + (it % nqt) * SUB;
-      float* L_ = sL + b * 64;
-      float* D_ = sD + b * 64;
+      const uint32_t L_ = smem_u32(sL) + b * 256, D_ = smem_u32(sD) + b * 256;
       if (half == 0 && row < SUB) {
         const int qi = qt0 + row;
         const bool qok = qi < sg.len;
         const int64_t idx = static_cast<int64_t>(hq) * a.T + sg.q_start + qi;
-        L_[row] = qok ? a.lse[idx] * kLog2e : INFINITY;
-        D_[row] = qok ? a.dsum[idx] : 0.f;
+        sts_f32(L_ + row * 4, qok ? a.lse[idx] * kLog2e : INFINITY);
+        sts_f32(D_ + row * 4, qok ? a.dsum[idx] : 0.f);
       }
       named_sync_256();
       mbar_wait(&s_full[b], (it >> 1) & 1);
@@ -402,22 +400,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int e = 0; e < 16; ++e) {
         const int ql = half * 32 + 2 * e;
         const int qi = qt0 + ql;
-        float p0 = exp2f(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -L_[ql]));
-        float p1 = exp2f(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -L_[ql + 1]));
+        const float l0 = lds_f32(L_ + ql * 4), l1 = lds_f32(L_ + ql * 4 + 4);
+        const float d0 = lds_f32(D_ + ql * 4), d1 = lds_f32(D_ + ql * 4 + 4);
+        float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -l0));
+        float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -l1));
         if (!full) {
           p0 = (kok && key <= sg.prefix + qi) ? p0 : 0.f;
           p1 = (kok && key <= sg.prefix + qi + 1) ? p1 : 0.f;
         }
         pp[e] = pack_bf16(p0, p1);
-        pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D_[ql]), p1 * (__uint_as_float(rp[2 * e + 1]) - D_[ql + 1]));
+        pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - d0), p1 * (__uint_as_float(rp[2 * e + 1]) - d1));
       }
       if (it >= 2) mbar_wait(&pds_free[b], ((it >> 1) & 1) ^ 1);
-      uint8_t* dP_ = sP + b * kBox128;
-      uint8_t* dS_ = sS + b * kBox128;
+      const uint32_t dP_ = smem_u32(sP) + b * kBox128, dS_ = smem_u32(sS) + b * kBox128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        *reinterpret_cast<uint4*>(dP_ + sw_off(row, half * 4 + c)) = make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
-        *reinterpret_cast<uint4*>(dS_ + sw_off(row, half * 4 + c)) = make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]);
+        sts128(dP_ + sw_off(row, half * 4 + c), make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]));
+        sts128(dS_ + sw_off(row, half * 4 + c), make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
       }
       fence_async_smem();
       mbar_arrive(&pds_full[b]);
