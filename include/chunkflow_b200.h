@@ -268,6 +268,10 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q,
                     const void* dout, void* dq, float* dk_acc, float* dv_acc,
                     int64_t acc_stride, const int32_t* segs, int64_t nseg,
                     int64_t T, int64_t H, int64_t KVH, int64_t dh);
+/* GEMM kernel selection (testing / A-B measurement): 0 = auto (CTA-pair
+ * tcgen05.mma.cta_group::2 kernel for large GEMMs), 1 = single-CTA kernel
+ * only, 2 = CTA pairs whenever M, N > 128. */
+int cf_debug_set_gemm_mode(int mode);
 int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
                const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
                int64_t m, int64_t n, int64_t k, int epi, const void* residual,

@@ -73,7 +73,7 @@ EXPORTS = [
     "cf_model_tensor_info", "cf_model_get_param", "cf_model_set_param",
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
-    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention",
+    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None

@@ -318,3 +318,10 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda, const void
 }
 
 }  // extern "C"
+
+extern "C" int cf_debug_set_gemm_mode(int mode) {
+  return cfb::guard([&] {
+    if (mode < 0 || mode > 2) throw cfb::ValidationError("gemm mode must be 0, 1 or 2");
+    cfk::set_gemm_mode(mode);
+  });
+}

@@ -15,7 +15,9 @@
 //   warps 4-7   epilogue                   tcgen05.ld -> fused op -> global
 // The epilogue of tile i overlaps the main loop of tile i+1 through the two
 // TMEM accumulators (tmem_full / tmem_empty mbarriers).
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -249,6 +251,217 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ----------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 tile.  CTA r loads A rows [m0 + 128r, +128) and B rows (N) [n0 +
+// 128r, +128); the leader issues tcgen05.mma.cta_group::2 (M256 N256 K16) and
+// each CTA's TMEM receives its own 128 rows x 256 columns.  Per SM this halves
+// the shared-memory bytes written by TMA and read by the tensor core per FLOP
+// (64 + 64 B/clk instead of 96 + 96 B/clk at full MMA rate), which is what
+// caps the single-CTA kernel at ~2/3 of the per-clock tensor peak.
+namespace pair {
+
+constexpr int kStages = 6;
+constexpr uint32_t kABytes = 128 * BK * 2;  // this CTA's half of A
+constexpr uint32_t kBBytes = 128 * BK * 2;  // this CTA's half of B
+constexpr size_t kSmem = 1024 + kStages * (kABytes + kBBytes) + 256;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // clear the CTA-pair bit -> leader's smem address
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t leader_addr(uint32_t local) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+  return r;
+}
+// Relaxed remote arrive: no data is published through these barriers (TMA
+// bytes are tracked by the transaction count, TMEM reads are ordered by the
+// tcgen05 fences), and a release.cluster arrive costs a GPU-scope MEMBAR.
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+template <bool A_MN, bool B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 2);  // leader arrive.expect_tx + peer remote arrive
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // one arrive per epilogue warp of both CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_tiles = g.num_m * g.num_n;  // num_m counts 256-row pair tiles
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full_leader0 = leader_addr(smem_u32(&full[0]));
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int mb = tile % g.num_m, nb = tile / g.num_m;
+        const int m0 = mb * 256 + static_cast<int>(rank) * 128;
+        const int n0 = nb * 256 + static_cast<int>(rank) * 128;
+        for (int kb = 0; kb < g.num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* a = sA + stage * kABytes;
+          uint8_t* b = sB + stage * kBBytes;
+          if (leader)
+            mbar_expect_tx(&full[stage], 2 * (kABytes + kBBytes));
+          else
+            arrive_remote(full_leader0 + stage * 8);
+          if constexpr (!A_MN) {
+            tma_load_2sm(a, &tmA, &full[stage], kb * BK, m0);
+          } else {
+            tma_load_2sm(a, &tmA, &full[stage], m0, kb * BK);
+            tma_load_2sm(a + kSlab, &tmA, &full[stage], m0 + 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2sm(b, &tmB, &full[stage], kb * BK, n0);
+          } else {
+            tma_load_2sm(b, &tmB, &full[stage], n0, kb * BK);
+            tma_load_2sm(b + kSlab, &tmB, &full[stage], n0 + 64, kb * BK);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(256, 256, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * 256);
+        for (int kb = 0; kb < g.num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kABytes);
+          const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = A_MN ? umma_desc_sw128(a0 + k * 2048, kSlab, 1024) : umma_desc_sw128(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b0 + k * 2048, kSlab, 1024) : umma_desc_sw128(b0 + k * 32, 16, 1024);
+            umma2(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          commit2_mc(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        commit2_mc(&tfull[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t tempty_leader0 = leader_addr(smem_u32(&tempty[0]));
+    for (int tile = pair; tile < num_tiles; tile += npairs) {
+      const int mb = tile % g.num_m, nb = tile / g.num_m;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * 256 + static_cast<int>(rank) * 128 + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * 256);
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (c == 7) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+        }
+        const int col0 = nb * 256 + c * 32;
+        if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+  }
+}
+
+}  // namespace pair
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -318,6 +531,56 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  bool ok = A_MN ? make_map(&ta, d.a, d.M, d.K, d.lda, 64, 64) : make_map(&ta, d.a, d.K, d.M, d.lda, BK, 128);
+  ok = ok && (B_MN ? make_map(&tb, d.b, d.N, d.K, d.ldb, 64, 64) : make_map(&tb, d.b, d.K, d.N, d.ldb, BK, 128));
+  if (!ok) return cudaErrorInvalidValue;
+  Args g;
+  g.M = static_cast<int>(d.M);
+  g.N = static_cast<int>(d.N);
+  g.K = static_cast<int>(d.K);
+  g.num_m = static_cast<int>((d.M + 255) / 256);
+  g.num_n = static_cast<int>((d.N + 255) / 256);
+  g.num_k = static_cast<int>((d.K + BK - 1) / BK);
+  g.C = d.c;
+  g.ldc = d.ldc;
+  g.R = d.r;
+  g.ldr = d.ldr;
+  auto kern = pair::gemm_pair_kernel<A_MN, B_MN, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pair::kSmem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles = g.num_m * g.num_n;
+  const int pairs = std::min(tiles, gemm_num_sms() / 2);
+  kern<<<2 * pairs, 256, pair::kSmem, st>>>(ta, tb, g);
+  return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t pair_by_epi(const GemmDesc& d, cudaStream_t st) {
+  switch (d.epi) {
+    case EPI_BF16: return launch_pair<A_MN, B_MN, EPI_BF16>(d, st);
+    case EPI_F32: return launch_pair<A_MN, B_MN, EPI_F32>(d, st);
+    case EPI_F32_ACC: return launch_pair<A_MN, B_MN, EPI_F32_ACC>(d, st);
+    case EPI_F32_RES: return launch_pair<A_MN, B_MN, EPI_F32_RES>(d, st);
+    case EPI_BF16_TANH: return launch_pair<A_MN, B_MN, EPI_BF16_TANH>(d, st);
+    case EPI_BF16_TANHGRAD: return launch_pair<A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t pair_by_major(const GemmDesc& d, cudaStream_t st) {
+  if (d.a_kmajor && d.b_kmajor) return pair_by_epi<false, false>(d, st);
+  if (d.a_kmajor && !d.b_kmajor) return pair_by_epi<false, true>(d, st);
+  if (!d.a_kmajor && !d.b_kmajor) return pair_by_epi<true, true>(d, st);
+  return pair_by_epi<true, false>(d, st);
+}
+
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t by_epi(const GemmDesc& d, cudaStream_t st) {
   switch (d.epi) {
@@ -357,9 +620,25 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
       (d.ldb % 8) || (reinterpret_cast<uintptr_t>(d.c) & 15) || (d.ldc % 8))
     return cudaErrorMisalignedAddress;
   const int64_t sms = gemm_num_sms();
+  const int mode = gemm_mode();
+  // CTA pairs for the large GEMMs (the step's hot path); single-CTA tiles for
+  // narrow / short problems where a 256 x 256 pair tile would idle.
+  const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
+  if (mode != 1 && d.M > 128 && d.N > 128 && (pair_tiles >= sms / 4 || mode == 2)) return pair_by_major(d, st);
   const int64_t tiles256 = ((d.M + BM - 1) / BM) * ((d.N + 255) / 256);
   const bool wide = d.N > 128 && tiles256 >= sms;
   return wide ? by_major<256>(d, st) : by_major<128>(d, st);
 }
+
+// 0 = auto (CTA pairs when large), 1 = single-CTA only, 2 = CTA pairs whenever M, N > 128 (tests).
+int& gemm_mode_ref() {
+  static int m = [] {
+    const char* e = std::getenv("CF_GEMM_MODE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return m;
+}
+int gemm_mode() { return gemm_mode_ref(); }
+void set_gemm_mode(int m) { gemm_mode_ref() = m; }
 
 }  // namespace cfk

@@ -32,5 +32,8 @@ struct GemmDesc {
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
 int gemm_num_sms();
+// 0 = auto (CTA-pair kernel for large GEMMs), 1 = single-CTA kernel only.
+int gemm_mode();
+void set_gemm_mode(int mode);
 
 }  // namespace cfk

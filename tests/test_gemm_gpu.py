@@ -7,7 +7,7 @@ import paper_2503_02356_b200.capi as capi
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(128, 256, 64), (296, 520, 200), (1024, 1536, 1024), (24, 40, 16), (256, 2000, 512)]
+SHAPES = [(128, 256, 64), (296, 520, 200), (1024, 1536, 1024), (24, 40, 16), (256, 2000, 512), (8192, 1536, 4096)]
 
 
 def _mk(rows, cols, seed):
@@ -15,10 +15,17 @@ def _mk(rows, cols, seed):
     return (torch.randn(rows, cols, generator=g, device="cuda") * 0.5).to(torch.bfloat16)
 
 
+@pytest.fixture(params=[1, 2], ids=["single-cta", "cta-pair"])
+def gemm_mode(request):
+    capi.check(capi.lib().cf_debug_set_gemm_mode(request.param))
+    yield request.param
+    capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+
+
 @pytest.mark.parametrize("a_k", [1, 0])
 @pytest.mark.parametrize("b_k", [1, 0])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_gemm_majors(ctx, a_k, b_k, shape):
+def test_gemm_majors(ctx, gemm_mode, a_k, b_k, shape):
     M, N, K = shape
     A = _mk(M, K, 1) if a_k else _mk(K, M, 1)   # stored [M,K] or [K,M]
     B = _mk(N, K, 2) if b_k else _mk(K, N, 2)   # stored [N,K] or [K,N]
@@ -36,7 +43,7 @@ def test_gemm_majors(ctx, a_k, b_k, shape):
 
 @pytest.mark.parametrize("epi", [capi.EPI_BF16, capi.EPI_F32_ACC, capi.EPI_F32_RES, capi.EPI_BF16_TANH,
                                  capi.EPI_BF16_TANHGRAD])
-def test_gemm_epilogues(ctx, epi):
+def test_gemm_epilogues(ctx, gemm_mode, epi):
     M, N, K = 384, 768, 320
     A = _mk(M, K, 3)
     B = _mk(K, N, 4)  # reference [in,out] weight layout (N-major B)
@@ -58,7 +65,7 @@ def test_gemm_epilogues(ctx, epi):
     assert err < (1e-2 if C.dtype == torch.bfloat16 else 1e-5), err
 
 
-def test_gemm_residual_aliases_output(ctx):
+def test_gemm_residual_aliases_output(ctx, gemm_mode):
     """x += O @ Wo with the residual read and written in place (EPI_F32_RES)."""
     M, N, K = 257, 512, 512
     A = _mk(M, K, 5)
