@@ -32,9 +32,13 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescale = 8.0f;  // log2 threshold for lazy O rescaling
 
+constexpr int KVS = 3;  // forward K/V ring depth
+
 struct TcArgs {
   const AttnSeg* segs;
   const AttnTile* tiles;  // 128-row query tiles
+  const __nv_bfloat16* q;
+  int64_t q_stride;
   __nv_bfloat16* o;
   int64_t o_stride;
   float* lse;
@@ -78,22 +82,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmV, TcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;
-  uint8_t* sK = sQ + kTile;      // 2 stages
-  uint8_t* sV = sK + 2 * kTile;  // 2 stages
-  uint8_t* sP = sV + 2 * kTile;  // 1 buffer
-  float* sRed = reinterpret_cast<float*>(sP + kTile);  // [2 parity][2 half][128 rows] row-max / row-sum exchange
+  // Q and P live in TMEM (A operands of S = QK^T and O += PV): shared memory
+  // only streams K and V (3-stage rings), halving smem operand traffic.
+  uint8_t* sK = sm;                      // KV stages
+  uint8_t* sV = sK + KVS * kTile;        // KV stages
+  float* sRed = reinterpret_cast<float*>(sV + KVS * kTile);  // [2 parity][2 half][128 rows] row-max / row-sum
   uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 512);
-  uint64_t* q_full = bar;
-  uint64_t* k_full = bar + 1;   // [2]
-  uint64_t* k_empty = bar + 3;  // [2]
-  uint64_t* v_full = bar + 5;   // [2]
-  uint64_t* v_empty = bar + 7;  // [2]
-  uint64_t* s_full = bar + 9;   // [2]
-  uint64_t* s_free = bar + 11;  // [2]
-  uint64_t* p_full = bar + 13;
-  uint64_t* p_free = bar + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* q_ready = bar;
+  uint64_t* k_full = bar + 1;           // [KVS]
+  uint64_t* k_empty = k_full + KVS;     // [KVS]
+  uint64_t* v_full = k_empty + KVS;     // [KVS]
+  uint64_t* v_empty = v_full + KVS;     // [KVS]
+  uint64_t* s_full = v_empty + KVS;     // [2]
+  uint64_t* s_free = s_full + 2;        // [2]
+  uint64_t* p_full = s_free + 2;
+  uint64_t* p_free = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + 1);
 
   const AttnTile tl = a.tiles[blockIdx.x];
   const AttnSeg sg = a.segs[tl.seg];
@@ -104,15 +108,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int nkt = (kv_len + TK - 1) / TK;
 
   if (threadIdx.x == 0) {
-    tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    mbar_init(q_ready, 256);
+    for (int i = 0; i < KVS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 256);
     }
@@ -127,15 +132,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS[2] = {tmem, tmem + 128};
   const uint32_t tO = tmem + 256;
+  const uint32_t tQ = tmem + 384;  // Q: 128 rows x 128 bf16 = 64 columns
+  const uint32_t tP = tmem + 448;  // P: 128 rows x 128 bf16 = 64 columns
 
   if (warp == 8) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, kTile);
-      tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
-      tma_load_2d(sQ + kBox, &tmQ, q_full, h * DH + 64, q_row0);
       for (int j = 0; j < nkt; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
+        const int st = j % KVS;
+        const uint32_t ph = (j / KVS) & 1;
         const int krow = sg.kv_row0 + j * TK;
         mbar_wait(&k_empty[st], ph ^ 1);
         mbar_expect_tx(&k_full[st], kTile);
@@ -151,31 +155,31 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
-      const uint32_t q0 = smem_u32(sQ), p0 = smem_u32(sP);
       auto issue_s = [&](int j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_full[st], ph);
-        mbar_wait(&s_free[st], ph ^ 1);
+        const int st = j % KVS, b = j & 1;
+        mbar_wait(&k_full[st], (j / KVS) & 1);
+        mbar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t k0 = smem_u32(sK + st * kTile);
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) umma_bf16(tS[st], kdesc(q0, ks), kdesc(k0, ks), idS, ks > 0 ? 1u : 0u);
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16_ts(tS[b], tQ + ks * 8, kdesc(k0, ks), idS, ks > 0 ? 1u : 0u);
         umma_commit(&k_empty[st]);
-        umma_commit(&s_full[st]);
+        umma_commit(&s_full[b]);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait(q_ready, 0);
+      tc_fence_after();
       issue_s(0);
       for (int j = 0; j < nkt; ++j) {
         if (j + 1 < nkt) issue_s(j + 1);
-        const int st = j & 1;
+        const int st = j % KVS;
         mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[st], (j >> 1) & 1);
+        mbar_wait(&v_full[st], (j / KVS) & 1);
         tc_fence_after();
         const uint32_t v0 = smem_u32(sV + st * kTile);
 #pragma unroll
         for (int ks = 0; ks < TK / 16; ++ks)
-          umma_bf16(tO, kdesc(p0, ks), mndesc(v0, ks), idO, (j > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_ts(tO, tP + ks * 8, mndesc(v0, ks), idO, (j > 0 || ks > 0) ? 1u : 0u);
         umma_commit(&v_empty[st]);
         umma_commit(p_free);
       }
@@ -188,6 +192,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int lim = sg.prefix + min(qi, sg.len - 1);    // last visible key
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t col0 = static_cast<uint32_t>(half * 64);
+    {
+      // stage this row's Q (this half's 64 dims) into TMEM as the A operand
+      uint32_t qw[32];
+      const bool qok = row < tl.count;
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + static_cast<int64_t>(q_row0 + row) * a.q_stride +
+                                                        static_cast<int64_t>(h) * DH + half * 64);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = qok ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
+        qw[4 * c] = v.x;
+        qw[4 * c + 1] = v.y;
+        qw[4 * c + 2] = v.z;
+        qw[4 * c + 3] = v.w;
+      }
+      tmem_st32(tQ + lane_off + half * 32, qw);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(q_ready);
+    }
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < nkt; ++j) {
       const int st = j & 1;
@@ -256,11 +279,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         tmem_st_wait();
       }
-      const uint32_t p_s = smem_u32(sP);
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        sts128(p_s + sw128_off(row, half * 8 + c), make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
-      fence_async_smem();
+      // P row -> TMEM (A operand of O += P V): this half's 64 keys = 32 columns
+      tmem_st32(tP + lane_off + half * 32, pk);
+      tmem_st_wait();
       tc_fence_before();
       mbar_arrive(p_full);
     }
@@ -738,8 +759,8 @@ cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32
       !map_rows(&mk, p.k, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride) ||
       !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
     return cudaErrorInvalidValue;
-  TcArgs a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
-  const size_t smem = 1024 + 6 * kTile + 512 * 4 + 256;
+  TcArgs a{p.segs, tiles128, p.q, p.q_stride, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
+  const size_t smem = 1024 + 2 * KVS * kTile + 512 * 4 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =

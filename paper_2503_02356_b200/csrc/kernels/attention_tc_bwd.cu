@@ -21,6 +21,8 @@ namespace {
 
 constexpr int DH = 128;
 constexpr int SUB = 64;                     // streamed sub-tile (keys for dQ, queries for dK/dV)
+constexpr int KS = 6, VS = 4;               // dQ kernel: K / V ring depths
+constexpr int QS = 4;                       // dK/dV kernel: Q/dO ring depth
 constexpr uint32_t kBox128 = 128 * 64 * 2;  // [128 rows][64 cols] bf16
 constexpr uint32_t kBox64 = 64 * 64 * 2;    // [64 rows][64 cols]
 constexpr float kLog2e = 1.4426950408889634f;
@@ -28,6 +30,14 @@ constexpr float kLog2e = 1.4426950408889634f;
 struct Args {
   const AttnSeg* segs;
   const AttnTile* tiles;  // 128-row tiles (queries for dQ, keys for dK/dV)
+  // raw rows for the per-CTA-invariant operands staged into TMEM
+  const __nv_bfloat16* q;
+  int64_t q_stride;
+  const __nv_bfloat16* dout;
+  int64_t dout_stride;
+  const __nv_bfloat16* k;
+  const __nv_bfloat16* v;
+  int64_t kv_stride;
   const float* lse;
   const float* dsum;
   __nv_bfloat16* dq;
@@ -40,6 +50,32 @@ struct Args {
 };
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One thread = one TMEM lane (row): copies 64 bf16 (this half's columns) of a
+// global row into 32 TMEM columns at `taddr` (A-operand layout: element k of
+// the row in column k/2).  Rows that do not exist are zero-filled.
+__device__ __forceinline__ void stage_row_tmem(uint32_t taddr, const __nv_bfloat16* src, bool ok) {
+  uint32_t w[32];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 v = ok ? __ldg(s4 + c) : make_uint4(0u, 0u, 0u, 0u);
+    w[4 * c] = v.x;
+    w[4 * c + 1] = v.y;
+    w[4 * c + 2] = v.z;
+    w[4 * c + 3] = v.w;
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]),
+      "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+      "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void named_sync_256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 constexpr int kThreads = 320;
 
@@ -63,22 +99,23 @@ __global__ void __launch_bounds__(kThreads, 1)
               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = sm;                   // 2 x [128][64]
-  uint8_t* sdO = sQ + 2 * kBox128;    // 2 x [128][64]
-  uint8_t* sK = sdO + 2 * kBox128;    // 3 stages x 2 x [64][64]
-  uint8_t* sV = sK + 3 * 2 * kBox64;  // 3 stages
-  uint8_t* sS = sV + 3 * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
+  // Q and dO (per-CTA invariant A operands of S and dP) live in TMEM.
+  // K is held until dQ of its sub-tile (late), V only until dP (early):
+  // separate rings, KS and VS deep, so loads are issued >= 2 sub-tiles ahead.
+  uint8_t* sK = sm;                    // KS stages x 2 x [64][64]
+  uint8_t* sV = sK + KS * 2 * kBox64;  // VS stages
+  uint8_t* sS = sV + VS * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * kBox128);
   uint64_t* q_full = bar;
-  uint64_t* k_full = bar + 1;    // [3]
-  uint64_t* k_empty = bar + 4;   // [3]
-  uint64_t* v_full = bar + 7;    // [3]
-  uint64_t* v_empty = bar + 10;  // [3]
-  uint64_t* s_full = bar + 13;   // [2]
-  uint64_t* s_free = bar + 15;   // [2]
-  uint64_t* ds_full = bar + 17;  // [2]
-  uint64_t* ds_free = bar + 19;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
+  uint64_t* k_full = bar + 1;              // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [VS]
+  uint64_t* v_empty = v_full + VS;         // [VS]
+  uint64_t* s_full = v_empty + VS;         // [2]
+  uint64_t* s_free = s_full + 2;           // [2]
+  uint64_t* ds_full = s_free + 2;          // [2]
+  uint64_t* ds_free = ds_full + 2;         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ds_free + 2);
 
   const AttnTile tl = a.tiles[blockIdx.x];
   const AttnSeg sg = a.segs[tl.seg];
@@ -93,10 +130,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmO);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 3; ++i) {
+    mbar_init(q_full, 256);  // softmax threads staging Q / dO into TMEM
+    for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
       mbar_init(&v_full[i], 1);
       mbar_init(&v_empty[i], 1);
     }
@@ -115,63 +154,58 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tS[2] = {tmem, tmem + 64};
   const uint32_t tP[2] = {tmem + 128, tmem + 192};
-  const uint32_t tQ = tmem + 256;
+  const uint32_t tQ = tmem + 256;     // dQ accumulator
+  const uint32_t tAq = tmem + 384;    // Q  (A operand, 64 columns)
+  const uint32_t tAo = tmem + 448;    // dO (A operand, 64 columns)
 
   if (warp == 8) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, 4 * kBox128);
-      tma_load_2d(sQ, &tmQ, q_full, h * DH, q_row0);
-      tma_load_2d(sQ + kBox128, &tmQ, q_full, h * DH + 64, q_row0);
-      tma_load_2d(sdO, &tmO, q_full, h * DH, q_row0);
-      tma_load_2d(sdO + kBox128, &tmO, q_full, h * DH + 64, q_row0);
       for (int j = 0; j < nkt; ++j) {
-        const int st = j % 3;
-        const uint32_t ph = (j / 3) & 1;
+        const int sk = j % KS, sv = j % VS;
         const int krow = sg.kv_row0 + j * SUB;
-        mbar_wait(&k_empty[st], ph ^ 1);
-        mbar_expect_tx(&k_full[st], 2 * kBox64);
-        tma_load_2d(sK + st * 2 * kBox64, &tmK, &k_full[st], g * DH, krow);
-        tma_load_2d(sK + st * 2 * kBox64 + kBox64, &tmK, &k_full[st], g * DH + 64, krow);
-        mbar_wait(&v_empty[st], ph ^ 1);
-        mbar_expect_tx(&v_full[st], 2 * kBox64);
-        tma_load_2d(sV + st * 2 * kBox64, &tmV, &v_full[st], g * DH, krow);
-        tma_load_2d(sV + st * 2 * kBox64 + kBox64, &tmV, &v_full[st], g * DH + 64, krow);
+        mbar_wait(&v_empty[sv], ((j / VS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[sv], 2 * kBox64);
+        tma_load_2d(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
+        tma_load_2d(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
+        mbar_wait(&k_empty[sk], ((j / KS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[sk], 2 * kBox64);
+        tma_load_2d(sK + sk * 2 * kBox64, &tmK, &k_full[sk], g * DH, krow);
+        tma_load_2d(sK + sk * 2 * kBox64 + kBox64, &tmK, &k_full[sk], g * DH + 64, krow);
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S, dP: N = 64 keys
       constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);  // dQ: N = dh, B = K (MN-major view)
-      const uint32_t q0 = smem_u32(sQ), o0 = smem_u32(sdO);
       auto issue_s = [&](int j) {
-        const int st = j % 3, b = j & 1;
-        const uint32_t ph = (j / 3) & 1;
-        mbar_wait(&k_full[st], ph);
-        mbar_wait(&v_full[st], ph);
+        const int sk = j % KS, sv = j % VS, b = j & 1;
+        mbar_wait(&k_full[sk], (j / KS) & 1);
+        mbar_wait(&v_full[sv], (j / VS) & 1);
         mbar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t k0 = smem_u32(sK + st * 2 * kBox64), v0 = smem_u32(sV + st * 2 * kBox64);
+        const uint32_t k0 = smem_u32(sK + sk * 2 * kBox64), v0 = smem_u32(sV + sv * 2 * kBox64);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16(tS[b], kdesc(q0, kBox128, ks), kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+          umma_bf16_ts(tS[b], tAq + ks * 8, kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16(tP[b], kdesc(o0, kBox128, ks), kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-        umma_commit(&v_empty[st]);
+          umma_bf16_ts(tP[b], tAo + ks * 8, kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(&v_empty[sv]);
         umma_commit(&s_full[b]);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait(q_full, 0);  // Q / dO staged into TMEM by the softmax warps
+      tc_fence_after();
       issue_s(0);
       for (int j = 0; j < nkt; ++j) {
         if (j + 1 < nkt) issue_s(j + 1);
-        const int st = j % 3, b = j & 1;
+        const int sk = j % KS, b = j & 1;
         mbar_wait(&ds_full[b], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t s0 = smem_u32(sS + b * kBox128), k0 = smem_u32(sK + st * 2 * kBox64);
+        const uint32_t s0 = smem_u32(sS + b * kBox128), k0 = smem_u32(sK + sk * 2 * kBox64);
 #pragma unroll
         for (int ks = 0; ks < SUB / 16; ++ks)
           umma_bf16(tQ, kdesc(s0, kBox128, ks), mndesc(k0, kBox64, ks), idQ, (j > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&k_empty[st]);
+        umma_commit(&k_empty[sk]);
         umma_commit(&ds_free[b]);
       }
     }
@@ -184,6 +218,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
     const float D = ok ? a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] : 0.f;
+    {
+      const bool rok = row < tl.count;
+      const int64_t r = q_row0 + row;
+      stage_row_tmem(tAq + lane_off + half * 32, a.q + r * a.q_stride + static_cast<int64_t>(h) * DH + half * 64, rok);
+      stage_row_tmem(tAo + lane_off + half * 32, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + half * 64,
+                     rok);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(q_full);
+    }
     for (int j = 0; j < nkt; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
@@ -254,23 +298,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = sm;                     // 2 x [128][64]
-  uint8_t* sV = sK + 2 * kBox128;       // 2 x [128][64]
-  uint8_t* sQ = sV + 2 * kBox128;       // 2 stages x 2 x [64][64]
-  uint8_t* sdO = sQ + 2 * 2 * kBox64;   // 2 stages x 2 x [64][64]
-  uint8_t* sP = sdO + 2 * 2 * kBox64;   // 2 x [128 keys][64 q]
-  uint8_t* sS = sP + 2 * kBox128;       // 2 x [128 keys][64 q]
-  float* sL = reinterpret_cast<float*>(sS + 2 * kBox128);  // [2][64]
-  float* sD = sL + 128;                                    // [2][64]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + 128);
-  uint64_t* kv_full = bar;
-  uint64_t* q_full = bar + 1;     // [2]
-  uint64_t* q_empty = bar + 3;    // [2]
-  uint64_t* s_full = bar + 5;     // [2]
-  uint64_t* s_free = bar + 7;     // [2]
-  uint64_t* pds_full = bar + 9;   // [2]
-  uint64_t* pds_free = bar + 11;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 14);
+  // K and V (per-CTA invariant A operands of S^T and dP^T) live in TMEM;
+  // S^T / dP^T are single-buffered (their readers release them right after
+  // tcgen05.ld), which leaves room for K, V next to the dV / dK accumulators.
+  uint8_t* sQ = sm;                      // QS stages x 2 x [64][64]
+  uint8_t* sdO = sQ + QS * 2 * kBox64;   // QS stages x 2 x [64][64]
+  uint8_t* sP = sdO + QS * 2 * kBox64;   // 2 x [128 keys][64 q]
+  uint8_t* sS = sP + 2 * kBox128;        // 2 x [128 keys][64 q]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * kBox128);
+  uint64_t* kv_full = bar;               // K / V staged into TMEM (256 arrivals)
+  uint64_t* q_full = bar + 1;            // [QS]
+  uint64_t* q_empty = q_full + QS;       // [QS]
+  uint64_t* s_full = q_empty + QS;       // [1]
+  uint64_t* s_free = s_full + 1;         // [1]
+  uint64_t* pds_full = s_free + 1;       // [2]
+  uint64_t* pds_free = pds_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pds_free + 2);
 
   const AttnTile tl = a.tiles[blockIdx.x];
   const AttnSeg sg = a.segs[tl.seg];
@@ -285,14 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmO);
-    tma_prefetch(&tmK);
-    tma_prefetch(&tmV);
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    mbar_init(kv_full, 256);
+    for (int i = 0; i < QS; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 256);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 256);
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&pds_full[i], 256);
       mbar_init(&pds_free[i], 1);
     }
@@ -303,59 +346,53 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 64};
-  const uint32_t tP[2] = {tmem + 128, tmem + 192};
-  const uint32_t tdV = tmem + 256, tdK = tmem + 384;
+  const uint32_t tS = tmem, tP = tmem + 64;  // S^T, dP^T (64 columns each)
+  const uint32_t tdV = tmem + 128, tdK = tmem + 256;
+  const uint32_t tAk = tmem + 384, tAv = tmem + 448;  // K, V A operands (64 columns each)
 
   if (warp == 8) {
     if (lane == 0) {
-      const int krow = sg.kv_row0 + key_first;
-      mbar_expect_tx(kv_full, 4 * kBox128);
-      tma_load_2d(sK, &tmK, kv_full, g * DH, krow);
-      tma_load_2d(sK + kBox128, &tmK, kv_full, g * DH + 64, krow);
-      tma_load_2d(sV, &tmV, kv_full, g * DH, krow);
-      tma_load_2d(sV + kBox128, &tmV, kv_full, g * DH + 64, krow);
       for (int it = 0; it < iters; ++it) {
-        const int b = it & 1;
+        const int qs = it % QS;
         const int hq = g * per + it / nqt;
         const int qrow = sg.q_start + i0 + (it % nqt) * SUB;
-        mbar_wait(&q_empty[b], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[b], 4 * kBox64);
-        uint8_t* q = sQ + b * 2 * kBox64;
-        uint8_t* o = sdO + b * 2 * kBox64;
-        tma_load_2d(q, &tmQ, &q_full[b], hq * DH, qrow);
-        tma_load_2d(q + kBox64, &tmQ, &q_full[b], hq * DH + 64, qrow);
-        tma_load_2d(o, &tmO, &q_full[b], hq * DH, qrow);
-        tma_load_2d(o + kBox64, &tmO, &q_full[b], hq * DH + 64, qrow);
+        mbar_wait(&q_empty[qs], ((it / QS) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qs], 4 * kBox64);
+        uint8_t* q = sQ + qs * 2 * kBox64;
+        uint8_t* o = sdO + qs * 2 * kBox64;
+        tma_load_2d(q, &tmQ, &q_full[qs], hq * DH, qrow);
+        tma_load_2d(q + kBox64, &tmQ, &q_full[qs], hq * DH + 64, qrow);
+        tma_load_2d(o, &tmO, &q_full[qs], hq * DH, qrow);
+        tma_load_2d(o + kBox64, &tmO, &q_full[qs], hq * DH + 64, qrow);
       }
     }
   } else if (warp == 9) {
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S^T, dP^T: N = 64 queries
       constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);  // dV, dK: N = dh, B MN-major view
-      const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV);
       auto issue_s = [&](int it) {
-        const int b = it & 1;
-        mbar_wait(&q_full[b], (it >> 1) & 1);
-        mbar_wait(&s_free[b], ((it >> 1) & 1) ^ 1);
+        const int qs = it % QS;
+        mbar_wait(&q_full[qs], (it / QS) & 1);
+        mbar_wait(s_free, (it & 1) ^ 1);
         tc_fence_after();
-        const uint32_t q0 = smem_u32(sQ + b * 2 * kBox64), o0 = smem_u32(sdO + b * 2 * kBox64);
+        const uint32_t q0 = smem_u32(sQ + qs * 2 * kBox64), o0 = smem_u32(sdO + qs * 2 * kBox64);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16(tS[b], kdesc(k0, kBox128, ks), kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+          umma_bf16_ts(tS, tAk + ks * 8, kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16(tP[b], kdesc(v0, kBox128, ks), kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-        umma_commit(&s_full[b]);
+          umma_bf16_ts(tP, tAv + ks * 8, kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(s_full);
       };
       mbar_wait(kv_full, 0);
+      tc_fence_after();
       issue_s(0);
       for (int it = 0; it < iters; ++it) {
         if (it + 1 < iters) issue_s(it + 1);
-        const int b = it & 1;
+        const int b = it & 1, qs = it % QS;
         mbar_wait(&pds_full[b], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t q0 = smem_u32(sQ + b * 2 * kBox64), o0 = smem_u32(sdO + b * 2 * kBox64);
+        const uint32_t q0 = smem_u32(sQ + qs * 2 * kBox64), o0 = smem_u32(sdO + qs * 2 * kBox64);
         const uint32_t p0 = smem_u32(sP + b * kBox128), s0 = smem_u32(sS + b * kBox128);
 #pragma unroll
         for (int ks = 0; ks < SUB / 16; ++ks)
@@ -363,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int ks = 0; ks < SUB / 16; ++ks)
           umma_bf16(tdK, kdesc(s0, kBox128, ks), mndesc(q0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&q_empty[b]);
+        umma_commit(&q_empty[qs]);
         umma_commit(&pds_free[b]);
       }
     }
@@ -373,40 +410,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int key = key_first + row;
     const bool kok = row < tl.count && key < kv_len;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    {
+      const int64_t r = sg.kv_row0 + key;
+      stage_row_tmem(tAk + lane_off + half * 32, a.k + r * a.kv_stride + static_cast<int64_t>(g) * DH + half * 64,
+                     kok);
+      stage_row_tmem(tAv + lane_off + half * 32, a.v + r * a.kv_stride + static_cast<int64_t>(g) * DH + half * 64,
+                     kok);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(kv_full);
+    }
     for (int it = 0; it < iters; ++it) {
       const int b = it & 1;
       const int hq = g * per + it / nqt;
       const int qt0 = i0 + (it % nqt) * SUB;
-      const uint32_t L_ = smem_u32(sL) + b * 256, D_ = smem_u32(sD) + b * 256;
-      if (half == 0 && row < SUB) {
-        const int qi = qt0 + row;
-        const bool qok = qi < sg.len;
-        const int64_t idx = static_cast<int64_t>(hq) * a.T + sg.q_start + qi;
-        sts_f32(L_ + row * 4, qok ? a.lse[idx] * kLog2e : INFINITY);
-        sts_f32(D_ + row * 4, qok ? a.dsum[idx] : 0.f);
-      }
-      named_sync_256();
-      mbar_wait(&s_full[b], (it >> 1) & 1);
+      // per-query LSE / D straight from global (every lane reads the same
+      // address -> one broadcast transaction; no smem staging, no barrier)
+      const int64_t qbase = static_cast<int64_t>(hq) * a.T + sg.q_start;
+      const float* Lg = a.lse + qbase;
+      const float* Dg = a.dsum + qbase;
+      mbar_wait(s_full, it & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
-      tmem_ld32(tS[b] + lane_off + half * 32, rs);
-      tmem_ld32(tP[b] + lane_off + half * 32, rp);
+      tmem_ld32(tS + lane_off + half * 32, rs);
+      tmem_ld32(tP + lane_off + half * 32, rp);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[b]);
+      mbar_arrive(s_free);
       const bool full = key_first + 127 < kv_len && key_first + 127 <= sg.prefix + qt0 && qt0 + SUB <= sg.len;
       uint32_t pp[16], pd[16];
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const int ql = half * 32 + 2 * e;
         const int qi = qt0 + ql;
-        const float l0 = lds_f32(L_ + ql * 4), l1 = lds_f32(L_ + ql * 4 + 4);
-        const float d0 = lds_f32(D_ + ql * 4), d1 = lds_f32(D_ + ql * 4 + 4);
+        const int q0c = min(qi, sg.len - 1), q1c = min(qi + 1, sg.len - 1);
+        const float l0 = __ldg(Lg + q0c) * kLog2e, l1 = __ldg(Lg + q1c) * kLog2e;
+        const float d0 = __ldg(Dg + q0c), d1 = __ldg(Dg + q1c);
         float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -l0));
         float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -l1));
         if (!full) {
-          p0 = (kok && key <= sg.prefix + qi) ? p0 : 0.f;
-          p1 = (kok && key <= sg.prefix + qi + 1) ? p1 : 0.f;
+          p0 = (kok && qi < sg.len && key <= sg.prefix + qi) ? p0 : 0.f;
+          p1 = (kok && qi + 1 < sg.len && key <= sg.prefix + qi + 1) ? p1 : 0.f;
         }
         pp[e] = pack_bf16(p0, p1);
         pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - d0), p1 * (__uint_as_float(rp[2 * e + 1]) - d1));
@@ -495,10 +539,10 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
       !map_rows(&q64, p.q, qc, p.T, p.q_stride, 64) || !map_rows(&o64, p.dout, qc, p.T, p.dout_stride, 64) ||
       !map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
     return cudaErrorInvalidValue;
-  Args a{p.segs, qtiles128, p.lse, p.dsum, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride,
-         p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
-  const size_t smem_dq = 1024 + 4 * kBox128 + 12 * kBox64 + 2 * kBox128 + 256;
-  const size_t smem_dkv = 1024 + 4 * kBox128 + 8 * kBox64 + 4 * kBox128 + 4 * 128 * 4 + 128;
+  Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.dq,
+         p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
+  const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256;
+  const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
