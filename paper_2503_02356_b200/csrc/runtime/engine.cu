@@ -99,7 +99,9 @@ constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0;
 void dp_unique_id(uint8_t* out) { nccl_check(nccl().get_id(out), "ncclGetUniqueId"); }
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id) {
-  if (world <= 1) return;
+  // world == 1 without an id: no communicator.  With an id, a 1-rank NCCL
+  // communicator is created (exercises the full DP path on one GPU).
+  if (world <= 1 && !id) return;
   Id128 u;
   std::memcpy(u.b, id, 128);
   auto init = reinterpret_cast<int (*)(void**, int, Id128, int)>(nccl().init_rank);
@@ -989,7 +991,7 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
   for (const auto& [sl, f] : recompute_pairs)
     if (f < 0 || slots[static_cast<size_t>(sl)] != slots[static_cast<size_t>(f)]) ++mism;
   double loss = total / norm;
-  if (ctx->world > 1) {
+  if (ctx->nccl_comm) {
     // DP: gradients and loss are sums of per-rank partials (global normalizer)
     double* dl = ex.loss_slots + nev;
     CK(cudaMemcpyAsync(dl, &loss, 8, cudaMemcpyHostToDevice, ex.s));
