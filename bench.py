@@ -111,6 +111,20 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
+TRAFFIC_FILE = "profiles/round1_gemm_traffic.json"
+
+
+def gemm_traffic():
+    """Per-launch DRAM bytes of the GEMM from the committed ncu --set full
+    capture (tools/gemm_traffic.py), with the algorithmic bytes of the same
+    launches for comparison; None when the capture is absent."""
+    try:
+        t = json.load(open(os.path.join(ROOT, TRAFFIC_FILE)))
+        return t["mean_dram_bytes_per_launch"], t["mean_algorithmic_bytes_per_launch"]
+    except Exception:
+        return None, None
+
+
 # ----------------------------------------------------------- CPU baseline
 def toy_flops(lengths, cfg, cs):
     """Algorithmic FLOPs of the reference toy run_plan (6NT + 12*L*d*pairs)."""
@@ -283,6 +297,7 @@ def run_b200(args):
             dist.destroy_process_group()
         return
     pk = peaks()
+    traffic = gemm_traffic()
     r0 = res[-1]
     gemm_tf = sum(r.gemm_flops for r in res) / (sum(r.gemm_ms for r in res) / 1e3) / 1e12
     attn_tf = sum(r.attn_flops for r in res) / max(1e-9, sum(r.attn_ms for r in res) / 1e3) / 1e12
@@ -310,7 +325,8 @@ def run_b200(args):
                 "frac_of_measured_sustained": mfu / pk["bf16_tflops_sustained"]},
         "roofline": {"bound": "tensor", "kernel": "tcgen05 GEMM (all projection/MLP/head GEMMs)",
                      "achieved": gemm_tf, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                     "frac": gemm_tf / pk["bf16_tflops_sustained"], "traffic": None,
+                     "frac": gemm_tf / pk["bf16_tflops_sustained"], "traffic": traffic[0],
+                     "traffic_algorithmic": traffic[1], "traffic_source": TRAFFIC_FILE,
                      "share_of_step": gemm_share, "peak_kind": "measured sustained (MEASURED_PEAKS.json)",
                      "attention_fwd": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s"},
                      "attention_bwd": {"achieved": attnb_tf, "share_of_step": attnb_share, "unit": "TFLOP/s",

@@ -47,7 +47,22 @@ struct Args {
   int64_t ldc;
   const void* R;  // fp32 residual (EPI_F32_RES) or bf16 aux (EPI_BF16_TANHGRAD)
   int64_t ldr;
+  int group_m;  // raster: tiles walk group_m M-blocks x all N-blocks, M fastest
 };
+
+// Grouped raster.  Persistent CTAs take consecutive tile indices, so one wave
+// is a contiguous index range; walking group_m M-blocks at a time makes that
+// range a near-square block of the output (e.g. 8 x 9 for 74 pairs), and the
+// operand slabs it streams are shared by ~8 tiles each in L2 instead of the
+// M operand being re-read from HBM once per wave.
+__device__ __forceinline__ void tile_coords(const Args& g, int tile, int& mb, int& nb) {
+  const int per_group = g.group_m * g.num_n;
+  const int first_m = (tile / per_group) * g.group_m;
+  const int gm = min(g.num_m - first_m, g.group_m);
+  const int r = tile - (tile / per_group) * per_group;
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
 
 template <int EPI>
 __device__ __forceinline__ void store_row32(const Args& g, int row, int col0, const uint32_t (&r)[32]) {
@@ -155,7 +170,8 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % g.num_m, nb = tile / g.num_m;
+        int mb, nb;
+        tile_coords(g, tile, mb, nb);
         for (int kb = 0; kb < g.num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * C::kABytes;
@@ -220,7 +236,8 @@ __global__ void __launch_bounds__(256, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int mb = tile % g.num_m, nb = tile / g.num_m;
+      int mb, nb;
+        tile_coords(g, tile, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
@@ -357,7 +374,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       uint32_t phase = 0;
       const uint32_t full_leader0 = leader_addr(smem_u32(&full[0]));
       for (int tile = pair; tile < num_tiles; tile += npairs) {
-        const int mb = tile % g.num_m, nb = tile / g.num_m;
+        int mb, nb;
+        tile_coords(g, tile, mb, nb);
         const int m0 = mb * 256 + static_cast<int>(rank) * 128;
         const int n0 = nb * 256 + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < g.num_k; ++kb) {
@@ -428,7 +446,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = leader_addr(smem_u32(&tempty[0]));
     for (int tile = pair; tile < num_tiles; tile += npairs) {
-      const int mb = tile % g.num_m, nb = tile / g.num_m;
+      int mb, nb;
+        tile_coords(g, tile, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + ew * 32 + lane;
@@ -495,6 +514,17 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_num_sms = 0;
 
+// M-blocks per raster group (CF_GEMM_GROUP overrides; 0 = M-fastest over the
+// whole output, the pre-grouping order).
+int raster_group(int num_m, int dflt) {
+  static const int env = [] {
+    const char* e = std::getenv("CF_GEMM_GROUP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const int gm = env >= 0 ? env : dflt;
+  return gm <= 0 || gm > num_m ? num_m : gm;
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   using C = Cfg<BN>;
@@ -509,6 +539,7 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   g.num_m = static_cast<int>((d.M + BM - 1) / BM);
   g.num_n = static_cast<int>((d.N + BN - 1) / BN);
   g.num_k = static_cast<int>((d.K + BK - 1) / BK);
+  g.group_m = raster_group(g.num_m, 16);
   g.C = d.c;
   g.ldc = d.ldc;
   g.R = d.r;
@@ -544,6 +575,7 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.num_m = static_cast<int>((d.M + 255) / 256);
   g.num_n = static_cast<int>((d.N + 255) / 256);
   g.num_k = static_cast<int>((d.K + BK - 1) / BK);
+  g.group_m = raster_group(g.num_m, 8);
   g.C = d.c;
   g.ldc = d.ldc;
   g.R = d.r;

@@ -1,5 +1,7 @@
 """Times the tcgen05 GEMM at the C2 per-layer shapes (T = 8192 tokens of one
 chunk, Llama-7B-shaped layer) through cf_op_gemm; TFLOP/s per shape."""
+import json
+import os
 import sys
 
 import torch
@@ -21,7 +23,10 @@ SH = [  # name, M, N, K, a_kmajor, b_kmajor, epi
     ("down wgrad", ffn, d, T, 0, 0, capi.EPI_F32_ACC),
     ("qkv wgrad", d, d + 2 * kvw, T, 0, 0, capi.EPI_F32_ACC),
     ("head fwd", T, 32000, d, 1, 0, capi.EPI_F32),
+    ("head dgrad", T, d, 32000, 1, 1, capi.EPI_F32),
+    ("head wgrad", d, 32000, T, 0, 0, capi.EPI_F32_ACC),
 ]
+ONCE = os.environ.get("GEMM_BENCH_ONCE") == "1"
 only = sys.argv[1] if len(sys.argv) > 1 else None
 for name, M, N, K, ak, bk, epi in SH:
     if only and only not in name:
@@ -34,6 +39,12 @@ for name, M, N, K, ak, bk, epi in SH:
     args = (A.data_ptr(), ak, A.shape[1], B.data_ptr(), bk, B.shape[1], C.data_ptr(), N, M, N, K, epi,
             R.data_ptr() if R is not None else 0, N)
     torch.cuda.synchronize()
+    if ONCE:  # one launch per shape, for an ncu capture with known shapes
+        ctx.gemm(*args)
+        ctx.synchronize()
+        io = (M * K + N * K) * 2 + M * N * (4 if f32 else 2) * (2 if epi in (capi.EPI_F32_ACC, capi.EPI_F32_RES) else 1)
+        print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "algorithmic_bytes": io}), flush=True)
+        continue
     for _ in range(2):
         ctx.gemm(*args)
     ctx.synchronize()
