@@ -11,6 +11,9 @@
 //
 // TMEM: S0 S1 dP0 dP1 (4 x 64 cols) + accumulators (dQ: 128; dV + dK: 256).
 #include <cfloat>
+#include <climits>
+#include <cstdio>
+#include <type_traits>
 
 #include "attention.h"
 #include "attention_tc.h"
@@ -76,7 +79,6 @@ __device__ __forceinline__ void stage_row_tmem(uint32_t taddr, const __nv_bfloat
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void named_sync_256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 constexpr int kThreads = 320;
 
 // 16-byte chunk c (0..7) of row r in a [rows][64] SW128 box
@@ -152,8 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 64};
-  const uint32_t tP[2] = {tmem + 128, tmem + 192};
+  // S[b] at tmem + 64b, dP[b] at tmem + 128 + 64b
   const uint32_t tQ = tmem + 256;     // dQ accumulator
   const uint32_t tAq = tmem + 384;    // Q  (A operand, 64 columns)
   const uint32_t tAo = tmem + 448;    // dO (A operand, 64 columns)
@@ -174,40 +175,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S, dP: N = 64 keys
-      constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);  // dQ: N = dh, B = K (MN-major view)
-      auto issue_s = [&](int j) {
-        const int sk = j % KS, sv = j % VS, b = j & 1;
-        mbar_wait(&k_full[sk], (j / KS) & 1);
-        mbar_wait(&v_full[sv], (j / VS) & 1);
-        mbar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k0 = smem_u32(sK + sk * 2 * kBox64), v0 = smem_u32(sV + sv * 2 * kBox64);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16_ts(tS[b], tAq + ks * 8, kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16_ts(tP[b], tAo + ks * 8, kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-        umma_commit(&v_empty[sv]);
-        umma_commit(&s_full[b]);
-      };
-      mbar_wait(q_full, 0);  // Q / dO staged into TMEM by the softmax warps
+    // whole warp, convergent (elect.sync inside the issue helpers)
+    constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S, dP: N = 64 keys
+    constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);  // dQ: N = dh, B = K (MN-major view)
+    const uint32_t sK0 = smem_u32(sK), sV0 = smem_u32(sV), sS0 = smem_u32(sS);
+    const uint32_t bKf = smem_u32(k_full), bKe = smem_u32(k_empty), bVf = smem_u32(v_full),
+                   bVe = smem_u32(v_empty), bSf = smem_u32(s_full), bSr = smem_u32(s_free),
+                   bDf = smem_u32(ds_full), bDr = smem_u32(ds_free);
+    int ik = 0, iv = 0, ck = 0;  // ring slots: K/V for the next S/dP issue, K for the next dQ
+    uint32_t pk = 0, pv = 0;
+    auto issue_s = [&](int j) {
+      const uint32_t b = j & 1;
+      mbar_wait_s(bKf + ik * 8, pk);
+      mbar_wait_s(bVf + iv * 8, pv);
+      mbar_wait_s(bSr + b * 8, ((j >> 1) & 1) ^ 1);
       tc_fence_after();
-      issue_s(0);
-      for (int j = 0; j < nkt; ++j) {
-        if (j + 1 < nkt) issue_s(j + 1);
-        const int sk = j % KS, b = j & 1;
-        mbar_wait(&ds_full[b], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t s0 = smem_u32(sS + b * kBox128), k0 = smem_u32(sK + sk * 2 * kBox64);
+      const uint32_t k0 = sK0 + ik * 2 * kBox64, v0 = sV0 + iv * 2 * kBox64;
 #pragma unroll
-        for (int ks = 0; ks < SUB / 16; ++ks)
-          umma_bf16(tQ, kdesc(s0, kBox128, ks), mndesc(k0, kBox64, ks), idQ, (j > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&k_empty[sk]);
-        umma_commit(&ds_free[b]);
-      }
+      for (int ks = 0; ks < DH / 16; ++ks)
+        umma_bf16_ts_w(tmem + b * 64, tAq + ks * 8, kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks)
+        umma_bf16_ts_w(tmem + 128 + b * 64, tAo + ks * 8, kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+      umma_commit_w(bVe + iv * 8);
+      umma_commit_w(bSf + b * 8);
+      if (++ik == KS) { ik = 0; pk ^= 1; }
+      if (++iv == VS) { iv = 0; pv ^= 1; }
+    };
+    mbar_wait(q_full, 0);  // Q / dO staged into TMEM by the softmax warps
+    tc_fence_after();
+    issue_s(0);
+    for (int j = 0; j < nkt; ++j) {
+      if (j + 1 < nkt) issue_s(j + 1);
+      const uint32_t b = j & 1;
+      mbar_wait_s(bDf + b * 8, (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t s0 = sS0 + b * kBox128, k0 = sK0 + ck * 2 * kBox64;
+#pragma unroll
+      for (int ks = 0; ks < SUB / 16; ++ks)
+        umma_bf16_w(tQ, kdesc(s0, kBox128, ks), mndesc(k0, kBox64, ks), idQ, (j > 0 || ks > 0) ? 1u : 0u);
+      umma_commit_w(bKe + ck * 8);
+      umma_commit_w(bDr + b * 8);
+      if (++ck == KS) ck = 0;
     }
   } else {
     const int quarter = warp & 3, half = warp >> 2;  // half: which 32 of the 64 key columns
@@ -228,37 +237,50 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(q_full);
     }
+    const uint32_t bSf = smem_u32(s_full), bSr = smem_u32(s_free), bDf = smem_u32(ds_full),
+                   bDr = smem_u32(ds_free), sS0 = smem_u32(sS);
+    const int klim = ok ? lim : -1;  // last visible key of this query row (-1: row absent)
+    const int tile_lim = sg.prefix + tl.first;  // smallest row limit of the tile
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
     for (int j = 0; j < nkt; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      const uint32_t b = j & 1;
+      mbar_wait_s(bSf + b * 8, (j >> 1) & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
-      tmem_ld32(tS[b] + lane_off + half * 32, rs);
-      tmem_ld32(tP[b] + lane_off + half * 32, rp);
+      tmem_ld32(tmem + b * 64 + lane_off + half * 32, rs);
+      tmem_ld32(tmem + 128 + b * 64 + lane_off + half * 32, rp);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(&s_free[b]);
-      const int key0 = j * SUB + half * 32;
-      const bool full = ok && j * SUB + SUB - 1 <= sg.prefix + tl.first;
+      mbar_arrive_s(bSr + b * 8);
       uint32_t pk[16];
+      // dS = P * (dP - D); P masked only on sub-tiles that cross the causal
+      // diagonal or the end of the segment (two separately compiled bodies)
+      auto body = [&](auto masked) {
+        const int key0 = j * SUB + half * 32;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int k0 = key0 + 2 * e;
-        float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
-        float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
-        if (!full) {
-          p0 = (ok && k0 <= lim) ? p0 : 0.f;
-          p1 = (ok && k0 + 1 <= lim) ? p1 : 0.f;
+        for (int e = 0; e < 16; ++e) {
+          float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
+          float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
+          if constexpr (decltype(masked)::value) {
+            p0 = key0 + 2 * e <= klim ? p0 : 0.f;
+            p1 = key0 + 2 * e + 1 <= klim ? p1 : 0.f;
+          }
+          pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
         }
-        pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
-      }
-      if (j >= 2) mbar_wait(&ds_free[b], ((j >> 1) & 1) ^ 1);
-      const uint32_t dst = smem_u32(sS) + b * kBox128;
+      };
+      if (j * SUB + SUB - 1 <= tile_lim)  // uniform: every row of the tile sees every key
+        body(std::false_type{});
+      else
+        body(std::true_type{});
+      if (j >= 2) mbar_wait_s(bDr + b * 8, ((j >> 1) & 1) ^ 1);
+      const uint32_t dst = sS0 + b * kBox128;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        sts128(dst + sw_off(row, half * 4 + c), make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+        sts128(dst + dst_off[c], make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
       fence_async_smem();
-      mbar_arrive(&ds_full[b]);
+      mbar_arrive_s(bDf + b * 8);
     }
     const int last = nkt - 1;
     mbar_wait(&ds_free[last & 1], (last >> 1) & 1);
@@ -305,7 +327,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sdO = sQ + QS * 2 * kBox64;   // QS stages x 2 x [64][64]
   uint8_t* sP = sdO + QS * 2 * kBox64;   // 2 x [128 keys][64 q]
   uint8_t* sS = sP + 2 * kBox128;        // 2 x [128 keys][64 q]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * kBox128);
+  uint8_t* sLD = sS + 2 * kBox128;       // QS stages x {LSE[64], D[64]} fp32 (staged with Q / dO)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sLD + QS * 512);
   uint64_t* kv_full = bar;               // K / V staged into TMEM (256 arrivals)
   uint64_t* q_full = bar + 1;            // [QS]
   uint64_t* q_empty = q_full + QS;       // [QS]
@@ -330,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmO);
     mbar_init(kv_full, 256);
     for (int i = 0; i < QS; ++i) {
-      mbar_init(&q_full[i], 1);
+      mbar_init(&q_full[i], 2);  // TMA expect_tx arrive + LSE / D staged arrive
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
@@ -349,14 +372,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tS = tmem, tP = tmem + 64;  // S^T, dP^T (64 columns each)
   const uint32_t tdV = tmem + 128, tdK = tmem + 256;
   const uint32_t tAk = tmem + 384, tAv = tmem + 448;  // K, V A operands (64 columns each)
+  const uint32_t sQ0 = smem_u32(sQ), sO0 = smem_u32(sdO), sP0 = smem_u32(sP), sS0 = smem_u32(sS),
+                 sLD0 = smem_u32(sLD);
+  const uint32_t bQf = smem_u32(q_full), bQe = smem_u32(q_empty), bSf = smem_u32(s_full),
+                 bSr = smem_u32(s_free), bPf = smem_u32(pds_full), bPr = smem_u32(pds_free);
 
   if (warp == 8) {
-    if (lane == 0) {
-      for (int it = 0; it < iters; ++it) {
-        const int qs = it % QS;
-        const int hq = g * per + it / nqt;
-        const int qrow = sg.q_start + i0 + (it % nqt) * SUB;
-        mbar_wait(&q_empty[qs], ((it / QS) & 1) ^ 1);
+    // whole warp: lane 0 issues the Q / dO TMA, every lane stages two of the
+    // 64 LSE / D values (plain loads: segment starts are not 16B-aligned)
+    int qs = 0, hi = 0, qi = 0;  // ring slot, q head within the group, query sub-tile
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      const int hq = g * per + hi;
+      const int qt0 = i0 + qi * SUB;
+      const int qrow = sg.q_start + qt0;
+      mbar_wait_s(bQe + qs * 8, ph ^ 1);
+      if (lane == 0) {
         mbar_expect_tx(&q_full[qs], 4 * kBox64);
         uint8_t* q = sQ + qs * 2 * kBox64;
         uint8_t* o = sdO + qs * 2 * kBox64;
@@ -365,44 +396,58 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(o, &tmO, &q_full[qs], hq * DH, qrow);
         tma_load_2d(o + kBox64, &tmO, &q_full[qs], hq * DH + 64, qrow);
       }
+      const int64_t base = static_cast<int64_t>(hq) * a.T + qrow;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int c = lane + 32 * h2;
+        const bool in = qt0 + c < sg.len;  // past the segment: masked by the consumer
+        sts_f32(sLD0 + qs * 512 + c * 4, in ? __ldg(a.lse + base + c) : 0.f);
+        sts_f32(sLD0 + qs * 512 + 256 + c * 4, in ? __ldg(a.dsum + base + c) : 0.f);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(bQf + qs * 8);
+      if (++qi == nqt) { qi = 0; ++hi; }
+      if (++qs == QS) { qs = 0; ph ^= 1; }
     }
   } else if (warp == 9) {
-    if (lane == 0) {
-      constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S^T, dP^T: N = 64 queries
-      constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);  // dV, dK: N = dh, B MN-major view
-      auto issue_s = [&](int it) {
-        const int qs = it % QS;
-        mbar_wait(&q_full[qs], (it / QS) & 1);
-        mbar_wait(s_free, (it & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t q0 = smem_u32(sQ + qs * 2 * kBox64), o0 = smem_u32(sdO + qs * 2 * kBox64);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16_ts(tS, tAk + ks * 8, kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16_ts(tP, tAv + ks * 8, kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-        umma_commit(s_full);
-      };
-      mbar_wait(kv_full, 0);
+    // whole warp, convergent (elect.sync inside the issue helpers)
+    constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S^T, dP^T: N = 64 queries
+    constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);  // dV, dK: N = dh, B MN-major view
+    int is = 0, cs = 0;  // ring slot of the next S^T issue / of the next dV,dK issue
+    uint32_t ps = 0;
+    auto issue_s = [&](int it) {
+      mbar_wait_s(bQf + is * 8, ps);
+      mbar_wait_s(bSr, (it & 1) ^ 1);
       tc_fence_after();
-      issue_s(0);
-      for (int it = 0; it < iters; ++it) {
-        if (it + 1 < iters) issue_s(it + 1);
-        const int b = it & 1, qs = it % QS;
-        mbar_wait(&pds_full[b], (it >> 1) & 1);
-        tc_fence_after();
-        const uint32_t q0 = smem_u32(sQ + qs * 2 * kBox64), o0 = smem_u32(sdO + qs * 2 * kBox64);
-        const uint32_t p0 = smem_u32(sP + b * kBox128), s0 = smem_u32(sS + b * kBox128);
+      const uint32_t q0 = sQ0 + is * 2 * kBox64, o0 = sO0 + is * 2 * kBox64;
 #pragma unroll
-        for (int ks = 0; ks < SUB / 16; ++ks)
-          umma_bf16(tdV, kdesc(p0, kBox128, ks), mndesc(o0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+      for (int ks = 0; ks < DH / 16; ++ks)
+        umma_bf16_ts_w(tS, tAk + ks * 8, kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
 #pragma unroll
-        for (int ks = 0; ks < SUB / 16; ++ks)
-          umma_bf16(tdK, kdesc(s0, kBox128, ks), mndesc(q0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
-        umma_commit(&q_empty[qs]);
-        umma_commit(&pds_free[b]);
-      }
+      for (int ks = 0; ks < DH / 16; ++ks)
+        umma_bf16_ts_w(tP, tAv + ks * 8, kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+      umma_commit_w(bSf);
+      if (++is == QS) { is = 0; ps ^= 1; }
+    };
+    mbar_wait(kv_full, 0);
+    tc_fence_after();
+    issue_s(0);
+    for (int it = 0; it < iters; ++it) {
+      if (it + 1 < iters) issue_s(it + 1);
+      const uint32_t b = it & 1;
+      mbar_wait_s(bPf + b * 8, (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t q0 = sQ0 + cs * 2 * kBox64, o0 = sO0 + cs * 2 * kBox64;
+      const uint32_t p0 = sP0 + b * kBox128, s0 = sS0 + b * kBox128;
+#pragma unroll
+      for (int ks = 0; ks < SUB / 16; ++ks)
+        umma_bf16_w(tdV, kdesc(p0, kBox128, ks), mndesc(o0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+      for (int ks = 0; ks < SUB / 16; ++ks)
+        umma_bf16_w(tdK, kdesc(s0, kBox128, ks), mndesc(q0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+      umma_commit_w(bQe + cs * 8);
+      umma_commit_w(bPr + b * 8);
+      if (++cs == QS) cs = 0;
     }
   } else {
     const int quarter = warp & 3, half = warp >> 2;  // half: which 32 of the 64 query columns
@@ -420,50 +465,67 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(kv_full);
     }
+    // query index range this key row sees: [qlo, len) (qlo = INT_MAX: row absent)
+    const int qlo = kok ? key - sg.prefix : INT_MAX;
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
+    int qs = 0, qi = 0;
+    uint32_t qph = 0;
     for (int it = 0; it < iters; ++it) {
-      const int b = it & 1;
-      const int hq = g * per + it / nqt;
-      const int qt0 = i0 + (it % nqt) * SUB;
-      // per-query LSE / D straight from global (every lane reads the same
-      // address -> one broadcast transaction; no smem staging, no barrier)
-      const int64_t qbase = static_cast<int64_t>(hq) * a.T + sg.q_start;
-      const float* Lg = a.lse + qbase;
-      const float* Dg = a.dsum + qbase;
-      mbar_wait(s_full, it & 1);
+      const uint32_t b = it & 1;
+      const int qt0 = i0 + qi * SUB;
+      mbar_wait_s(bSf, it & 1);
       tc_fence_after();
       uint32_t rs[32], rp[32];
       tmem_ld32(tS + lane_off + half * 32, rs);
       tmem_ld32(tP + lane_off + half * 32, rp);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive(s_free);
-      const bool full = key_first + 127 < kv_len && key_first + 127 <= sg.prefix + qt0 && qt0 + SUB <= sg.len;
+      mbar_arrive_s(bSr);
+      mbar_wait_s(bQf + qs * 8, qph);  // LSE / D of this slot (already complete: S^T waited on it)
+      const uint32_t lrow = sLD0 + qs * 512 + half * 128;
       uint32_t pp[16], pd[16];
+      auto body = [&](auto masked) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int ql = half * 32 + 2 * e;
-        const int qi = qt0 + ql;
-        const int q0c = min(qi, sg.len - 1), q1c = min(qi + 1, sg.len - 1);
-        const float l0 = __ldg(Lg + q0c) * kLog2e, l1 = __ldg(Lg + q1c) * kLog2e;
-        const float d0 = __ldg(Dg + q0c), d1 = __ldg(Dg + q1c);
-        float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -l0));
-        float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -l1));
-        if (!full) {
-          p0 = (kok && qi < sg.len && key <= sg.prefix + qi) ? p0 : 0.f;
-          p1 = (kok && qi + 1 < sg.len && key <= sg.prefix + qi + 1) ? p1 : 0.f;
+        for (int c4 = 0; c4 < 8; ++c4) {
+          const float4 L = lds_f32x4(lrow + c4 * 16);
+          const float4 Dv = lds_f32x4(lrow + 256 + c4 * 16);
+          const float l[4] = {L.x * kLog2e, L.y * kLog2e, L.z * kLog2e, L.w * kLog2e};
+          const float d[4] = {Dv.x, Dv.y, Dv.z, Dv.w};
+          float p[4], ds[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int col = c4 * 4 + u;
+            p[u] = ex2(fmaf(__uint_as_float(rs[col]), a.sl2, -l[u]));
+            if constexpr (decltype(masked)::value) {
+              const int qq = qt0 + half * 32 + col;
+              p[u] = (qq >= qlo && qq < sg.len) ? p[u] : 0.f;
+            }
+            ds[u] = p[u] * (__uint_as_float(rp[col]) - d[u]);
+          }
+          pp[2 * c4] = pack_bf16(p[0], p[1]);
+          pp[2 * c4 + 1] = pack_bf16(p[2], p[3]);
+          pd[2 * c4] = pack_bf16(ds[0], ds[1]);
+          pd[2 * c4 + 1] = pack_bf16(ds[2], ds[3]);
         }
-        pp[e] = pack_bf16(p0, p1);
-        pd[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - d0), p1 * (__uint_as_float(rp[2 * e + 1]) - d1));
-      }
-      if (it >= 2) mbar_wait(&pds_free[b], ((it >> 1) & 1) ^ 1);
-      const uint32_t dP_ = smem_u32(sP) + b * kBox128, dS_ = smem_u32(sS) + b * kBox128;
+      };
+      // uniform: every key of the tile sees every query of the sub-tile
+      if (key_first + 127 < kv_len && key_first + 127 <= sg.prefix + qt0 && qt0 + SUB <= sg.len)
+        body(std::false_type{});
+      else
+        body(std::true_type{});
+      if (it >= 2) mbar_wait_s(bPr + b * 8, ((it >> 1) & 1) ^ 1);
+      const uint32_t dP_ = sP0 + b * kBox128, dS_ = sS0 + b * kBox128;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        sts128(dP_ + sw_off(row, half * 4 + c), make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]));
-        sts128(dS_ + sw_off(row, half * 4 + c), make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
+        sts128(dP_ + dst_off[c], make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]));
+        sts128(dS_ + dst_off[c], make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
       }
       fence_async_smem();
-      mbar_arrive(&pds_full[b]);
+      mbar_arrive_s(bPf + b * 8);
+      if (++qi == nqt) qi = 0;
+      if (++qs == QS) { qs = 0; qph ^= 1; }
     }
     const int last = iters - 1;
     mbar_wait(&pds_free[last & 1], (last >> 1) & 1);
@@ -542,7 +604,7 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.dq,
          p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
   const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256;
-  const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + 256;
+  const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
