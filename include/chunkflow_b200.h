@@ -181,6 +181,58 @@ int cf_plan_partition(const cf_plan* global, int64_t world, int64_t rank,
 int cf_plan_rank_tokens(const cf_plan* global, int64_t world, int64_t* tokens);
 void cf_plan_destroy(cf_plan* plan);
 
+/* ---- pipeline-parallel planning (pipeline.hpp; config C5) ---- */
+
+/* TraceEventKind (pipeline.hpp:51) */
+#define CF_PP_FORWARD 0   /* first-pass forward */
+#define CF_PP_RECOMPUTE 1 /* just-in-time recompute forward (F') */
+#define CF_PP_BACKWARD 2
+
+/* CostModel (pipeline.hpp:24-47) */
+typedef struct cf_pp_cost {
+  double gamma;
+  double alpha;
+  double beta;
+  double backward_multiplier;
+  double hop_latency;
+} cf_pp_cost;
+
+/* TraceEvent (pipeline.hpp:53-58); chunk_id is the plan's chunk id. */
+typedef struct cf_pp_op {
+  int64_t kind;
+  int64_t chunk_id;
+  double start;
+  double end;
+} cf_pp_op;
+
+/* PipelineTrace summary + bubble_ratio (pipeline.hpp:64-72, 325-331). */
+typedef struct cf_pp_result {
+  double makespan;
+  double bubble_ratio;          /* reference convention: recompute = bubble */
+  double occupancy_bubble;      /* SPEC.md:344-345 convention: recompute = busy */
+  int64_t ops_per_stage;        /* every stage runs the same number of ops */
+} cf_pp_result;
+
+/* simulate_state_aware_1f1b (pipeline.hpp:250-319): stage s's op stream is
+ * build_stage_order (:178-210) under retention budget k; backward_first = 1
+ * is DispatchPolicy::kBackwardFirst.  fwd_cost / bwd_cost (optional, one per
+ * plan chunk in plan order) replace the cost model with measured per-chunk
+ * times (simulator-in-the-loop).  ops (optional) receives num_stages x
+ * ops_per_stage records, stage-major, in dispatch order; busy/busy_total
+ * (optional) num_stages entries each. */
+int cf_pp_simulate(const cf_plan* plan, int64_t num_stages, int64_t k,
+                   const cf_pp_cost* cost, int backward_first,
+                   const double* fwd_cost, const double* bwd_cost,
+                   cf_pp_op* ops, double* busy, double* busy_total,
+                   cf_pp_result* result);
+/* simulate_1f1b (pipeline.hpp:218-242): whole sequences as microbatches. */
+int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages,
+                        const cf_pp_cost* cost, cf_pp_op* ops, double* busy,
+                        double* busy_total, cf_pp_result* result);
+/* Layer range [begin, end) that stage `stage` of `num_stages` executes. */
+int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages,
+                       int64_t* begin, int64_t* end);
+
 /* SplitMix64 token payload exactly as chunkflow_main.cpp:427-443: one
  * stream over all sequences in order, next_below(vocab) per token. */
 int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab,

@@ -256,6 +256,26 @@ class Reference(_Lib):
         return mk.value, bb.value
 
 
+    def pp_trace(self, lengths, chunk_size, k, stages, cost=(0.0, 1.0, 0.0, 2.0, 0.0), mode=1,
+                 backward_first=True, ids=None):
+        """Full reference trace: (ops[stages, per, 4] = kind, chunk, start, end;
+        busy; busy_total; makespan; bubble)."""
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        c5 = np.ascontiguousarray(cost, np.float64)
+        per, mk, bb = C.c_int64(), C.c_double(), C.c_double()
+        args = lambda ops, busy, busy_t: (  # noqa: E731
+            _p(ids, PI64), _p(lengths, PI64), I64(len(lengths)), I64(chunk_size), I64(k), I64(stages),
+            _p(c5, PD), C.c_int(mode), C.c_int(int(backward_first)), ops, C.byref(per), busy, busy_t,
+            C.byref(mk), C.byref(bb))
+        self._check(self.lib.cfr_pp_trace(*args(None, None, None)))
+        ops = np.zeros((stages, per.value, 4), np.float64)
+        busy = np.zeros(stages, np.float64)
+        busy_t = np.zeros(stages, np.float64)
+        self._check(self.lib.cfr_pp_trace(*args(_p(ops, PD), _p(busy, PD), _p(busy_t, PD))))
+        return ops, busy, busy_t, mk.value, bb.value
+
+
 def c1_batch(oracle: Oracle):
     """Config C1 canonical batch: synthesize(eval_table5, 32,
     seed=3) plus sequence id 32 of 2048 tokens; tokens SplitMix64(5)."""

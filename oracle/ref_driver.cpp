@@ -287,3 +287,52 @@ int cfr_simulate(const int64_t* ids, const int64_t* lengths, int64_t n,
 }
 
 }  // extern "C"
+
+extern "C" {
+// Full trace export of the reference simulator (pipeline.hpp): per stage the
+// dispatched ops (kind, chunk id, start, end), stage-major; busy/busy_total
+// per stage.  mode 0 = simulate_1f1b, 1 = simulate_state_aware_1f1b.
+// Returns ops per stage through *per (call with ops = NULL to size).
+int cfr_pp_trace(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t cs, int64_t k, int64_t stages,
+                 const double* cost5, int mode, int backward_first, double* ops, int64_t* per, double* busy,
+                 double* busy_total, double* makespan, double* bubble) {
+  return guarded([&] {
+    cf::CostModel cm;
+    cm.gamma = cost5[0];
+    cm.alpha = cost5[1];
+    cm.beta = cost5[2];
+    cm.backward_multiplier = cost5[3];
+    cm.hop_latency = cost5[4];
+    cf::PipelineTrace tr;
+    if (mode == 0) {
+      std::vector<std::int64_t> lens(lengths, lengths + n);
+      tr = cf::simulate_1f1b(lens, static_cast<int>(stages), cm);
+    } else {
+      const cf::ChunkPlan cp = cf::construct_chunks(make_batch(ids, lengths, n, nullptr), cs);
+      cf::PipelineConfig pc;
+      pc.num_stages = static_cast<int>(stages);
+      pc.k = k;
+      pc.chunk_size = cs;
+      tr = cf::simulate_state_aware_1f1b(cp, pc, cm,
+                                         backward_first ? cf::DispatchPolicy::kBackwardFirst
+                                                        : cf::DispatchPolicy::kForwardFirst);
+    }
+    *per = static_cast<int64_t>(tr.stages[0].size());
+    for (size_t s = 0; s < tr.stages.size(); ++s) {
+      if (busy) busy[s] = tr.busy[s];
+      if (busy_total) busy_total[s] = tr.busy_total[s];
+      if (ops)
+        for (size_t i = 0; i < tr.stages[s].size(); ++i) {
+          double* o = ops + 4 * (s * static_cast<size_t>(*per) + i);
+          const cf::TraceEvent& e = tr.stages[s][i];
+          o[0] = static_cast<double>(static_cast<int>(e.kind));
+          o[1] = static_cast<double>(e.chunk_id);
+          o[2] = e.start;
+          o[3] = e.end;
+        }
+    }
+    *makespan = tr.makespan;
+    *bubble = cf::bubble_ratio(tr);
+  });
+}
+}  // extern "C"

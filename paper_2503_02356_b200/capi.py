@@ -26,6 +26,9 @@ DIAG_DT = np.dtype([(k, np.int64) for k in
                     ("peak_retained_tokens", "recompute_token_count",
                      "num_violations")])
 
+PP_OP_DT = np.dtype([("kind", np.int64), ("chunk_id", np.int64), ("start", np.float64), ("end", np.float64)])
+PP_FORWARD, PP_RECOMPUTE, PP_BACKWARD = 0, 1, 2
+
 ARCH_TOY, ARCH_LLAMA = 0, 1
 EPI_BF16, EPI_F32, EPI_F32_ACC, EPI_F32_RES, EPI_BF16_TANH, EPI_BF16_TANHGRAD = range(6)
 
@@ -42,6 +45,16 @@ class ModelCfg(C.Structure):
 class RunOpts(C.Structure):
     _fields_ = [("corrupt_kv_grads", C.c_int32), ("accumulate_grads", C.c_int32),
                 ("normalizer_override", C.c_double)]
+
+
+class PpCost(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("alpha", C.c_double), ("beta", C.c_double),
+                ("backward_multiplier", C.c_double), ("hop_latency", C.c_double)]
+
+
+class PpResult(C.Structure):
+    _fields_ = [("makespan", C.c_double), ("bubble_ratio", C.c_double),
+                ("occupancy_bubble", C.c_double), ("ops_per_stage", C.c_int64)]
 
 
 class RunResult(C.Structure):
@@ -66,7 +79,7 @@ EXPORTS = [
     "cf_last_error", "cf_version", "cf_plan_build", "cf_plan_build_group",
     "cf_plan_counts", "cf_plan_export", "cf_plan_export_groups",
     "cf_plan_violation", "cf_plan_listing", "cf_plan_partition",
-    "cf_plan_rank_tokens", "cf_plan_destroy", "cf_gen_tokens", "cf_synthesize", "cf_sample_batch",
+    "cf_plan_rank_tokens", "cf_plan_destroy", "cf_pp_simulate", "cf_pp_simulate_1f1b", "cf_pp_stage_layers", "cf_gen_tokens", "cf_synthesize", "cf_sample_batch",
     "cf_ctx_create",
     "cf_ctx_destroy", "cf_ctx_stream", "cf_ctx_set_profiling", "cf_nccl_unique_id", "cf_ctx_init_dp",
     "cf_model_create", "cf_model_destroy", "cf_model_num_tensors",
@@ -191,6 +204,50 @@ class Plan:
         if getattr(self, "h", None) and self.h.value and _lib is not None:
             _lib.cf_plan_destroy(self.h)
             self.h = C.c_void_p()
+
+
+def _pp_cost(cost):
+    if isinstance(cost, PpCost):
+        return cost
+    c = dict(gamma=0.0, alpha=1.0, beta=0.0, backward_multiplier=2.0, hop_latency=0.0)
+    c.update(cost or {})
+    return PpCost(**c)
+
+
+def pp_simulate(plan: "Plan", stages, k, cost=None, backward_first=True, fwd_cost=None, bwd_cost=None):
+    """simulate_state_aware_1f1b + bubble_ratio (pipeline.hpp:250-331).
+    Returns (ops[stages, per] of PP_OP_DT, busy, busy_total, PpResult)."""
+    c = _pp_cost(cost)
+    r = PpResult()
+    fw = None if fwd_cost is None else np.ascontiguousarray(fwd_cost, np.float64)
+    bw = None if bwd_cost is None else np.ascontiguousarray(bwd_cost, np.float64)
+    args = (plan.h, C.c_int64(stages), C.c_int64(k), C.byref(c), C.c_int(int(backward_first)),
+            None if fw is None else _p(fw), None if bw is None else _p(bw))
+    check(lib().cf_pp_simulate(*args, None, None, None, C.byref(r)))
+    ops = np.zeros((stages, r.ops_per_stage), PP_OP_DT)
+    busy = np.zeros(stages, np.float64)
+    busy_t = np.zeros(stages, np.float64)
+    check(lib().cf_pp_simulate(*args, _p(ops), _p(busy), _p(busy_t), C.byref(r)))
+    return ops, busy, busy_t, r
+
+
+def pp_simulate_1f1b(lengths, stages, cost=None):
+    """simulate_1f1b + bubble_ratio (pipeline.hpp:218-242, 325-331)."""
+    lengths = np.ascontiguousarray(lengths, np.int64)
+    c = _pp_cost(cost)
+    r = PpResult()
+    ops = np.zeros((stages, 2 * len(lengths)), PP_OP_DT)
+    busy = np.zeros(stages, np.float64)
+    busy_t = np.zeros(stages, np.float64)
+    check(lib().cf_pp_simulate_1f1b(_p(lengths), C.c_int64(len(lengths)), C.c_int64(stages), C.byref(c),
+                                    _p(ops), _p(busy), _p(busy_t), C.byref(r)))
+    return ops, busy, busy_t, r
+
+
+def pp_stage_layers(layers, stage, stages):
+    b, e = C.c_int64(), C.c_int64()
+    check(lib().cf_pp_stage_layers(C.c_int64(layers), C.c_int64(stage), C.c_int64(stages), C.byref(b), C.byref(e)))
+    return b.value, e.value
 
 
 def synthesize(count, seed, preset=1, bounds=(), fracs=(), max_length=0):

@@ -5,6 +5,7 @@
 
 #include "../../../include/chunkflow_b200.h"
 #include "../host/plan.hpp"
+#include "../host/pp.hpp"
 #include "capi_util.hpp"
 
 namespace cfb {
@@ -174,6 +175,83 @@ int cf_gen_tokens(const int64_t* lengths, int64_t n, int64_t vocab, uint64_t see
         tokens_out[o++] = static_cast<int32_t>(r % v);
       }
   });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- pipeline
+namespace {
+
+cfb::PpCost to_cost(const cf_pp_cost* c) {
+  cfb::PpCost pc;
+  if (c) {
+    pc.gamma = c->gamma;
+    pc.alpha = c->alpha;
+    pc.beta = c->beta;
+    pc.bwd_mult = c->backward_multiplier;
+    pc.hop = c->hop_latency;
+  }
+  return pc;
+}
+
+void emit(const cfb::PpChunks& info, const cfb::PpTrace& tr, cf_pp_op* ops, double* busy, double* busy_total,
+          cf_pp_result* res) {
+  const size_t per = tr.stages.empty() ? 0 : tr.stages[0].size();
+  for (size_t s = 0; s < tr.stages.size(); ++s) {
+    if (tr.stages[s].size() != per) throw std::logic_error("stages ran different op counts");
+    if (busy) busy[s] = tr.busy[s];
+    if (busy_total) busy_total[s] = tr.busy_total[s];
+    if (ops)
+      for (size_t i = 0; i < per; ++i) {
+        const cfb::PpTimedOp& o = tr.stages[s][i];
+        ops[s * per + i] = {o.kind, info.ids[static_cast<size_t>(o.pos)], o.start, o.end};
+      }
+  }
+  if (res) {
+    res->makespan = tr.makespan;
+    res->bubble_ratio = cfb::pp_bubble(tr);
+    double idle = 0;
+    for (double b : tr.busy_total) idle += tr.makespan - b;
+    res->occupancy_bubble = tr.makespan > 0 ? idle / (static_cast<double>(tr.stages.size()) * tr.makespan) : 0.0;
+    res->ops_per_stage = static_cast<int64_t>(per);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cf_pp_simulate(const cf_plan* plan, int64_t num_stages, int64_t k, const cf_pp_cost* cost, int backward_first,
+                   const double* fwd_cost, const double* bwd_cost, cf_pp_op* ops, double* busy, double* busy_total,
+                   cf_pp_result* result) {
+  return cfb::guard([&] {
+    if (num_stages < 1) throw cfb::ValidationError("num_stages must be at least 1");
+    cfb::PpChunks info = cfb::pp_chunks(plan->p, k, to_cost(cost));
+    for (size_t i = 0; i < info.fwd.size(); ++i) {
+      if (fwd_cost) info.fwd[i] = fwd_cost[i];
+      if (bwd_cost) info.bwd[i] = bwd_cost[i];
+      if (info.fwd[i] < 0 || info.bwd[i] < 0) throw cfb::ValidationError("measured costs must be non-negative");
+    }
+    std::vector<std::vector<cfb::PpOp>> orders;
+    for (int64_t s = 0; s < num_stages; ++s)
+      orders.push_back(cfb::pp_stage_order(info, s, num_stages, backward_first != 0));
+    emit(info, cfb::pp_dispatch(orders, info.fwd, info.bwd, to_cost(cost).hop), ops, busy, busy_total, result);
+  });
+}
+
+int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages, const cf_pp_cost* cost,
+                        cf_pp_op* ops, double* busy, double* busy_total, cf_pp_result* result) {
+  return cfb::guard([&] {
+    if (num_stages < 1) throw cfb::ValidationError("num_stages must be at least 1");
+    const cfb::PpChunks info = cfb::pp_microbatches(std::vector<int64_t>(lengths, lengths + n), to_cost(cost));
+    std::vector<std::vector<cfb::PpOp>> orders;
+    for (int64_t s = 0; s < num_stages; ++s) orders.push_back(cfb::pp_stage_order(info, s, num_stages, false));
+    emit(info, cfb::pp_dispatch(orders, info.fwd, info.bwd, to_cost(cost).hop), ops, busy, busy_total, result);
+  });
+}
+
+int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages, int64_t* begin, int64_t* end) {
+  return cfb::guard([&] { cfb::pp_stage_layers(num_layers, stage, num_stages, begin, end); });
 }
 
 }  // extern "C"

@@ -1,0 +1,166 @@
+// Pipeline-parallel planning: see pp.hpp.
+#include "pp.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <set>
+#include <stdexcept>
+
+namespace cfb {
+
+void PpCost::validate() const {
+  if (gamma < 0 || alpha < 0 || beta < 0 || hop < 0)
+    throw ValidationError("cost-model coefficients must be non-negative");
+  if (bwd_mult <= 0) throw ValidationError("backward multiplier must be positive");
+}
+
+PpChunks pp_chunks(const Plan& plan, int64_t k, const PpCost& cost) {
+  if (plan.chunks.empty()) throw ValidationError("chunk plan has no chunks");
+  if (k < 1) throw ValidationError("retention budget k must be at least 1");
+  cost.validate();
+  const size_t m = plan.chunks.size();
+  PpChunks c;
+  c.fwd.resize(m);
+  c.bwd.resize(m);
+  c.discarded.assign(m, 0);
+  c.ids.resize(m);
+  c.prefix.assign(m, 0);
+  std::map<int64_t, size_t> pos;
+  for (size_t i = 0; i < m; ++i) pos[plan.chunks[i].id] = i;
+  // group id -> running token count while walking members in index order
+  for (const auto& [g, members] : plan.groups) {
+    int64_t run = 0;
+    const int64_t n = static_cast<int64_t>(members.size());
+    for (int64_t j = 0; j < n; ++j) {
+      const size_t p = pos.at(members[static_cast<size_t>(j)]);
+      c.prefix[p] = run;
+      run += plan.chunks[p].total;
+      if (n > k && plan.chunks[p].index < n - k) c.discarded[p] = 1;
+    }
+  }
+  for (size_t i = 0; i < m; ++i) {
+    const Chunk& ch = plan.chunks[i];
+    c.ids[i] = ch.id;
+    const double len = static_cast<double>(ch.total);
+    const double pre = ch.kind == kDependent ? static_cast<double>(c.prefix[i]) : 0.0;
+    c.fwd[i] = cost.fwd(len, pre);
+    c.bwd[i] = cost.bwd_mult * c.fwd[i];
+  }
+  std::set<int64_t> seen;
+  for (size_t i = 0; i < m; ++i) {
+    const Chunk& ch = plan.chunks[i];
+    if (ch.kind != kDependent) {
+      c.bwd_queue.push_back(static_cast<int64_t>(i));
+    } else if (seen.insert(ch.group).second) {
+      const std::vector<int64_t>& members = plan.groups.at(ch.group);
+      for (auto it = members.rbegin(); it != members.rend(); ++it)
+        c.bwd_queue.push_back(static_cast<int64_t>(pos.at(*it)));
+    }
+  }
+  return c;
+}
+
+PpChunks pp_microbatches(const std::vector<int64_t>& lengths, const PpCost& cost) {
+  if (lengths.empty()) throw ValidationError("no microbatches to simulate");
+  cost.validate();
+  PpChunks c;
+  for (size_t i = 0; i < lengths.size(); ++i) {
+    c.fwd.push_back(cost.fwd(static_cast<double>(lengths[i]), 0.0));
+    c.bwd.push_back(cost.bwd_mult * c.fwd.back());
+    c.discarded.push_back(0);
+    c.ids.push_back(static_cast<int64_t>(i));
+    c.bwd_queue.push_back(static_cast<int64_t>(i));
+    c.prefix.push_back(0);
+  }
+  return c;
+}
+
+std::vector<PpOp> pp_stage_order(const PpChunks& c, int64_t stage, int64_t stages, bool backward_first) {
+  const int64_t m = static_cast<int64_t>(c.fwd.size());
+  std::vector<PpOp> ops;
+  ops.reserve(static_cast<size_t>(2 * m + 1));
+  int64_t next = 0;  // forwards are issued in plan order; `next` is the first not yet issued
+  const int64_t warm = std::min(stages - stage, m);
+  while (next < warm) ops.push_back({kPpForward, next++});
+  for (int64_t b : c.bwd_queue) {
+    if (!backward_first && next < m) ops.push_back({kPpForward, next++});
+    while (next <= b) ops.push_back({kPpForward, next++});  // enablers: b and everything before it
+    if (c.discarded[static_cast<size_t>(b)]) ops.push_back({kPpRecompute, b});
+    ops.push_back({kPpBackward, b});
+    if (backward_first && next < m) ops.push_back({kPpForward, next++});
+  }
+  return ops;
+}
+
+PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vector<double>& fwd,
+                    const std::vector<double>& bwd, double hop) {
+  const int64_t P = static_cast<int64_t>(orders.size());
+  const size_t m = fwd.size();
+  PpTrace t;
+  t.stages.resize(static_cast<size_t>(P));
+  t.busy.assign(static_cast<size_t>(P), 0.0);
+  t.busy_total.assign(static_cast<size_t>(P), 0.0);
+  const double kUnset = -1.0;
+  // end time of (stage, first-pass forward | backward, position)
+  std::vector<std::vector<double>> f_end(static_cast<size_t>(P), std::vector<double>(m, kUnset));
+  std::vector<std::vector<double>> b_end(static_cast<size_t>(P), std::vector<double>(m, kUnset));
+  std::vector<size_t> next(static_cast<size_t>(P), 0);
+  std::vector<double> free_at(static_cast<size_t>(P), 0.0);
+  size_t left = 0;
+  for (const auto& o : orders) left += o.size();
+  while (left) {
+    bool moved = false;
+    for (int64_t s = 0; s < P; ++s) {
+      const auto& ord = orders[static_cast<size_t>(s)];
+      size_t& i = next[static_cast<size_t>(s)];
+      for (; i < ord.size(); ++i) {
+        const PpOp& op = ord[i];
+        const size_t p = static_cast<size_t>(op.pos);
+        double ready = 0.0;
+        if (op.kind == kPpForward) {
+          if (s > 0) {  // activation from the previous stage
+            const double e = f_end[static_cast<size_t>(s - 1)][p];
+            if (e == kUnset) break;
+            ready = e + hop;
+          }
+        } else if (s + 1 < P) {  // F' and B wait for the next stage's backward
+          const double e = b_end[static_cast<size_t>(s + 1)][p];
+          if (e == kUnset) break;
+          ready = e + hop;
+        }
+        const double dur = op.kind == kPpBackward ? bwd[p] : fwd[p];
+        const double start = std::max(free_at[static_cast<size_t>(s)], ready);
+        const double end = start + dur;
+        t.stages[static_cast<size_t>(s)].push_back({op.kind, op.pos, start, end});
+        if (op.kind == kPpForward) f_end[static_cast<size_t>(s)][p] = end;
+        if (op.kind == kPpBackward) b_end[static_cast<size_t>(s)][p] = end;
+        free_at[static_cast<size_t>(s)] = end;
+        t.busy_total[static_cast<size_t>(s)] += dur;
+        if (op.kind != kPpRecompute) t.busy[static_cast<size_t>(s)] += dur;
+        t.makespan = std::max(t.makespan, end);
+        --left;
+        moved = true;
+      }
+    }
+    if (!moved) throw std::logic_error("pipeline dispatch reached a dependency deadlock");
+  }
+  return t;
+}
+
+double pp_bubble(const PpTrace& t) {
+  if (t.stages.empty()) throw ValidationError("empty trace");
+  if (t.makespan <= 0.0) return 0.0;
+  double idle = 0.0;
+  for (double b : t.busy) idle += t.makespan - b;
+  return idle / (static_cast<double>(t.stages.size()) * t.makespan);
+}
+
+void pp_stage_layers(int64_t layers, int64_t stage, int64_t stages, int64_t* begin, int64_t* end) {
+  if (stages < 1 || stage < 0 || stage >= stages) throw ValidationError("stage index out of range");
+  if (layers < stages) throw ValidationError("fewer layers than pipeline stages");
+  *begin = layers * stage / stages;
+  *end = layers * (stage + 1) / stages;
+}
+
+}  // namespace cfb

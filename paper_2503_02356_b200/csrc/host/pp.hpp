@@ -1,0 +1,77 @@
+// Pipeline-parallel planning for the chunk-aware 1F1B schedule (config C5).
+//
+// The reference only *simulates* pipelines (pipeline.hpp:164-331); here the
+// same per-stage instruction streams drive the real stage executor
+// (runtime/engine.cu), and the same earliest-feasible dispatch times them
+// for the bubble prediction.  Output is bit-exact with the reference
+// (tests/test_pp_plan.py pins op order, start/end times and bubble ratio).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace cfb {
+
+// TraceEventKind (pipeline.hpp:51): first-pass forward, just-in-time
+// recompute forward of a discarded chunk, backward.
+enum : int64_t { kPpForward = 0, kPpRecompute = 1, kPpBackward = 2 };
+
+// CostModel (pipeline.hpp:24-47): fwd = gamma + alpha*len + beta*len^2 +
+// beta*len*prefix (beta*len^2, not the causal half: Appendix B-8),
+// bwd = backward_multiplier * fwd.
+struct PpCost {
+  double gamma = 0.0, alpha = 1.0, beta = 0.0, bwd_mult = 2.0, hop = 0.0;
+  void validate() const;
+  double fwd(double len, double prefix) const { return gamma + alpha * len + beta * len * len + beta * len * prefix; }
+};
+
+struct PpOp {
+  int64_t kind;
+  int64_t pos;  // plan position (index into plan.chunks)
+};
+
+// ChunkTimingInfo (pipeline.hpp:164-170) for one microbatch list.
+struct PpChunks {
+  std::vector<double> fwd, bwd;
+  std::vector<uint8_t> discarded;     // needs F' before its B
+  std::vector<int64_t> ids;           // chunk id per position
+  std::vector<int64_t> bwd_queue;     // plan order, dependent groups reversed
+  std::vector<int64_t> prefix;        // tokens of earlier group members
+};
+
+// State-aware view of a chunk plan under retention budget k
+// (simulate_state_aware_1f1b, pipeline.hpp:258-304).
+PpChunks pp_chunks(const Plan& plan, int64_t k, const PpCost& cost);
+// Plain 1F1B over whole sequences (simulate_1f1b, pipeline.hpp:218-236).
+PpChunks pp_microbatches(const std::vector<int64_t>& lengths, const PpCost& cost);
+
+// Per-stage static op stream (build_stage_order, pipeline.hpp:178-210):
+// min(P-s, M) warm-up forwards, then per backward-queue entry the enabling
+// forwards, F' for a discarded chunk, B, and one more forward (backward-
+// first policy; forward-first places that forward before the entry).
+std::vector<PpOp> pp_stage_order(const PpChunks& c, int64_t stage, int64_t stages, bool backward_first);
+
+struct PpTimedOp {
+  int64_t kind, pos;
+  double start, end;
+};
+struct PpTrace {
+  std::vector<std::vector<PpTimedOp>> stages;
+  double makespan = 0.0;
+  std::vector<double> busy, busy_total;  // busy excludes recompute forwards
+};
+
+// Earliest-feasible list scheduling over fixed stage orders (run_dispatch,
+// pipeline.hpp:98-162).  Throws std::logic_error on a dependency deadlock.
+PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vector<double>& fwd,
+                    const std::vector<double>& bwd, double hop);
+// bubble_ratio (pipeline.hpp:325-331): recompute counts as bubble.
+double pp_bubble(const PpTrace& t);
+
+// Layer range [begin, end) of a stage under the even split the executor
+// uses (embedding on stage 0; final norm + head + loss on the last stage).
+void pp_stage_layers(int64_t layers, int64_t stage, int64_t stages, int64_t* begin, int64_t* end);
+
+}  // namespace cfb

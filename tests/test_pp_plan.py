@@ -1,0 +1,130 @@
+"""Pipeline-parallel planning (product C++, host/pp.cpp through the C-ABI) is
+bit-exact with the reference simulator (pipeline.hpp): per-stage op streams
+(build_stage_order :178-210), dispatch times (run_dispatch :98-162),
+makespan and bubble_ratio (:325-331), for the state-aware and the plain
+1F1B schedules.  The reference runs from oracle/_ref (compiled in place)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2503_02356_b200 as cf
+from paper_2503_02356_b200 import capi
+from oracle.oracle import c1_batch
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.json")))
+
+
+def _product_trace(lengths, cs, k, stages, cost, backward_first=True):
+    plan = cf.Plan.build(lengths, cs, k)
+    c = dict(zip(("gamma", "alpha", "beta", "backward_multiplier", "hop_latency"), cost))
+    ops, busy, busy_t, r = capi.pp_simulate(plan, stages, k, c, backward_first)
+    return ops, busy, busy_t, r
+
+
+def _compare(reference, lengths, cs, k, stages, cost=(0.0, 1.0, 0.0, 2.0, 0.0), backward_first=True):
+    rops, rbusy, rbusy_t, rmk, rbb = reference.pp_trace(lengths, cs, k, stages, cost, 1, backward_first)
+    ops, busy, busy_t, r = _product_trace(lengths, cs, k, stages, cost, backward_first)
+    assert ops.shape == rops.shape[:2]
+    assert np.array_equal(ops["kind"], rops[..., 0].astype(np.int64))
+    assert np.array_equal(ops["chunk_id"], rops[..., 1].astype(np.int64))
+    # bitwise: same additions in the same order
+    assert np.array_equal(ops["start"], rops[..., 2]) and np.array_equal(ops["end"], rops[..., 3])
+    assert np.array_equal(busy, rbusy) and np.array_equal(busy_t, rbusy_t)
+    assert r.makespan == rmk and r.bubble_ratio == rbb
+    return r
+
+
+def test_worked_batch_golden():
+    """test_pipeline.cpp:141-211 / SURVEY §6: 56 / 54 / 46 / 60 units."""
+    sim = GOLD["simulator"]
+    _, _, _, r = capi.pp_simulate_1f1b([1, 1, 2, 4], 4)
+    assert (r.makespan, r.bubble_ratio) == tuple(sim["1f1b"])
+    for key, cs, k in (("sa_k1", 2, 1), ("sa_k2", 2, 2), ("sa_cs4", 4, 1)):
+        _, _, _, r = capi.pp_simulate(cf.Plan.build([1, 1, 2, 4], cs, k), 4, k)
+        assert (r.makespan, r.bubble_ratio) == tuple(sim[key]), key
+    assert round(100 * capi.pp_simulate(cf.Plan.build([1, 1, 2, 4], 2, 1), 4, 1)[3].bubble_ratio, 2) == 55.56
+
+
+@pytest.mark.parametrize("stages", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("cs,k", [(2, 1), (2, 2), (4, 1), (1, 1), (1, 3)])
+def test_worked_batch_traces(reference, stages, cs, k):
+    _compare(reference, [1, 1, 2, 4], cs, k, stages)
+    _compare(reference, [1, 1, 2, 4], cs, k, stages, backward_first=False)
+    _compare(reference, [1, 1, 2, 4], cs, k, stages, cost=(0.5, 1.0, 0.25, 1.5, 0.75))
+
+
+def test_c1_batch_traces(reference, oracle):
+    lengths, _ = c1_batch(oracle)
+    for stages in (2, 4, 8):
+        for k in (1, 2, 3):
+            _compare(reference, lengths, 512, k, stages, cost=(0.0, 1.0, 1.05e-5, 2.0, 3.0))
+
+
+def test_random_traces(reference):
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        n = int(rng.integers(1, 40))
+        cs = int(rng.integers(4, 300))
+        lengths = rng.integers(1, 4 * cs, n)
+        stages = int(rng.integers(1, 9))
+        k = int(rng.integers(1, 5))
+        cost = (float(rng.random()), float(rng.random()) + 0.1, float(rng.random()) * 1e-3,
+                float(rng.random()) * 3 + 0.5, float(rng.random()) * 5)
+        _compare(reference, lengths, cs, k, stages, cost, backward_first=bool(rng.integers(0, 2)))
+
+
+def test_1f1b_random(reference):
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        lengths = rng.integers(1, 500, int(rng.integers(1, 30)))
+        stages = int(rng.integers(1, 9))
+        cost = (0.0, 1.0, float(rng.random()) * 1e-3, 2.0, float(rng.random()))
+        rops, rbusy, rbusy_t, rmk, rbb = reference.pp_trace(lengths, 1, 1, stages, cost, 0, False)
+        ops, busy, busy_t, r = capi.pp_simulate_1f1b(
+            lengths, stages, dict(zip(("gamma", "alpha", "beta", "backward_multiplier", "hop_latency"), cost)))
+        assert np.array_equal(ops["kind"], rops[..., 0].astype(np.int64))
+        assert np.array_equal(ops["chunk_id"], rops[..., 1].astype(np.int64))
+        assert np.array_equal(ops["start"], rops[..., 2]) and np.array_equal(ops["end"], rops[..., 3])
+        assert (r.makespan, r.bubble_ratio) == (rmk, rbb)
+
+
+def test_measured_costs_override():
+    """Simulator-in-the-loop: per-chunk measured costs replace the model."""
+    plan = cf.Plan.build([1, 1, 2, 4], 2, 1)
+    n = plan.counts()[0]
+    fw = np.arange(1, n + 1, dtype=np.float64)
+    _, _, _, r1 = capi.pp_simulate(plan, 2, 1, fwd_cost=fw, bwd_cost=2 * fw)
+    _, _, _, r2 = capi.pp_simulate(plan, 2, 1, cost={"alpha": 0.0, "gamma": 1.0})
+    assert r1.makespan > r2.makespan > 0
+    ops, busy, busy_t, r = capi.pp_simulate(plan, 1, 1, fwd_cost=fw, bwd_cost=2 * fw)
+    # one stage: no bubble except recompute time
+    assert busy_t[0] == r.makespan and r.occupancy_bubble == 0.0
+
+
+def test_stage_ops_cover_every_chunk():
+    plan = cf.Plan.build([300, 40, 5000, 900, 77], 1024, 2)
+    ch = plan.export()[0]
+    ops, _, _, r = capi.pp_simulate(plan, 4, 2)
+    for s in range(4):
+        f = ops[s][ops[s]["kind"] == capi.PP_FORWARD]["chunk_id"]
+        b = ops[s][ops[s]["kind"] == capi.PP_BACKWARD]["chunk_id"]
+        assert sorted(f.tolist()) == sorted(ch["chunk_id"].tolist()) == sorted(b.tolist())
+        assert f.tolist() == ch["chunk_id"].tolist()  # forwards in plan order
+
+
+def test_validation_errors():
+    plan = cf.Plan.build([1, 1, 2, 4], 2, 1)
+    with pytest.raises(capi.CfError):
+        capi.pp_simulate(plan, 0, 1)
+    with pytest.raises(capi.CfError):
+        capi.pp_simulate(plan, 2, 0)
+    with pytest.raises(capi.CfError):
+        capi.pp_simulate(plan, 2, 1, cost={"alpha": -1.0})
+    with pytest.raises(capi.CfError):
+        capi.pp_simulate(plan, 2, 1, cost={"backward_multiplier": 0.0})
+    assert capi.pp_stage_layers(64, 3, 4) == (48, 64)
+    assert capi.pp_stage_layers(2, 1, 2) == (1, 2)
+    with pytest.raises(capi.CfError):
+        capi.pp_stage_layers(2, 0, 3)
