@@ -305,6 +305,33 @@ int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids,
                      double normalizer_override, cf_run_result* result);
 int cf_ctx_synchronize(cf_ctx* ctx);
 
+/* ---- pipeline-parallel execution (config C5; the reference only simulates
+ *      this, pipeline.hpp:214-319) ---- */
+
+/* Stage `stage` of `num_stages` of the model cfg describes: global layers
+ * cf_pp_stage_layers(...), the embedding on stage 0, final norm + head + loss
+ * on the last stage.  Weights equal the full model's (same SplitMix64 draws);
+ * tensor names keep global layer numbers. */
+int cf_model_create_stage(cf_ctx* ctx, const cf_model_cfg* cfg, int64_t stage,
+                          int64_t num_stages, cf_model** out);
+/* PP x DP communicators: rank = replica * num_stages + stage; id128 from
+ * cf_nccl_unique_id on rank 0.  Gradients are all-reduced over the ranks of
+ * the same stage; activations/gradients cross stage links with NCCL p2p. */
+int cf_ctx_init_pp(cf_ctx* ctx, int rank, int world, int num_stages,
+                   const uint8_t* id128);
+/* This rank's stage of the chunk-aware 1F1B step: runs the stage's op stream
+ * (build_stage_order semantics, retention budget k) with fp32 [T, d]
+ * activations sent up and gradients sent down.  result->loss is the loss on
+ * the last stage (0 elsewhere). */
+int cf_pp_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, int64_t k,
+                   const cf_run_opts* opts, cf_run_result* result);
+/* Every stage of one pipeline on this context's device (models[i] = stage
+ * i): the same op streams in dispatch order with in-memory hand-over.
+ * Gradients are bitwise those of cf_step_run on the unsplit model. */
+int cf_pp_run_local(cf_ctx* ctx, cf_model* const* models, int64_t num_stages,
+                    cf_step* step, int64_t k, const cf_run_opts* opts,
+                    cf_run_result* result);
+
 /* ---- operator level (kernel unit tests); all pointers are device ---- */
 
 /* C[M,N] (+)= sum_k A(m,k) B(n,k).  a_kmajor: A stored [M,K] (else [K,M]);

@@ -86,7 +86,8 @@ EXPORTS = [
     "cf_model_tensor_info", "cf_model_get_param", "cf_model_set_param",
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
-    "cf_step_destroy", "cf_backward_full", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
+    "cf_pp_run_local", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None
@@ -296,6 +297,10 @@ class Context:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid else None
         check(lib().cf_ctx_init_dp(self.h, C.c_int(rank), C.c_int(world), buf))
 
+    def init_pp(self, rank, world, num_stages, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        check(lib().cf_ctx_init_pp(self.h, C.c_int(rank), C.c_int(world), C.c_int(num_stages), buf))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = (C.c_uint8 * 128)()
@@ -326,11 +331,17 @@ class Context:
 class Model:
     """Device model (ToyModelParams / Llama-shaped) with fp32 gradients."""
 
-    def __init__(self, ctx: Context, cfg: ModelCfg):
+    def __init__(self, ctx: Context, cfg: ModelCfg, stage=None, num_stages=1):
+        """Whole model, or (stage, num_stages) = one pipeline stage's slice."""
         self.ctx = ctx
         self.cfg = cfg
         self.h = C.c_void_p()
-        check(lib().cf_model_create(ctx.h, C.byref(cfg), C.byref(self.h)))
+        self.stage, self.num_stages = (0, 1) if stage is None else (stage, num_stages)
+        if stage is None:
+            check(lib().cf_model_create(ctx.h, C.byref(cfg), C.byref(self.h)))
+        else:
+            check(lib().cf_model_create_stage(ctx.h, C.byref(cfg), C.c_int64(stage), C.c_int64(num_stages),
+                                              C.byref(self.h)))
 
     def num_tensors(self):
         return lib().cf_model_num_tensors(self.h)
@@ -414,6 +425,22 @@ class Step:
         o = RunOpts(int(corrupt), int(accumulate), normalizer)
         r = RunResult()
         check(lib().cf_step_run(self.model.ctx.h, self.model.h, self.h, C.byref(o), C.byref(r)))
+        return r
+
+    def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
+        """This rank's pipeline stage (cf_pp_step_run; needs Context.init_pp)."""
+        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        r = RunResult()
+        check(lib().cf_pp_step_run(self.model.ctx.h, self.model.h, self.h, C.c_int64(k), C.byref(o), C.byref(r)))
+        return r
+
+    def run_pp_local(self, models, k, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
+        """All pipeline stages on this device (cf_pp_run_local)."""
+        arr = (C.c_void_p * len(models))(*[m.h.value for m in models])
+        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        r = RunResult()
+        check(lib().cf_pp_run_local(self.model.ctx.h, arr, C.c_int64(len(models)), self.h, C.c_int64(k),
+                                    C.byref(o), C.byref(r)))
         return r
 
     def close(self):

@@ -98,6 +98,56 @@ int cf_model_create(cf_ctx* ctx, const cf_model_cfg* cfg, cf_model** out) {
   });
 }
 
+int cf_model_create_stage(cf_ctx* ctx, const cf_model_cfg* cfg, int64_t stage, int64_t num_stages, cf_model** out) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(cfg, "cfg");
+    need(out, "out");
+    auto h = std::make_unique<cf_model>();
+    h->ctx = ctx;
+    h->m = cfb::model_create(&ctx->c, *cfg, stage, num_stages);
+    *out = h.release();
+  });
+}
+
+int cf_ctx_init_pp(cf_ctx* ctx, int rank, int world, int num_stages, const uint8_t* id128) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(id128, "nccl id");
+    cfb::pp_init(&ctx->c, rank, world, num_stages, id128);
+  });
+}
+
+int cf_pp_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, int64_t k, const cf_run_opts* opts,
+                   cf_run_result* result) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    need(step, "step");
+    cf_run_opts o{};
+    if (opts) o = *opts;
+    cfb::pp_step_run(&ctx->c, model->m, step, k, o, result);
+  });
+}
+
+int cf_pp_run_local(cf_ctx* ctx, cf_model* const* models, int64_t num_stages, cf_step* step, int64_t k,
+                    const cf_run_opts* opts, cf_run_result* result) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(models, "models");
+    need(step, "step");
+    if (num_stages < 1) throw cfb::ValidationError("num_stages must be at least 1");
+    std::vector<cfb::Model*> ms;
+    for (int64_t s = 0; s < num_stages; ++s) {
+      need(models[s], "models[i]");
+      ms.push_back(models[s]->m);
+    }
+    cf_run_opts o{};
+    if (opts) o = *opts;
+    cfb::pp_step_run_local(&ctx->c, ms.data(), num_stages, step, k, o, result);
+  });
+}
+
 void cf_model_destroy(cf_model* model) {
   if (!model) return;
   cfb::model_destroy(model->m);

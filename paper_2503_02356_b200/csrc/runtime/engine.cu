@@ -23,10 +23,12 @@
 #include <memory>
 #include <numeric>
 #include <set>
+#include <tuple>
 
 #include "../capi/capi_util.hpp"
 #include "../kernels/attention_tc.h"
 #include "../kernels/gemm.h"
+#include "../host/pp.hpp"
 #include "engine.hpp"
 
 namespace cfb {
@@ -71,6 +73,9 @@ struct Nccl {
   int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   const char* (*err)(int) = nullptr;
   void* init_rank = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*split)(void*, int, int, void**, void*) = nullptr;  // ncclCommSplit (NCCL >= 2.18)
 };
 struct Id128 {
   char b[128];
@@ -85,6 +90,9 @@ Nccl& nccl() {
         dlsym(n.h, "ncclAllReduce"));
     n.err = reinterpret_cast<const char* (*)(int)>(dlsym(n.h, "ncclGetErrorString"));
     n.init_rank = dlsym(n.h, "ncclCommInitRank");
+    n.send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(n.h, "ncclSend"));
+    n.recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(n.h, "ncclRecv"));
+    n.split = reinterpret_cast<int (*)(void*, int, int, void**, void*)>(dlsym(n.h, "ncclCommSplit"));
     if (!n.get_id || !n.all_reduce || !n.init_rank) throw NcclError("NCCL symbols missing");
   }
   return n;
@@ -92,7 +100,7 @@ Nccl& nccl() {
 void nccl_check(int r, const char* what) {
   if (r != 0) throw NcclError(std::string(what) + ": " + (nccl().err ? nccl().err(r) : "error"));
 }
-constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0;
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclNoColor = -1;
 
 }  // namespace
 
@@ -111,8 +119,57 @@ void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id) {
   ctx->world = world;
 }
 
+// Pipeline x data parallel layout (config C5): rank = replica * stages +
+// stage.  From one world communicator: the DP group of each stage (same
+// stage across replicas) and, for every neighbouring stage pair of a
+// replica, two 2-rank links (activations up, gradients down), each used by
+// exactly one sender and one receiver in the same op order on both sides —
+// forwards in plan order, backwards in backward-queue order — so the
+// streams of different links can never wait on each other in a cycle.
+void pp_init(Ctx* ctx, int rank, int world, int stages, const uint8_t* id) {
+  if (stages < 1 || world % stages) throw ValidationError("world size must be a multiple of the stage count");
+  if (rank < 0 || rank >= world) throw ValidationError("bad rank");
+  Nccl& n = nccl();
+  if (!n.split || !n.send || !n.recv) throw NcclError("NCCL without ncclCommSplit/ncclSend/ncclRecv");
+  Id128 u;
+  std::memcpy(u.b, id, 128);
+  auto init = reinterpret_cast<int (*)(void**, int, Id128, int)>(n.init_rank);
+  CK(cudaSetDevice(ctx->device));
+  void* world_comm = nullptr;
+  nccl_check(init(&world_comm, world, u, rank), "ncclCommInitRank");
+  const int s = rank % stages, rep = rank / stages, dp = world / stages;
+  ctx->stage = s;
+  ctx->stages = stages;
+  void* dpc = nullptr;
+  nccl_check(n.split(world_comm, s, rep, &dpc, nullptr), "ncclCommSplit(dp)");
+  if (dp > 1) {
+    ctx->nccl_comm = dpc;
+    ctx->rank = rep;
+    ctx->world = dp;
+  }
+  // link j joins stages j and j+1 of a replica; even links first, then odd
+  auto link_color = [&](int parity) {
+    if (s % 2 == parity && s + 1 < stages) return rep * stages + s;  // lower end of link s
+    if (s % 2 != parity && s > 0) return rep * stages + s - 1;       // upper end of link s-1
+    return kNcclNoColor;
+  };
+  for (int parity = 0; parity < 2; ++parity)
+    for (int dir = 0; dir < 2; ++dir) {
+      void* c = nullptr;
+      nccl_check(n.split(world_comm, link_color(parity), s, &c, nullptr), "ncclCommSplit(link)");
+      if (!c) continue;
+      const bool up = s % 2 == parity;  // this link goes to stage s+1
+      if (up)
+        (dir == 0 ? ctx->act_up : ctx->grad_up) = c;
+      else
+        (dir == 0 ? ctx->act_down : ctx->grad_down) = c;
+    }
+  for (auto& ls : ctx->link_stream)
+    if (!ls) CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+}
+
 // ------------------------------------------------------------------ model
-Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
+Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage, int64_t stages) {
   auto m = std::make_unique<Model>();
   m->ctx = ctx;
   m->cfg = cfg;
@@ -128,7 +185,10 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
   m->KVH = cfg.num_kv_heads;
   m->dh = m->d / m->H;
   m->kvw = m->KVH * m->dh;
-  m->L = cfg.num_layers;
+  pp_stage_layers(cfg.num_layers, stage, stages, &m->l_begin, &m->l_end);
+  m->L = m->l_end - m->l_begin;
+  m->has_embed = stage == 0;
+  m->has_head = stage == stages - 1;
   m->ffn = m->llama ? cfg.ffn_width : 2 * m->d;
   if (m->ffn < 1) throw ValidationError("llama arch needs ffn_width");
   if (m->llama && (m->dh % 2)) throw ValidationError("RoPE needs an even head dim");
@@ -146,7 +206,7 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
     bool f32;
   };
   std::vector<Piece> pieces;
-  pieces.push_back({m->V * m->d, false});  // emb
+  if (m->has_embed) pieces.push_back({m->V * m->d, false});  // emb
   for (int64_t l = 0; l < m->L; ++l) {
     pieces.push_back({m->d * m->qkv_w, false});
     pieces.push_back({m->d * m->d, false});
@@ -157,8 +217,10 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
       pieces.push_back({m->d, true});
     }
   }
-  if (m->llama) pieces.push_back({m->d, true});
-  pieces.push_back({m->d * Vp, false});  // head [d, Vp]
+  if (m->has_head) {
+    if (m->llama) pieces.push_back({m->d, true});
+    pieces.push_back({m->d * Vp, false});  // head [d, Vp]
+  }
   int64_t wbytes = 0, gelems = 0;
   std::vector<int64_t> woff, goff;
   for (const Piece& p : pieces) {
@@ -178,8 +240,10 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
   size_t pi = 0;
   auto wptr = [&](size_t i) { return wb + woff[i]; };
   auto gptr = [&](size_t i) { return m->grads + goff[i]; };
-  m->emb = reinterpret_cast<bf16*>(wptr(pi));
-  m->d_emb = gptr(pi++);
+  if (m->has_embed) {
+    m->emb = reinterpret_cast<bf16*>(wptr(pi));
+    m->d_emb = gptr(pi++);
+  }
   m->layers.resize(static_cast<size_t>(m->L));
   for (auto& ly : m->layers) {
     ly.wqkv = reinterpret_cast<bf16*>(wptr(pi));
@@ -198,12 +262,14 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
       ly.d_g2 = gptr(pi++);
     }
   }
-  if (m->llama) {
-    m->gf = reinterpret_cast<float*>(wptr(pi));
-    m->d_gf = gptr(pi++);
+  if (m->has_head) {
+    if (m->llama) {
+      m->gf = reinterpret_cast<float*>(wptr(pi));
+      m->d_gf = gptr(pi++);
+    }
+    m->head = reinterpret_cast<bf16*>(wptr(pi));
+    m->d_head = gptr(pi++);
   }
-  m->head = reinterpret_cast<bf16*>(wptr(pi));
-  m->d_head = gptr(pi++);
 
   // Reference tensor order (toy_model.hpp:116-126; llama extension).
   auto add = [&](std::string name, int64_t r, int64_t c, void* w, float* g, int64_t ld, bool gain) {
@@ -217,10 +283,10 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
     s.is_gain = gain;
     m->slots.push_back(s);
   };
-  add("embedding", m->V, m->d, m->emb, m->d_emb, m->d, false);
+  if (m->has_embed) add("embedding", m->V, m->d, m->emb, m->d_emb, m->d, false);
   for (int64_t l = 0; l < m->L; ++l) {
     Layer& ly = m->layers[static_cast<size_t>(l)];
-    const std::string p = "layer" + std::to_string(l) + ".";
+    const std::string p = "layer" + std::to_string(m->l_begin + l) + ".";
     if (m->llama) add(p + "attn_norm", 1, m->d, ly.g1, ly.d_g1, m->d, true);
     add(p + "wq", m->d, m->d, ly.wqkv, ly.d_wqkv, m->qkv_w, false);
     add(p + "wk", m->d, m->kvw, ly.wqkv + m->d, ly.d_wqkv + m->d, m->qkv_w, false);
@@ -236,13 +302,18 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
       add(p + "w2", m->ffn, m->d, ly.w2, ly.d_w2, m->d, false);
     }
   }
-  if (m->llama) add("final_norm", 1, m->d, m->gf, m->d_gf, m->d, true);
-  add("head", m->d, m->V, m->head, m->d_head, Vp, false);
+  if (m->has_head) {
+    if (m->llama) add("final_norm", 1, m->d, m->gf, m->d_gf, m->d, true);
+    add("head", m->d, m->V, m->head, m->d_head, Vp, false);
+  }
 
   // init_model (toy_model.hpp:128-132): one SplitMix64 stream in tensor
   // order, regenerated per element on the device (every rank identical).
+  // A pipeline stage starts at the draw its first tensor has in the full
+  // model, so stage slices hold exactly the full model's values.
   const double scale = 1.0 / std::sqrt(static_cast<double>(m->d));
-  int64_t draw = 0;
+  const int64_t per_layer = 2 * m->d * m->d + 2 * m->d * m->kvw + m->d * m->gu_w + m->ffn * m->d;
+  int64_t draw = m->has_embed ? 0 : m->V * m->d + m->l_begin * per_layer;
   for (Slot& s : m->slots) {
     m->num_params += s.rows * s.cols;
     if (s.is_gain) {
@@ -254,7 +325,7 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg) {
                               scale, ctx->stream));
     draw += s.rows * s.cols;
   }
-  if (Vp != m->V)  // zero the head's pad columns
+  if (m->has_head && Vp != m->V)  // zero the head's pad columns
     CK(cudaMemset2DAsync(m->head + m->V, static_cast<size_t>(Vp) * 2, 0, static_cast<size_t>(Vp - m->V) * 2,
                          static_cast<size_t>(m->d), ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -360,7 +431,9 @@ struct cf_step {
   int64_t meta_len = 0;
   double normalizer = 0;
   int64_t tokens = 0;
-  double model_flops = 0, hw_flops = 0;
+  // algorithmic FLOPs split into one layer's share and the
+  // LM head's, so a pipeline stage can report its own slice
+  double mf_layer = 0, mf_head = 0, hw_layer = 0, hw_head = 0;
   std::map<int64_t, int64_t> group_len;  // group -> sequence length
   cfb::Plan plan_copy;
 };
@@ -391,9 +464,9 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
     if (b.tokens_host[i] < 0 || b.tokens_host[i] >= m->V)
       throw ValidationError("token id " + std::to_string(b.tokens_host[i]) + " out of vocabulary range");
 
-  const double Nmm = static_cast<double>(m->L * (m->d * m->qkv_w + m->d * m->d + m->d * m->gu_w + m->ffn * m->d) +
-                                         m->d * m->V);
-  const double attn_unit = static_cast<double>(m->L * m->H * m->dh);
+  const double Nlayer = static_cast<double>(m->d * m->qkv_w + m->d * m->d + m->d * m->gu_w + m->ffn * m->d);
+  const double Nhead = static_cast<double>(m->d * m->V);
+  const double attn_unit = static_cast<double>(m->H * m->dh);
   std::vector<int32_t> meta;
   auto put = [&](int32_t v) { meta.push_back(v); };
   auto here = [&]() { return static_cast<int64_t>(meta.size()); };
@@ -532,14 +605,17 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
     cm.nuniq = static_cast<int64_t>(uniq.size());
     while (meta.size() % 4) put(0);
     st->tokens += cm.T;
-    st->model_flops += 6.0 * Nmm * static_cast<double>(cm.T) + 12.0 * attn_unit * cm.pairs;
+    st->mf_layer += 6.0 * Nlayer * static_cast<double>(cm.T) + 12.0 * attn_unit * cm.pairs;
+    st->mf_head += 6.0 * Nhead * static_cast<double>(cm.T);
     st->chunks.push_back(cm);
   }
-  st->hw_flops = st->model_flops;
+  st->hw_layer = st->mf_layer;
+  st->hw_head = st->mf_head;
   for (const Event& e : plan.events)
     if (e.recompute) {
       const ChunkMeta& cm = st->chunks[static_cast<size_t>(st->pos_of.at(e.chunk))];
-      st->hw_flops += 2.0 * Nmm * static_cast<double>(cm.T) + 4.0 * attn_unit * cm.pairs;
+      st->hw_layer += 2.0 * Nlayer * static_cast<double>(cm.T) + 4.0 * attn_unit * cm.pairs;
+      st->hw_head += 2.0 * Nhead * static_cast<double>(cm.T);
     }
   st->meta_len = static_cast<int64_t>(meta.size());
   CK(cudaMallocHost(&st->meta_host, static_cast<size_t>(st->meta_len + 4) * 4));
@@ -627,7 +703,7 @@ struct Exec {
       t.lse = a.take<float>(L_ * m->H * T);
       t.x_mid = a.take<float>(L_ * T * d);
       t.act = a.take<bf16>(L_ * T * m->gu_w);
-      if (retain) t.dlogits = a.take<bf16>(T * Vp);
+      if (retain && m->has_head) t.dlogits = a.take<bf16>(T * Vp);
       t.tab = a.take<float2>(T * std::max<int64_t>(1, m->dh / 2));
     };
     Arena measure{nullptr, 0};
@@ -679,14 +755,16 @@ struct Exec {
   }
 
   // Forward of one chunk (segment_forward per segment, toy_model.hpp:206-334).
+  // A pipeline stage without the embedding finds its input already in
+  // t.x_in[0]; one without the head leaves its output in t.x_in[L].
   void forward(const ChunkMeta& cm, Tape& t, GroupState* gs, int64_t slot, bool retain) {
     const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8);
     const int32_t* tok = meta<const int32_t>(cm.o_tok);
     const int32_t* tgt = meta<const int32_t>(cm.o_tgt);
     bf16* A = static_cast<bf16*>(pool_alloc(ctx, T * std::max(d, m->ffn) * 2));
-    float* logits = static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4));
-    float* row_loss = logits + T * Vp;
-    L(cfk::embed_fwd(tok, m->emb, d, T, t.x_in, s), "embed");
+    float* logits = m->has_head ? static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4)) : nullptr;
+    float* row_loss = m->has_head ? logits + T * Vp : nullptr;
+    if (m->has_embed) L(cfk::embed_fwd(tok, m->emb, d, T, t.x_in, s), "embed");
     if (m->llama)
       L(cfk::rope_table(meta<const int32_t>(cm.o_pos), T, static_cast<int>(m->dh), m->cfg.rope_theta, t.tab, s),
         "rope_table");
@@ -731,26 +809,30 @@ struct Exec {
         gemm(act, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
       }
     }
-    const float* xL = t.x_in + m->L * T * d;
-    if (m->llama)
-      L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
-    else
-      L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
-    gemm(A, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
-    L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, tgt, inv_norm, row_loss, retain ? t.dlogits : nullptr, s), "ce");
-    L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
+    if (m->has_head) {
+      const float* xL = t.x_in + m->L * T * d;
+      if (m->llama)
+        L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+      else
+        L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+      gemm(A, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
+      L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, tgt, inv_norm, row_loss, retain ? t.dlogits : nullptr, s), "ce");
+      L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
+      pool_free(ctx, logits);
+    }
     pool_free(ctx, A);
-    pool_free(ctx, logits);
   }
 
-  // Backward of one chunk (segment_backward, toy_model.hpp:341-520).
-  void backward(const ChunkMeta& cm, Tape& t, GroupState* gs) {
+  // Backward of one chunk (segment_backward, toy_model.hpp:341-520).  A
+  // pipeline stage without the head passes the gradient of its output in
+  // dx_io; a stage without the embedding gets its input gradient back there.
+  void backward(const ChunkMeta& cm, Tape& t, GroupState* gs, float* dx_io = nullptr) {
     const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8), qw = m->qkv_w, kvw = m->kvw;
     const float eps = static_cast<float>(m->cfg.rms_eps);
     float *dx, *dmid, *da, *dsum, *rstd, *dkv_local = nullptr;
     bf16 *A, *xb, *dh, *dgu, *dqkv;
     auto carve = [&](Arena& a) {
-      dx = a.take<float>(T * d);
+      dx = dx_io ? dx_io : a.take<float>(T * d);
       dmid = a.take<float>(T * d);
       da = a.take<float>(T * d);
       A = a.take<bf16>(T * std::max(d, m->ffn));  // bf16 activations (recomputed)
@@ -769,18 +851,20 @@ struct Exec {
     void* scratch = a.base;
 
     // Output head + CE (toy_model.hpp:369-388): dHead += xf^T dlogits, dxf = dlogits head^T.
-    const float* xL = t.x_in + m->L * T * d;
-    if (m->llama)
-      L(cfk::rmsnorm_fwd(xL, m->gf, T, d, eps, A, s), "rmsnorm");
-    else
-      L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
-    gemm(A, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
-    if (m->llama) {
-      gemm(t.dlogits, 1, Vp, m->head, 1, Vp, da, d, T, d, m->V, cfk::EPI_F32);
-      L(cfk::rmsnorm_bwd(xL, m->gf, da, nullptr, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
-      L(cfk::gain_grad(xL, da, rstd, T, d, m->d_gf, s), "gain_grad");
-    } else {
-      gemm(t.dlogits, 1, Vp, m->head, 1, Vp, dx, d, T, d, m->V, cfk::EPI_F32);
+    if (m->has_head) {
+      const float* xL = t.x_in + m->L * T * d;
+      if (m->llama)
+        L(cfk::rmsnorm_fwd(xL, m->gf, T, d, eps, A, s), "rmsnorm");
+      else
+        L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+      gemm(A, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
+      if (m->llama) {
+        gemm(t.dlogits, 1, Vp, m->head, 1, Vp, da, d, T, d, m->V, cfk::EPI_F32);
+        L(cfk::rmsnorm_bwd(xL, m->gf, da, nullptr, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
+        L(cfk::gain_grad(xL, da, rstd, T, d, m->d_gf, s), "gain_grad");
+      } else {
+        gemm(t.dlogits, 1, Vp, m->head, 1, Vp, dx, d, T, d, m->V, cfk::EPI_F32);
+      }
     }
 
     for (int64_t l = m->L - 1; l >= 0; --l) {
@@ -860,151 +944,232 @@ struct Exec {
       }
     }
     // Embedding (toy_model.hpp:514-519), deterministic per-token sums.
-    L(cfk::embed_bwd(dx, d, meta<const int32_t>(cm.o_order), meta<const int32_t>(cm.o_uniq),
-                     meta<const int32_t>(cm.o_uoff), cm.nuniq, m->d_emb, s),
-      "embed_bwd");
+    if (m->has_embed)
+      L(cfk::embed_bwd(dx, d, meta<const int32_t>(cm.o_order), meta<const int32_t>(cm.o_uniq),
+                       meta<const int32_t>(cm.o_uoff), cm.nuniq, m->d_emb, s),
+        "embed_bwd");
     pool_free(ctx, scratch);
   }
 };
 
 }  // namespace
 
-void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res) {
-  const Plan& plan = *st->plan;
-  if (!plan.violations.empty()) throw ValidationError("execution plan is invalid: " + plan.violations.front());
-  Exec ex;
-  ex.ctx = ctx;
-  ex.m = m;
-  ex.st = st;
-  ex.s = ctx->stream;
-  ex.corrupt = opts.corrupt_kv_grads != 0;
-  const double norm = opts.normalizer_override > 0 ? opts.normalizer_override : st->normalizer;
-  ex.inv_norm = static_cast<float>(1.0 / norm);
-  const int64_t nev = static_cast<int64_t>(plan.events.size());
-  if (ctx->pool) {
-    uint64_t zero = 0;
-    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &zero);
-  }
-  ex.loss_slots = static_cast<double*>(pool_alloc(ctx, (nev + 1) * 8));
-  CK(cudaMemsetAsync(ex.loss_slots, 0, static_cast<size_t>(nev + 1) * 8, ex.s));
-  if (!opts.accumulate_grads) CK(cudaMemsetAsync(m->grads, 0, static_cast<size_t>(m->grad_numel) * 4, ex.s));
+namespace {
 
+// Per-stage state of one training step (the B200 counterpart of run_plan's
+// locals, plan_runner.hpp:84-110): retained tapes, per-group KV state, stage
+// inputs kept for just-in-time recompute, loss slots and the run_plan
+// instrumentation counters.  With one stage it runs plan.events directly;
+// pipeline stages feed it their op streams (host/pp.hpp).
+struct StageRunner {
+  Exec ex;
+  Ctx* ctx;
+  Model* m;
+  cf_step* st;
+  double norm = 0;
+  int64_t nslots = 0;
   std::map<int64_t, Tape> live;
   std::map<int64_t, GroupState> groups;
+  std::map<int64_t, float*> kept_in;  // discarded chunk -> stage input, until its F'
   std::map<int64_t, int64_t> first_slot;
   std::vector<std::pair<int64_t, int64_t>> recompute_pairs;  // (slot, first slot)
   std::vector<int64_t> first_pass_slots;
   int64_t held = 0, peak = 0, violations = 0, recomputes = 0;
+  int64_t io_bytes = 0;  // stage-boundary buffers held (kept inputs)
 
-  for (int64_t ei = 0; ei < nev; ++ei) {
-    const Event& e = plan.events[static_cast<size_t>(ei)];
-    auto pit = st->pos_of.find(e.chunk);
-    if (pit == st->pos_of.end()) throw ValidationError("plan references unknown chunk " + std::to_string(e.chunk));
-    const ChunkMeta& cm = st->chunks[static_cast<size_t>(pit->second)];
-    GroupState* gs = nullptr;
-    if (cm.dependent) {
-      auto git = groups.find(cm.group);
-      if (git == groups.end()) {
-        GroupState g;
-        g.S = cm.seq_len;
-        const int64_t n = static_cast<int64_t>(plan.groups.at(cm.group).size());
-        g.contributions.assign(static_cast<size_t>(n), 0);
-        g.saved.assign(static_cast<size_t>(n), false);
-        const int64_t kvb = m->L * g.S * m->kvw * 2;
-        const int64_t bytes = 3 * 256 + 2 * kvb + m->L * g.S * 2 * m->kvw * 4;
-        g.mem = pool_alloc(ctx, bytes);
-        Arena a{static_cast<char*>(g.mem), 0};
-        g.kc = a.take<bf16>(m->L * g.S * m->kvw);
-        g.vc = a.take<bf16>(m->L * g.S * m->kvw);
-        g.dkv = a.take<float>(m->L * g.S * 2 * m->kvw);
-        CK(cudaMemsetAsync(g.dkv, 0, static_cast<size_t>(m->L * g.S * 2 * m->kvw) * 4, ex.s));
-        ex.kv_bytes += bytes;
-        ex.kv_peak = std::max(ex.kv_peak, ex.kv_bytes);
-        git = groups.emplace(cm.group, std::move(g)).first;
-      }
-      gs = &git->second;
+  StageRunner(Ctx* c, Model* mm, cf_step* s, const cf_run_opts& opts, int64_t slots)
+      : ctx(c), m(mm), st(s), nslots(slots) {
+    const Plan& plan = *st->plan;
+    if (!plan.violations.empty()) throw ValidationError("execution plan is invalid: " + plan.violations.front());
+    ex.ctx = ctx;
+    ex.m = m;
+    ex.st = st;
+    ex.s = ctx->stream;
+    ex.corrupt = opts.corrupt_kv_grads != 0;
+    norm = opts.normalizer_override > 0 ? opts.normalizer_override : st->normalizer;
+    ex.inv_norm = static_cast<float>(1.0 / norm);
+    ex.loss_slots = static_cast<double*>(pool_alloc(ctx, (nslots + 1) * 8));
+    CK(cudaMemsetAsync(ex.loss_slots, 0, static_cast<size_t>(nslots + 1) * 8, ex.s));
+    if (!opts.accumulate_grads) CK(cudaMemsetAsync(m->grads, 0, static_cast<size_t>(m->grad_numel) * 4, ex.s));
+  }
+
+  const ChunkMeta& chunk(int64_t id) const {
+    auto it = st->pos_of.find(id);
+    if (it == st->pos_of.end()) throw ValidationError("plan references unknown chunk " + std::to_string(id));
+    return st->chunks[static_cast<size_t>(it->second)];
+  }
+  int64_t group_size(const ChunkMeta& cm) const {
+    return static_cast<int64_t>(st->plan->groups.at(cm.group).size());
+  }
+  int64_t kv_state_bytes(int64_t S) const {
+    return 3 * 256 + 2 * m->L * S * m->kvw * 2 + m->L * S * 2 * m->kvw * 4;
+  }
+
+  GroupState* group_for(const ChunkMeta& cm) {
+    if (!cm.dependent) return nullptr;
+    auto git = groups.find(cm.group);
+    if (git == groups.end()) {
+      GroupState g;
+      g.S = cm.seq_len;
+      const int64_t n = group_size(cm);
+      g.contributions.assign(static_cast<size_t>(n), 0);
+      g.saved.assign(static_cast<size_t>(n), false);
+      const int64_t bytes = kv_state_bytes(g.S);
+      g.mem = pool_alloc(ctx, bytes);
+      Arena a{static_cast<char*>(g.mem), 0};
+      g.kc = a.take<bf16>(m->L * g.S * m->kvw);
+      g.vc = a.take<bf16>(m->L * g.S * m->kvw);
+      g.dkv = a.take<float>(m->L * g.S * 2 * m->kvw);
+      CK(cudaMemsetAsync(g.dkv, 0, static_cast<size_t>(m->L * g.S * 2 * m->kvw) * 4, ex.s));
+      ex.kv_bytes += bytes;
+      ex.kv_peak = std::max(ex.kv_peak, ex.kv_bytes);
+      git = groups.emplace(cm.group, std::move(g)).first;
     }
-    if (e.kind != kBackward) {
-      const bool retain = e.kind == kFwdRetain;
-      Tape t = ex.alloc_tape(cm.T, retain);
-      ex.forward(cm, t, gs, ei, retain);
-      if (gs && e.save_kv) gs->saved[static_cast<size_t>(cm.index)] = true;
-      if (!e.recompute) {
-        first_slot[e.chunk] = ei;
-        first_pass_slots.push_back(ei);
-      } else {
-        ++recomputes;
-        auto f = first_slot.find(e.chunk);
-        recompute_pairs.emplace_back(ei, f == first_slot.end() ? -1 : f->second);
+    return &git->second;
+  }
+
+  // Forward of chunk `id` into loss slot `slot`.  `in` is the stage input
+  // ([T, d] fp32, pool memory owned by the runner from here on) on stages
+  // without the embedding; a recompute forward uses the input kept by the
+  // chunk's first pass (keep_in).  Returns the stage output for the next
+  // stage (caller-owned pool memory) or null on the last stage / for F'.
+  float* forward(int64_t id, bool retain, bool recompute, bool save_kv, int64_t slot, float* in, bool keep_in) {
+    const ChunkMeta& cm = chunk(id);
+    GroupState* gs = group_for(cm);
+    const size_t act = static_cast<size_t>(cm.T * m->d) * 4;
+    Tape t = ex.alloc_tape(cm.T, retain);
+    if (!m->has_embed) {
+      float* src = in;
+      if (recompute) {
+        auto k = kept_in.find(id);
+        if (k == kept_in.end()) throw ValidationError("recompute of chunk " + std::to_string(id) + " without its stage input");
+        src = k->second;
       }
-      if (retain) {
-        if (live.count(e.chunk)) ex.free_tape(live[e.chunk]);
-        live[e.chunk] = t;
-        held += cm.T;
-        peak = std::max(peak, held);
-      } else {
-        ex.free_tape(t);
-      }
-      continue;
+      if (!src) throw ValidationError("stage input missing for chunk " + std::to_string(id));
+      CK(cudaMemcpyAsync(t.x_in, src, act, cudaMemcpyDeviceToDevice, ex.s));
     }
-    auto lit = live.find(e.chunk);
+    ex.forward(cm, t, gs, slot, retain);
+    if (gs && save_kv) gs->saved[static_cast<size_t>(cm.index)] = true;
+    if (!recompute) {
+      first_slot[id] = slot;
+      first_pass_slots.push_back(slot);
+    } else {
+      ++recomputes;
+      auto f = first_slot.find(id);
+      recompute_pairs.emplace_back(slot, f == first_slot.end() ? -1 : f->second);
+    }
+    float* out = nullptr;
+    if (!m->has_head && !recompute) {
+      out = static_cast<float*>(pool_alloc(ctx, static_cast<int64_t>(act)));
+      CK(cudaMemcpyAsync(out, t.x_in + m->L * cm.T * m->d, act, cudaMemcpyDeviceToDevice, ex.s));
+    }
+    if (retain) {
+      if (live.count(id)) ex.free_tape(live[id]);
+      live[id] = t;
+      held += cm.T;
+      peak = std::max(peak, held);
+    } else {
+      ex.free_tape(t);
+    }
+    if (recompute) {
+      auto k = kept_in.find(id);
+      if (k != kept_in.end()) {
+        pool_free(ctx, k->second);
+        io_bytes -= static_cast<int64_t>(act);
+        kept_in.erase(k);
+      }
+    } else if (in) {
+      if (keep_in) {
+        kept_in[id] = in;
+        io_bytes += static_cast<int64_t>(act);
+      } else {
+        pool_free(ctx, in);
+      }
+    }
+    return out;
+  }
+
+  // Backward of chunk `id`.  `dy` is the gradient of the stage output (pool
+  // memory, owned by the runner from here on) on stages without the head.
+  // Returns the gradient of the stage input for the previous stage (caller-
+  // owned) or null on the first stage.
+  float* backward(int64_t id, float* dy) {
+    const ChunkMeta& cm = chunk(id);
+    GroupState* gs = group_for(cm);
+    auto lit = live.find(id);
     if (lit == live.end())
-      throw ValidationError("backward of chunk " + std::to_string(e.chunk) + " without retained activations");
-    if (gs) {
+      throw ValidationError("backward of chunk " + std::to_string(id) + " without retained activations");
+    if (gs) {  // KV-gradient completeness (plan_runner.hpp:266-275)
       const int64_t n = static_cast<int64_t>(gs->contributions.size());
       if (gs->saved[static_cast<size_t>(cm.index)] &&
           gs->contributions[static_cast<size_t>(cm.index)] != n - 1 - cm.index)
         ++violations;
     }
-    ex.backward(cm, lit->second, gs);
+    float* dx = dy;
+    if (!m->has_head && !dy) throw ValidationError("output gradient missing for chunk " + std::to_string(id));
+    if (!dx && !m->has_embed) dx = static_cast<float*>(pool_alloc(ctx, cm.T * m->d * 4));
+    ex.backward(cm, lit->second, gs, dx);
     if (gs) {
       for (int64_t i = 0; i < cm.index; ++i) ++gs->contributions[static_cast<size_t>(i)];
       if (cm.index == 0) {  // group complete: release its KV state
-        const int64_t bytes = 3 * 256 + 2 * m->L * gs->S * m->kvw * 2 + m->L * gs->S * 2 * m->kvw * 4;
         pool_free(ctx, gs->mem);
-        ex.kv_bytes -= bytes;
+        ex.kv_bytes -= kv_state_bytes(gs->S);
         groups.erase(cm.group);
       }
     }
     ex.free_tape(lit->second);
     live.erase(lit);
     held -= cm.T;
+    if (m->has_embed) {
+      if (dx) pool_free(ctx, dx);
+      return nullptr;
+    }
+    return dx;
   }
-  for (auto& kv : live) ex.free_tape(kv.second);
-  for (auto& kv : groups) pool_free(ctx, kv.second.mem);
 
-  std::vector<double> slots(static_cast<size_t>(nev + 1));
-  CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nev + 1) * 8, cudaMemcpyDeviceToHost, ex.s));
-  CK(cudaStreamSynchronize(ex.s));
-  double cls_ms[3] = {0, 0, 0}, cls_flops[3] = {0, 0, 0};
-  int64_t cls_n[3] = {0, 0, 0};
-  for (const auto& r : ex.recs) {
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, r.a, r.b));
-    cls_ms[r.cls] += ms;
-    cls_flops[r.cls] += r.flops;
-    cls_n[r.cls] += r.n;
-  }
-  double total = 0;
-  for (int64_t sl : first_pass_slots) total += slots[static_cast<size_t>(sl)];
-  int64_t mism = 0;
-  for (const auto& [sl, f] : recompute_pairs)
-    if (f < 0 || slots[static_cast<size_t>(sl)] != slots[static_cast<size_t>(f)]) ++mism;
-  double loss = total / norm;
-  if (ctx->nccl_comm) {
-    // DP: gradients and loss are sums of per-rank partials (global normalizer)
-    double* dl = ex.loss_slots + nev;
-    CK(cudaMemcpyAsync(dl, &loss, 8, cudaMemcpyHostToDevice, ex.s));
-    nccl_check(nccl().all_reduce(m->grads, m->grads, static_cast<size_t>(m->grad_numel), kNcclFloat32, kNcclSum,
-                                 ctx->nccl_comm, ex.s),
-               "ncclAllReduce(grads)");
-    nccl_check(nccl().all_reduce(dl, dl, 1, kNcclFloat64, kNcclSum, ctx->nccl_comm, ex.s), "ncclAllReduce(loss)");
-    CK(cudaMemcpyAsync(&loss, dl, 8, cudaMemcpyDeviceToHost, ex.s));
+  // Loss read-back, recompute-loss check, DP all-reduce, result fields.
+  void finish(cf_run_result* res, bool dp_reduce) {
+    for (auto& kv : live) ex.free_tape(kv.second);
+    live.clear();
+    for (auto& kv : groups) pool_free(ctx, kv.second.mem);
+    groups.clear();
+    for (auto& kv : kept_in) pool_free(ctx, kv.second);
+    kept_in.clear();
+    std::vector<double> slots(static_cast<size_t>(nslots + 1));
+    CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nslots + 1) * 8, cudaMemcpyDeviceToHost,
+                       ex.s));
     CK(cudaStreamSynchronize(ex.s));
-  }
-  pool_free(ctx, ex.loss_slots);
-  ctx->launches += ex.launches;
-  if (res) {
+    double cls_ms[3] = {0, 0, 0}, cls_flops[3] = {0, 0, 0};
+    int64_t cls_n[3] = {0, 0, 0};
+    for (const auto& r : ex.recs) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, r.a, r.b));
+      cls_ms[r.cls] += ms;
+      cls_flops[r.cls] += r.flops;
+      cls_n[r.cls] += r.n;
+    }
+    double total = 0;
+    for (int64_t sl : first_pass_slots) total += slots[static_cast<size_t>(sl)];
+    int64_t mism = 0;
+    if (m->has_head)
+      for (const auto& [sl, f] : recompute_pairs)
+        if (f < 0 || slots[static_cast<size_t>(sl)] != slots[static_cast<size_t>(f)]) ++mism;
+    double loss = total / norm;
+    if (dp_reduce && ctx->nccl_comm) {
+      // DP: gradients and loss are sums of per-rank partials (global normalizer)
+      double* dl = ex.loss_slots + nslots;
+      CK(cudaMemcpyAsync(dl, &loss, 8, cudaMemcpyHostToDevice, ex.s));
+      nccl_check(nccl().all_reduce(m->grads, m->grads, static_cast<size_t>(m->grad_numel), kNcclFloat32, kNcclSum,
+                                   ctx->nccl_comm, ex.s),
+                 "ncclAllReduce(grads)");
+      nccl_check(nccl().all_reduce(dl, dl, 1, kNcclFloat64, kNcclSum, ctx->nccl_comm, ex.s), "ncclAllReduce(loss)");
+      CK(cudaMemcpyAsync(&loss, dl, 8, cudaMemcpyDeviceToHost, ex.s));
+      CK(cudaStreamSynchronize(ex.s));
+    }
+    pool_free(ctx, ex.loss_slots);
+    ex.loss_slots = nullptr;
+    ctx->launches += ex.launches;
+    if (!res) return;
     res->loss = loss;
     res->peak_retained_tokens = peak;
     res->recompute_forward_count = recomputes;
@@ -1018,8 +1183,9 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
     uint64_t high = 0;
     if (ctx->pool) cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &high);
     res->peak_hbm_bytes = res->static_hbm_bytes + static_cast<int64_t>(high);
-    res->model_flops = st->model_flops;
-    res->hw_flops = st->hw_flops;
+    const double L_ = static_cast<double>(m->L);
+    res->model_flops = st->mf_layer * L_ + (m->has_head ? st->mf_head : 0.0);
+    res->hw_flops = st->hw_layer * L_ + (m->has_head ? st->hw_head : 0.0);
     res->gemm_ms = cls_ms[0];
     res->gemm_flops = cls_flops[0];
     res->gemm_launches = cls_n[0];
@@ -1031,6 +1197,229 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
     res->attn_bwd_launches = cls_n[2];
     res->other_launches = ex.launches - cls_n[0] - cls_n[1] - cls_n[2];
   }
+};
+
+void reset_pool_high(Ctx* ctx) {
+  if (ctx->pool) {
+    uint64_t zero = 0;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &zero);
+  }
+}
+
+// The stage's view of the plan: chunk-aware 1F1B op stream + per-position
+// flags (pipeline.hpp:250-304 with scheduler.hpp:87-100 KV actions).
+struct StagePlan {
+  PpChunks info;
+  std::vector<std::vector<PpOp>> orders;
+};
+StagePlan stage_plan(const cf_step* st, int64_t k, int64_t stages) {
+  StagePlan sp;
+  sp.info = pp_chunks(*st->plan, k, PpCost{});
+  for (int64_t s = 0; s < stages; ++s) sp.orders.push_back(pp_stage_order(sp.info, s, stages, true));
+  return sp;
+}
+bool first_pass_saves_kv(const cf_step* st, const ChunkMeta& cm) {
+  return cm.dependent && cm.index + 1 < static_cast<int64_t>(st->plan->groups.at(cm.group).size());
+}
+
+}  // namespace
+
+void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res) {
+  if (!m->has_embed || !m->has_head) throw ValidationError("a pipeline-stage model needs cf_pp_step_run");
+  const Plan& plan = *st->plan;
+  reset_pool_high(ctx);
+  StageRunner r(ctx, m, st, opts, static_cast<int64_t>(plan.events.size()));
+  for (size_t ei = 0; ei < plan.events.size(); ++ei) {
+    const Event& e = plan.events[ei];
+    if (e.kind == kBackward)
+      r.backward(e.chunk, nullptr);
+    else
+      r.forward(e.chunk, e.kind == kFwdRetain, e.recompute, e.save_kv, static_cast<int64_t>(ei), nullptr, false);
+  }
+  r.finish(res, true);
+}
+
+void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t P, cf_step* st, int64_t k, const cf_run_opts& opts,
+                       cf_run_result* res) {
+  if (P < 1) throw ValidationError("num_stages must be at least 1");
+  for (int64_t s = 0; s < P; ++s) {
+    int64_t b = 0, e = 0;
+    pp_stage_layers(models[0]->cfg.num_layers, s, P, &b, &e);
+    const Model* ms = models[s];
+    if (!ms || ms->l_begin != b || ms->l_end != e || ms->has_embed != (s == 0) || ms->has_head != (s == P - 1) ||
+        std::memcmp(&ms->cfg, &models[0]->cfg, sizeof(cf_model_cfg)) != 0)
+      throw ValidationError("models[" + std::to_string(s) + "] is not stage " + std::to_string(s) + " of " +
+                            std::to_string(P) + " of the same model");
+  }
+  const StagePlan sp = stage_plan(st, k, P);
+  // one global order consistent with every cross-stage dependency: the
+  // simulated dispatch order (start time, then stage)
+  const PpTrace tr = pp_dispatch(sp.orders, sp.info.fwd, sp.info.bwd, 0.0);
+  std::vector<std::tuple<double, int64_t, size_t>> seq;
+  for (int64_t s = 0; s < P; ++s)
+    for (size_t i = 0; i < tr.stages[static_cast<size_t>(s)].size(); ++i)
+      seq.emplace_back(tr.stages[static_cast<size_t>(s)][i].start, s, i);
+  std::sort(seq.begin(), seq.end());
+  reset_pool_high(ctx);
+  std::vector<std::unique_ptr<StageRunner>> run;
+  for (int64_t s = 0; s < P; ++s)
+    run.emplace_back(new StageRunner(ctx, models[s], st, opts,
+                                     static_cast<int64_t>(tr.stages[static_cast<size_t>(s)].size())));
+  std::map<std::pair<int64_t, int64_t>, float*> act, grad;  // (stage, position) -> hand-over buffer
+  auto take = [](std::map<std::pair<int64_t, int64_t>, float*>& box, int64_t s, int64_t p) {
+    auto it = box.find({s, p});
+    if (it == box.end()) throw std::logic_error("pipeline hand-over buffer missing");
+    float* b = it->second;
+    box.erase(it);
+    return b;
+  };
+  for (const auto& [start, s, i] : seq) {
+    const PpTimedOp& op = tr.stages[static_cast<size_t>(s)][i];
+    const int64_t id = sp.info.ids[static_cast<size_t>(op.pos)];
+    StageRunner& r = *run[static_cast<size_t>(s)];
+    const ChunkMeta& cm = r.chunk(id);
+    const int64_t slot = static_cast<int64_t>(i);
+    if (op.kind == kPpForward) {
+      const bool disc = sp.info.discarded[static_cast<size_t>(op.pos)] != 0;
+      float* in = s > 0 ? take(act, s, op.pos) : nullptr;
+      float* out = r.forward(id, !disc, false, first_pass_saves_kv(st, cm), slot, in, disc);
+      if (out) act[{s + 1, op.pos}] = out;
+    } else if (op.kind == kPpRecompute) {
+      r.forward(id, true, true, false, slot, nullptr, false);
+    } else {
+      float* dy = s + 1 < P ? take(grad, s, op.pos) : nullptr;
+      float* dx = r.backward(id, dy);
+      if (dx) grad[{s - 1, op.pos}] = dx;
+    }
+  }
+  if (!act.empty() || !grad.empty()) throw std::logic_error("unconsumed pipeline hand-over buffers");
+  cf_run_result total{};
+  for (int64_t s = 0; s < P; ++s) {
+    cf_run_result rs{};
+    run[static_cast<size_t>(s)]->finish(&rs, true);
+    if (s == P - 1) {
+      total.loss = rs.loss;
+      total.recompute_loss_mismatches = rs.recompute_loss_mismatches;
+      total.peak_retained_tokens = rs.peak_retained_tokens;
+      total.recompute_forward_count = rs.recompute_forward_count;
+      total.tokens = rs.tokens;
+    }
+    total.kv_completeness_violations += rs.kv_completeness_violations;
+    total.gpu_launches += rs.gpu_launches;
+    total.static_hbm_bytes += rs.static_hbm_bytes;
+    total.act_hbm_bytes += rs.act_hbm_bytes;
+    total.kv_hbm_bytes += rs.kv_hbm_bytes;
+    total.model_flops += rs.model_flops;
+    total.hw_flops += rs.hw_flops;
+    total.gemm_ms += rs.gemm_ms;
+    total.gemm_flops += rs.gemm_flops;
+    total.gemm_launches += rs.gemm_launches;
+    total.attn_ms += rs.attn_ms;
+    total.attn_flops += rs.attn_flops;
+    total.attn_launches += rs.attn_launches;
+    total.attn_bwd_ms += rs.attn_bwd_ms;
+    total.attn_bwd_flops += rs.attn_bwd_flops;
+    total.attn_bwd_launches += rs.attn_bwd_launches;
+    total.other_launches += rs.other_launches;
+  }
+  uint64_t high = 0;
+  if (ctx->pool) cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &high);
+  total.peak_hbm_bytes = total.static_hbm_bytes + static_cast<int64_t>(high);
+  if (res) *res = total;
+}
+
+namespace {
+
+// One stage-boundary transfer on a link stream, ordered against the compute
+// stream with events in both directions.
+struct LinkOp {
+  float* buf;
+  cudaEvent_t done;
+};
+
+cudaEvent_t new_event() {
+  cudaEvent_t e;
+  CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+LinkOp link_xfer(Ctx* ctx, int li, void* comm, int peer, float* buf, size_t n, bool send) {
+  cudaStream_t ls = ctx->link_stream[li];
+  cudaEvent_t ready = new_event(), done = new_event();
+  CK(cudaEventRecord(ready, ctx->stream));  // buffer allocated / produced on the compute stream
+  CK(cudaStreamWaitEvent(ls, ready, 0));
+  if (send)
+    nccl_check(nccl().send(buf, n, kNcclFloat32, peer, comm, ls), "ncclSend");
+  else
+    nccl_check(nccl().recv(buf, n, kNcclFloat32, peer, comm, ls), "ncclRecv");
+  CK(cudaEventRecord(done, ls));
+  if (!send) CK(cudaStreamWaitEvent(ctx->stream, done, 0));  // consumer waits for the data
+  CK(cudaEventDestroy(ready));
+  return {buf, done};
+}
+
+}  // namespace
+
+void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& opts, cf_run_result* res) {
+  const int64_t P = ctx->stages, s = ctx->stage;
+  {
+    int64_t b = 0, e = 0;
+    pp_stage_layers(m->cfg.num_layers, s, P, &b, &e);
+    if (m->l_begin != b || m->l_end != e || m->has_embed != (s == 0) || m->has_head != (s == P - 1))
+      throw ValidationError("model is not stage " + std::to_string(s) + " of " + std::to_string(P));
+  }
+  if (P > 1 && ((s + 1 < P && (!ctx->act_up || !ctx->grad_up)) || (s > 0 && (!ctx->act_down || !ctx->grad_down))))
+    throw ValidationError("pipeline links not initialised (cf_ctx_init_pp)");
+  const StagePlan sp = stage_plan(st, k, P);
+  const std::vector<PpOp>& order = sp.orders[static_cast<size_t>(s)];
+  reset_pool_high(ctx);
+  StageRunner r(ctx, m, st, opts, static_cast<int64_t>(order.size()));
+  std::vector<LinkOp> sends;  // output buffers in flight to a neighbour
+  auto reap = [&](bool all) {
+    for (size_t i = 0; i < sends.size();) {
+      if (all) CK(cudaEventSynchronize(sends[i].done));
+      if (all || cudaEventQuery(sends[i].done) == cudaSuccess) {
+        CK(cudaStreamWaitEvent(ctx->stream, sends[i].done, 0));
+        pool_free(ctx, sends[i].buf);
+        CK(cudaEventDestroy(sends[i].done));
+        sends[i] = sends.back();
+        sends.pop_back();
+      } else {
+        ++i;
+      }
+    }
+  };
+  std::vector<cudaEvent_t> recv_done;
+  for (size_t i = 0; i < order.size(); ++i) {
+    reap(false);
+    const PpOp& op = order[i];
+    const int64_t id = sp.info.ids[static_cast<size_t>(op.pos)];
+    const ChunkMeta& cm = r.chunk(id);
+    const size_t n = static_cast<size_t>(cm.T * m->d);
+    if (op.kind == kPpForward) {
+      float* in = nullptr;
+      if (s > 0) {
+        in = static_cast<float*>(pool_alloc(ctx, static_cast<int64_t>(n) * 4));
+        recv_done.push_back(link_xfer(ctx, 1, ctx->act_down, 0, in, n, false).done);
+      }
+      const bool disc = sp.info.discarded[static_cast<size_t>(op.pos)] != 0;
+      float* out = r.forward(id, !disc, false, first_pass_saves_kv(st, cm), static_cast<int64_t>(i), in, disc);
+      if (out) sends.push_back(link_xfer(ctx, 0, ctx->act_up, 1, out, n, true));
+    } else if (op.kind == kPpRecompute) {
+      r.forward(id, true, true, false, static_cast<int64_t>(i), nullptr, false);
+    } else {
+      float* dy = nullptr;
+      if (s + 1 < P) {
+        dy = static_cast<float*>(pool_alloc(ctx, static_cast<int64_t>(n) * 4));
+        recv_done.push_back(link_xfer(ctx, 2, ctx->grad_up, 1, dy, n, false).done);
+      }
+      float* dx = r.backward(id, dy);
+      if (dx) sends.push_back(link_xfer(ctx, 3, ctx->grad_down, 0, dx, n, true));
+    }
+  }
+  reap(true);
+  for (cudaEvent_t e : recv_done) CK(cudaEventDestroy(e));
+  r.finish(res, true);
 }
 
 void run_plan(Ctx* ctx, Model* m, const Plan& plan, const Batch& b, const cf_run_opts& opts, cf_run_result* res) {

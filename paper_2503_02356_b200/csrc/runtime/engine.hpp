@@ -28,6 +28,15 @@ struct Ctx {
   // data-parallel group (NCCL loaded at runtime)
   void* nccl_comm = nullptr;
   int rank = 0, world = 1;
+  // pipeline-parallel links (cf_ctx_init_pp): one 2-rank communicator per
+  // direction per neighbouring stage, each driven from its own stream, so
+  // activation and gradient traffic never queue behind each other.
+  int stage = 0, stages = 1;
+  void* act_up = nullptr;    // send activations to stage+1
+  void* grad_up = nullptr;   // receive gradients from stage+1
+  void* act_down = nullptr;  // receive activations from stage-1
+  void* grad_down = nullptr; // send gradients to stage-1
+  cudaStream_t link_stream[4] = {nullptr, nullptr, nullptr, nullptr};
   // per-launch CUDA-event timing (cf_ctx_set_profiling)
   bool profile = false;
   std::vector<cudaEvent_t> event_pool;
@@ -60,6 +69,10 @@ struct Model {
   Ctx* ctx = nullptr;
   cf_model_cfg cfg{};
   bool llama = false;
+  // pipeline stage slice: global layers [l_begin, l_end); embedding on the
+  // first stage, final norm + head + loss on the last (L = local count)
+  int64_t l_begin = 0, l_end = 0;
+  bool has_embed = true, has_head = true;
   int64_t V, d, H, KVH, dh, kvw, ffn, L, qkv_w, gu_w;
   bf16* emb = nullptr;
   bf16* head = nullptr;
@@ -72,7 +85,7 @@ struct Model {
   int64_t grad_numel = 0, wbytes = 0, num_params = 0;
 };
 
-Model* model_create(Ctx* ctx, const cf_model_cfg& cfg);
+Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage = 0, int64_t stages = 1);
 void model_destroy(Model* m);
 void model_get_param(Model* m, int64_t idx, double* host);
 void model_set_param(Model* m, int64_t idx, const double* host);
@@ -90,6 +103,17 @@ void run_plan(Ctx* ctx, Model* m, const Plan& plan, const Batch& b, const cf_run
 cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b);
 void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res);
 void step_destroy(cf_step* st);
+// Pipeline-parallel step of one stage on this rank (ctx has PP links): the
+// stage's chunk-aware 1F1B op stream (host/pp.hpp) with NCCL send/recv of
+// fp32 [T, d] activations and gradients.
+void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& opts, cf_run_result* res);
+// All stages of one pipeline in this process on one device (stage i uses
+// models[i]): the same per-stage op streams, executed in dispatch order with
+// in-memory hand-over between stages.  Results are summed over stages (loss
+// and loss checks come from the last stage).
+void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t stages, cf_step* st, int64_t k,
+                       const cf_run_opts& opts, cf_run_result* res);
+void pp_init(Ctx* ctx, int rank, int world, int stages, const uint8_t* id128);
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id128);
 void dp_unique_id(uint8_t* out128);

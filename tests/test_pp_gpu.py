@@ -1,0 +1,130 @@
+"""Pipeline-parallel execution on the GPU (cf_pp_run_local: every stage of one
+pipeline on this device, chunk-aware 1F1B op streams of build_stage_order,
+pipeline.hpp:178-210, with stage-boundary hand-over of fp32 activations and
+gradients).  A stage split only moves where layers run, so the loss and every
+parameter gradient must be BITWISE those of the unsplit model's cf_step_run
+(same kernels, same accumulation order: backwards follow the plan order with
+dependent groups reversed in both schedules); the oracle then pins the
+unsplit model (tests/test_parity_gpu.py)."""
+import numpy as np
+import pytest
+
+import paper_2503_02356_b200 as cf
+from paper_2503_02356_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # name, arch, vocab, d, heads, kv_heads, layers, ffn, lengths, chunk, k, stages
+    ("toy-p2", 0, 64, 64, 4, 2, 2, 0, [8, 8, 16, 40, 70], 32, 1, 2),
+    ("toy-p4-k2", 0, 64, 64, 4, 2, 4, 0, [5, 12, 31, 130, 64, 9, 200], 32, 2, 4),
+    ("llama-p2-group", 1, 96, 128, 4, 2, 2, 256, [8, 30, 64, 150, 33], 64, 1, 2),
+    ("llama-p3-dh128", 1, 120, 256, 2, 1, 3, 512, [200, 90, 333, 700], 128, 1, 3),
+    ("llama-p4-k3", 1, 120, 256, 2, 1, 4, 512, [40, 900, 77, 260], 128, 3, 4),
+]
+
+
+def _grads_by_name(model):
+    out = {}
+    for i in range(model.num_tensors()):
+        name, _, _ = model.tensor_info(i)
+        out[name] = model.get_grad(i)
+    return out
+
+
+def _params_by_name(model):
+    return {model.tensor_info(i)[0]: model.get_param(i) for i in range(model.num_tensors())}
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_pp_local_bitwise_equals_unsplit(ctx, case):
+    _, arch, V, d, H, KVH, L, ffn, lengths, cs, k, P = case
+    cfg = cf.model_cfg(arch=arch, vocab=V, d=d, heads=H, kv_heads=KVH, layers=L, ffn=ffn, seed=7)
+    lengths = np.array(lengths, np.int64)
+    tokens = cf.gen_tokens(lengths, V, 11)
+    plan = cf.Plan.build(lengths, cs, k)
+
+    full = cf.Model(ctx, cfg)
+    st = cf.Step(full, plan, lengths, tokens)
+    ref = st.run()
+    ref_grads = _grads_by_name(full)
+    ref_params = _params_by_name(full)
+    st.close()
+
+    stages = [cf.Model(ctx, cfg, stage=s, num_stages=P) for s in range(P)]
+    # stage slices hold exactly the full model's weights (same SplitMix64 draws)
+    names = []
+    for m in stages:
+        for name, w in _params_by_name(m).items():
+            assert np.array_equal(w, ref_params[name]), name
+            names.append(name)
+    assert sorted(names) == sorted(ref_params)
+
+    sp = cf.Step(stages[0], plan, lengths, tokens)
+    r = sp.run_pp_local(stages, k)
+    assert r.loss == ref.loss
+    assert r.recompute_loss_mismatches == 0 and r.kv_completeness_violations == 0
+    assert r.recompute_forward_count == ref.recompute_forward_count
+    assert abs(r.model_flops - ref.model_flops) <= 1e-9 * ref.model_flops
+    for m in stages:
+        for name, g in _grads_by_name(m).items():
+            assert np.array_equal(g, ref_grads[name]), name
+    # a second step reproduces itself (deterministic kernels, no stale state)
+    r2 = sp.run_pp_local(stages, k)
+    assert r2.loss == r.loss
+    sp.close()
+    for m in stages:
+        m.close()
+    full.close()
+
+
+def test_pp_local_matches_simulated_op_count(ctx):
+    cfg = cf.model_cfg(arch=1, vocab=96, d=128, heads=4, kv_heads=2, layers=2, ffn=256, seed=3)
+    lengths = np.array([300, 20, 41], np.int64)
+    tokens = cf.gen_tokens(lengths, 96, 5)
+    plan = cf.Plan.build(lengths, 64, 1)
+    stages = [cf.Model(ctx, cfg, stage=s, num_stages=2) for s in range(2)]
+    sp = cf.Step(stages[0], plan, lengths, tokens)
+    r = sp.run_pp_local(stages, 1)
+    ops, _, _, res = capi.pp_simulate(plan, 2, 1)
+    n_recompute = int((ops[-1]["kind"] == capi.PP_RECOMPUTE).sum())
+    assert r.recompute_forward_count == n_recompute == 4  # 300 tokens @64 -> 5 chunks, K=1
+    sp.close()
+
+
+def test_pp_stage_misuse_fails_loudly(ctx):
+    cfg = cf.model_cfg(arch=0, vocab=64, d=64, heads=4, kv_heads=2, layers=2, seed=7)
+    lengths = np.array([8, 40], np.int64)
+    tokens = cf.gen_tokens(lengths, 64, 1)
+    plan = cf.Plan.build(lengths, 32, 1)
+    s0, s1 = (cf.Model(ctx, cfg, stage=s, num_stages=2) for s in range(2))
+    st = cf.Step(s0, plan, lengths, tokens)
+    with pytest.raises(capi.CfError):
+        st.run_pp_local([s1, s0], 1)  # wrong stage order
+    with pytest.raises(capi.CfError):
+        st.run()  # a stage slice cannot run the unsplit step
+    with pytest.raises(capi.CfError):
+        st.run_pp(1)  # no pipeline links on this context
+    st.close()
+
+
+def test_pp_rank_path_one_stage_equals_step_run():
+    """cf_pp_step_run (the per-rank NCCL path) with one stage and a 1-rank
+    PP x DP layout: no links, the DP split communicator all-reduces over one
+    rank — results bitwise those of cf_step_run."""
+    c = cf.Context(0)
+    c.init_pp(0, 1, 1, cf.Context.nccl_unique_id())
+    cfg = cf.model_cfg(arch=1, vocab=96, d=128, heads=4, kv_heads=2, layers=2, ffn=256, seed=3)
+    lengths = np.array([300, 20, 41], np.int64)
+    tokens = cf.gen_tokens(lengths, 96, 5)
+    plan = cf.Plan.build(lengths, 64, 1)
+    m = cf.Model(c, cfg)
+    st = cf.Step(m, plan, lengths, tokens)
+    ref = st.run()
+    g_ref = m.grads_flat()
+    r = st.run_pp(1)
+    assert r.loss == ref.loss and r.kv_completeness_violations == 0 and r.recompute_loss_mismatches == 0
+    assert np.array_equal(m.grads_flat(), g_ref)
+    st.close()
+    m.close()
+    c.close()
