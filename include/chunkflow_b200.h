@@ -299,6 +299,12 @@ int cf_step_prepare(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
 int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step,
                 const cf_run_opts* opts, cf_run_result* result);
 void cf_step_destroy(cf_step* step);
+/* Device time of every executed op (forward / recompute / backward, the
+ * CF_PP_* kinds) of the step's last run when the context profiles
+ * (cf_ctx_set_profiling): measured per-chunk costs for cf_pp_simulate.
+ * Arrays may be NULL to query *n. */
+int cf_step_op_times(const cf_step* step, int64_t* n, int64_t* kinds,
+                     int64_t* chunk_ids, double* ms);
 /* backward_full (toy_model.hpp:575): every sequence alone, unchunked. */
 int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids,
                      const int64_t* lengths, const int32_t* tokens, int64_t n,

@@ -87,7 +87,7 @@ EXPORTS = [
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
-    "cf_pp_run_local", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_pp_run_local", "cf_step_op_times", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None
@@ -426,6 +426,16 @@ class Step:
         r = RunResult()
         check(lib().cf_step_run(self.model.ctx.h, self.model.h, self.h, C.byref(o), C.byref(r)))
         return r
+
+    def op_times(self):
+        """(kinds, chunk_ids, ms) of every op of the last run (profiling on)."""
+        n = C.c_int64()
+        check(lib().cf_step_op_times(self.h, C.byref(n), None, None, None))
+        kinds = np.zeros(n.value, np.int64)
+        ids = np.zeros(n.value, np.int64)
+        ms = np.zeros(n.value, np.float64)
+        check(lib().cf_step_op_times(self.h, C.byref(n), _p(kinds), _p(ids), _p(ms)))
+        return kinds, ids, ms
 
     def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
         """This rank's pipeline stage (cf_pp_step_run; needs Context.init_pp)."""

@@ -249,6 +249,14 @@ int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, const cf_run_opts* 
 
 void cf_step_destroy(cf_step* step) { cfb::step_destroy(step); }
 
+int cf_step_op_times(const cf_step* step, int64_t* n, int64_t* kinds, int64_t* chunk_ids, double* ms) {
+  return cfb::guard([&] {
+    need(step, "step");
+    need(n, "n");
+    cfb::step_op_times(step, n, kinds, chunk_ids, ms);
+  });
+}
+
 int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids, const int64_t* lengths,
                      const int32_t* tokens, int64_t n, double normalizer_override, cf_run_result* result) {
   return cfb::guard([&] {

@@ -436,6 +436,9 @@ struct cf_step {
   double mf_layer = 0, mf_head = 0, hw_layer = 0, hw_head = 0;
   std::map<int64_t, int64_t> group_len;  // group -> sequence length
   cfb::Plan plan_copy;
+  // device time of every op of the last run when the context profiles
+  // (cf_step_op_times): kind (CF_PP_*), chunk id, milliseconds
+  std::vector<std::array<double, 3>> op_times;
 };
 
 namespace cfb {
@@ -624,6 +627,15 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
   CK(cudaMemcpyAsync(st->meta_dev, st->meta_host, static_cast<size_t>(st->meta_len) * 4, cudaMemcpyHostToDevice,
                      ctx->stream));
   return st.release();
+}
+
+void step_op_times(const cf_step* st, int64_t* n, int64_t* kinds, int64_t* ids, double* ms) {
+  *n = static_cast<int64_t>(st->op_times.size());
+  for (size_t i = 0; i < st->op_times.size(); ++i) {
+    if (kinds) kinds[i] = static_cast<int64_t>(st->op_times[i][0]);
+    if (ids) ids[i] = static_cast<int64_t>(st->op_times[i][1]);
+    if (ms) ms[i] = st->op_times[i][2];
+  }
 }
 
 void step_destroy(cf_step* st) {
@@ -976,6 +988,18 @@ struct StageRunner {
   std::vector<int64_t> first_pass_slots;
   int64_t held = 0, peak = 0, violations = 0, recomputes = 0;
   int64_t io_bytes = 0;  // stage-boundary buffers held (kept inputs)
+  struct OpMark {
+    int64_t kind, id;
+    cudaEvent_t a, b;
+  };
+  std::vector<OpMark> marks;  // per-op device time when profiling
+  cudaEvent_t op_begin() { return ctx->profile ? ex.mark() : nullptr; }
+  void op_end(cudaEvent_t a, int64_t kind, int64_t id) {
+    if (!ctx->profile) return;
+    cudaEvent_t b = ex.ev();
+    CK(cudaEventRecord(b, ex.s));
+    marks.push_back({kind, id, a, b});
+  }
 
   StageRunner(Ctx* c, Model* mm, cf_step* s, const cf_run_opts& opts, int64_t slots)
       : ctx(c), m(mm), st(s), nslots(slots) {
@@ -1034,6 +1058,7 @@ struct StageRunner {
   // chunk's first pass (keep_in).  Returns the stage output for the next
   // stage (caller-owned pool memory) or null on the last stage / for F'.
   float* forward(int64_t id, bool retain, bool recompute, bool save_kv, int64_t slot, float* in, bool keep_in) {
+    cudaEvent_t t0 = op_begin();
     const ChunkMeta& cm = chunk(id);
     GroupState* gs = group_for(cm);
     const size_t act = static_cast<size_t>(cm.T * m->d) * 4;
@@ -1086,6 +1111,7 @@ struct StageRunner {
         pool_free(ctx, in);
       }
     }
+    op_end(t0, recompute ? kPpRecompute : kPpForward, id);
     return out;
   }
 
@@ -1094,6 +1120,7 @@ struct StageRunner {
   // Returns the gradient of the stage input for the previous stage (caller-
   // owned) or null on the first stage.
   float* backward(int64_t id, float* dy) {
+    cudaEvent_t t0 = op_begin();
     const ChunkMeta& cm = chunk(id);
     GroupState* gs = group_for(cm);
     auto lit = live.find(id);
@@ -1120,6 +1147,7 @@ struct StageRunner {
     ex.free_tape(lit->second);
     live.erase(lit);
     held -= cm.T;
+    op_end(t0, kPpBackward, id);
     if (m->has_embed) {
       if (dx) pool_free(ctx, dx);
       return nullptr;
@@ -1147,6 +1175,11 @@ struct StageRunner {
       cls_ms[r.cls] += ms;
       cls_flops[r.cls] += r.flops;
       cls_n[r.cls] += r.n;
+    }
+    for (const OpMark& mk : marks) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, mk.a, mk.b));
+      st->op_times.push_back({static_cast<double>(mk.kind), static_cast<double>(mk.id), static_cast<double>(ms)});
     }
     double total = 0;
     for (int64_t sl : first_pass_slots) total += slots[static_cast<size_t>(sl)];
@@ -1227,6 +1260,7 @@ bool first_pass_saves_kv(const cf_step* st, const ChunkMeta& cm) {
 void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res) {
   if (!m->has_embed || !m->has_head) throw ValidationError("a pipeline-stage model needs cf_pp_step_run");
   const Plan& plan = *st->plan;
+  st->op_times.clear();
   reset_pool_high(ctx);
   StageRunner r(ctx, m, st, opts, static_cast<int64_t>(plan.events.size()));
   for (size_t ei = 0; ei < plan.events.size(); ++ei) {
@@ -1260,6 +1294,7 @@ void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t P, cf_step* st, i
     for (size_t i = 0; i < tr.stages[static_cast<size_t>(s)].size(); ++i)
       seq.emplace_back(tr.stages[static_cast<size_t>(s)][i].start, s, i);
   std::sort(seq.begin(), seq.end());
+  st->op_times.clear();
   reset_pool_high(ctx);
   std::vector<std::unique_ptr<StageRunner>> run;
   for (int64_t s = 0; s < P; ++s)
@@ -1372,6 +1407,7 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
     throw ValidationError("pipeline links not initialised (cf_ctx_init_pp)");
   const StagePlan sp = stage_plan(st, k, P);
   const std::vector<PpOp>& order = sp.orders[static_cast<size_t>(s)];
+  st->op_times.clear();
   reset_pool_high(ctx);
   StageRunner r(ctx, m, st, opts, static_cast<int64_t>(order.size()));
   std::vector<LinkOp> sends;  // output buffers in flight to a neighbour

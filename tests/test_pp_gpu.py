@@ -110,8 +110,8 @@ def test_pp_stage_misuse_fails_loudly(ctx):
 
 def test_pp_rank_path_one_stage_equals_step_run():
     """cf_pp_step_run (the per-rank NCCL path) with one stage and a 1-rank
-    PP x DP layout: no links, the DP split communicator all-reduces over one
-    rank — results bitwise those of cf_step_run."""
+    PP x DP layout (no links, no DP group) — results bitwise those of
+    cf_step_run."""
     c = cf.Context(0)
     c.init_pp(0, 1, 1, cf.Context.nccl_unique_id())
     cfg = cf.model_cfg(arch=1, vocab=96, d=128, heads=4, kv_heads=2, layers=2, ffn=256, seed=3)

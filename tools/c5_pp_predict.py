@@ -1,0 +1,125 @@
+"""Config C5 (BASELINE.json): Qwen2.5-32B-shaped, PP=4 x DP=2 chunk-aware 1F1B,
+chunk 16K — simulator-in-the-loop prediction from MEASURED stage costs
+(SURVEY §8f-1), because every gpurun call gets exactly one B200.
+
+1. Measure on one B200, per chunk, the device time of every forward /
+   recompute / backward of one pipeline stage's worth of layers (16 of 64)
+   on the real C5 chunk plan (cf_step_op_times): a 16-layer model with the
+   LM head (= the last stage, the heaviest) and a 1-layer model, so that
+   per-layer and head costs separate:
+       layer(c) = (t16(c) - t1(c)) / 15,  head(c) = t1(c) - layer(c).
+2. Stage costs: stage 0 = 16 layers (+ embedding, ~0), stages 1-2 = 16
+   layers, stage 3 = 16 layers + head.  The reference simulator applies one
+   cost per chunk to every stage, so the prediction uses the last-stage cost
+   (upper bound on the makespan) and, for comparison, the middle-stage cost.
+3. DP=2: the 2-block global plan is split by the LPT unit partition
+   (cf_plan_partition); each replica's sub-plan is simulated with the
+   product's cf_pp_simulate (bit-exact with pipeline.hpp) on those costs.
+   Step time = slowest replica's makespan + the stage-gradient all-reduce
+   estimate (2 ranks, fp32, NVLink ~ 700 GB/s bus bandwidth).
+
+Writes one JSON object (stdout)."""
+import json
+import sys
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2503_02356_b200 as cf  # noqa: E402
+from paper_2503_02356_b200 import capi  # noqa: E402
+
+QWEN = dict(vocab=152064, d=5120, heads=40, kv_heads=8, ffn=27648, seed=1)
+LAYERS, STAGES, DP, CHUNK, K = 64, 4, 2, 16384, 1
+
+
+def block(seed):
+    short = capi.synthesize(999, seed, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
+    return np.concatenate([short, [37888]]).astype(np.int64)
+
+
+def measure(ctx, layers, plan, lengths, tokens, ids):
+    m = cf.Model(ctx, cf.model_cfg(arch=cf.ARCH_LLAMA, layers=layers, **QWEN))
+    st = cf.Step(m, plan, lengths, tokens, ids)
+    st.run()  # warm-up
+    ctx.set_profiling(True)
+    r = st.run()
+    ctx.set_profiling(False)
+    kinds, cids, ms = st.op_times()
+    st.close()
+    m.close()
+    return r, kinds, cids, ms
+
+
+def main():
+    ctx = cf.Context(0)
+    blocks = [block(b + 1) for b in range(DP)]
+    lengths = np.concatenate(blocks)
+    ids = np.arange(len(lengths), dtype=np.int64)
+    tokens = np.concatenate([cf.gen_tokens(bl, QWEN["vocab"], b + 1) for b, bl in enumerate(blocks)])
+    gplan = cf.Plan.build(lengths, CHUNK, K, ids)
+    replicas = [gplan.partition(DP, r) for r in range(DP)]
+    out = {"workload": "C5: Qwen2.5-32B-shaped (d 5120, 64 L, 40 H, GQA-8, ffn 27648, V 152064), PP=4 x DP=2, "
+                       "chunk 16384, K=1, two 1,000-seq long-tail blocks",
+           "method": "per-chunk stage costs measured on one B200 (16-layer and 1-layer models on replica 0's "
+                     "sub-plan), chunk-aware 1F1B timed by cf_pp_simulate (bit-exact with pipeline.hpp)"}
+    # measure on replica 0's sub-plan (its chunks are representative of both)
+    r16, k16, c16, t16 = measure(ctx, 16, replicas[0], lengths, tokens, ids)
+    r1, k1, c1, t1 = measure(ctx, 1, replicas[0], lengths, tokens, ids)
+    assert np.array_equal(k16, k1) and np.array_equal(c16, c1)
+    layer = (t16 - t1) / 15.0
+    head = t1 - layer
+    fw, bw = {}, {}
+    for kind, cid, lay, hd in zip(k16, c16, layer, head):
+        if kind == capi.PP_FORWARD:
+            fw[int(cid)] = (lay, hd)
+        elif kind == capi.PP_BACKWARD:
+            bw[int(cid)] = (lay, hd)
+    out["measured"] = {"stage16_step_s": float(t16.sum() / 1e3), "one_layer_step_s": float(t1.sum() / 1e3),
+                       "peak_hbm_gb_16_layers": r16.peak_hbm_bytes / 1e9,
+                       "static_gb_16_layers": r16.static_hbm_bytes / 1e9,
+                       "activations_gb_16_layers": r16.act_hbm_bytes / 1e9,
+                       "kv_state_gb_16_layers": r16.kv_hbm_bytes / 1e9,
+                       "model_tflops_16_layers": r16.model_flops / (t16.sum() / 1e3) / 1e12}
+    per_stage = LAYERS // STAGES
+    grad_bytes = 4 * (per_stage * (QWEN["d"] * (QWEN["d"] + 2 * 1024) + QWEN["d"] ** 2 + 3 * QWEN["d"] * QWEN["ffn"])
+                      + QWEN["d"] * QWEN["vocab"])
+    allreduce_ms = 2 * (DP - 1) / DP * grad_bytes / 700e9 * 1e3
+    res = {}
+    for label, with_head in (("last_stage_cost", True), ("middle_stage_cost", False)):
+        spans, bubbles, occ = [], [], []
+        for rp in replicas:
+            ch = rp.export()[0]
+            # costs of this replica's chunks: measured where replica 0 has the chunk, else by token count
+            f = np.zeros(len(ch))
+            b = np.zeros(len(ch))
+            ref_tok = {int(c["chunk_id"]): int(c["total_tokens"]) for c in replicas[0].export()[0]}
+            per_tok_f = np.mean([(v[0] * per_stage + (v[1] if with_head else 0)) / ref_tok[c] for c, v in fw.items()])
+            per_tok_b = np.mean([(v[0] * per_stage + (v[1] if with_head else 0)) / ref_tok[c] for c, v in bw.items()])
+            for i, c in enumerate(ch):
+                cid = int(c["chunk_id"])
+                if cid in fw and cid in bw:
+                    f[i] = fw[cid][0] * per_stage + (fw[cid][1] if with_head else 0)
+                    b[i] = bw[cid][0] * per_stage + (bw[cid][1] if with_head else 0)
+                else:
+                    f[i] = per_tok_f * int(c["total_tokens"])
+                    b[i] = per_tok_b * int(c["total_tokens"])
+            _, _, _, pr = capi.pp_simulate(rp, STAGES, K, fwd_cost=f, bwd_cost=b)
+            spans.append(pr.makespan)
+            bubbles.append(pr.bubble_ratio)
+            occ.append(pr.occupancy_bubble)
+        step_ms = max(spans) + allreduce_ms
+        res[label] = {"makespan_ms_per_replica": spans, "bubble_ratio": bubbles,
+                      "bubble_ratio_recompute_as_busy": occ, "allreduce_ms_est": allreduce_ms,
+                      "step_ms": step_ms, "tokens_per_s_8gpu": float(lengths.sum()) / (step_ms / 1e3)}
+    # whole-sequence 1F1B on the same replica for the paper's comparison
+    seqs = sorted({int(s["sequence_id"]) for s in replicas[0].export()[1]})
+    r0_lengths = lengths[seqs]
+    _, _, _, p1 = capi.pp_simulate_1f1b(r0_lengths, STAGES, {"alpha": 1.0, "beta": 1.05e-5})
+    out["prediction"] = res
+    out["reference_1f1b_whole_sequence_bubble_cost_model"] = p1.bubble_ratio
+    out["tokens_global"] = int(lengths.sum())
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
