@@ -3,6 +3,8 @@
 // result is bitwise reproducible run to run (needed for the reference's
 // recompute-loss check, plan_runner.hpp:232-241).
 #include <algorithm>
+#include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ops.h"
@@ -200,6 +202,150 @@ __global__ void swiglu_bwd_kernel(const bf16* gu, const bf16* dh, int64_t T, int
     }
     *reinterpret_cast<uint4*>(dgu + t * 2 * ffn + j) = pack8(og);
     *reinterpret_cast<uint4*>(dgu + t * 2 * ffn + ffn + j) = pack8(ou);
+  }
+}
+
+// Row-resident RMSNorm: one 128-thread CTA per row, the row held in
+// registers (NV float4 per thread, d <= NV*512), so x is read exactly once;
+// block reduction through 4 warp partials (every thread sums them in the
+// same order -> deterministic).
+constexpr int kRowThreads = 128;
+template <int NV>
+__global__ __launch_bounds__(kRowThreads) void rmsnorm_row_kernel(const float* __restrict__ x,
+                                                                   const float* __restrict__ gain, int d, float eps,
+                                                                   bf16* __restrict__ y) {
+  __shared__ float red[kRowThreads / 32];
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * d;
+  float4 v[NV];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    v[i] = c < d ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  ss = red[0] + red[1] + red[2] + red[3];
+  const float r = rsqrtf(ss / static_cast<float>(d) + eps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    if (c < d) {
+      const float4 g = *reinterpret_cast<const float4*>(gain + c);
+      uint2 o;
+      o.x = pack_bf16(v[i].x * r * g.x, v[i].y * r * g.y);
+      o.y = pack_bf16(v[i].z * r * g.z, v[i].w * r * g.w);
+      *reinterpret_cast<uint2*>(y + row * d + c) = o;
+    }
+  }
+}
+
+// Fused RMSNorm backward + gain gradient (+ bf16 copy of the result): a CTA
+// owns a contiguous row range, holds its columns of the gain and of the
+// gain-gradient partial in registers, and streams x / dy / dres once.
+//   dx = dres + r*dy*g - x*r^3*<dy*g, x>/d,   part[cta][c] = sum_rows dy*x*r
+template <int NV>
+__global__ __launch_bounds__(kRowThreads) void rmsnorm_bwd_rows_kernel(
+    const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ dy, const float* dres,
+    int64_t T, int d, float eps, int64_t rows_per_cta, float* dx, bf16* __restrict__ dx_bf16,
+    float* __restrict__ part) {
+  __shared__ float red[2][2][kRowThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4 g[NV], acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    g[i] = c < d ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r0 = blockIdx.x * rows_per_cta, r1 = min(T, r0 + rows_per_cta);
+  for (int64_t row = r0; row < r1; ++row) {
+    const int par = static_cast<int>(row & 1);
+    const float* xr = x + row * d;
+    const float* gr = dy + row * d;
+    float4 xv[NV], gv[NV];
+    float ss = 0.f, dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (threadIdx.x + i * kRowThreads) * 4;
+      xv[i] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[i] = c < d ? __ldcs(reinterpret_cast<const float4*>(gr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      ss += xv[i].x * xv[i].x + xv[i].y * xv[i].y + xv[i].z * xv[i].z + xv[i].w * xv[i].w;
+      dot += gv[i].x * g[i].x * xv[i].x + gv[i].y * g[i].y * xv[i].y + gv[i].z * g[i].z * xv[i].z +
+             gv[i].w * g[i].w * xv[i].w;
+    }
+    ss = warp_sum(ss);
+    dot = warp_sum(dot);
+    if (lane == 0) {
+      red[par][0][w] = ss;
+      red[par][1][w] = dot;
+    }
+    __syncthreads();
+    ss = red[par][0][0] + red[par][0][1] + red[par][0][2] + red[par][0][3];
+    dot = red[par][1][0] + red[par][1][1] + red[par][1][2] + red[par][1][3];
+    const float r = rsqrtf(ss / static_cast<float>(d) + eps);
+    const float k = r * r * r * dot / static_cast<float>(d);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = (threadIdx.x + i * kRowThreads) * 4;
+      if (c >= d) continue;
+      float4 o = dres ? *reinterpret_cast<const float4*>(dres + row * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      o.x += r * gv[i].x * g[i].x - xv[i].x * k;
+      o.y += r * gv[i].y * g[i].y - xv[i].y * k;
+      o.z += r * gv[i].z * g[i].z - xv[i].z * k;
+      o.w += r * gv[i].w * g[i].w - xv[i].w * k;
+      *reinterpret_cast<float4*>(dx + row * d + c) = o;
+      if (dx_bf16) {
+        uint2 b;
+        b.x = pack_bf16(o.x, o.y);
+        b.y = pack_bf16(o.z, o.w);
+        *reinterpret_cast<uint2*>(dx_bf16 + row * d + c) = b;
+      }
+      acc[i].x += gv[i].x * xv[i].x * r;
+      acc[i].y += gv[i].y * xv[i].y * r;
+      acc[i].z += gv[i].z * xv[i].z * r;
+      acc[i].w += gv[i].w * xv[i].w * r;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    if (c < d) *reinterpret_cast<float4*>(part + blockIdx.x * static_cast<int64_t>(d) + c) = acc[i];
+  }
+}
+
+// RoPE rotate-half, 8 consecutive frequency pairs per thread (16-byte loads
+// of both halves); heads [0,H) are q, [H, H+KVH) are k.
+__global__ void rope_qk_vec_kernel(bf16* qkv, int64_t ld, int64_t T, int H, int KVH, int dh, int64_t col_k,
+                                   const float2* __restrict__ tab, int inverse_q_only) {
+  const int half = dh / 2, g8 = half / 8;
+  const int heads = inverse_q_only ? H : H + KVH;
+  const int64_t n = T * heads * g8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i % g8) * 8;
+    const int64_t th = i / g8;
+    const int hh = static_cast<int>(th % heads);
+    const int64_t t = th / heads;
+    bf16* p = qkv + t * ld + (hh < H ? static_cast<int64_t>(hh) * dh : col_k + static_cast<int64_t>(hh - H) * dh);
+    float a[8], b[8], oa[8], ob[8];
+    unpack8(*reinterpret_cast<const uint4*>(p + j), a);
+    unpack8(*reinterpret_cast<const uint4*>(p + j + half), b);
+    const float4* tp = reinterpret_cast<const float4*>(tab + t * half + j);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float4 cs = tp[e];  // (cos, sin) of pairs j+2e, j+2e+1
+      const float s0 = inverse_q_only ? -cs.y : cs.y, s1 = inverse_q_only ? -cs.w : cs.w;
+      oa[2 * e] = a[2 * e] * cs.x - b[2 * e] * s0;
+      ob[2 * e] = b[2 * e] * cs.x + a[2 * e] * s0;
+      oa[2 * e + 1] = a[2 * e + 1] * cs.z - b[2 * e + 1] * s1;
+      ob[2 * e + 1] = b[2 * e + 1] * cs.z + a[2 * e + 1] * s1;
+    }
+    *reinterpret_cast<uint4*>(p + j) = pack8(oa);
+    *reinterpret_cast<uint4*>(p + j + half) = pack8(ob);
   }
 }
 
@@ -431,10 +577,32 @@ cudaError_t embed_fwd(const int32_t* tok, const bf16* E, int64_t d, int64_t T, f
   embed_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(tok, E, d, T, x);
   return cudaGetLastError();
 }
+template <int MaxNV = 16, class F>
+bool dispatch_nv(int64_t d, F&& f) {
+  const int64_t nv = (d + 4 * kRowThreads - 1) / (4 * kRowThreads);
+  if (nv > MaxNV) return false;
+  switch (nv) {
+    case 1: f(std::integral_constant<int, 1>()); return true;
+    case 2: f(std::integral_constant<int, 2>()); return true;
+    case 4: f(std::integral_constant<int, 4>()); return true;
+    case 6: f(std::integral_constant<int, 6>()); return true;
+    case 8: f(std::integral_constant<int, 8>()); return true;
+    case 10: f(std::integral_constant<int, 10>()); return true;
+    case 12: f(std::integral_constant<int, 12>()); return true;
+    case 16: f(std::integral_constant<int, 16>()); return true;
+    default: return false;
+  }
+}
+
 cudaError_t rmsnorm_fwd(const float* x, const float* gain, int64_t T, int64_t d, float eps, bf16* y,
                         cudaStream_t st) {
   if (T == 0) return cudaSuccess;
-  rmsnorm_fwd_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(x, gain, T, d, eps, y);
+  const bool row_kernel = (d % 4) == 0 && dispatch_nv(d, [&](auto nv) {
+    rmsnorm_row_kernel<decltype(nv)::value><<<static_cast<unsigned>(T), kRowThreads, 0, st>>>(
+        x, gain, static_cast<int>(d), eps, y);
+  });
+  if (!row_kernel)
+    rmsnorm_fwd_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(x, gain, T, d, eps, y);
   return cudaGetLastError();
 }
 cudaError_t to_bf16(const float* x, bf16* y, int64_t n, cudaStream_t st) {
@@ -445,13 +613,25 @@ cudaError_t rope_table(const int32_t* pos, int64_t T, int dh, double theta, floa
   rope_table_kernel<<<blocks_for(T * (dh / 2)), kThreads, 0, st>>>(pos, T, dh / 2, dh, theta, tab);
   return cudaGetLastError();
 }
+// 16-byte vector path when the half head width is a multiple of 8 and every
+// row / column base is 16-byte aligned.
+inline bool rope_vec_ok(const void* p, int64_t ld, int dh, int64_t col_k) {
+  return (dh / 2) % 8 == 0 && ld % 8 == 0 && col_k % 8 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
 cudaError_t rope_qk(bf16* qkv, int64_t ld, int64_t T, int H, int KVH, int dh, int64_t col_k, const float2* tab,
                     cudaStream_t st) {
-  rope_qk_kernel<<<blocks_for(T * (H + KVH) * (dh / 2)), kThreads, 0, st>>>(qkv, ld, T, H, KVH, dh, col_k, tab, 0);
+  if (rope_vec_ok(qkv, ld, dh, col_k))
+    rope_qk_vec_kernel<<<blocks_for(T * (H + KVH) * (dh / 16)), kThreads, 0, st>>>(qkv, ld, T, H, KVH, dh, col_k,
+                                                                                  tab, 0);
+  else
+    rope_qk_kernel<<<blocks_for(T * (H + KVH) * (dh / 2)), kThreads, 0, st>>>(qkv, ld, T, H, KVH, dh, col_k, tab, 0);
   return cudaGetLastError();
 }
 cudaError_t rope_bwd_q(bf16* dqkv, int64_t ld, int64_t T, int H, int dh, const float2* tab, cudaStream_t st) {
-  rope_qk_kernel<<<blocks_for(T * H * (dh / 2)), kThreads, 0, st>>>(dqkv, ld, T, H, 0, dh, 0, tab, 1);
+  if (rope_vec_ok(dqkv, ld, dh, 0))
+    rope_qk_vec_kernel<<<blocks_for(T * H * (dh / 16)), kThreads, 0, st>>>(dqkv, ld, T, H, 0, dh, 0, tab, 1);
+  else
+    rope_qk_kernel<<<blocks_for(T * H * (dh / 2)), kThreads, 0, st>>>(dqkv, ld, T, H, 0, dh, 0, tab, 1);
   return cudaGetLastError();
 }
 cudaError_t kv_store(const bf16* qkv, int64_t ld, int64_t T, int64_t kvw, int64_t col_k, int64_t col_v, bf16* kc,
@@ -483,6 +663,38 @@ cudaError_t rmsnorm_bwd(const float* x, const float* gain, const float* dy, cons
   rmsnorm_bwd_kernel<<<static_cast<unsigned>((T * 32 + 255) / 256), 256, 0, st>>>(x, gain, dy, dres, T, d, eps, dx,
                                                                                     rstd);
   return cudaGetLastError();
+}
+cudaError_t rmsnorm_bwd_fused(const float* x, const float* gain, const float* dy, const float* dres, int64_t T,
+                              int64_t d, float eps, float* dx, bf16* dx_bf16, float* dgain, cudaStream_t st) {
+  if (T == 0) return cudaSuccess;
+  if (d % 4) return cudaErrorInvalidValue;
+  // one wave at the occupancy the register footprint allows (row state and
+  // gain partial live in registers: ~20 regs per float4 column group)
+  const int64_t nv = (d + 4 * kRowThreads - 1) / (4 * kRowThreads);
+  const int64_t per_sm = nv <= 4 ? 8 : nv <= 8 ? 3 : 2;
+  const int64_t ctas = std::min<int64_t>(T, 148 * per_sm);
+  const int64_t rows = (T + ctas - 1) / ctas;
+  const int64_t grid = (T + rows - 1) / rows;
+  float* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, static_cast<size_t>(grid * d) * 4, st);
+  if (e != cudaSuccess) return e;
+  const bool ok = dispatch_nv<12>(d, [&](auto nv) {
+    if constexpr (decltype(nv)::value <= 12)
+    rmsnorm_bwd_rows_kernel<decltype(nv)::value><<<static_cast<unsigned>(grid), kRowThreads, 0, st>>>(
+        x, gain, dy, dres, T, static_cast<int>(d), eps, rows, dx, dx_bf16, part);
+  });
+  if (!ok) {
+    cudaFreeAsync(part, st);
+    return cudaErrorInvalidValue;
+  }
+  gain_grad_reduce_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, st>>>(part, static_cast<int>(grid), d,
+                                                                                 dgain);
+  e = cudaGetLastError();
+  cudaFreeAsync(part, st);
+  return e;
+}
+bool rmsnorm_bwd_fused_ok(int64_t d) {
+  return d % 4 == 0 && dispatch_nv<12>(d, [](auto) {});
 }
 cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d, float* dgain,
                       cudaStream_t st) {

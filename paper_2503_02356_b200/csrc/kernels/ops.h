@@ -41,6 +41,13 @@ cudaError_t sum_f64(const float* v, int64_t n, double* out, cudaStream_t st);
 // dx = dres + d(rmsnorm)/dx^T dy  (dres may alias dx; may be null); writes rstd.
 cudaError_t rmsnorm_bwd(const float* x, const float* gain, const float* dy, const float* dres, int64_t T, int64_t d,
                         float eps, float* dx, float* rstd, cudaStream_t st);
+// Fused: dx = dres + d(rmsnorm)/dx^T dy (dres may alias dx; may be null),
+// optional bf16 copy of dx, and dgain[c] += sum_t dy*x*rstd (fixed order:
+// per-CTA row-range partials, then a column reduction).  Needs d % 4 == 0
+// and d <= 8192 (rmsnorm_bwd_fused_ok).
+cudaError_t rmsnorm_bwd_fused(const float* x, const float* gain, const float* dy, const float* dres, int64_t T,
+                              int64_t d, float eps, float* dx, bf16* dx_bf16, float* dgain, cudaStream_t st);
+bool rmsnorm_bwd_fused_ok(int64_t d);
 // dgain[c] += sum_t dy[t,c] * x[t,c] * rstd[t]   (fixed order)
 cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d, float* dgain,
                       cudaStream_t st);

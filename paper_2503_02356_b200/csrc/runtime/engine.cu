@@ -416,6 +416,12 @@ struct Tape {
   bf16* act = nullptr;    // L x T x gu_w
   bf16* dlogits = nullptr;// T x Vp
   float2* tab = nullptr;  // T x dh/2
+  // llama, retained tapes only: the GEMM inputs the backward would
+  // otherwise recompute — normed activations and the SwiGLU output
+  bf16* xn1 = nullptr;    // L x T x d   rmsnorm(x_in)
+  bf16* xn2 = nullptr;    // L x T x d   rmsnorm(x_mid)
+  bf16* h = nullptr;      // L x T x ffn swiglu(gate, up)
+  bf16* xnf = nullptr;    // T x d       final norm
   int64_t bytes = 0;
 };
 
@@ -717,6 +723,12 @@ struct Exec {
       t.act = a.take<bf16>(L_ * T * m->gu_w);
       if (retain && m->has_head) t.dlogits = a.take<bf16>(T * Vp);
       t.tab = a.take<float2>(T * std::max<int64_t>(1, m->dh / 2));
+      if (retain && m->llama) {
+        t.xn1 = a.take<bf16>(L_ * T * d);
+        t.xn2 = a.take<bf16>(L_ * T * d);
+        t.h = a.take<bf16>(L_ * T * m->ffn);
+        if (m->has_head) t.xnf = a.take<bf16>(T * d);
+      }
     };
     Arena measure{nullptr, 0};
     carve(measure);
@@ -786,11 +798,12 @@ struct Exec {
       float* xm = t.x_mid + l * T * d;
       bf16* qkv = t.qkv + l * T * m->qkv_w;
       bf16* act = t.act + l * T * m->gu_w;
+      bf16* xn1 = t.xn1 ? t.xn1 + l * T * d : A;
       if (m->llama)
-        L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+        L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), xn1, s), "rmsnorm");
       else
-        L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
-      gemm(A, 1, d, ly.wqkv, 0, m->qkv_w, qkv, m->qkv_w, T, m->qkv_w, d, cfk::EPI_BF16);
+        L(cfk::to_bf16(x, xn1, T * d, s), "to_bf16");
+      gemm(xn1, 1, d, ly.wqkv, 0, m->qkv_w, qkv, m->qkv_w, T, m->qkv_w, d, cfk::EPI_BF16);
       if (m->llama)
         L(cfk::rope_qk(qkv, m->qkv_w, T, static_cast<int>(m->H), static_cast<int>(m->KVH), static_cast<int>(m->dh),
                        d, t.tab, s),
@@ -811,10 +824,12 @@ struct Exec {
       gemm(t.o + l * T * d, 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
       float* xn = t.x_in + (l + 1) * T * d;
       if (m->llama) {
-        L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
-        gemm(A, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
-        L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");
-        gemm(A, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
+        bf16* xn2 = t.xn2 ? t.xn2 + l * T * d : A;
+        L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), xn2, s), "rmsnorm");
+        gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
+        bf16* hl = t.h ? t.h + l * T * m->ffn : A;
+        L(cfk::swiglu_fwd(act, T, m->ffn, hl, s), "swiglu");
+        gemm(hl, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
       } else {
         L(cfk::to_bf16(xm, A, T * d, s), "to_bf16");
         gemm(A, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->ffn, d, cfk::EPI_BF16_TANH);
@@ -823,11 +838,12 @@ struct Exec {
     }
     if (m->has_head) {
       const float* xL = t.x_in + m->L * T * d;
+      bf16* xnf = t.xnf ? t.xnf : A;
       if (m->llama)
-        L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+        L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), xnf, s), "rmsnorm");
       else
-        L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
-      gemm(A, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
+        L(cfk::to_bf16(xL, xnf, T * d, s), "to_bf16");
+      gemm(xnf, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
       L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, tgt, inv_norm, row_loss, retain ? t.dlogits : nullptr, s), "ce");
       L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
       pool_free(ctx, logits);
@@ -863,17 +879,31 @@ struct Exec {
     void* scratch = a.base;
 
     // Output head + CE (toy_model.hpp:369-388): dHead += xf^T dlogits, dxf = dlogits head^T.
+    // RMSNorm backward; the fused kernel also leaves bf16(out) in xb (the
+    // next dgrad/wgrad GEMM input) and accumulates the gain gradient
+    const bool fused = m->llama && cfk::rmsnorm_bwd_fused_ok(d);
+    auto norm_bwd = [&](const float* xin, const float* gain, const float* dres, float* out, float* dgain) {
+      if (fused) {
+        L(cfk::rmsnorm_bwd_fused(xin, gain, da, dres, T, d, eps, out, xb, dgain, s), "rmsnorm_bwd_fused", 2);
+      } else {
+        L(cfk::rmsnorm_bwd(xin, gain, da, dres, T, d, eps, out, rstd, s), "rmsnorm_bwd");
+        L(cfk::gain_grad(xin, da, rstd, T, d, dgain, s), "gain_grad", 2);
+      }
+    };
     if (m->has_head) {
       const float* xL = t.x_in + m->L * T * d;
-      if (m->llama)
-        L(cfk::rmsnorm_fwd(xL, m->gf, T, d, eps, A, s), "rmsnorm");
-      else
-        L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
-      gemm(A, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
+      const bf16* xnf = t.xnf;
+      if (!xnf) {
+        if (m->llama)
+          L(cfk::rmsnorm_fwd(xL, m->gf, T, d, eps, A, s), "rmsnorm");
+        else
+          L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+        xnf = A;
+      }
+      gemm(xnf, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
       if (m->llama) {
         gemm(t.dlogits, 1, Vp, m->head, 1, Vp, da, d, T, d, m->V, cfk::EPI_F32);
-        L(cfk::rmsnorm_bwd(xL, m->gf, da, nullptr, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
-        L(cfk::gain_grad(xL, da, rstd, T, d, m->d_gf, s), "gain_grad");
+        norm_bwd(xL, m->gf, nullptr, dx, m->d_gf);
       } else {
         gemm(t.dlogits, 1, Vp, m->head, 1, Vp, dx, d, T, d, m->V, cfk::EPI_F32);
       }
@@ -886,17 +916,20 @@ struct Exec {
       const bf16* act = t.act + l * T * m->gu_w;
       const bf16* O = t.o + l * T * d;
       // FFN (toy_model.hpp:409-425)
-      L(cfk::to_bf16(dx, xb, T * d, s), "to_bf16");
+      // bf16(dx) is left in xb by the previous norm_bwd, except when dx came
+      // from the next pipeline stage
+      if (!fused || (l == m->L - 1 && !m->has_head)) L(cfk::to_bf16(dx, xb, T * d, s), "to_bf16");
       if (m->llama) {
         gemm(xb, 1, d, ly.w2, 1, d, dh, m->ffn, T, m->ffn, d, cfk::EPI_BF16);
-        L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");  // recompute h
-        gemm(A, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
+        const bf16* hl = t.h ? t.h + l * T * m->ffn : A;
+        if (!t.h) L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");  // recompute h
+        gemm(hl, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
         L(cfk::swiglu_bwd(act, dh, T, m->ffn, dgu, s), "swiglu_bwd");
-        L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, eps, A, s), "rmsnorm");  // recompute xn2
-        gemm(A, 0, d, dgu, 0, m->gu_w, ly.d_w1, m->gu_w, d, m->gu_w, T, cfk::EPI_F32_ACC);
+        const bf16* xn2 = t.xn2 ? t.xn2 + l * T * d : A;
+        if (!t.xn2) L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, eps, A, s), "rmsnorm");  // recompute xn2
+        gemm(xn2, 0, d, dgu, 0, m->gu_w, ly.d_w1, m->gu_w, d, m->gu_w, T, cfk::EPI_F32_ACC);
         gemm(dgu, 1, m->gu_w, ly.w1, 1, m->gu_w, da, d, T, d, m->gu_w, cfk::EPI_F32);
-        L(cfk::rmsnorm_bwd(xm, ly.g2, da, dx, T, d, eps, dmid, rstd, s), "rmsnorm_bwd");
-        L(cfk::gain_grad(xm, da, rstd, T, d, ly.d_g2, s), "gain_grad");
+        norm_bwd(xm, ly.g2, dx, dmid, ly.d_g2);
       } else {
         gemm(xb, 1, d, ly.w2, 1, d, dgu, m->ffn, T, m->ffn, d, cfk::EPI_BF16_TANHGRAD, act, m->ffn);
         gemm(act, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
@@ -905,7 +938,7 @@ struct Exec {
         gemm(A, 0, d, dgu, 0, m->ffn, ly.d_w1, m->gu_w, d, m->ffn, T, cfk::EPI_F32_ACC);
       }
       // Attention output projection (toy_model.hpp:427-434)
-      L(cfk::to_bf16(dmid, xb, T * d, s), "to_bf16");
+      if (!fused) L(cfk::to_bf16(dmid, xb, T * d, s), "to_bf16");
       bf16* dO = A;  // reuse
       gemm(xb, 1, d, ly.wo, 1, d, dO, d, T, d, d, cfk::EPI_BF16);
       gemm(O, 0, d, xb, 0, d, ly.d_wo, d, d, d, T, cfk::EPI_F32_ACC);
@@ -942,15 +975,17 @@ struct Exec {
       if (m->llama)
         L(cfk::rope_bwd_q(dqkv, qw, T, static_cast<int>(m->H), static_cast<int>(m->dh), t.tab, s), "rope_bwd");
       // Projections (toy_model.hpp:497-511)
-      if (m->llama)
-        L(cfk::rmsnorm_fwd(x, ly.g1, T, d, eps, A, s), "rmsnorm");  // recompute xn
-      else
-        L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
-      gemm(A, 0, d, dqkv, 0, qw, ly.d_wqkv, qw, d, qw, T, cfk::EPI_F32_ACC);
+      const bf16* xn1 = t.xn1 ? t.xn1 + l * T * d : A;
+      if (!t.xn1) {
+        if (m->llama)
+          L(cfk::rmsnorm_fwd(x, ly.g1, T, d, eps, A, s), "rmsnorm");  // recompute xn
+        else
+          L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
+      }
+      gemm(xn1, 0, d, dqkv, 0, qw, ly.d_wqkv, qw, d, qw, T, cfk::EPI_F32_ACC);
       if (m->llama) {
         gemm(dqkv, 1, qw, ly.wqkv, 1, qw, da, d, T, d, qw, cfk::EPI_F32);
-        L(cfk::rmsnorm_bwd(x, ly.g1, da, dmid, T, d, eps, dx, rstd, s), "rmsnorm_bwd");
-        L(cfk::gain_grad(x, da, rstd, T, d, ly.d_g1, s), "gain_grad");
+        norm_bwd(x, ly.g1, dmid, dx, ly.d_g1);
       } else {
         gemm(dqkv, 1, qw, ly.wqkv, 1, qw, dx, d, T, d, qw, cfk::EPI_F32_RES, dmid, d);
       }
