@@ -342,7 +342,8 @@ int cf_pp_run_local(cf_ctx* ctx, cf_model* const* models, int64_t num_stages,
 
 /* C[M,N] (+)= sum_k A(m,k) B(n,k).  a_kmajor: A stored [M,K] (else [K,M]);
  * b_kmajor: B stored [N,K] (else [K,N]).  epi: 0 store bf16, 1 store fp32,
- * 2 accumulate into fp32, 3 bf16 store of acc + residual(bf16). */
+ * 2 accumulate into fp32, 3 fp32 store of acc + residual(fp32), 4 bf16 tanh,
+ * 5 bf16 acc*(1-R^2) (toy FFN backward). */
 /* Chunked causal attention over packed segments (toy_model.hpp:263-302
  * forward, :436-486 backward).  segs: host int32 [nseg][4] = {q_start, len,
  * kv_row0, prefix}.  impl 0 = warp-MMA kernels, 1 = tcgen05 (head_dim 128).

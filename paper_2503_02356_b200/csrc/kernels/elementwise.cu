@@ -247,17 +247,19 @@ __global__ __launch_bounds__(kRowThreads) void rmsnorm_row_kernel(const float* _
 // owns a contiguous row range, holds its columns of the gain and of the
 // gain-gradient partial in registers, and streams x / dy / dres once.
 //   dx = dres + r*dy*g - x*r^3*<dy*g, x>/d,   part[cta][c] = sum_rows dy*x*r
+constexpr int kBwdThreads = 256;
 template <int NV>
-__global__ __launch_bounds__(kRowThreads) void rmsnorm_bwd_rows_kernel(
+__global__ __launch_bounds__(kBwdThreads) void rmsnorm_bwd_rows_kernel(
     const float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ dy, const float* dres,
     int64_t T, int d, float eps, int64_t rows_per_cta, float* dx, bf16* __restrict__ dx_bf16,
     float* __restrict__ part) {
-  __shared__ float red[2][2][kRowThreads / 32];
+  constexpr int W = kBwdThreads / 32;
+  __shared__ float red[2][2][W];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float4 g[NV], acc[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    const int c = (threadIdx.x + i * kBwdThreads) * 4;
     g[i] = c < d ? *reinterpret_cast<const float4*>(gain + c) : make_float4(0.f, 0.f, 0.f, 0.f);
     acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -266,13 +268,18 @@ __global__ __launch_bounds__(kRowThreads) void rmsnorm_bwd_rows_kernel(
     const int par = static_cast<int>(row & 1);
     const float* xr = x + row * d;
     const float* gr = dy + row * d;
-    float4 xv[NV], gv[NV];
+    float4 xv[NV], gv[NV], rv[NV];
     float ss = 0.f, dot = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const int c = (threadIdx.x + i * kRowThreads) * 4;
-      xv[i] = c < d ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      gv[i] = c < d ? __ldcs(reinterpret_cast<const float4*>(gr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int c = (threadIdx.x + i * kBwdThreads) * 4;
+      const bool in = c < d;
+      xv[i] = in ? *reinterpret_cast<const float4*>(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[i] = in ? __ldcs(reinterpret_cast<const float4*>(gr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      rv[i] = (in && dres) ? *reinterpret_cast<const float4*>(dres + row * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
       ss += xv[i].x * xv[i].x + xv[i].y * xv[i].y + xv[i].z * xv[i].z + xv[i].w * xv[i].w;
       dot += gv[i].x * g[i].x * xv[i].x + gv[i].y * g[i].y * xv[i].y + gv[i].z * g[i].z * xv[i].z +
              gv[i].w * g[i].w * xv[i].w;
@@ -284,20 +291,25 @@ __global__ __launch_bounds__(kRowThreads) void rmsnorm_bwd_rows_kernel(
       red[par][1][w] = dot;
     }
     __syncthreads();
-    ss = red[par][0][0] + red[par][0][1] + red[par][0][2] + red[par][0][3];
-    dot = red[par][1][0] + red[par][1][1] + red[par][1][2] + red[par][1][3];
+    ss = 0.f;
+    dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      ss += red[par][0][i];
+      dot += red[par][1][i];
+    }
     const float r = rsqrtf(ss / static_cast<float>(d) + eps);
     const float k = r * r * r * dot / static_cast<float>(d);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const int c = (threadIdx.x + i * kRowThreads) * 4;
+      const int c = (threadIdx.x + i * kBwdThreads) * 4;
       if (c >= d) continue;
-      float4 o = dres ? *reinterpret_cast<const float4*>(dres + row * d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 o = rv[i];
       o.x += r * gv[i].x * g[i].x - xv[i].x * k;
       o.y += r * gv[i].y * g[i].y - xv[i].y * k;
       o.z += r * gv[i].z * g[i].z - xv[i].z * k;
       o.w += r * gv[i].w * g[i].w - xv[i].w * k;
-      *reinterpret_cast<float4*>(dx + row * d + c) = o;
+      __stcs(reinterpret_cast<float4*>(dx + row * d + c), o);
       if (dx_bf16) {
         uint2 b;
         b.x = pack_bf16(o.x, o.y);
@@ -312,8 +324,28 @@ __global__ __launch_bounds__(kRowThreads) void rmsnorm_bwd_rows_kernel(
   }
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    const int c = (threadIdx.x + i * kRowThreads) * 4;
+    const int c = (threadIdx.x + i * kBwdThreads) * 4;
     if (c < d) *reinterpret_cast<float4*>(part + blockIdx.x * static_cast<int64_t>(d) + c) = acc[i];
+  }
+}
+
+// Column sums of the per-CTA gain partials, fixed order: block = 32
+// columns x 8 row-groups (strided rows), then the 8 group sums in order.
+__global__ void gain_reduce_cols_kernel(const float* __restrict__ part, int parts, int64_t d,
+                                        float* __restrict__ dgain) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (c < d)
+    for (int i = grp; i < parts; i += 8) s += part[i * d + c];
+  red[grp][lane] = s;
+  __syncthreads();
+  if (grp == 0 && c < d) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += red[i][lane];
+    dgain[c] += t;
   }
 }
 
@@ -670,31 +702,45 @@ cudaError_t rmsnorm_bwd_fused(const float* x, const float* gain, const float* dy
   if (d % 4) return cudaErrorInvalidValue;
   // one wave at the occupancy the register footprint allows (row state and
   // gain partial live in registers: ~20 regs per float4 column group)
-  const int64_t nv = (d + 4 * kRowThreads - 1) / (4 * kRowThreads);
-  const int64_t per_sm = nv <= 4 ? 8 : nv <= 8 ? 3 : 2;
-  const int64_t ctas = std::min<int64_t>(T, 148 * per_sm);
-  const int64_t rows = (T + ctas - 1) / ctas;
-  const int64_t grid = (T + rows - 1) / rows;
+  const int64_t nv = (d + 4 * kBwdThreads - 1) / (4 * kBwdThreads);
+  // one wave at the occupancy the register footprint allows (the row and
+  // the gain partial live in registers); the row split depends only on T
+  // and d, so the reduction order is fixed
   float* part = nullptr;
-  cudaError_t e = cudaMallocAsync(&part, static_cast<size_t>(grid * d) * 4, st);
-  if (e != cudaSuccess) return e;
-  const bool ok = dispatch_nv<12>(d, [&](auto nv) {
-    if constexpr (decltype(nv)::value <= 12)
-    rmsnorm_bwd_rows_kernel<decltype(nv)::value><<<static_cast<unsigned>(grid), kRowThreads, 0, st>>>(
-        x, gain, dy, dres, T, static_cast<int>(d), eps, rows, dx, dx_bf16, part);
-  });
-  if (!ok) {
-    cudaFreeAsync(part, st);
-    return cudaErrorInvalidValue;
+  int64_t rows = 0, grid = 0;
+  cudaError_t e = cudaSuccess;
+  bool ok = true;
+  auto go = [&](auto nvc) {
+    auto* kern = rmsnorm_bwd_rows_kernel<decltype(nvc)::value>;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdThreads, 0);
+    const int64_t ctas = std::min<int64_t>(T, 148 * std::max(1, per_sm));
+    rows = (T + ctas - 1) / ctas;
+    grid = (T + rows - 1) / rows;
+    e = cudaMallocAsync(&part, static_cast<size_t>(grid * d) * 4, st);
+    if (e != cudaSuccess) return;
+    kern<<<static_cast<unsigned>(grid), kBwdThreads, 0, st>>>(x, gain, dy, dres, T, static_cast<int>(d), eps, rows,
+                                                             dx, dx_bf16, part);
+  };
+  switch (nv) {
+    case 1: go(std::integral_constant<int, 1>()); break;
+    case 2: go(std::integral_constant<int, 2>()); break;
+    case 3: go(std::integral_constant<int, 3>()); break;
+    case 4: go(std::integral_constant<int, 4>()); break;
+    case 5: go(std::integral_constant<int, 5>()); break;
+    case 6: go(std::integral_constant<int, 6>()); break;
+    default: ok = false;
   }
-  gain_grad_reduce_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, st>>>(part, static_cast<int>(grid), d,
-                                                                                 dgain);
+  if (!ok) return cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  gain_reduce_cols_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(part, static_cast<int>(grid), d,
+                                                                               dgain);
   e = cudaGetLastError();
   cudaFreeAsync(part, st);
   return e;
 }
 bool rmsnorm_bwd_fused_ok(int64_t d) {
-  return d % 4 == 0 && dispatch_nv<12>(d, [](auto) {});
+  return d % 4 == 0 && d <= 6 * 4 * kBwdThreads;
 }
 cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_t T, int64_t d, float* dgain,
                       cudaStream_t st) {
