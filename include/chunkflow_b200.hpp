@@ -190,6 +190,79 @@ inline PlanDiagnostics validate_plan(const ExecutionPlan& plan) {
   return out;
 }
 
+// --- pipeline.hpp:24-72 types and the simulator entry points
+struct CostModel {  // pipeline.hpp:24-47
+  double gamma = 0.0, alpha = 1.0, beta = 0.0, backward_multiplier = 2.0, hop_latency = 0.0;
+};
+struct PipelineConfig {  // pipeline.hpp:49-53
+  int num_stages = 1;
+  int64_t k = 1;
+  int64_t chunk_size = 0;
+};
+enum class TraceEventKind { kForward, kRecomputeForward, kBackward };
+struct TraceEvent {
+  TraceEventKind kind = TraceEventKind::kForward;
+  int64_t chunk_id = 0;
+  double start = 0.0, end = 0.0;
+};
+struct PipelineTrace {  // pipeline.hpp:64-72
+  std::vector<std::vector<TraceEvent>> stages;
+  double makespan = 0.0;
+  std::vector<double> busy, busy_total;
+  double bubble = 0.0;  // bubble_ratio(), computed by the library
+};
+enum class DispatchPolicy { kBackwardFirst, kForwardFirst };
+
+namespace detail {
+inline PipelineTrace unpack_trace(const std::vector<cf_pp_op>& ops, const std::vector<double>& busy,
+                                  const std::vector<double>& busy_total, const cf_pp_result& r, int stages) {
+  PipelineTrace t;
+  t.makespan = r.makespan;
+  t.bubble = r.bubble_ratio;
+  t.busy = busy;
+  t.busy_total = busy_total;
+  t.stages.resize(static_cast<size_t>(stages));
+  for (int s = 0; s < stages; ++s)
+    for (int64_t i = 0; i < r.ops_per_stage; ++i) {
+      const cf_pp_op& o = ops[static_cast<size_t>(s * r.ops_per_stage + i)];
+      t.stages[static_cast<size_t>(s)].push_back({static_cast<TraceEventKind>(o.kind), o.chunk_id, o.start, o.end});
+    }
+  return t;
+}
+inline cf_pp_cost to_cost(const CostModel& c) {
+  return {c.gamma, c.alpha, c.beta, c.backward_multiplier, c.hop_latency};
+}
+}  // namespace detail
+
+// simulate_state_aware_1f1b (pipeline.hpp:250)
+inline PipelineTrace simulate_state_aware_1f1b(const ChunkPlan& plan, const PipelineConfig& cfg, const CostModel& cost,
+                                               DispatchPolicy policy = DispatchPolicy::kBackwardFirst) {
+  auto h = detail::build(plan.ids, plan.lengths, plan.chunk_size, cfg.k);
+  const cf_pp_cost c = detail::to_cost(cost);
+  cf_pp_result r{};
+  const int bf = policy == DispatchPolicy::kBackwardFirst ? 1 : 0;
+  check(cf_pp_simulate(h->get(), cfg.num_stages, cfg.k, &c, bf, nullptr, nullptr, nullptr, nullptr, nullptr, &r));
+  std::vector<cf_pp_op> ops(static_cast<size_t>(cfg.num_stages * r.ops_per_stage));
+  std::vector<double> busy(static_cast<size_t>(cfg.num_stages)), busy_total(busy.size());
+  check(cf_pp_simulate(h->get(), cfg.num_stages, cfg.k, &c, bf, nullptr, nullptr, ops.data(), busy.data(),
+                       busy_total.data(), &r));
+  return detail::unpack_trace(ops, busy, busy_total, r, cfg.num_stages);
+}
+
+// simulate_1f1b (pipeline.hpp:218)
+inline PipelineTrace simulate_1f1b(const std::vector<int64_t>& lengths, int num_stages, const CostModel& cost) {
+  const cf_pp_cost c = detail::to_cost(cost);
+  cf_pp_result r{};
+  std::vector<cf_pp_op> ops(static_cast<size_t>(num_stages) * 2 * lengths.size());
+  std::vector<double> busy(static_cast<size_t>(num_stages)), busy_total(busy.size());
+  check(cf_pp_simulate_1f1b(lengths.data(), static_cast<int64_t>(lengths.size()), num_stages, &c, ops.data(),
+                            busy.data(), busy_total.data(), &r));
+  return detail::unpack_trace(ops, busy, busy_total, r, num_stages);
+}
+
+// bubble_ratio (pipeline.hpp:325): recompute forwards count as bubble.
+inline double bubble_ratio(const PipelineTrace& t) { return t.bubble; }
+
 // RAII device context + model (ToyModelParams on the GPU).
 class Device {
  public:

@@ -16,3 +16,4 @@ def test_cpp_facade_builds_and_plans(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "chunks=4 events=9 peak=2 recompute=2 groups=1" in out
     assert "ValidationError: chunk_size must be at least 1" in out
+    assert "makespans=56,54,46 bubble=55.56 stage0_ops=9" in out
