@@ -181,6 +181,51 @@ int cf_plan_partition(const cf_plan* global, int64_t world, int64_t rank,
 int cf_plan_rank_tokens(const cf_plan* global, int64_t world, int64_t* tokens);
 void cf_plan_destroy(cf_plan* plan);
 
+/* ---- wire formats of the reference's planning tools ----
+ * Text outputs: the full length is returned in *len; up to cap-1 bytes plus
+ * a terminating NUL are written to buf (buf may be NULL to size). */
+
+/* chunk_plan_to_json(plan).dump(2) + "\n" (chunker.hpp:233): byte-identical
+ * to chunk_plan.json written by `chunkflow pack`. */
+int cf_plan_chunk_json(const cf_plan* plan, char* buf, size_t cap, size_t* len);
+/* execution_plan_to_json(plan).dump(2) + "\n" (scheduler.hpp:300):
+ * execution_plan.json of `chunkflow schedule`. */
+int cf_plan_exec_json(const cf_plan* plan, char* buf, size_t cap, size_t* len);
+/* chunk_plan_from_json (chunker.hpp:261) + schedule_step(k) + validate_plan:
+ * runs a chunk_plan.json produced by the reference.  CF_EPARSE on a
+ * malformed document. */
+int cf_plan_from_chunk_json(const char* json, int64_t k, cf_plan** out);
+/* load_lengths (dataset.hpp:112): line-delimited records {id?, length,
+ * tokens?}.  Call with NULL arrays to get *n and *n_tokens; has_tokens[i] is
+ * 1 when record i carries its token list (concatenated into tokens). */
+int cf_dataset_load_jsonl(const char* text, int64_t* n, int64_t* ids, int64_t* lengths,
+                          int64_t* has_tokens, int64_t* n_tokens, int32_t* tokens);
+/* write_records (dataset.hpp:169); tokens may be NULL (lengths only). */
+int cf_dataset_write_jsonl(const int64_t* ids, const int64_t* lengths, const int32_t* tokens,
+                           int64_t n, char* buf, size_t cap, size_t* len);
+
+/* ---- memory model (memory_model.hpp) ---- */
+typedef struct cf_mem_coeffs { /* MemoryModelCoefficients (:20-33) */
+  double base_gib;
+  double per_chunk_token_gib;
+  double per_context_token_gib;
+  double gqa_ratio;
+} cf_mem_coeffs;
+/* calibrate (memory_model.hpp:59): least squares of peak_gib on
+ * [1, k*chunk_size, gqa_ratio*context_len]. */
+int cf_mem_calibrate(const int64_t* chunk_size, const int64_t* k, const int64_t* context_len,
+                     const double* peak_gib, int64_t n, double gqa_ratio, cf_mem_coeffs* out,
+                     double* max_residual_gib);
+/* predict_peak (memory_model.hpp:47) */
+int cf_mem_predict(const cf_mem_coeffs* c, int64_t chunk_size, int64_t k, int64_t context_len,
+                   double* peak_gib);
+/* parse_measurements (memory_model.hpp:142): CSV rows chunk_size,k,
+ * context_len,peak_gib (optional header).  NULL arrays to size *n. */
+int cf_mem_parse_csv(const char* csv, int64_t* n, int64_t* chunk_size, int64_t* k,
+                     int64_t* context_len, double* peak_gib);
+/* coefficients_to_json(c).dump(2) + "\n" (memory_model.hpp:133) */
+int cf_mem_coeffs_json(const cf_mem_coeffs* c, char* buf, size_t cap, size_t* len);
+
 /* ---- pipeline-parallel planning (pipeline.hpp; config C5) ---- */
 
 /* TraceEventKind (pipeline.hpp:51) */

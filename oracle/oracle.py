@@ -60,10 +60,10 @@ class _Lib:
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
         self.lib = C.CDLL(path)
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _fn(self, name):
-        return self.lib[self.prefix + name]
+        return getattr(self.lib, self.prefix + name)
 
     def _check(self, rc):
         if rc != 0:
@@ -210,6 +210,7 @@ class Reference(_Lib):
     def __init__(self):
         super().__init__(os.path.join(HERE, "_ref", "libcfref.so"))
         self.lib.cfr_toy_num_params.restype = C.c_int64
+        self.lib.cfr_last_error.restype = C.c_char_p
 
     def num_params(self, cfg):
         return self.lib.cfr_toy_num_params(C.byref(cfg))
@@ -274,6 +275,33 @@ class Reference(_Lib):
         busy_t = np.zeros(stages, np.float64)
         self._check(self.lib.cfr_pp_trace(*args(_p(ops, PD), _p(busy, PD), _p(busy_t, PD))))
         return ops, busy, busy_t, mk.value, bb.value
+
+
+    def _text(self, call):
+        n = C.c_size_t()
+        self._check(call(None, C.c_size_t(0), C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self._check(call(buf, C.c_size_t(n.value + 1), C.byref(n)))
+        return buf.raw[:n.value].decode()
+
+    def plan_json(self, lengths, chunk_size, k=1, which=0, ids=None):
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        return self._text(lambda b, c, n: self.lib.cfr_plan_json(
+            _p(ids, PI64), _p(lengths, PI64), I64(len(lengths)), I64(chunk_size), I64(k), C.c_int(which), b, c, n))
+
+    def schedule_json(self, doc: str, k):
+        return self._text(lambda b, c, n: self.lib.cfr_schedule_json(doc.encode(), I64(k), b, c, n))
+
+    def jsonl_roundtrip(self, text: str):
+        return self._text(lambda b, c, n: self.lib.cfr_jsonl_roundtrip(text.encode(), b, c, n))
+
+    def calibrate(self, csv: str, gqa=1.0):
+        coeffs = np.zeros(4, np.float64)
+        res = C.c_double()
+        doc = self._text(lambda b, c, n: self.lib.cfr_calibrate(csv.encode(), C.c_double(gqa), _p(coeffs, PD),
+                                                               C.byref(res), b, c, n))
+        return coeffs, res.value, doc
 
 
 def c1_batch(oracle: Oracle):

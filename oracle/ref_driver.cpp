@@ -8,12 +8,14 @@
 // Built by oracle/Makefile; outputs only into oracle/_ref/.
 #include <chunkflow/chunker.hpp>
 #include <chunkflow/dataset.hpp>
+#include <chunkflow/memory_model.hpp>
 #include <chunkflow/pipeline.hpp>
 #include <chunkflow/plan_runner.hpp>
 #include <chunkflow/scheduler.hpp>
 #include <chunkflow/toy_model.hpp>
 
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "../include/chunkflow_b200.h"
@@ -333,6 +335,69 @@ int cfr_pp_trace(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t 
     }
     *makespan = tr.makespan;
     *bubble = cf::bubble_ratio(tr);
+  });
+}
+}  // extern "C"
+
+// ---- wire formats + memory model of the reference (chunker.hpp:233-292,
+//      scheduler.hpp:300-328, dataset.hpp:112-176, memory_model.hpp)
+namespace {
+void put(const std::string& s, char* buf, size_t cap, size_t* len) {
+  *len = s.size();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+}
+}  // namespace
+
+extern "C" {
+// which: 0 = chunk_plan.json of `pack`, 1 = execution_plan.json of `schedule`
+int cfr_plan_json(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t cs, int64_t k, int which,
+                  char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    const cf::ChunkPlan p = cf::construct_chunks(make_batch(ids, lengths, n, nullptr), cs);
+    if (which == 0) {
+      put(cf::chunk_plan_to_json(p).dump(2) + "\n", buf, cap, len);
+    } else {
+      put(cf::execution_plan_to_json(cf::schedule_step(p, k)).dump(2) + "\n", buf, cap, len);
+    }
+  });
+}
+// `schedule` on a chunk-plan document: chunk_plan_from_json -> schedule_step -> execution_plan.json
+int cfr_schedule_json(const char* doc, int64_t k, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(doc);
+    } catch (const nlohmann::json::exception& e) {
+      throw cf::ParseError(e.what());
+    }
+    put(cf::execution_plan_to_json(cf::schedule_step(cf::chunk_plan_from_json(j), k)).dump(2) + "\n", buf, cap,
+        len);
+  });
+}
+// load_lengths -> write_records round trip (the canonical JSONL of a file)
+int cfr_jsonl_roundtrip(const char* text, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    std::istringstream in(text);
+    std::ostringstream out;
+    cf::write_records(out, cf::load_lengths(in));
+    put(out.str(), buf, cap, len);
+  });
+}
+int cfr_calibrate(const char* csv, double gqa, double* coeffs4, double* max_resid, char* buf, size_t cap,
+                  size_t* len) {
+  return guarded([&] {
+    std::istringstream in(csv);
+    const cf::CalibrationResult r = cf::calibrate(cf::parse_measurements(in), gqa);
+    coeffs4[0] = r.coefficients.base;
+    coeffs4[1] = r.coefficients.per_chunk_token;
+    coeffs4[2] = r.coefficients.per_context_token;
+    coeffs4[3] = r.coefficients.gqa_ratio;
+    *max_resid = r.max_residual_gib;
+    put(cf::coefficients_to_json(r.coefficients).dump(2) + "\n", buf, cap, len);
   });
 }
 }  // extern "C"

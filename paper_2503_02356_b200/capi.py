@@ -57,6 +57,11 @@ class PpResult(C.Structure):
                 ("occupancy_bubble", C.c_double), ("ops_per_stage", C.c_int64)]
 
 
+class MemCoeffs(C.Structure):
+    _fields_ = [("base_gib", C.c_double), ("per_chunk_token_gib", C.c_double),
+                ("per_context_token_gib", C.c_double), ("gqa_ratio", C.c_double)]
+
+
 class RunResult(C.Structure):
     _fields_ = [("loss", C.c_double), ("peak_retained_tokens", C.c_int64),
                 ("recompute_forward_count", C.c_int64),
@@ -87,7 +92,9 @@ EXPORTS = [
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
-    "cf_pp_run_local", "cf_step_op_times", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_pp_run_local", "cf_step_op_times", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
+    "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
+    "cf_mem_coeffs_json", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None
@@ -191,6 +198,21 @@ class Plan:
         check(lib().cf_plan_listing(self.h, buf, C.c_size_t(n.value + 1), None))
         return buf.value.decode()
 
+    def chunk_json(self) -> str:
+        """chunk_plan.json text of `chunkflow pack` (chunker.hpp:233)."""
+        return _text(lambda buf, cap, n: lib().cf_plan_chunk_json(self.h, buf, cap, n))
+
+    def exec_json(self) -> str:
+        """execution_plan.json text of `chunkflow schedule` (scheduler.hpp:300)."""
+        return _text(lambda buf, cap, n: lib().cf_plan_exec_json(self.h, buf, cap, n))
+
+    @classmethod
+    def from_chunk_json(cls, text: str, k: int):
+        """chunk_plan_from_json + schedule_step (chunker.hpp:261)."""
+        h = C.c_void_p()
+        check(lib().cf_plan_from_chunk_json(text.encode(), C.c_int64(k), C.byref(h)))
+        return cls(h)
+
     def partition(self, world, rank):
         h = C.c_void_p()
         check(lib().cf_plan_partition(self.h, C.c_int64(world), C.c_int64(rank), C.byref(h)))
@@ -249,6 +271,69 @@ def pp_stage_layers(layers, stage, stages):
     b, e = C.c_int64(), C.c_int64()
     check(lib().cf_pp_stage_layers(C.c_int64(layers), C.c_int64(stage), C.c_int64(stages), C.byref(b), C.byref(e)))
     return b.value, e.value
+
+
+def _text(call):
+    n = C.c_size_t()
+    check(call(None, C.c_size_t(0), C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(call(buf, C.c_size_t(n.value + 1), C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def dataset_load_jsonl(text: str):
+    """load_lengths (dataset.hpp:112) -> (ids, lengths, has_tokens, tokens)."""
+    raw = text.encode()
+    n, nt = C.c_int64(), C.c_int64()
+    check(lib().cf_dataset_load_jsonl(raw, C.byref(n), None, None, None, C.byref(nt), None))
+    ids = np.zeros(n.value, np.int64)
+    lengths = np.zeros(n.value, np.int64)
+    has = np.zeros(n.value, np.int64)
+    tok = np.zeros(max(1, nt.value), np.int32)
+    check(lib().cf_dataset_load_jsonl(raw, C.byref(n), _p(ids), _p(lengths), _p(has), C.byref(nt), _p(tok)))
+    return ids, lengths, has.astype(bool), tok[:nt.value]
+
+
+def dataset_write_jsonl(ids, lengths, tokens=None) -> str:
+    """write_records (dataset.hpp:169)."""
+    ids = np.ascontiguousarray(ids, np.int64)
+    lengths = np.ascontiguousarray(lengths, np.int64)
+    tok = None if tokens is None else np.ascontiguousarray(tokens, np.int32)
+    return _text(lambda buf, cap, n: lib().cf_dataset_write_jsonl(
+        _p(ids), _p(lengths), None if tok is None else _p(tok), C.c_int64(len(ids)), buf, cap, n))
+
+
+def mem_calibrate(chunk_size, k, context_len, peak_gib, gqa_ratio=1.0):
+    """calibrate (memory_model.hpp:59) -> (MemCoeffs, max_residual_gib)."""
+    cs = np.ascontiguousarray(chunk_size, np.int64)
+    kk = np.ascontiguousarray(k, np.int64)
+    ctx = np.ascontiguousarray(context_len, np.int64)
+    pk = np.ascontiguousarray(peak_gib, np.float64)
+    out, res = MemCoeffs(), C.c_double()
+    check(lib().cf_mem_calibrate(_p(cs), _p(kk), _p(ctx), _p(pk), C.c_int64(len(cs)), C.c_double(gqa_ratio),
+                                 C.byref(out), C.byref(res)))
+    return out, res.value
+
+
+def mem_predict(coeffs: MemCoeffs, chunk_size, k, context_len):
+    out = C.c_double()
+    check(lib().cf_mem_predict(C.byref(coeffs), C.c_int64(chunk_size), C.c_int64(k), C.c_int64(context_len),
+                               C.byref(out)))
+    return out.value
+
+
+def mem_parse_csv(text: str):
+    raw = text.encode()
+    n = C.c_int64()
+    check(lib().cf_mem_parse_csv(raw, C.byref(n), None, None, None, None))
+    cs, kk, ctx = (np.zeros(n.value, np.int64) for _ in range(3))
+    pk = np.zeros(n.value, np.float64)
+    check(lib().cf_mem_parse_csv(raw, C.byref(n), _p(cs), _p(kk), _p(ctx), _p(pk)))
+    return cs, kk, ctx, pk
+
+
+def mem_coeffs_json(coeffs: MemCoeffs) -> str:
+    return _text(lambda buf, cap, n: lib().cf_mem_coeffs_json(C.byref(coeffs), buf, cap, n))
 
 
 def synthesize(count, seed, preset=1, bounds=(), fracs=(), max_length=0):

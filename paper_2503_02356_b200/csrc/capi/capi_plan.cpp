@@ -6,6 +6,7 @@
 #include "../../../include/chunkflow_b200.h"
 #include "../host/plan.hpp"
 #include "../host/pp.hpp"
+#include "../host/wire.hpp"
 #include "capi_util.hpp"
 
 namespace cfb {
@@ -252,6 +253,110 @@ int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages, c
 
 int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages, int64_t* begin, int64_t* end) {
   return cfb::guard([&] { cfb::pp_stage_layers(num_layers, stage, num_stages, begin, end); });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------- wire formats
+namespace {
+void put_text(const std::string& s, char* buf, size_t cap, size_t* len) {
+  if (len) *len = s.size();
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+}
+cfb::MemCoeffs from_c(const cf_mem_coeffs* c) {
+  return {c->base_gib, c->per_chunk_token_gib, c->per_context_token_gib, c->gqa_ratio};
+}
+}  // namespace
+
+extern "C" {
+
+int cf_plan_chunk_json(const cf_plan* plan, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] { put_text(cfb::chunk_plan_to_json(plan->p).dump(2) + "\n", buf, cap, len); });
+}
+
+int cf_plan_exec_json(const cf_plan* plan, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] { put_text(cfb::execution_plan_to_json(plan->p).dump(2) + "\n", buf, cap, len); });
+}
+
+int cf_plan_from_chunk_json(const char* json, int64_t k, cf_plan** out) {
+  return cfb::guard([&] {
+    if (!json || !out) throw cfb::ValidationError("null argument");
+    auto h = std::make_unique<cf_plan>();
+    h->p = cfb::chunk_plan_from_json(cfb::Json::parse(json));
+    cfb::schedule_step(h->p, k);
+    *out = h.release();
+  });
+}
+
+int cf_dataset_load_jsonl(const char* text, int64_t* n, int64_t* ids, int64_t* lengths, int64_t* has_tokens,
+                          int64_t* n_tokens, int32_t* tokens) {
+  return cfb::guard([&] {
+    if (!text || !n) throw cfb::ValidationError("null argument");
+    const std::vector<cfb::SeqRecord> recs = cfb::load_lengths(text);
+    *n = static_cast<int64_t>(recs.size());
+    int64_t nt = 0;
+    for (size_t i = 0; i < recs.size(); ++i) {
+      if (ids) ids[i] = recs[i].id;
+      if (lengths) lengths[i] = recs[i].length;
+      if (has_tokens) has_tokens[i] = recs[i].tokens.empty() ? 0 : 1;
+      if (tokens) std::copy(recs[i].tokens.begin(), recs[i].tokens.end(), tokens + nt);
+      nt += static_cast<int64_t>(recs[i].tokens.size());
+    }
+    if (n_tokens) *n_tokens = nt;
+  });
+}
+
+int cf_dataset_write_jsonl(const int64_t* ids, const int64_t* lengths, const int32_t* tokens, int64_t n, char* buf,
+                           size_t cap, size_t* len) {
+  return cfb::guard([&] {
+    std::vector<cfb::SeqRecord> recs(static_cast<size_t>(n));
+    int64_t off = 0;
+    for (int64_t i = 0; i < n; ++i) {
+      recs[static_cast<size_t>(i)].id = ids[i];
+      recs[static_cast<size_t>(i)].length = lengths[i];
+      if (tokens) {
+        recs[static_cast<size_t>(i)].tokens.assign(tokens + off, tokens + off + lengths[i]);
+        off += lengths[i];
+      }
+    }
+    put_text(cfb::write_records(recs), buf, cap, len);
+  });
+}
+
+int cf_mem_calibrate(const int64_t* chunk_size, const int64_t* k, const int64_t* context_len, const double* peak_gib,
+                     int64_t n, double gqa_ratio, cf_mem_coeffs* out, double* max_residual_gib) {
+  return cfb::guard([&] {
+    std::vector<cfb::MemMeasurement> ms;
+    for (int64_t i = 0; i < n; ++i) ms.push_back({chunk_size[i], k[i], context_len[i], peak_gib[i]});
+    const cfb::MemCoeffs c = cfb::calibrate(ms, gqa_ratio, max_residual_gib);
+    *out = {c.base, c.per_chunk_token, c.per_context_token, c.gqa_ratio};
+  });
+}
+
+int cf_mem_predict(const cf_mem_coeffs* c, int64_t chunk_size, int64_t k, int64_t context_len, double* peak_gib) {
+  return cfb::guard([&] { *peak_gib = cfb::predict_peak(from_c(c), chunk_size, k, context_len); });
+}
+
+int cf_mem_parse_csv(const char* csv, int64_t* n, int64_t* chunk_size, int64_t* k, int64_t* context_len,
+                     double* peak_gib) {
+  return cfb::guard([&] {
+    const auto ms = cfb::parse_measurements(csv ? csv : "");
+    *n = static_cast<int64_t>(ms.size());
+    for (size_t i = 0; i < ms.size(); ++i) {
+      if (chunk_size) chunk_size[i] = ms[i].chunk_size;
+      if (k) k[i] = ms[i].k;
+      if (context_len) context_len[i] = ms[i].context_len;
+      if (peak_gib) peak_gib[i] = ms[i].peak_gib;
+    }
+  });
+}
+
+int cf_mem_coeffs_json(const cf_mem_coeffs* c, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] { put_text(cfb::coefficients_to_json(from_c(c)).dump(2) + "\n", buf, cap, len); });
 }
 
 }  // extern "C"

@@ -36,6 +36,9 @@ int guard(F&& f) {
   } catch (const ValidationError& e) {
     g_last_error = e.what();
     return CF_EVALIDATION;
+  } catch (const ParseError& e) {
+    g_last_error = e.what();
+    return CF_EPARSE;
   } catch (const CudaError& e) {
     g_last_error = e.what();
     return CF_ECUDA;

@@ -15,6 +15,9 @@ namespace cfb {
 struct ValidationError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct ParseError : std::runtime_error {  // chunkflow::ParseError (common.hpp:20)
+  using std::runtime_error::runtime_error;
+};
 
 enum : int64_t { kStandalone = 0, kDependent = 1 };
 enum : int64_t { kFwdDiscard = 0, kFwdRetain = 1, kBackward = 2 };
