@@ -274,6 +274,11 @@ int cf_pp_simulate(const cf_plan* plan, int64_t num_stages, int64_t k,
 int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages,
                         const cf_pp_cost* cost, cf_pp_op* ops, double* busy,
                         double* busy_total, cf_pp_result* result);
+/* export_trace (pipeline.hpp:353-396) of num_stages x ops_per_stage records
+ * (stage-major, e.g. cf_pp_simulate's output, or a measured timeline built
+ * from cf_step_op_times): format 0 = chrome-trace JSON, 1 = table Gantt. */
+int cf_pp_export_trace(const cf_pp_op* ops, int64_t num_stages, int64_t ops_per_stage,
+                       int format, char* buf, size_t cap, size_t* len);
 /* Layer range [begin, end) that stage `stage` of `num_stages` executes. */
 int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages,
                        int64_t* begin, int64_t* end);

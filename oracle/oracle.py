@@ -304,6 +304,15 @@ class Reference(_Lib):
         return coeffs, res.value, doc
 
 
+    def export_trace(self, lengths, chunk_size, k, stages, cost=(0.0, 1.0, 0.0, 2.0, 0.0), mode=1, chrome=True):
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64)
+        c5 = np.ascontiguousarray(cost, np.float64)
+        return self._text(lambda b, c, n: self.lib.cfr_export_trace(
+            _p(ids, PI64), _p(lengths, PI64), I64(len(lengths)), I64(chunk_size), I64(k), I64(stages), _p(c5, PD),
+            C.c_int(mode), C.c_int(0 if chrome else 1), b, c, n))
+
+
 def c1_batch(oracle: Oracle):
     """Config C1 canonical batch: synthesize(eval_table5, 32,
     seed=3) plus sequence id 32 of 2048 tokens; tokens SplitMix64(5)."""

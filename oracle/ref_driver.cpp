@@ -401,3 +401,26 @@ int cfr_calibrate(const char* csv, double gqa, double* coeffs4, double* max_resi
   });
 }
 }  // extern "C"
+
+extern "C" int cfr_export_trace(const int64_t* ids, const int64_t* lengths, int64_t n, int64_t cs, int64_t k,
+                                int64_t stages, const double* cost5, int mode, int format, char* buf, size_t cap,
+                                size_t* len) {
+  return guarded([&] {
+    cf::CostModel cm;
+    cm.gamma = cost5[0];
+    cm.alpha = cost5[1];
+    cm.beta = cost5[2];
+    cm.backward_multiplier = cost5[3];
+    cm.hop_latency = cost5[4];
+    cf::PipelineTrace tr;
+    if (mode == 0) {
+      tr = cf::simulate_1f1b(std::vector<std::int64_t>(lengths, lengths + n), static_cast<int>(stages), cm);
+    } else {
+      cf::PipelineConfig pc;
+      pc.num_stages = static_cast<int>(stages);
+      pc.k = k;
+      tr = cf::simulate_state_aware_1f1b(cf::construct_chunks(make_batch(ids, lengths, n, nullptr), cs), pc, cm);
+    }
+    put(cf::export_trace(tr, format == 0 ? cf::TraceFormat::kChromeTrace : cf::TraceFormat::kTable), buf, cap, len);
+  });
+}

@@ -94,7 +94,7 @@ EXPORTS = [
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
     "cf_pp_run_local", "cf_step_op_times", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
-    "cf_mem_coeffs_json", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None
@@ -265,6 +265,14 @@ def pp_simulate_1f1b(lengths, stages, cost=None):
     check(lib().cf_pp_simulate_1f1b(_p(lengths), C.c_int64(len(lengths)), C.c_int64(stages), C.byref(c),
                                     _p(ops), _p(busy), _p(busy_t), C.byref(r)))
     return ops, busy, busy_t, r
+
+
+def pp_export_trace(ops, chrome=True) -> str:
+    """export_trace (pipeline.hpp:353-396) of ops[stages, per] (PP_OP_DT)."""
+    ops = np.ascontiguousarray(ops, PP_OP_DT)
+    st, per = ops.shape
+    return _text(lambda buf, cap, n: lib().cf_pp_export_trace(_p(ops), C.c_int64(st), C.c_int64(per),
+                                                              C.c_int(0 if chrome else 1), buf, cap, n))
 
 
 def pp_stage_layers(layers, stage, stages):

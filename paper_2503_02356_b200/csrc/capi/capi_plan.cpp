@@ -360,3 +360,19 @@ int cf_mem_coeffs_json(const cf_mem_coeffs* c, char* buf, size_t cap, size_t* le
 }
 
 }  // extern "C"
+
+extern "C" int cf_pp_export_trace(const cf_pp_op* ops, int64_t num_stages, int64_t ops_per_stage, int format,
+                                  char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] {
+    if (format != 0 && format != 1) throw cfb::ValidationError("unknown trace format");
+    if (num_stages < 0 || ops_per_stage < 0 || (num_stages * ops_per_stage > 0 && !ops))
+      throw cfb::ValidationError("bad trace arrays");
+    std::vector<std::vector<cfb::TraceOp>> st(static_cast<size_t>(num_stages));
+    for (int64_t s = 0; s < num_stages; ++s)
+      for (int64_t i = 0; i < ops_per_stage; ++i) {
+        const cf_pp_op& o = ops[s * ops_per_stage + i];
+        st[static_cast<size_t>(s)].push_back({o.kind, o.chunk_id, o.start, o.end});
+      }
+    put_text(cfb::export_trace(st, format == 0), buf, cap, len);
+  });
+}

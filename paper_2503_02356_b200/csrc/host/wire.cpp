@@ -430,6 +430,42 @@ Plan chunk_plan_from_json(const Json& doc) {
   return plan;
 }
 
+// ------------------------------------------------------------ trace export
+std::string export_trace(const std::vector<std::vector<TraceOp>>& stages, bool chrome) {
+  static const char* kName[3] = {"F", "F'", "B"};
+  auto name = [](int64_t k) { return (k >= 0 && k < 3) ? kName[k] : "?"; };
+  if (chrome) {
+    Json events = Json::array();
+    auto num = [](double v) { return v == std::floor(v) ? Json::integer(static_cast<int64_t>(v)) : Json::number(v); };
+    for (size_t s = 0; s < stages.size(); ++s)
+      for (const TraceOp& e : stages[s]) {
+        Json x = Json::object();
+        x.o["name"] = Json::string(std::string(name(e.kind)) + " chunk" + std::to_string(e.chunk));
+        x.o["ph"] = Json::string("X");
+        x.o["ts"] = num(e.start * 1000.0);
+        x.o["dur"] = num((e.end - e.start) * 1000.0);
+        x.o["pid"] = Json::integer(static_cast<int64_t>(s));
+        x.o["tid"] = Json::integer(0);
+        events.a.push_back(std::move(x));
+      }
+    Json doc = Json::object();
+    doc.o["traceEvents"] = std::move(events);
+    return doc.dump(2) + "\n";
+  }
+  std::string out;
+  for (size_t s = 0; s < stages.size(); ++s) {
+    out += "stage " + std::to_string(s);
+    for (const TraceOp& e : stages[s]) {
+      char cell[96];
+      std::snprintf(cell, sizeof(cell), " | %-2s c%lld %.2f-%.2f", name(e.kind), static_cast<long long>(e.chunk),
+                    e.start, e.end);
+      out += cell;
+    }
+    out += "\n";
+  }
+  return out;
+}
+
 // ----------------------------------------------------------------- JSONL
 std::vector<SeqRecord> load_lengths(const std::string& text) {
   std::vector<SeqRecord> set;

@@ -78,6 +78,15 @@ Json execution_plan_to_json(const Plan& plan);
 // Chunks, segments and groups of a chunk-plan document (not scheduled).
 Plan chunk_plan_from_json(const Json& doc);
 
+// export_trace (pipeline.hpp:340-396) of a per-stage timeline: chrome-trace
+// JSON (1 time unit = 1000 us, "X" events, pid = stage) or the table Gantt.
+// Each stage's events are (kind CF_PP_*, chunk id, start, end).
+struct TraceOp {
+  int64_t kind, chunk;
+  double start, end;
+};
+std::string export_trace(const std::vector<std::vector<TraceOp>>& stages, bool chrome);
+
 struct SeqRecord {
   int64_t id = 0, length = 0;
   std::vector<int32_t> tokens;  // empty = lengths only

@@ -128,3 +128,35 @@ def test_validation_errors():
     assert capi.pp_stage_layers(2, 1, 2) == (1, 2)
     with pytest.raises(capi.CfError):
         capi.pp_stage_layers(2, 0, 3)
+
+
+@pytest.mark.parametrize("chrome", [True, False])
+def test_export_trace_matches_reference(reference, oracle, chrome):
+    """export_trace (pipeline.hpp:353-396): table text byte-identical; chrome-
+    trace documents equal value for value (floats compared exactly — the
+    product prints the shortest round-trip digits, nlohmann's Grisu2 now and
+    then a 17th digit of the same double)."""
+    lengths, _ = c1_batch(oracle)
+
+    def same(mine, ref):
+        if chrome:
+            assert json.loads(mine) == json.loads(ref)
+        else:
+            assert mine == ref
+
+    cases = [([1, 1, 2, 4], 2, 1, 4, (0.0, 1.0, 0.0, 2.0, 0.0)), ([1, 1, 2, 4], 2, 2, 3, (0.25, 1.0, 0.1, 1.5, 0.5)),
+             (lengths, 512, 2, 4, (0.0, 1.0, 1.05e-5, 2.0, 3.0))]
+    for lens, cs, k, stages, cost in cases:
+        c = dict(zip(("gamma", "alpha", "beta", "backward_multiplier", "hop_latency"), cost))
+        ops, _, _, _ = capi.pp_simulate(cf.Plan.build(lens, cs, k), stages, k, c)
+        same(capi.pp_export_trace(ops, chrome), reference.export_trace(lens, cs, k, stages, cost, 1, chrome))
+    ops, _, _, _ = capi.pp_simulate_1f1b([1, 1, 2, 4], 4)
+    assert capi.pp_export_trace(ops, chrome) == reference.export_trace([1, 1, 2, 4], 1, 1, 4, mode=0, chrome=chrome)
+    for lens, cs, k, stages, cost in cases[:2]:  # integral / short decimals: bytes equal too
+        c = dict(zip(("gamma", "alpha", "beta", "backward_multiplier", "hop_latency"), cost))
+        ops2, _, _, _ = capi.pp_simulate(cf.Plan.build(lens, cs, k), stages, k, c)
+        assert capi.pp_export_trace(ops2, chrome) == reference.export_trace(lens, cs, k, stages, cost, 1, chrome)
+    if chrome:
+        doc = json.loads(capi.pp_export_trace(ops, True))
+        assert doc["traceEvents"][0] == {"dur": 1000, "name": "F chunk0", "ph": "X", "pid": 0, "tid": 0, "ts": 0}
+        assert capi.pp_export_trace(np.zeros((0, 0), capi.PP_OP_DT), True) == '{\n  "traceEvents": []\n}\n'

@@ -103,7 +103,10 @@ def main():
                 else:
                     f[i] = per_tok_f * int(c["total_tokens"])
                     b[i] = per_tok_b * int(c["total_tokens"])
-            _, _, _, pr = capi.pp_simulate(rp, STAGES, K, fwd_cost=f, bwd_cost=b)
+            ops, _, _, pr = capi.pp_simulate(rp, STAGES, K, fwd_cost=f, bwd_cost=b)
+            if with_head and rp is replicas[0]:  # predicted timeline, chrome-trace (1 unit = 1 ms here)
+                with open("gpurun_out/c5_pp_trace.json", "w") as fh:
+                    fh.write(capi.pp_export_trace(ops, True))
             spans.append(pr.makespan)
             bubbles.append(pr.bubble_ratio)
             occ.append(pr.occupancy_bubble)
