@@ -396,7 +396,9 @@ int cf_pp_run_local(cf_ctx* ctx, cf_model* const* models, int64_t num_stages,
  * 5 bf16 acc*(1-R^2) (toy FFN backward). */
 /* Chunked causal attention over packed segments (toy_model.hpp:263-302
  * forward, :436-486 backward).  segs: host int32 [nseg][4] = {q_start, len,
- * kv_row0, prefix}.  impl 0 = warp-MMA kernels, 1 = tcgen05 (head_dim 128).
+ * kv_row0, prefix}.  impl 0 = warp-MMA kernels, 1 = tcgen05 (head_dim 128),
+ * 2 = first tcgen05 backward, 3 = ping-pong tcgen05 forward (two q heads of a
+ * GQA group per CTA; H/KVH even).
  * Backward writes dq and ADDS dK/dV into the fp32 accumulators. */
 int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q,
                     int64_t q_stride, const void* k, const void* v,

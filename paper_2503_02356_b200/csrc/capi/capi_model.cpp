@@ -341,7 +341,12 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t 
     p.dsum = dsum;
     cudaError_t e;
     if (!backward) {
-      if (impl == 1) {
+      if (impl == 3) {
+        if (!cfk::attn_fwd_pp_supported(p))
+          throw cfb::ValidationError("ping-pong attention needs head_dim 128 and an even GQA group");
+        e = cfk::attn_forward_tc_pp(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),
+                                    static_cast<int32_t>(q128.second), kv_rows, st);
+      } else if (impl == 1) {
         if (!cfk::attn_tc_supported(p)) throw cfb::ValidationError("tcgen05 attention needs head_dim 128");
         e = cfk::attn_forward_tc(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),
                                  static_cast<int32_t>(q128.second), kv_rows, st);

@@ -9,6 +9,11 @@ bool attn_tc_supported(const AttnParams& p);
 // tiles128: 128-query tiles per segment; kv_rows: rows addressable in p.k/p.v.
 cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32_t ntiles, int64_t kv_rows,
                             cudaStream_t st);
+// Ping-pong forward (attention_tc_fwd2.cu): one CTA = 128 queries x two q
+// heads of one GQA group sharing the K/V stream; needs H/KVH even.
+bool attn_fwd_pp_supported(const AttnParams& p);
+cudaError_t attn_forward_tc_pp(const AttnParams& p, const AttnTile* tiles128, int32_t ntiles, int64_t kv_rows,
+                               cudaStream_t st);
 // dsum, then dQ (written) and dK/dV (added into the fp32 accumulators).
 // Pipelined version (attention_tc_bwd.cu): 64-wide streamed sub-tiles,
 // double-buffered S/dP in TMEM.

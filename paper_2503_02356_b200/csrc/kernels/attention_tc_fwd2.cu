@@ -1,0 +1,368 @@
+// tcgen05 attention forward, two q heads per CTA in ping-pong (sm_100a,
+// head_dim 128).  Same math as attn_fwd_tc_kernel (attention_tc.cu;
+// reference toy_model.hpp:263-302), restructured so the tensor core always
+// has the other head's MMAs to run while one head's softmax executes:
+//
+//   CTA = 128 queries x q heads (h0, h0+1) of one GQA group: both heads
+//   stream the SAME K/V tiles (loaded once into a 2-stage smem ring).
+//   TMEM (512 cols): head w owns S_w (128 fp32 cols; P_w bf16 is written
+//   over its first 64 cols) and O_w (128 cols).  Q_w lives in smem.
+//   MMA issue order per key tile j (one thread):
+//       [P_0(j)] O_0 += P_0 V_j ; S_0(j+1) = Q_0 K_{j+1}^T ;
+//       [P_1(j)] O_1 += P_1 V_j ; S_1(j+1) = Q_1 K_{j+1}^T
+//   so softmax_0(j+1) overlaps PV_1(j) + S_1(j+1), and vice versa.  A later
+//   MMA into S_w is issued after the PV that read P_w, and tcgen05 MMAs of
+//   one thread complete in order, so s_full_w(j) also certifies PV_w(j-1)
+//   (O_w stable for the lazy rescale, P_w region free).
+//   warps 0-3: softmax of head 0 (thread = query row, full 128-key rows,
+//   two passes over TMEM: row max, then exp2 / sum / bf16 P); warps 4-7:
+//   head 1; warp 8: TMA producer; warp 9: MMA issuer.
+#include <cfloat>
+
+#include "attention.h"
+#include "attention_tc.h"
+#include "common.cuh"
+
+namespace cfk {
+namespace {
+
+constexpr int TK = 128, DH = 128;
+constexpr uint32_t kBox = 128 * 64 * 2;  // [128 rows][64 cols] bf16
+constexpr uint32_t kTile = 2 * kBox;     // 128 x 128
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescale = 8.0f;
+constexpr int KS = 3, VS = 2;  // K / V ring depths (K runs one tile further ahead)
+constexpr int kThreads = 320;
+
+struct Args {
+  const AttnSeg* segs;
+  const AttnTile* tiles;
+  __nv_bfloat16* o;
+  int64_t o_stride;
+  float* lse;
+  int32_t T, H, KVH;
+  float sl2;
+};
+
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + (ks >> 2) * kBox + (ks & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int ks) {
+  return umma_desc_sw128(base + ks * 2048, kBox, 1024);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_pp_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                       // 2 heads
+  uint8_t* sK = sQ + 2 * kTile;           // KS stages
+  uint8_t* sV = sK + KS * kTile;          // VS stages
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VS * kTile);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;                 // [KS]
+  uint64_t* k_empty = k_full + KS;
+  uint64_t* v_full = k_empty + KS;            // [VS]
+  uint64_t* v_empty = v_full + VS;
+  uint64_t* s_full = v_empty + VS;            // [2 heads]
+  uint64_t* p_full = s_full + 2;              // [2 heads]
+  uint64_t* o_done = p_full + 2;              // [2 heads]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int h0 = 2 * blockIdx.y, g = h0 / (a.H / a.KVH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q_row0 = sg.q_start + tl.first;
+  const int kv_len = sg.prefix + tl.first + tl.count;
+  const int nkt = (kv_len + TK - 1) / TK;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&s_full[w], 1);
+      mbar_init(&p_full[w], 128);
+      mbar_init(&o_done[w], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * kTile);
+      for (int w = 0; w < 2; ++w) {
+        tma_load_2d(sQ + w * kTile, &tmQ, q_full, (h0 + w) * DH, q_row0);
+        tma_load_2d(sQ + w * kTile + kBox, &tmQ, q_full, (h0 + w) * DH + 64, q_row0);
+      }
+      // K runs one tile ahead of V: K_j is needed by S(j) one MMA step
+      // before V_j is needed by PV(j)
+      auto load_k = [&](int j) {
+        const int st = j % KS;
+        mbar_wait(&k_empty[st], ((j / KS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[st], kTile);
+        tma_load_2d(sK + st * kTile, &tmK, &k_full[st], g * DH, sg.kv_row0 + j * TK);
+        tma_load_2d(sK + st * kTile + kBox, &tmK, &k_full[st], g * DH + 64, sg.kv_row0 + j * TK);
+      };
+      load_k(0);
+      for (int j = 0; j < nkt; ++j) {
+        if (j + 1 < nkt) load_k(j + 1);
+        const int st = j % VS;
+        mbar_wait(&v_empty[st], ((j / VS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[st], kTile);
+        tma_load_2d(sV + st * kTile, &tmV, &v_full[st], g * DH, sg.kv_row0 + j * TK);
+        tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], g * DH + 64, sg.kv_row0 + j * TK);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
+      const uint32_t q0 = smem_u32(sQ);
+      auto issue_s = [&](int w, int j) {
+        const uint32_t k0 = smem_u32(sK + (j % KS) * kTile);
+        const uint32_t qw = q0 + w * kTile;
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks)
+          umma_bf16(tmem + 256 * w, kdesc(qw, ks), kdesc(k0, ks), idS, ks > 0 ? 1u : 0u);
+        umma_commit(&s_full[w]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      umma_commit(&k_empty[0]);
+      for (int j = 0; j < nkt; ++j) {
+        const int sv = j % VS;
+        const bool more = j + 1 < nkt;
+        const int sk = (j + 1) % KS;
+        const uint32_t v0 = smem_u32(sV + sv * kTile);
+        for (int w = 0; w < 2; ++w) {
+          mbar_wait(&p_full[w], j & 1);
+          if (w == 0) mbar_wait(&v_full[sv], (j / VS) & 1);
+          tc_fence_after();
+          const uint32_t tS = tmem + 256 * w, tO = tS + 128;
+#pragma unroll
+          for (int ks = 0; ks < TK / 16; ++ks)
+            umma_bf16_ts(tO, tS + ks * 8, mndesc(v0, ks), idO, (j > 0 || ks > 0) ? 1u : 0u);
+          if (w == 1) umma_commit(&v_empty[sv]);
+          if (more) {
+            if (w == 0) {
+              mbar_wait(&k_full[sk], ((j + 1) / KS) & 1);
+              tc_fence_after();
+            }
+            issue_s(w, j + 1);
+            if (w == 1) umma_commit(&k_empty[sk]);
+          } else {
+            umma_commit(&o_done[w]);
+          }
+        }
+      }
+    }
+  } else {
+    // softmax: warps 0-3 head h0, warps 4-7 head h0+1; thread = query row
+    const int w = warp >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int qi = tl.first + row;
+    const int lim = sg.prefix + min(qi, sg.len - 1);
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + 256 * w + lane_off, tO = tS + 128;
+    const float sl2 = a.sl2;
+    float m = -FLT_MAX, l = 0.f;
+    for (int j = 0; j < nkt; ++j) {
+      mbar_wait(&s_full[w], j & 1);
+      tc_fence_after();
+      const int key0 = j * TK;
+      const bool full = key0 + TK - 1 <= sg.prefix + tl.first;
+      // pass 1: row max (all four 32-column loads in flight at once)
+      float pm[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+      {
+        uint32_t r[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r[c]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (full) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[c][e]));
+          } else {
+#pragma unroll
+            for (int e = 0; e < 32; ++e)
+              if (key0 + c * 32 + e <= lim) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[c][e]));
+          }
+        }
+      }
+      const float tmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * sl2;  // sl2 > 0
+      float alpha = 1.f;
+      bool rescale = false;
+      if (tmax > m + kRescale || j == 0) {
+        const float mn = fmaxf(m, tmax);
+        alpha = ex2(m - mn);
+        rescale = j > 0;
+        m = mn;
+      }
+      if (rescale) {  // PV_w(j-1) is complete (s_full_w(j) was committed after it)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          tmem_st32(tO + c * 32, r);
+        }
+      }
+      // pass 2: p = 2^(s*sl2 - m) -> bf16 pairs over the first 64 columns of
+      // S; the next chunk's TMEM load is in flight while this one computes
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t rb[2][32];
+      tmem_ld32(tS, rb[0]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c + 1 < 4) tmem_ld32(tS + (c + 1) * 32, rb[(c + 1) & 1]);
+        const uint32_t(&r)[32] = rb[c & 1];
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int k = key0 + c * 32 + 2 * e;
+          float p0 = ex2(fmaf(__uint_as_float(r[2 * e]), sl2, -m));
+          float p1 = ex2(fmaf(__uint_as_float(r[2 * e + 1]), sl2, -m));
+          if (!full) {
+            p0 = k <= lim ? p0 : 0.f;
+            p1 = k + 1 <= lim ? p1 : 0.f;
+          }
+          ps[e & 3] += p0 + p1;
+          pk[e] = pack_bf16(p0, p1);
+        }
+        // S columns [16c, 16c+16) belong to chunk c/2 <= c, already in registers
+        tmem_st16(tS + c * 16, pk);
+        if (c + 1 < 4) tmem_ld_wait();
+      }
+      l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_full[w]);
+    }
+    mbar_wait(&o_done[w], 0);
+    tc_fence_after();
+    const int h = h0 + w;
+    const bool ok = qi < sg.len && row < tl.count;
+    const float inv = 1.f / l;
+    __nv_bfloat16* orow = a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + static_cast<int64_t>(h) * DH;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tO + c * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          dst[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * inv, __uint_as_float(r[8 * q + 1]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 2]) * inv, __uint_as_float(r[8 * q + 3]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 4]) * inv, __uint_as_float(r[8 * q + 5]) * inv),
+                              pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv));
+      }
+    }
+    if (ok) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uint64_t ld) {
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<EncodeFn>(p);
+  }
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {64, 128};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool attn_fwd_pp_supported(const AttnParams& p) {
+  return attn_tc_supported(p) && (p.H / p.KVH) % 2 == 0 && (reinterpret_cast<uintptr_t>(p.q) & 15) == 0;
+}
+
+cudaError_t attn_forward_tc_pp(const AttnParams& p, const AttnTile* tiles128, int32_t ntiles, int64_t kv_rows,
+                               cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  if (!attn_fwd_pp_supported(p)) return cudaErrorInvalidValue;
+  CUtensorMap mq, mk, mv;
+  if (!map_rows(&mq, p.q, static_cast<uint64_t>(p.H) * DH, static_cast<uint64_t>(p.T), p.q_stride) ||
+      !map_rows(&mk, p.k, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride) ||
+      !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
+    return cudaErrorInvalidValue;
+  Args a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
+  const size_t smem = 1024 + (2 + KS + VS) * kTile + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  attn_fwd_pp_kernel<<<dim3(ntiles, p.H / 2), kThreads, smem, st>>>(mq, mk, mv, a);
+  return cudaGetLastError();
+}
+
+}  // namespace cfk

@@ -814,7 +814,11 @@ struct Exec {
           "kv_store");
       AttnParams p = attn_params(cm, t, l, gs);
       cudaEvent_t t0 = mark();
-      if (cfk::attn_tc_supported(p))
+      if (cfk::attn_fwd_pp_supported(p))
+        L(cfk::attn_forward_tc_pp(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
+                                  cm.dependent ? gs->S : T, s),
+          "attn_fwd_tc_pp");
+      else if (cfk::attn_tc_supported(p))
         L(cfk::attn_forward_tc(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
                                cm.dependent ? gs->S : T, s),
           "attn_fwd_tc");

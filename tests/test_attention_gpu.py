@@ -50,10 +50,10 @@ def _inputs(c, seed=0):
 
 
 @pytest.mark.parametrize("name", list(CASES))
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 3])
 def test_attention_forward(ctx, name, impl):
     c = CASES[name]
-    if impl == 1 and c["dh"] != 128:
+    if impl in (1, 3) and c["dh"] != 128 or (impl == 3 and (c["H"] // c["KVH"]) % 2):
         pytest.skip("tcgen05 path is head_dim 128")
     H, KVH, dh, T, R = c["H"], c["KVH"], c["dh"], c["T"], c["R"]
     q, k, v = _inputs(c)

@@ -32,7 +32,8 @@ def run(impl, bwd):
                   KVH, dh)
 
 
-for name, impl, bwd, fl in (("fwd tcgen05", 1, False, 4), ("fwd mma.sync", 0, False, 4),
+for name, impl, bwd, fl in (("fwd tcgen05 ping-pong", 3, False, 4), ("fwd tcgen05", 1, False, 4),
+                            ("fwd mma.sync", 0, False, 4),
                             ("bwd tcgen05 pipelined", 1, True, 8), ("bwd tcgen05 v1", 2, True, 8),
                             ("bwd mma.sync", 0, True, 8)):
     run(1, False)

@@ -42,7 +42,7 @@ def run(impl, bwd):
                   KVH, dh)
 
 
-for name, impl, bwd, fl in (("fwd tcgen05", 1, False, 4), 
+for name, impl, bwd, fl in (("fwd tcgen05 ping-pong", 3, False, 4), ("fwd tcgen05", 1, False, 4), 
                             ("fwd mma.sync", 0, False, 4), ("bwd tcgen05", 1, True, 8), ("bwd mma.sync", 0, True, 8)):
     run(1, False)
     run(impl, bwd)
