@@ -14,9 +14,10 @@
 //   MMA into S_w is issued after the PV that read P_w, and tcgen05 MMAs of
 //   one thread complete in order, so s_full_w(j) also certifies PV_w(j-1)
 //   (O_w stable for the lazy rescale, P_w region free).
-//   warps 0-3: softmax of head 0 (thread = query row, full 128-key rows,
-//   two passes over TMEM: row max, then exp2 / sum / bf16 P); warps 4-7:
-//   head 1; warp 8: TMA producer; warp 9: MMA issuer.
+//   warps 0-7: softmax of head 0 (two warps per query row, 64 keys each,
+//   S read from TMEM once, half-row maxima exchanged through smem); warps
+//   8-15: head 1; warp 16: TMA producer; warp 17: MMA issuer.  576 threads
+//   cap registers at 96 per thread.
 #include <cfloat>
 
 #include "attention.h"
@@ -32,8 +33,8 @@ constexpr uint32_t kTile = 2 * kBox;     // 128 x 128
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescale = 8.0f;
-constexpr int KS = 3, VS = 2;  // K / V ring depths (K runs one tile further ahead)
-constexpr int kThreads = 320;
+constexpr int KS = 2, VS = 2;  // K / V ring depths
+constexpr int kThreads = 576;  // 16 softmax warps + TMA + MMA
 
 struct Args {
   const AttnSeg* segs;
@@ -50,14 +51,6 @@ __device__ __forceinline__ uint64_t kdesc(uint32_t base, int ks) {
 }
 __device__ __forceinline__ uint64_t mndesc(uint32_t base, int ks) {
   return umma_desc_sw128(base + ks * 2048, kBox, 1024);
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -80,7 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = sm;                       // 2 heads
   uint8_t* sK = sQ + 2 * kTile;           // KS stages
   uint8_t* sV = sK + KS * kTile;          // VS stages
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + VS * kTile);
+  float* sRed = reinterpret_cast<float*>(sV + VS * kTile);  // [2 heads][2 parity][2 half][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 1024);
   uint64_t* q_full = bar;
   uint64_t* k_full = bar + 1;                 // [KS]
   uint64_t* k_empty = k_full + KS;
@@ -114,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&s_full[w], 1);
-      mbar_init(&p_full[w], 128);
+      mbar_init(&p_full[w], 256);
       mbar_init(&o_done[w], 1);
     }
     fence_mbar_init();
@@ -125,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {
+  if (warp == 16) {
     if (lane == 0) {
       mbar_expect_tx(q_full, 2 * kTile);
       for (int w = 0; w < 2; ++w) {
@@ -151,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sV + st * kTile + kBox, &tmV, &v_full[st], g * DH + 64, sg.kv_row0 + j * TK);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     if (lane == 0) {
       constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
@@ -198,40 +192,41 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // softmax: warps 0-3 head h0, warps 4-7 head h0+1; thread = query row
-    const int w = warp >> 2, quarter = warp & 3;
+    // softmax: warps 0-7 head h0, warps 8-15 head h0+1; two warps per query
+    // row (warp w and w+4 of a head share TMEM lanes), 64 keys each
+    const int w = warp >> 3, quarter = warp & 3, half = (warp >> 2) & 1;
     const int row = quarter * 32 + lane;
     const int qi = tl.first + row;
     const int lim = sg.prefix + min(qi, sg.len - 1);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tS = tmem + 256 * w + lane_off, tO = tS + 128;
+    const uint32_t red = smem_u32(sRed) + w * 2048;  // [2 parity][2 half][128 rows] per head
     const float sl2 = a.sl2;
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < nkt; ++j) {
       mbar_wait(&s_full[w], j & 1);
       tc_fence_after();
-      const int key0 = j * TK;
-      const bool full = key0 + TK - 1 <= sg.prefix + tl.first;
-      // pass 1: row max (all four 32-column loads in flight at once)
-      float pm[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-      {
-        uint32_t r[4][32];
+      const int key0 = j * TK + half * 64;
+      const bool full = j * TK + TK - 1 <= sg.prefix + tl.first;
+      // this half-row of S, read from TMEM once (kept as raw bits)
+      uint32_t r[2][32];
+      tmem_ld32(tS + half * 64, r[0]);
+      tmem_ld32(tS + half * 64 + 32, r[1]);
+      tmem_ld_wait();
+      if (!full) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(tS + c * 32, r[c]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (full) {
-#pragma unroll
-            for (int e = 0; e < 32; ++e) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[c][e]));
-          } else {
-#pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (key0 + c * 32 + e <= lim) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[c][e]));
-          }
-        }
+        for (int e = 0; e < 64; ++e)
+          if (key0 + e > lim) r[e >> 5][e & 31] = 0xff7fffffu;  // -FLT_MAX: ex2 underflows to 0
       }
-      const float tmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])) * sl2;  // sl2 > 0
+      float pm[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+#pragma unroll
+      for (int e = 0; e < 64; ++e) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[e >> 5][e & 31]));
+      float tmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
+      // exchange half-row maxima with the partner warp; after this barrier
+      // both halves hold their S values, so P may overwrite any S column
+      sts_f32(red + (j & 1) * 1024 + (half * 128 + row) * 4, tmax);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + w * 4 + quarter) : "memory");
+      tmax = fmaxf(tmax, lds_f32(red + (j & 1) * 1024 + ((half ^ 1) * 128 + row) * 4)) * sl2;  // sl2 > 0
       float alpha = 1.f;
       bool rescale = false;
       if (tmax > m + kRescale || j == 0) {
@@ -240,59 +235,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         rescale = j > 0;
         m = mn;
       }
-      if (rescale) {  // PV_w(j-1) is complete (s_full_w(j) was committed after it)
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+      for (int e = 0; e < 32; ++e) {
+        const float p0 = ex2(fmaf(__uint_as_float(r[e >> 4][(2 * e) & 31]), sl2, -m));
+        const float p1 = ex2(fmaf(__uint_as_float(r[e >> 4][(2 * e + 1) & 31]), sl2, -m));
+        ps[e & 3] += p0 + p1;
+        pk[e] = pack_bf16(p0, p1);
+      }
+      l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
+      tmem_st32(tS + half * 32, pk);  // P (bf16 pairs) over S columns [0, 64)
+      if (rescale) {  // after P (S registers dead); PV_w(j-1) is complete (s_full_w(j) followed it)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
-          tmem_ld32(tO + c * 32, r);
+          tmem_ld32(tO + half * 64 + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-          tmem_st32(tO + c * 32, r);
+          tmem_st32(tO + half * 64 + c * 32, r);
         }
       }
-      // pass 2: p = 2^(s*sl2 - m) -> bf16 pairs over the first 64 columns of
-      // S; the next chunk's TMEM load is in flight while this one computes
-      float ps[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t rb[2][32];
-      tmem_ld32(tS, rb[0]);
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c + 1 < 4) tmem_ld32(tS + (c + 1) * 32, rb[(c + 1) & 1]);
-        const uint32_t(&r)[32] = rb[c & 1];
-        uint32_t pk[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int k = key0 + c * 32 + 2 * e;
-          float p0 = ex2(fmaf(__uint_as_float(r[2 * e]), sl2, -m));
-          float p1 = ex2(fmaf(__uint_as_float(r[2 * e + 1]), sl2, -m));
-          if (!full) {
-            p0 = k <= lim ? p0 : 0.f;
-            p1 = k + 1 <= lim ? p1 : 0.f;
-          }
-          ps[e & 3] += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
-        }
-        // S columns [16c, 16c+16) belong to chunk c/2 <= c, already in registers
-        tmem_st16(tS + c * 16, pk);
-        if (c + 1 < 4) tmem_ld_wait();
-      }
-      l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[w]);
     }
+    // combine the half-row sums (the pair re-syncs before the buffer is reused)
+    sts_f32(red + (nkt & 1) * 1024 + (half * 128 + row) * 4, l);
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + w * 4 + quarter) : "memory");
+    l += lds_f32(red + (nkt & 1) * 1024 + ((half ^ 1) * 128 + row) * 4);
     mbar_wait(&o_done[w], 0);
     tc_fence_after();
     const int h = h0 + w;
     const bool ok = qi < sg.len && row < tl.count;
     const float inv = 1.f / l;
-    __nv_bfloat16* orow = a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + static_cast<int64_t>(h) * DH;
+    __nv_bfloat16* orow =
+        a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + static_cast<int64_t>(h) * DH + half * 64;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
-      tmem_ld32(tO + c * 32, r);
+      tmem_ld32(tO + half * 64 + c * 32, r);
       tmem_ld_wait();
       if (ok) {
         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
@@ -304,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                               pack_bf16(__uint_as_float(r[8 * q + 6]) * inv, __uint_as_float(r[8 * q + 7]) * inv));
       }
     }
-    if (ok) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
+    if (ok && half == 0) a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] = (m + log2f(l)) * kLn2;
   }
   tc_fence_before();
   __syncthreads();
@@ -353,7 +336,7 @@ cudaError_t attn_forward_tc_pp(const AttnParams& p, const AttnTile* tiles128, in
       !map_rows(&mv, p.v, static_cast<uint64_t>(p.KVH) * DH, static_cast<uint64_t>(kv_rows), p.kv_stride))
     return cudaErrorInvalidValue;
   Args a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
-  const size_t smem = 1024 + (2 + KS + VS) * kTile + 256;
+  const size_t smem = 1024 + (2 + KS + VS) * kTile + 1024 * 4 + 256;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
