@@ -42,7 +42,9 @@ struct Args {
   const __nv_bfloat16* v;
   int64_t kv_stride;
   const float* lse;
-  const float* dsum;
+  float* dsum;               // D = rowsum(dO * O): written by the dQ kernel, read by dK/dV
+  const __nv_bfloat16* o;    // attention output O (for D)
+  int64_t o_stride;
   __nv_bfloat16* dq;
   int64_t dq_stride;
   float* dk_acc;
@@ -56,8 +58,11 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 
 // One thread = one TMEM lane (row): copies 64 bf16 (this half's columns) of a
 // global row into 32 TMEM columns at `taddr` (A-operand layout: element k of
-// the row in column k/2).  Rows that do not exist are zero-filled.
-__device__ __forceinline__ void stage_row_tmem(uint32_t taddr, const __nv_bfloat16* src, bool ok) {
+// the row in column k/2).  Rows that do not exist are zero-filled.  With
+// `dot_with` set, also returns sum_k row[k] * dot_with[k] (the D = dO.O
+// softmax-statistic reduction, fused into the dQ kernel's staging).
+__device__ __forceinline__ float stage_row_tmem(uint32_t taddr, const __nv_bfloat16* src, bool ok,
+                                                const __nv_bfloat16* dot_with = nullptr) {
   uint32_t w[32];
   const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
@@ -77,6 +82,25 @@ __device__ __forceinline__ void stage_row_tmem(uint32_t taddr, const __nv_bfloat
       "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
       "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
       : "memory");
+  float acc = 0.f;
+  if (dot_with && ok) {
+    const uint4* o4 = reinterpret_cast<const uint4*>(dot_with);
+    float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint4 ov = __ldg(o4 + c);
+      const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&w[4 * c + e]);
+        const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+        part[e] = fmaf(__low2float(a2), __low2float(b2), part[e]);
+        part[e] = fmaf(__high2float(a2), __high2float(b2), part[e]);
+      }
+    }
+    acc = (part[0] + part[1]) + (part[2] + part[3]);
+  }
+  return acc;
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 constexpr int kThreads = 320;
@@ -107,7 +131,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sK = sm;                    // KS stages x 2 x [64][64]
   uint8_t* sV = sK + KS * 2 * kBox64;  // VS stages
   uint8_t* sS = sV + VS * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 2 * kBox128);
+  float* sRowD = reinterpret_cast<float*>(sS + 2 * kBox128);  // [2 half][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRowD + 256);
   uint64_t* q_full = bar;
   uint64_t* k_full = bar + 1;              // [KS]
   uint64_t* k_empty = k_full + KS;         // [KS]
@@ -226,16 +251,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lim = sg.prefix + min(qi, sg.len - 1);
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
-    const float D = ok ? a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] : 0.f;
+    float D;
     {
       const bool rok = row < tl.count;
       const int64_t r = q_row0 + row;
       stage_row_tmem(tAq + lane_off + half * 32, a.q + r * a.q_stride + static_cast<int64_t>(h) * DH + half * 64, rok);
-      stage_row_tmem(tAo + lane_off + half * 32, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + half * 64,
-                     rok);
+      const float dpart = stage_row_tmem(
+          tAo + lane_off + half * 32, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + half * 64, ok,
+          a.o + r * a.o_stride + static_cast<int64_t>(h) * DH + half * 64);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(q_full);
+      // D = rowsum(dO * O): the two half-rows meet in smem (fixed order)
+      sRowD[half * 128 + row] = dpart;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      D = sRowD[row] + sRowD[128 + row];
+      if (ok && half == 0) a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] = D;
     }
     const uint32_t bSf = smem_u32(s_full), bSr = smem_u32(s_free), bDf = smem_u32(ds_full),
                    bDr = smem_u32(ds_free), sS0 = smem_u32(sS);
@@ -601,9 +632,10 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
       !map_rows(&q64, p.q, qc, p.T, p.q_stride, 64) || !map_rows(&o64, p.dout, qc, p.T, p.dout_stride, 64) ||
       !map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
     return cudaErrorInvalidValue;
-  Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.dq,
-         p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
-  const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256;
+  Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.o,
+         p.o_stride, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e,
+         p.scale};
+  const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256 * 4 + 256;
   const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
   static bool attr = false;
   if (!attr) {
@@ -614,8 +646,7 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  cudaError_t e = attn_dsum(p, st);
-  if (e != cudaSuccess) return e;
+  // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
   dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   a.tiles = ktiles128;
   if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kThreads, smem_dkv, st>>>(q64, o64, k128, v128, a);
