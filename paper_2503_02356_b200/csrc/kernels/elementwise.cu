@@ -549,6 +549,50 @@ __global__ void dkv_to_dqkv_kernel(const float* dk, const float* dv, int64_t acc
   }
 }
 
+// Vector form: 8 consecutive columns of one head-half per thread (two float4
+// of dK, of its rotate-half partner and of dV; one 16-byte bf16 store each).
+__global__ void dkv_to_dqkv_vec_kernel(const float* __restrict__ dk, const float* __restrict__ dv, int64_t acc_ld,
+                                       int64_t T, int KVH, int dh, const float2* __restrict__ tab,
+                                       bf16* __restrict__ dqkv, int64_t ld, int64_t col_k, int64_t col_v) {
+  const int half = dh / 2, g8 = dh / 8;
+  const int64_t n = T * KVH * g8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / (KVH * g8);
+    const int64_t c = (i % (KVH * g8)) * 8;  // column within [0, kvw)
+    const int j = static_cast<int>(c % dh);
+    const float* kr = dk + t * acc_ld + c;
+    const float* vr = dv + t * acc_ld + c;
+    float kv[8], vv[8], out[8];
+    *reinterpret_cast<float4*>(kv) = *reinterpret_cast<const float4*>(kr);
+    *reinterpret_cast<float4*>(kv + 4) = *reinterpret_cast<const float4*>(kr + 4);
+    *reinterpret_cast<float4*>(vv) = *reinterpret_cast<const float4*>(vr);
+    *reinterpret_cast<float4*>(vv + 4) = *reinterpret_cast<const float4*>(vr + 4);
+    if (tab) {
+      const bool lo = j < half;
+      const int jj = lo ? j : j - half;
+      float pv[8];
+      const float* pr = lo ? kr + half : kr - half;  // rotate-half partner
+      *reinterpret_cast<float4*>(pv) = *reinterpret_cast<const float4*>(pr);
+      *reinterpret_cast<float4*>(pv + 4) = *reinterpret_cast<const float4*>(pr + 4);
+      const float4* tp = reinterpret_cast<const float4*>(tab + t * half + jj);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 cs = tp[e];  // (cos, sin) of pairs jj+2e, jj+2e+1
+        // lo: dx0 = dy0 c + dy1 s;  hi: dx1 = dy1 c - dy0 s
+        out[2 * e] = lo ? kv[2 * e] * cs.x + pv[2 * e] * cs.y : kv[2 * e] * cs.x - pv[2 * e] * cs.y;
+        out[2 * e + 1] =
+            lo ? kv[2 * e + 1] * cs.z + pv[2 * e + 1] * cs.w : kv[2 * e + 1] * cs.z - pv[2 * e + 1] * cs.w;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) out[e] = kv[e];
+    }
+    *reinterpret_cast<uint4*>(dqkv + t * ld + col_k + c) = pack8(out);
+    *reinterpret_cast<uint4*>(dqkv + t * ld + col_v + c) = pack8(vv);
+  }
+}
+
 __global__ void scale_rows_kernel(float* x, int64_t rows, int64_t cols, int64_t ld, float s) {
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -758,8 +802,15 @@ cudaError_t gain_grad(const float* x, const float* dy, const float* rstd, int64_
 }
 cudaError_t dkv_to_dqkv(const float* dk, const float* dv, int64_t acc_ld, int64_t T, int KVH, int dh,
                         const float2* tab, bf16* dqkv, int64_t ld, int64_t col_k, int64_t col_v, cudaStream_t st) {
-  dkv_to_dqkv_kernel<<<blocks_for(T * KVH * dh), kThreads, 0, st>>>(dk, dv, acc_ld, T, KVH, dh, tab, dqkv, ld, col_k,
-                                                                   col_v);
+  const bool vec = dh % 16 == 0 && acc_ld % 4 == 0 && ld % 8 == 0 && col_k % 8 == 0 && col_v % 8 == 0 &&
+                   (reinterpret_cast<uintptr_t>(dk) & 15) == 0 && (reinterpret_cast<uintptr_t>(dv) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dqkv) & 15) == 0;
+  if (vec)
+    dkv_to_dqkv_vec_kernel<<<blocks_for(T * KVH * (dh / 8)), kThreads, 0, st>>>(dk, dv, acc_ld, T, KVH, dh, tab, dqkv,
+                                                                               ld, col_k, col_v);
+  else
+    dkv_to_dqkv_kernel<<<blocks_for(T * KVH * dh), kThreads, 0, st>>>(dk, dv, acc_ld, T, KVH, dh, tab, dqkv, ld,
+                                                                     col_k, col_v);
   return cudaGetLastError();
 }
 cudaError_t scale_rows_f32(float* x, int64_t rows, int64_t cols, int64_t ld, float s, cudaStream_t st) {
