@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchunkflow_b200.so")
+# CF_LIB selects another build of the library (A/B kernel measurements)
+LIB_PATH = os.environ.get("CF_LIB") or os.path.join(_HERE, "libchunkflow_b200.so")
 
 CHUNK_DT = np.dtype([(k, np.int64) for k in
                      ("chunk_id", "kind", "group_id", "index_in_group",

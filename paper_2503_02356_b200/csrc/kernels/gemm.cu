@@ -129,6 +129,52 @@ __device__ __forceinline__ void store_row32(const Args& g, int row, int col0, co
   }
 }
 
+// Epilogues that read a fp32 row segment (residual R or the accumulated C)
+// prefetch the next 32-column chunk while the current one is stored: the
+// per-row loads otherwise serialise one DRAM latency per chunk.
+template <int EPI>
+constexpr bool kEpiReads = EPI == EPI_F32_RES || EPI == EPI_F32_ACC;
+
+template <int EPI>
+__device__ __forceinline__ void prefetch_row32(const Args& g, int row, int col0, float4 (&v)[8]) {
+  if (row >= g.M || col0 >= g.N) return;
+  const float* src = EPI == EPI_F32_RES ? reinterpret_cast<const float*>(g.R) + static_cast<int64_t>(row) * g.ldr + col0
+                                        : reinterpret_cast<const float*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+  if (col0 + 32 <= g.N) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = reinterpret_cast<const float4*>(src)[q];
+  } else {
+    float* f = reinterpret_cast<float*>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) f[j] = col0 + j < g.N ? src[j] : 0.f;
+  }
+}
+
+// fp32 store of acc + v (v = prefetched residual or previous C)
+template <int EPI>
+__device__ __forceinline__ void store_row32_pre(const Args& g, int row, int col0, const uint32_t (&r)[32],
+                                                const float4 (&v)[8]) {
+  if (row >= g.M) return;
+  float* c = reinterpret_cast<float*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+  if (col0 + 32 <= g.N) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 o = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                             __uint_as_float(r[4 * q + 3]));
+      o.x += v[q].x;
+      o.y += v[q].y;
+      o.z += v[q].z;
+      o.w += v[q].w;
+      reinterpret_cast<float4*>(c)[q] = o;
+    }
+  } else {
+    const float* f = reinterpret_cast<const float*>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < g.N) c[j] = __uint_as_float(r[j]) + f[j];
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args g) {
@@ -242,7 +288,9 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
+      float4 pre[8];
+      if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * BN, pre);
+#pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
@@ -252,7 +300,15 @@ __global__ void __launch_bounds__(256, 1)
           mbar_arrive(&tempty[acc]);
         }
         const int col0 = nb * BN + c * 32;
-        if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        if constexpr (kEpiReads<EPI>) {
+          float4 nxt[8];
+          if (c + 1 < BN / 32) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
+          if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
+        } else {
+          if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        }
       }
       if (++acc == 2) {
         acc = 0;
@@ -452,7 +508,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * 256);
-#pragma unroll 1
+      float4 pre[8];
+      if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * 256, pre);
+#pragma unroll
       for (int c = 0; c < 8; ++c) {
         uint32_t r[32];
         tmem_ld32(tbase + c * 32, r);
@@ -463,7 +521,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
         }
         const int col0 = nb * 256 + c * 32;
-        if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        if constexpr (kEpiReads<EPI>) {
+          float4 nxt[8];
+          if (c + 1 < 8) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
+          if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
+        } else {
+          if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        }
       }
       if (++acc == 2) {
         acc = 0;
