@@ -381,6 +381,14 @@ int cf_ctx_init_pp(cf_ctx* ctx, int rank, int world, int num_stages,
  * the last stage (0 elsewhere). */
 int cf_pp_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, int64_t k,
                    const cf_run_opts* opts, cf_run_result* result);
+/* In-process pipeline links (testing the per-rank path on one device): each
+ * stage's context — driven by its own host thread — attaches to one shared
+ * cf_pp_local; cf_pp_step_run then exchanges stage-boundary buffers through
+ * host mailboxes, CUDA events and device copies instead of NCCL. */
+typedef struct cf_pp_local cf_pp_local;
+int cf_pp_local_create(int num_stages, cf_pp_local** out);
+void cf_pp_local_destroy(cf_pp_local* pipe);
+int cf_ctx_init_pp_local(cf_ctx* ctx, cf_pp_local* pipe, int stage);
 /* Every stage of one pipeline on this context's device (models[i] = stage
  * i): the same op streams in dispatch order with in-memory hand-over.
  * Gradients are bitwise those of cf_step_run on the unsplit model. */

@@ -93,7 +93,7 @@ EXPORTS = [
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
-    "cf_pp_run_local", "cf_step_op_times", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
+    "cf_pp_run_local", "cf_step_op_times", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
@@ -113,7 +113,8 @@ def lib():
         L.cf_model_num_tensors.restype = C.c_int64
         L.cf_model_num_params.restype = C.c_int64
         vp = C.c_void_p
-        for name in ("cf_plan_destroy", "cf_ctx_destroy", "cf_model_destroy", "cf_step_destroy"):
+        for name in ("cf_plan_destroy", "cf_ctx_destroy", "cf_model_destroy", "cf_step_destroy",
+                     "cf_pp_local_destroy"):
             getattr(L, name).argtypes = [vp]
             getattr(L, name).restype = None
         L.cf_model_num_tensors.argtypes = [vp]
@@ -391,6 +392,10 @@ class Context:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid else None
         check(lib().cf_ctx_init_dp(self.h, C.c_int(rank), C.c_int(world), buf))
 
+    def init_pp_local(self, pipe: "LocalPipe", stage):
+        """Attach to an in-process pipeline (cf_ctx_init_pp_local)."""
+        check(lib().cf_ctx_init_pp_local(self.h, pipe.h, C.c_int(stage)))
+
     def init_pp(self, rank, world, num_stages, uid: bytes):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         check(lib().cf_ctx_init_pp(self.h, C.c_int(rank), C.c_int(world), C.c_int(num_stages), buf))
@@ -419,6 +424,20 @@ class Context:
     def close(self):
         if self.h and self.h.value:
             lib().cf_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+class LocalPipe:
+    """In-process pipeline links (cf_pp_local): one context per stage, each
+    driven by its own thread through Step.run_pp."""
+
+    def __init__(self, num_stages):
+        self.h = C.c_void_p()
+        check(lib().cf_pp_local_create(C.c_int(num_stages), C.byref(self.h)))
+
+    def close(self):
+        if self.h and self.h.value:
+            lib().cf_pp_local_destroy(self.h)
             self.h = C.c_void_p()
 
 

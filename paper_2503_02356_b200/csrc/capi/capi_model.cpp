@@ -118,6 +118,33 @@ int cf_ctx_init_pp(cf_ctx* ctx, int rank, int world, int num_stages, const uint8
   });
 }
 
+struct cf_pp_local {
+  cfb::LocalPipe* p = nullptr;
+};
+
+int cf_pp_local_create(int num_stages, cf_pp_local** out) {
+  return cfb::guard([&] {
+    need(out, "out");
+    auto h = std::make_unique<cf_pp_local>();
+    h->p = cfb::local_pipe_create(num_stages);
+    *out = h.release();
+  });
+}
+
+void cf_pp_local_destroy(cf_pp_local* pipe) {
+  if (!pipe) return;
+  cfb::local_pipe_destroy(pipe->p);
+  delete pipe;
+}
+
+int cf_ctx_init_pp_local(cf_ctx* ctx, cf_pp_local* pipe, int stage) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(pipe, "pipe");
+    cfb::pp_init_local(&ctx->c, pipe->p, stage);
+  });
+}
+
 int cf_pp_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, int64_t k, const cf_run_opts* opts,
                    cf_run_result* result) {
   return cfb::guard([&] {

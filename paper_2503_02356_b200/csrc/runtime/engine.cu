@@ -23,6 +23,12 @@
 #include <memory>
 #include <numeric>
 #include <set>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <tuple>
 
 #include "../capi/capi_util.hpp"
@@ -1402,13 +1408,51 @@ void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t P, cf_step* st, i
   if (res) *res = total;
 }
 
+// ------------------------------------------------- in-process stage links
+struct LocalMsg {
+  float* buf = nullptr;
+  size_t n = 0;
+  cudaEvent_t ready = nullptr;     // sender: buffer produced
+  cudaEvent_t consumed = nullptr;  // receiver: buffer copied out
+  std::atomic<bool> taken{false};  // `consumed` has been recorded
+};
+struct LocalLink {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::shared_ptr<LocalMsg>> q;
+};
+struct LocalPipe {
+  int stages = 0;
+  std::vector<std::unique_ptr<LocalLink>> act, grad;  // act[s]: s -> s+1, grad[s]: s+1 -> s
+};
+
+LocalPipe* local_pipe_create(int stages) {
+  if (stages < 1) throw ValidationError("num_stages must be at least 1");
+  auto p = std::make_unique<LocalPipe>();
+  p->stages = stages;
+  for (int s = 0; s + 1 < stages; ++s) {
+    p->act.emplace_back(new LocalLink);
+    p->grad.emplace_back(new LocalLink);
+  }
+  return p.release();
+}
+void local_pipe_destroy(LocalPipe* p) { delete p; }
+void pp_init_local(Ctx* ctx, LocalPipe* p, int stage) {
+  if (!p || stage < 0 || stage >= p->stages) throw ValidationError("bad local pipeline stage");
+  ctx->local = p;
+  ctx->stage = stage;
+  ctx->stages = p->stages;
+}
+
 namespace {
 
-// One stage-boundary transfer on a link stream, ordered against the compute
-// stream with events in both directions.
+// One stage-boundary transfer, ordered against the compute stream with
+// events in both directions: NCCL p2p on a link stream, or (in-process
+// pipeline) a device copy on the receiver's compute stream.
 struct LinkOp {
   float* buf;
-  cudaEvent_t done;
+  cudaEvent_t done;                // NCCL: transfer complete
+  std::shared_ptr<LocalMsg> msg;   // local send: receiver's copy-out
 };
 
 cudaEvent_t new_event() {
@@ -1417,7 +1461,51 @@ cudaEvent_t new_event() {
   return e;
 }
 
+LocalLink* local_link(Ctx* ctx, int li) {
+  LocalPipe* p = ctx->local;
+  const int s = ctx->stage;
+  switch (li) {
+    case 0: return p->act[static_cast<size_t>(s)].get();       // act up
+    case 1: return p->act[static_cast<size_t>(s - 1)].get();   // act down
+    case 2: return p->grad[static_cast<size_t>(s)].get();      // grad from above
+    default: return p->grad[static_cast<size_t>(s - 1)].get(); // grad down
+  }
+}
+
+LinkOp local_xfer(Ctx* ctx, int li, float* buf, size_t n, bool send) {
+  LocalLink* L = local_link(ctx, li);
+  if (send) {
+    auto msg = std::make_shared<LocalMsg>();
+    msg->buf = buf;
+    msg->n = n;
+    msg->ready = new_event();
+    msg->consumed = new_event();
+    CK(cudaEventRecord(msg->ready, ctx->stream));
+    {
+      std::lock_guard<std::mutex> lk(L->mu);
+      L->q.push_back(msg);
+    }
+    L->cv.notify_all();
+    return {buf, nullptr, msg};
+  }
+  std::shared_ptr<LocalMsg> msg;
+  {
+    std::unique_lock<std::mutex> lk(L->mu);
+    if (!L->cv.wait_for(lk, std::chrono::seconds(120), [&] { return !L->q.empty(); }))
+      throw std::logic_error("in-process pipeline: receive timed out (stage op streams disagree)");
+    msg = L->q.front();
+    L->q.pop_front();
+  }
+  if (msg->n != n) throw std::logic_error("in-process pipeline: transfer size mismatch");
+  CK(cudaStreamWaitEvent(ctx->stream, msg->ready, 0));
+  CK(cudaMemcpyAsync(buf, msg->buf, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaEventRecord(msg->consumed, ctx->stream));
+  msg->taken.store(true, std::memory_order_release);
+  return {buf, nullptr, nullptr};
+}
+
 LinkOp link_xfer(Ctx* ctx, int li, void* comm, int peer, float* buf, size_t n, bool send) {
+  if (ctx->local) return local_xfer(ctx, li, buf, n, send);
   cudaStream_t ls = ctx->link_stream[li];
   cudaEvent_t ready = new_event(), done = new_event();
   CK(cudaEventRecord(ready, ctx->stream));  // buffer allocated / produced on the compute stream
@@ -1429,7 +1517,32 @@ LinkOp link_xfer(Ctx* ctx, int li, void* comm, int peer, float* buf, size_t n, b
   CK(cudaEventRecord(done, ls));
   if (!send) CK(cudaStreamWaitEvent(ctx->stream, done, 0));  // consumer waits for the data
   CK(cudaEventDestroy(ready));
-  return {buf, done};
+  return {buf, done, nullptr};
+}
+
+// A send buffer may be released once the transfer (NCCL) or the receiver's
+// copy (in-process) has completed; `wait` blocks until then.
+bool send_complete(LinkOp& op, bool wait) {
+  if (op.msg) {
+    while (!op.msg->taken.load(std::memory_order_acquire)) {
+      if (!wait) return false;
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    if (wait) CK(cudaEventSynchronize(op.msg->consumed));
+    return cudaEventQuery(op.msg->consumed) == cudaSuccess;
+  }
+  if (wait) CK(cudaEventSynchronize(op.done));
+  return cudaEventQuery(op.done) == cudaSuccess;
+}
+cudaEvent_t send_event(const LinkOp& op) { return op.msg ? op.msg->consumed : op.done; }
+void release_send(LinkOp& op) {
+  if (op.msg) {
+    CK(cudaEventDestroy(op.msg->ready));
+    CK(cudaEventDestroy(op.msg->consumed));
+    op.msg.reset();
+  } else {
+    CK(cudaEventDestroy(op.done));
+  }
 }
 
 }  // namespace
@@ -1442,7 +1555,8 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
     if (m->l_begin != b || m->l_end != e || m->has_embed != (s == 0) || m->has_head != (s == P - 1))
       throw ValidationError("model is not stage " + std::to_string(s) + " of " + std::to_string(P));
   }
-  if (P > 1 && ((s + 1 < P && (!ctx->act_up || !ctx->grad_up)) || (s > 0 && (!ctx->act_down || !ctx->grad_down))))
+  if (P > 1 && !ctx->local &&
+      ((s + 1 < P && (!ctx->act_up || !ctx->grad_up)) || (s > 0 && (!ctx->act_down || !ctx->grad_down))))
     throw ValidationError("pipeline links not initialised (cf_ctx_init_pp)");
   const StagePlan sp = stage_plan(st, k, P);
   const std::vector<PpOp>& order = sp.orders[static_cast<size_t>(s)];
@@ -1452,11 +1566,10 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
   std::vector<LinkOp> sends;  // output buffers in flight to a neighbour
   auto reap = [&](bool all) {
     for (size_t i = 0; i < sends.size();) {
-      if (all) CK(cudaEventSynchronize(sends[i].done));
-      if (all || cudaEventQuery(sends[i].done) == cudaSuccess) {
-        CK(cudaStreamWaitEvent(ctx->stream, sends[i].done, 0));
+      if (send_complete(sends[i], all)) {
+        CK(cudaStreamWaitEvent(ctx->stream, send_event(sends[i]), 0));
         pool_free(ctx, sends[i].buf);
-        CK(cudaEventDestroy(sends[i].done));
+        release_send(sends[i]);
         sends[i] = sends.back();
         sends.pop_back();
       } else {
@@ -1493,7 +1606,8 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
     }
   }
   reap(true);
-  for (cudaEvent_t e : recv_done) CK(cudaEventDestroy(e));
+  for (cudaEvent_t e : recv_done)
+    if (e) CK(cudaEventDestroy(e));
   r.finish(res, true);
 }
 

@@ -37,6 +37,9 @@ struct Ctx {
   void* act_down = nullptr;  // receive activations from stage-1
   void* grad_down = nullptr; // send gradients to stage-1
   cudaStream_t link_stream[4] = {nullptr, nullptr, nullptr, nullptr};
+  // in-process pipeline (test transport): stages are contexts in one process
+  // exchanging stage-boundary buffers through host mailboxes + CUDA events
+  struct LocalPipe* local = nullptr;
   // per-launch CUDA-event timing (cf_ctx_set_profiling)
   bool profile = false;
   std::vector<cudaEvent_t> event_pool;
@@ -115,6 +118,13 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
 void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t stages, cf_step* st, int64_t k,
                        const cf_run_opts& opts, cf_run_result* res);
 void pp_init(Ctx* ctx, int rank, int world, int stages, const uint8_t* id128);
+// In-process links for cf_pp_step_run: every stage's context (one host thread
+// each) attaches to one LocalPipe; same op streams and buffer life cycle as
+// the NCCL links, with device-to-device copies instead of ncclSend/Recv.
+struct LocalPipe;
+LocalPipe* local_pipe_create(int stages);
+void local_pipe_destroy(LocalPipe* p);
+void pp_init_local(Ctx* ctx, LocalPipe* p, int stage);
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id128);
 void dp_unique_id(uint8_t* out128);

@@ -128,3 +128,60 @@ def test_pp_rank_path_one_stage_equals_step_run():
     st.close()
     m.close()
     c.close()
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[0] in ("toy-p2", "llama-p3-dh128", "llama-p4-k3")],
+                         ids=lambda c: c[0])
+def test_pp_rank_path_threads_bitwise(ctx, case):
+    """The per-rank stage runner (cf_pp_step_run) with P stages as P contexts,
+    each driven by its own host thread, exchanging activations / gradients
+    through in-process links (the NCCL links' op order and buffer life cycle
+    with device copies): loss and every gradient bitwise equal the unsplit
+    model.  A disagreement between the stages' op streams would deadlock and
+    surface as the links' receive timeout."""
+    import threading
+
+    _, arch, V, d, H, KVH, L, ffn, lengths, cs, k, P = case
+    cfg = cf.model_cfg(arch=arch, vocab=V, d=d, heads=H, kv_heads=KVH, layers=L, ffn=ffn, seed=7)
+    lengths = np.array(lengths, np.int64)
+    tokens = cf.gen_tokens(lengths, V, 11)
+    plan = cf.Plan.build(lengths, cs, k)
+    full = cf.Model(ctx, cfg)
+    st = cf.Step(full, plan, lengths, tokens)
+    ref = st.run()
+    ref_grads = _grads_by_name(full)
+    st.close()
+    full.close()
+
+    pipe = capi.LocalPipe(P)
+    ctxs = [cf.Context(0) for _ in range(P)]
+    models, steps, results, errors = [], [], [None] * P, []
+    for s_ in range(P):
+        ctxs[s_].init_pp_local(pipe, s_)
+        models.append(cf.Model(ctxs[s_], cfg, stage=s_, num_stages=P))
+        steps.append(cf.Step(models[s_], plan, lengths, tokens))
+
+    def work(s_):
+        try:
+            results[s_] = steps[s_].run_pp(k)
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    for _ in range(2):  # twice: no stale state across steps
+        threads = [threading.Thread(target=work, args=(s_,)) for s_ in range(P)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert not errors, errors
+        assert results[-1].loss == ref.loss
+        assert sum(r.kv_completeness_violations for r in results) == 0
+        assert results[-1].recompute_loss_mismatches == 0
+        for m in models:
+            for name, g in _grads_by_name(m).items():
+                assert np.array_equal(g, ref_grads[name]), name
+    for s_ in range(P):
+        steps[s_].close()
+        models[s_].close()
+        ctxs[s_].close()
+    pipe.close()
