@@ -104,6 +104,38 @@ __device__ __forceinline__ float stage_row_tmem(uint32_t taddr, const __nv_bfloa
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 constexpr int kThreads = 320;
+// dK/dV kernel: 16 softmax-side warps (4 per TMEM lane quarter, 16 query
+// columns each) + TMA + MMA; 576 threads cap registers at 96 per thread
+constexpr int kDkvThreads = 576;
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+// stage_row_tmem for 32 bf16 (16 TMEM columns)
+__device__ __forceinline__ void stage_row_tmem16(uint32_t taddr, const __nv_bfloat16* src, bool ok) {
+  uint32_t w[16];
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 v = ok ? __ldg(s4 + c) : make_uint4(0u, 0u, 0u, 0u);
+    w[4 * c] = v.x;
+    w[4 * c + 1] = v.y;
+    w[4 * c + 2] = v.z;
+    w[4 * c + 3] = v.w;
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+      : "memory");
+}
 
 // 16-byte chunk c (0..7) of row r in a [rows][64] SW128 box
 __device__ __forceinline__ uint32_t sw_off(int r, int c) {
@@ -346,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ------------------------------------------------------------- dK / dV
 // CTA = 128 keys x one kv head (sole owner of those rows); queries streamed
 // in 64-query sub-tiles over every q head of the GQA group.
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDkvThreads, 1)
     dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
   extern __shared__ uint8_t smem_raw[];
@@ -382,15 +414,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmO);
-    mbar_init(kv_full, 256);
+    mbar_init(kv_full, 512);
     for (int i = 0; i < QS; ++i) {
       mbar_init(&q_full[i], 2);  // TMA expect_tx arrive + LSE / D staged arrive
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 256);
+    mbar_init(s_free, 512);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&pds_full[i], 256);
+      mbar_init(&pds_full[i], 512);
       mbar_init(&pds_free[i], 1);
     }
     fence_mbar_init();
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bQf = smem_u32(q_full), bQe = smem_u32(q_empty), bSf = smem_u32(s_full),
                  bSr = smem_u32(s_free), bPf = smem_u32(pds_full), bPr = smem_u32(pds_free);
 
-  if (warp == 8) {
+  if (warp == 16) {
     // whole warp: lane 0 issues the Q / dO TMA, every lane stages two of the
     // 64 LSE / D values (plain loads: segment starts are not 16B-aligned)
     int qs = 0, hi = 0, qi = 0;  // ring slot, q head within the group, query sub-tile
@@ -440,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++qi == nqt) { qi = 0; ++hi; }
       if (++qs == QS) { qs = 0; ph ^= 1; }
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // whole warp, convergent (elect.sync inside the issue helpers)
     constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);  // S^T, dP^T: N = 64 queries
     constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);  // dV, dK: N = dh, B MN-major view
@@ -481,26 +513,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (++cs == QS) cs = 0;
     }
   } else {
-    const int quarter = warp & 3, half = warp >> 2;  // half: which 32 of the 64 query columns
+    const int quarter = warp & 3, part = warp >> 2;  // part: which 16 of the 64 query columns
     const int row = quarter * 32 + lane;                // key row within the tile
     const int key = key_first + row;
     const bool kok = row < tl.count && key < kv_len;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     {
       const int64_t r = sg.kv_row0 + key;
-      stage_row_tmem(tAk + lane_off + half * 32, a.k + r * a.kv_stride + static_cast<int64_t>(g) * DH + half * 64,
-                     kok);
-      stage_row_tmem(tAv + lane_off + half * 32, a.v + r * a.kv_stride + static_cast<int64_t>(g) * DH + half * 64,
-                     kok);
+      stage_row_tmem16(tAk + lane_off + part * 16, a.k + r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32,
+                       kok);
+      stage_row_tmem16(tAv + lane_off + part * 16, a.v + r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32,
+                       kok);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(kv_full);
     }
     // query index range this key row sees: [qlo, len) (qlo = INT_MAX: row absent)
     const int qlo = kok ? key - sg.prefix : INT_MAX;
-    uint32_t dst_off[4];
+    uint32_t dst_off[2];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
+    for (int c = 0; c < 2; ++c) dst_off[c] = sw_off(row, part * 2 + c);
     int qs = 0, qi = 0;
     uint32_t qph = 0;
     for (int it = 0; it < iters; ++it) {
@@ -508,18 +540,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int qt0 = i0 + qi * SUB;
       mbar_wait_s(bSf, it & 1);
       tc_fence_after();
-      uint32_t rs[32], rp[32];
-      tmem_ld32(tS + lane_off + half * 32, rs);
-      tmem_ld32(tP + lane_off + half * 32, rp);
+      uint32_t rs[16], rp[16];
+      tmem_ld16(tS + lane_off + part * 16, rs);
+      tmem_ld16(tP + lane_off + part * 16, rp);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive_s(bSr);
       mbar_wait_s(bQf + qs * 8, qph);  // LSE / D of this slot (already complete: S^T waited on it)
-      const uint32_t lrow = sLD0 + qs * 512 + half * 128;
-      uint32_t pp[16], pd[16];
+      const uint32_t lrow = sLD0 + qs * 512 + part * 64;
+      uint32_t pp[8], pd[8];
       auto body = [&](auto masked) {
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
+        for (int c4 = 0; c4 < 4; ++c4) {
           const float4 L = lds_f32x4(lrow + c4 * 16);
           const float4 Dv = lds_f32x4(lrow + 256 + c4 * 16);
           const float l[4] = {L.x * kLog2e, L.y * kLog2e, L.z * kLog2e, L.w * kLog2e};
@@ -530,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = c4 * 4 + u;
             p[u] = ex2(fmaf(__uint_as_float(rs[col]), a.sl2, -l[u]));
             if constexpr (decltype(masked)::value) {
-              const int qq = qt0 + half * 32 + col;
+              const int qq = qt0 + part * 16 + col;
               p[u] = (qq >= qlo && qq < sg.len) ? p[u] : 0.f;
             }
             ds[u] = p[u] * (__uint_as_float(rp[col]) - d[u]);
@@ -549,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (it >= 2) mbar_wait_s(bPr + b * 8, ((it >> 1) & 1) ^ 1);
       const uint32_t dP_ = sP0 + b * kBox128, dS_ = sS0 + b * kBox128;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         sts128(dP_ + dst_off[c], make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]));
         sts128(dS_ + dst_off[c], make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
       }
@@ -563,9 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     float* dkr = a.dk_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
     float* dvr = a.dv_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
-#pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
-      const int c = half * 2 + cc;
+    {
+      const int c = part;  // 32-column chunk of dK / dV
       uint32_t rk[32], rv[32];
       tmem_ld32(tdK + lane_off + c * 32, rk);
       tmem_ld32(tdV + lane_off + c * 32, rv);
@@ -649,7 +680,7 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
   dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   a.tiles = ktiles128;
-  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kThreads, smem_dkv, st>>>(q64, o64, k128, v128, a);
+  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, k128, v128, a);
   return cudaGetLastError();
 }
 
