@@ -130,7 +130,10 @@ typedef struct cf_run_result {
   double model_flops;        /* algorithmic FLOPs (no recompute) */
   double hw_flops;           /* incl. recompute */
   /* per-kernel-class device time, filled when cf_ctx_set_profiling(ctx,1):
-   * CUDA events on the context stream around every launch of the class */
+   * CUDA events around every launch of the class on the stream it runs on;
+   * *_ms is the union of those intervals (time with >= 1 launch of the
+   * class in flight), so overlapping side-stream launches are not counted
+   * twice */
   double gemm_ms, gemm_flops;
   int64_t gemm_launches;
   double attn_ms, attn_flops; /* attention forward */

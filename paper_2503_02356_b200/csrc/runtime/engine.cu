@@ -695,16 +695,16 @@ struct Exec {
     }
     return ctx->event_pool[ev_used++];
   }
-  cudaEvent_t mark() {
+  cudaEvent_t mark(cudaStream_t on = nullptr) {
     if (!ctx->profile) return nullptr;
     cudaEvent_t a = ev();
-    CK(cudaEventRecord(a, s));
+    CK(cudaEventRecord(a, on ? on : s));
     return a;
   }
-  void close(cudaEvent_t a, int cls, double flops, int n) {
+  void close(cudaEvent_t a, int cls, double flops, int n, cudaStream_t on = nullptr) {
     if (!ctx->profile) return;
     cudaEvent_t b = ev();
-    CK(cudaEventRecord(b, s));
+    CK(cudaEventRecord(b, on ? on : s));
     recs.push_back({a, b, cls, flops, n});
   }
   void gemm(const void* a, int a_k, int64_t lda, const void* b, int b_k, int64_t ldb, void* c, int64_t ldc, int64_t M,
@@ -1212,14 +1212,32 @@ struct StageRunner {
     CK(cudaMemcpyAsync(slots.data(), ex.loss_slots, static_cast<size_t>(nslots + 1) * 8, cudaMemcpyDeviceToHost,
                        ex.s));
     CK(cudaStreamSynchronize(ex.s));
+    // per-class device time = union of the class's launch intervals (the
+    // time during which at least one launch of the class was in flight);
+    // equals the plain sum for launches serialised on one stream
     double cls_ms[3] = {0, 0, 0}, cls_flops[3] = {0, 0, 0};
     int64_t cls_n[3] = {0, 0, 0};
+    std::vector<std::pair<double, double>> iv[3];
     for (const auto& r : ex.recs) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, r.a, r.b));
-      cls_ms[r.cls] += ms;
+      float t0 = 0, t1 = 0;
+      CK(cudaEventElapsedTime(&t0, ex.recs.front().a, r.a));
+      CK(cudaEventElapsedTime(&t1, ex.recs.front().a, r.b));
+      iv[r.cls].emplace_back(t0, t1);
       cls_flops[r.cls] += r.flops;
       cls_n[r.cls] += r.n;
+    }
+    for (int c = 0; c < 3; ++c) {
+      std::sort(iv[c].begin(), iv[c].end());
+      double end = -1e300;
+      for (const auto& [a0, a1] : iv[c]) {
+        if (a0 >= end) {
+          cls_ms[c] += a1 - a0;
+          end = a1;
+        } else if (a1 > end) {
+          cls_ms[c] += a1 - end;
+          end = a1;
+        }
+      }
     }
     for (const OpMark& mk : marks) {
       float ms = 0;
