@@ -185,3 +185,25 @@ def test_pp_rank_path_threads_bitwise(ctx, case):
         models[s_].close()
         ctxs[s_].close()
     pipe.close()
+
+
+def test_reference_cli_artifacts_run_on_gpu(ctx, reference):
+    """Drop-in flow: the reference's `pack` artefacts (chunk_plan.json from
+    chunk_plan_to_json, dataset.jsonl from write_records) read by the product
+    and executed on the GPU give the same loss and gradients as the plan the
+    product builds from the batch directly."""
+    from oracle.oracle import c1_batch, Oracle
+    lengths, tokens = c1_batch(Oracle())
+    doc = reference.plan_json(lengths, 512, 2, 0)
+    offs = np.concatenate([[0], np.cumsum(lengths)])
+    jsonl = "".join('{"id":%d,"length":%d,"tokens":[%s]}\n' % (i, n, ",".join(map(str, tokens[offs[i]:offs[i + 1]])))
+                    for i, n in enumerate(lengths))
+    ids, lens, has, tok = capi.dataset_load_jsonl(jsonl)
+    assert has.all() and np.array_equal(lens, lengths) and np.array_equal(tok, tokens)
+    cfg = cf.model_cfg(arch=0, vocab=256, d=256, heads=4, kv_heads=2, layers=2, seed=1)
+    m = cf.Model(ctx, cfg)
+    r1 = m.run_plan(cf.Plan.from_chunk_json(doc, 2), lens, tok, ids)
+    g1 = m.grads_flat()
+    r2 = m.run_plan(cf.Plan.build(lengths, 512, 2), lengths, tokens)
+    assert r1.loss == r2.loss and np.array_equal(g1, m.grads_flat())
+    m.close()
