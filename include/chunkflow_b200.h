@@ -282,6 +282,28 @@ int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages,
  * from cf_step_op_times): format 0 = chrome-trace JSON, 1 = table Gantt. */
 int cf_pp_export_trace(const cf_pp_op* ops, int64_t num_stages, int64_t ops_per_stage,
                        int format, char* buf, size_t cap, size_t* len);
+/* grid_search (tuner.hpp:39-112) over chunk_sizes x ks on batches sampled
+ * from the sequence set (ids/lengths): state-aware 1F1B makespan (cost
+ * model) averaged over batches_to_sample batches, feasibility from the memory
+ * model at the longest sampled sequence vs budget_gib.  Writes ncs x nk rows
+ * (chunk-size-major), the best (chunk_size, k) (-1 when none is feasible),
+ * the number of simulations, and optionally the reference's CSV table
+ * (csv = 1, tuner_table_csv) or ranked report (csv = 0, tuner_report) text. */
+typedef struct cf_tune_row {
+  int64_t chunk_size;
+  int64_t k;
+  double mean_time;
+  double predicted_peak_gib;
+  int64_t feasible;
+} cf_tune_row;
+int cf_tune_grid_search(const int64_t* ids, const int64_t* lengths, int64_t n,
+                        const int64_t* chunk_sizes, int64_t ncs, const int64_t* ks,
+                        int64_t nk, int64_t num_stages, const cf_pp_cost* cost,
+                        const cf_mem_coeffs* mem, double budget_gib,
+                        int64_t global_batch_size, int64_t batches_to_sample,
+                        uint64_t seed, cf_tune_row* table, int64_t* best_chunk_size,
+                        int64_t* best_k, int64_t* evaluations, int csv, char* buf,
+                        size_t cap, size_t* len);
 /* Layer range [begin, end) that stage `stage` of `num_stages` executes. */
 int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages,
                        int64_t* begin, int64_t* end);

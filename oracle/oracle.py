@@ -313,6 +313,19 @@ class Reference(_Lib):
             C.c_int(mode), C.c_int(0 if chrome else 1), b, c, n))
 
 
+    def tune(self, lengths, css, ks, stages, cost, mem, budget, gbs, nb, seed, csv=True, ids=None):
+        lengths = np.ascontiguousarray(lengths, np.int64)
+        ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+        css = np.ascontiguousarray(css, np.int64)
+        ks = np.ascontiguousarray(ks, np.int64)
+        c5 = np.ascontiguousarray(cost, np.float64)
+        m4 = np.ascontiguousarray(mem, np.float64)
+        return self._text(lambda b, c, n: self.lib.cfr_tune(
+            _p(ids, PI64), _p(lengths, PI64), I64(len(lengths)), _p(css, PI64), I64(len(css)), _p(ks, PI64),
+            I64(len(ks)), I64(stages), _p(c5, PD), _p(m4, PD), C.c_double(budget), I64(gbs), I64(nb),
+            C.c_uint64(seed), C.c_int(int(csv)), b, c, n))
+
+
 def c1_batch(oracle: Oracle):
     """Config C1 canonical batch: synthesize(eval_table5, 32,
     seed=3) plus sequence id 32 of 2048 tokens; tokens SplitMix64(5)."""

@@ -12,6 +12,7 @@
 #include <chunkflow/pipeline.hpp>
 #include <chunkflow/plan_runner.hpp>
 #include <chunkflow/scheduler.hpp>
+#include <chunkflow/tuner.hpp>
 #include <chunkflow/toy_model.hpp>
 
 #include <cstring>
@@ -422,5 +423,32 @@ extern "C" int cfr_export_trace(const int64_t* ids, const int64_t* lengths, int6
       tr = cf::simulate_state_aware_1f1b(cf::construct_chunks(make_batch(ids, lengths, n, nullptr), cs), pc, cm);
     }
     put(cf::export_trace(tr, format == 0 ? cf::TraceFormat::kChromeTrace : cf::TraceFormat::kTable), buf, cap, len);
+  });
+}
+
+// grid_search + its CSV table and ranked report (tuner.hpp)
+extern "C" int cfr_tune(const int64_t* ids, const int64_t* lengths, int64_t n, const int64_t* css, int64_t ncs,
+                        const int64_t* ks, int64_t nk, int64_t stages, const double* cost5, const double* mem4,
+                        double budget, int64_t gbs, int64_t nb, uint64_t seed, int csv, char* buf, size_t cap,
+                        size_t* len) {
+  return guarded([&] {
+    cf::SequenceSet set = make_batch(ids, lengths, n, nullptr).sequences;
+    cf::PipelineConfig pc;
+    pc.num_stages = static_cast<int>(stages);
+    cf::CostModel cm;
+    cm.gamma = cost5[0];
+    cm.alpha = cost5[1];
+    cm.beta = cost5[2];
+    cm.backward_multiplier = cost5[3];
+    cm.hop_latency = cost5[4];
+    cf::MemoryModelCoefficients mc;
+    mc.base = mem4[0];
+    mc.per_chunk_token = mem4[1];
+    mc.per_context_token = mem4[2];
+    mc.gqa_ratio = mem4[3];
+    const cf::TunerResult r = cf::grid_search(set, std::vector<std::int64_t>(css, css + ncs),
+                                              std::vector<std::int64_t>(ks, ks + nk), pc, cm, mc, budget, gbs, nb,
+                                              seed);
+    put(csv ? cf::tuner_table_csv(r) : cf::tuner_report(r), buf, cap, len);
   });
 }

@@ -95,7 +95,7 @@ EXPORTS = [
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
     "cf_pp_run_local", "cf_step_op_times", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
-    "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
 
 _lib = None
@@ -275,6 +275,33 @@ def pp_export_trace(ops, chrome=True) -> str:
     st, per = ops.shape
     return _text(lambda buf, cap, n: lib().cf_pp_export_trace(_p(ops), C.c_int64(st), C.c_int64(per),
                                                               C.c_int(0 if chrome else 1), buf, cap, n))
+
+
+TUNE_ROW_DT = np.dtype([("chunk_size", np.int64), ("k", np.int64), ("mean_time", np.float64),
+                        ("predicted_peak_gib", np.float64), ("feasible", np.int64)])
+
+
+def tune_grid_search(lengths, chunk_sizes, ks, stages, cost=None, mem=None, budget_gib=80.0, global_batch_size=256,
+                     batches_to_sample=4, seed=0, ids=None, text="report"):
+    """grid_search (tuner.hpp:39): returns (table, best_cs, best_k, evaluations, text);
+    text = "report" (tuner_report) or "csv" (tuner_table_csv)."""
+    lengths = np.ascontiguousarray(lengths, np.int64)
+    ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+    css = np.ascontiguousarray(chunk_sizes, np.int64)
+    kk = np.ascontiguousarray(ks, np.int64)
+    c = _pp_cost(cost)
+    m = mem if isinstance(mem, MemCoeffs) else MemCoeffs(*(mem or (0.0, 0.0, 0.0, 1.0)))
+    table = np.zeros(len(css) * len(kk), TUNE_ROW_DT)
+    bc, bk, ev = C.c_int64(), C.c_int64(), C.c_int64()
+
+    def call(buf, cap, n):
+        return lib().cf_tune_grid_search(_p(ids), _p(lengths), C.c_int64(len(lengths)), _p(css), C.c_int64(len(css)),
+                                         _p(kk), C.c_int64(len(kk)), C.c_int64(stages), C.byref(c), C.byref(m),
+                                         C.c_double(budget_gib), C.c_int64(global_batch_size),
+                                         C.c_int64(batches_to_sample), C.c_uint64(seed), _p(table), C.byref(bc),
+                                         C.byref(bk), C.byref(ev), C.c_int(int(text == "csv")), buf, cap, n)
+    txt = _text(call)
+    return table, bc.value, bk.value, ev.value, txt
 
 
 def pp_stage_layers(layers, stage, stages):

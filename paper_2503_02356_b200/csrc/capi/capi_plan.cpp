@@ -376,3 +376,25 @@ extern "C" int cf_pp_export_trace(const cf_pp_op* ops, int64_t num_stages, int64
     put_text(cfb::export_trace(st, format == 0), buf, cap, len);
   });
 }
+
+extern "C" int cf_tune_grid_search(const int64_t* ids, const int64_t* lengths, int64_t n, const int64_t* chunk_sizes,
+                                   int64_t ncs, const int64_t* ks, int64_t nk, int64_t num_stages,
+                                   const cf_pp_cost* cost, const cf_mem_coeffs* mem, double budget_gib,
+                                   int64_t global_batch_size, int64_t batches_to_sample, uint64_t seed,
+                                   cf_tune_row* table, int64_t* best_chunk_size, int64_t* best_k,
+                                   int64_t* evaluations, int csv, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] {
+    if (n < 0 || ncs < 0 || nk < 0 || !mem) throw cfb::ValidationError("bad tuner arguments");
+    const cfb::TuneResult r = cfb::grid_search(
+        std::vector<int64_t>(ids, ids + n), std::vector<int64_t>(lengths, lengths + n),
+        std::vector<int64_t>(chunk_sizes, chunk_sizes + ncs), std::vector<int64_t>(ks, ks + nk), num_stages,
+        to_cost(cost), from_c(mem), budget_gib, global_batch_size, batches_to_sample, seed);
+    for (size_t i = 0; table && i < r.table.size(); ++i)
+      table[i] = {r.table[i].chunk_size, r.table[i].k, r.table[i].mean_time, r.table[i].predicted_peak_gib,
+                  r.table[i].feasible ? 1 : 0};
+    if (best_chunk_size) *best_chunk_size = r.has_best ? r.best_chunk_size : -1;
+    if (best_k) *best_k = r.has_best ? r.best_k : -1;
+    if (evaluations) *evaluations = r.evaluations;
+    if (buf || len) put_text(csv ? cfb::tuner_table_csv(r) : cfb::tuner_report(r), buf, cap, len);
+  });
+}

@@ -3,9 +3,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <limits>
 #include <set>
 #include <stdexcept>
+
+#include "wire.hpp"
 
 namespace cfb {
 
@@ -161,6 +164,111 @@ void pp_stage_layers(int64_t layers, int64_t stage, int64_t stages, int64_t* beg
   if (layers < stages) throw ValidationError("fewer layers than pipeline stages");
   *begin = layers * stage / stages;
   *end = layers * (stage + 1) / stages;
+}
+
+}  // namespace cfb
+
+// ------------------------------------------------------------------ tuner
+namespace cfb {
+
+TuneResult grid_search(const std::vector<int64_t>& ids, const std::vector<int64_t>& lengths,
+                       const std::vector<int64_t>& chunk_sizes, const std::vector<int64_t>& ks, int64_t stages,
+                       const PpCost& cost, const MemCoeffs& mem, double budget_gib, int64_t global_batch_size,
+                       int64_t batches_to_sample, uint64_t seed) {
+  if (chunk_sizes.empty() || ks.empty()) throw ValidationError("tuner grid must not be empty");
+  if (budget_gib <= 0) throw ValidationError("memory budget must be positive");
+  if (batches_to_sample < 1) throw ValidationError("batches_to_sample must be at least 1");
+  if (lengths.empty()) throw ValidationError("cannot tune on an empty sequence set");
+  if (global_batch_size < 1) throw ValidationError("global batch size must be at least 1");
+  cost.validate();
+  if (mem.base < 0 || mem.per_chunk_token < 0 || mem.per_context_token < 0 || mem.gqa_ratio < 0)
+    throw ValidationError("memory-model coefficients must be non-negative");
+  if (stages < 1) throw ValidationError("num_stages must be at least 1");
+  const int64_t n = static_cast<int64_t>(lengths.size());
+  const int64_t steps = (n + global_batch_size - 1) / global_batch_size;
+  std::vector<std::pair<std::vector<int64_t>, std::vector<int64_t>>> batches;  // (ids, lengths)
+  int64_t max_len = 0;
+  for (int64_t t = 0; t < batches_to_sample; ++t) {
+    const std::vector<int64_t> idx = sample_batch(n, global_batch_size, t % steps, seed);
+    if (idx.empty()) break;
+    std::vector<int64_t> bi, bl;
+    for (int64_t i : idx) {
+      bi.push_back(ids[static_cast<size_t>(i)]);
+      bl.push_back(lengths[static_cast<size_t>(i)]);
+      max_len = std::max(max_len, lengths[static_cast<size_t>(i)]);
+    }
+    batches.emplace_back(std::move(bi), std::move(bl));
+  }
+  TuneResult r;
+  for (int64_t cs : chunk_sizes)
+    for (int64_t k : ks) {
+      const int64_t k_eff = stages == 1 ? 1 : k;
+      TuneRow row;
+      row.chunk_size = cs;
+      row.k = k;
+      row.predicted_peak_gib = predict_peak(mem, cs, k_eff, max_len);
+      row.feasible = row.predicted_peak_gib <= budget_gib;
+      double total = 0.0;
+      for (const auto& [bi, bl] : batches) {
+        const Plan plan = construct_chunks(bi.data(), bl.data(), static_cast<int64_t>(bi.size()), cs);
+        const PpChunks info = pp_chunks(plan, k_eff, cost);
+        std::vector<std::vector<PpOp>> orders;
+        for (int64_t s = 0; s < stages; ++s) orders.push_back(pp_stage_order(info, s, stages, true));
+        total += pp_dispatch(orders, info.fwd, info.bwd, cost.hop).makespan;
+        ++r.evaluations;
+      }
+      row.mean_time = total / static_cast<double>(batches.size());
+      r.table.push_back(row);
+    }
+  const TuneRow* best = nullptr;
+  for (const TuneRow& c : r.table) {
+    if (!c.feasible) continue;
+    if (!best || c.mean_time < best->mean_time ||
+        (c.mean_time == best->mean_time &&
+         (c.chunk_size > best->chunk_size || (c.chunk_size == best->chunk_size && c.k < best->k))))
+      best = &c;
+  }
+  if (best) {
+    r.has_best = true;
+    r.best_chunk_size = best->chunk_size;
+    r.best_k = best->k;
+  }
+  return r;
+}
+
+namespace {
+std::string fixed(double v, int prec) {
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.*f", prec, v);
+  return buf;
+}
+}  // namespace
+
+std::string tuner_table_csv(const TuneResult& r) {
+  std::string out = "chunk_size,k,mean_time,predicted_peak_gib,feasible\n";
+  for (const TuneRow& row : r.table)
+    out += std::to_string(row.chunk_size) + "," + std::to_string(row.k) + "," + fixed(row.mean_time, 6) + "," +
+           fixed(row.predicted_peak_gib, 3) + "," + (row.feasible ? "1" : "0") + "\n";
+  return out;
+}
+
+std::string tuner_report(const TuneResult& r) {
+  std::vector<TuneRow> ranked = r.table;
+  std::stable_sort(ranked.begin(), ranked.end(), [](const TuneRow& a, const TuneRow& b) {
+    if (a.feasible != b.feasible) return a.feasible;
+    if (a.mean_time != b.mean_time) return a.mean_time < b.mean_time;
+    if (a.chunk_size != b.chunk_size) return a.chunk_size > b.chunk_size;
+    return a.k < b.k;
+  });
+  std::string out = r.has_best ? "best: chunk_size=" + std::to_string(r.best_chunk_size) +
+                                     " k=" + std::to_string(r.best_k) + "\n"
+                               : std::string("no feasible configuration\n");
+  out += "evaluations: " + std::to_string(r.evaluations) + "\n";
+  for (const TuneRow& row : ranked)
+    out += "chunk_size=" + std::to_string(row.chunk_size) + " k=" + std::to_string(row.k) +
+           " mean_time=" + fixed(row.mean_time, 3) + " predicted_peak_gib=" + fixed(row.predicted_peak_gib, 3) +
+           (row.feasible ? " feasible" : " infeasible") + "\n";
+  return out;
 }
 
 }  // namespace cfb

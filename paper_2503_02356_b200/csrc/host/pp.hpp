@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
 #include "plan.hpp"
@@ -73,5 +74,33 @@ double pp_bubble(const PpTrace& t);
 // Layer range [begin, end) of a stage under the even split the executor
 // uses (embedding on stage 0; final norm + head + loss on the last stage).
 void pp_stage_layers(int64_t layers, int64_t stage, int64_t stages, int64_t* begin, int64_t* end);
+
+}  // namespace cfb
+
+namespace cfb {
+
+// grid_search (tuner.hpp:39-112): for every (chunk_size, k) candidate, chunk
+// the same sampled batches (sample_batch, dataset.hpp:242), time them with
+// the state-aware 1F1B simulator and average the makespan; feasibility from
+// the linear memory model at the longest sampled sequence (memory_model.hpp:
+// 47).  k is forced to 1 with one stage.  Ties prefer larger chunk_size,
+// then smaller k.
+struct TuneRow {
+  int64_t chunk_size = 0, k = 1;
+  double mean_time = 0.0, predicted_peak_gib = 0.0;
+  bool feasible = false;
+};
+struct TuneResult {
+  bool has_best = false;
+  int64_t best_chunk_size = 0, best_k = 0, evaluations = 0;
+  std::vector<TuneRow> table;
+};
+struct MemCoeffs;
+TuneResult grid_search(const std::vector<int64_t>& ids, const std::vector<int64_t>& lengths,
+                       const std::vector<int64_t>& chunk_sizes, const std::vector<int64_t>& ks, int64_t stages,
+                       const PpCost& cost, const MemCoeffs& mem, double budget_gib, int64_t global_batch_size,
+                       int64_t batches_to_sample, uint64_t seed);
+std::string tuner_table_csv(const TuneResult& r);  // tuner.hpp:114-124
+std::string tuner_report(const TuneResult& r);     // tuner.hpp:126-150
 
 }  // namespace cfb

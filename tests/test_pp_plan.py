@@ -160,3 +160,54 @@ def test_export_trace_matches_reference(reference, oracle, chrome):
         doc = json.loads(capi.pp_export_trace(ops, True))
         assert doc["traceEvents"][0] == {"dur": 1000, "name": "F chunk0", "ph": "X", "pid": 0, "tid": 0, "ts": 0}
         assert capi.pp_export_trace(np.zeros((0, 0), capi.PP_OP_DT), True) == '{\n  "traceEvents": []\n}\n'
+
+
+def _tune_both(reference, lengths, css, ks, stages, cost, mem, budget, gbs, nb, seed):
+    c = dict(zip(("gamma", "alpha", "beta", "backward_multiplier", "hop_latency"), cost))
+    out = []
+    for text in ("csv", "report"):
+        table, bc, bk, ev, txt = capi.tune_grid_search(lengths, css, ks, stages, c, mem, budget, gbs, nb, seed,
+                                                       text=text)
+        assert txt == reference.tune(lengths, css, ks, stages, cost, mem, budget, gbs, nb, seed, csv=text == "csv")
+        out.append((table, bc, bk, ev))
+    return out[0]
+
+
+def test_tuner_worked_batch(reference):
+    """test_tuner.cpp: worked batch, 4 stages, budget grid {2,4} x {1,2}: best (2, 2); 54 / 46 / 60 / 60."""
+    table, bc, bk, ev = _tune_both(reference, [1, 1, 2, 4], [2, 4], [1, 2], 4, (0.0, 1.0, 0.0, 2.0, 0.0),
+                                   (0.0, 0.0, 0.0, 1.0), 1e9, 4, 1, 1)
+    assert (bc, bk, ev) == (2, 2, 4)
+    assert table["mean_time"].tolist() == [54.0, 46.0, 60.0, 60.0]
+    # single stage forces k = 1; memory budget 5 with peak = k * cs
+    table, bc, bk, ev = _tune_both(reference, [3, 5, 2, 7, 4, 6], [2, 4, 8], [1, 2, 4], 1,
+                                   (1.0, 1.0, 0.0, 2.0, 0.0), (0.0, 1.0, 0.0, 1.0), 5.0, 6, 1, 1)
+    assert (bc, bk) == (4, 1) and not table[(table["chunk_size"] == 8) & (table["k"] == 1)]["feasible"][0]
+    # nothing feasible
+    _, bc, bk, _ = _tune_both(reference, [1, 1, 2, 4], [2, 4], [1, 2], 4, (0.0, 1.0, 0.0, 2.0, 0.0),
+                              (10.0, 0.0, 0.0, 1.0), 1.0, 4, 1, 1)
+    assert (bc, bk) == (-1, -1)
+
+
+def test_tuner_random_and_c1(reference, oracle):
+    lengths, _ = c1_batch(oracle)
+    _tune_both(reference, lengths, [256, 512, 1024], [1, 2, 4], 4, (0.5, 1.0, 1.05e-5, 2.0, 1.0),
+               (34.87, 2.9e-3, 1.7e-5, 0.25), 60.0, 16, 3, 5)
+    rng = np.random.default_rng(17)
+    for _ in range(15):
+        n = int(rng.integers(1, 60))
+        lens = rng.integers(1, 3000, n)
+        css = sorted(set(int(x) for x in rng.integers(16, 2048, int(rng.integers(1, 4)))))
+        ks = sorted(set(int(x) for x in rng.integers(1, 5, int(rng.integers(1, 3)))))
+        _tune_both(reference, lens, css, ks, int(rng.integers(1, 6)),
+                   (float(rng.random()), 1.0, float(rng.random()) * 1e-4, 2.0, float(rng.random())),
+                   (float(rng.random()) * 40, 1e-3, 1e-5, 1.0), float(rng.random()) * 60 + 1,
+                   int(rng.integers(1, n + 3)), int(rng.integers(1, 5)), int(rng.integers(0, 100)))
+
+
+def test_tuner_validation():
+    for kw in (dict(chunk_sizes=[]), dict(budget_gib=0.0), dict(batches_to_sample=0)):
+        args = dict(lengths=[1, 2, 3], chunk_sizes=[2], ks=[1], stages=2)
+        args.update(kw)
+        with pytest.raises(capi.CfError):
+            capi.tune_grid_search(**args)

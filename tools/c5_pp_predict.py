@@ -120,6 +120,50 @@ def main():
     _, _, _, p1 = capi.pp_simulate_1f1b(r0_lengths, STAGES, {"alpha": 1.0, "beta": 1.05e-5})
     out["prediction"] = res
     out["reference_1f1b_whole_sequence_bubble_cost_model"] = p1.bubble_ratio
+    # simulator-in-the-loop: fit the reference CostModel
+    # fwd = gamma + alpha*len + beta*(len^2 + len*prefix) to the measured
+    # last-stage forward times, backward_multiplier = mean(bwd / fwd), then
+    # grid_search (tuner.hpp:39) over (chunk_size, K) with those costs and a
+    # per-stage memory model measured on the same 16-layer stage
+    ch0 = replicas[0].export()[0]
+    seg0 = replicas[0].export()[1]
+    pre = {}
+    for c in ch0:
+        if c["kind"] == 1:
+            s0 = seg0[c["seg_offset"]]
+            pre[int(c["chunk_id"])] = int(s0["start_token"])
+    X, y, ratio = [], [], []
+    for c in ch0:
+        cid = int(c["chunk_id"])
+        if cid not in fw or cid not in bw:
+            continue
+        ln, p_ = float(c["total_tokens"]), float(pre.get(cid, 0))
+        f_ms = fw[cid][0] * per_stage + fw[cid][1]
+        b_ms = bw[cid][0] * per_stage + bw[cid][1]
+        X.append([1.0, ln, ln * ln + ln * p_])
+        y.append(f_ms)
+        ratio.append(b_ms / f_ms)
+    coef, *_ = np.linalg.lstsq(np.array(X), np.array(y), rcond=None)
+    gamma, alpha, beta = (max(0.0, float(v)) for v in coef)
+    bmult = float(np.mean(ratio))
+    fit = {"gamma_ms": gamma, "alpha_ms_per_token": alpha, "beta_ms_per_token2": beta,
+           "backward_multiplier": bmult, "chunks_fitted": len(y),
+           "max_rel_residual": float(np.max(np.abs(np.array(X) @ np.array([gamma, alpha, beta]) - np.array(y))
+                                        / np.array(y)))}
+    GIB = float(1 << 30)
+    stage_static = r16.static_hbm_bytes / GIB
+    per_tok = r16.act_hbm_bytes / GIB / CHUNK  # K=1 retained tape of one 16K chunk
+    per_ctx = 16 * 1024 * 12 / GIB             # K/V bf16 + dK/dV fp32 per context token, 16 layers
+    mem = (stage_static, per_tok, per_ctx, 1.0)
+    table, bc, bk, ev, report = capi.tune_grid_search(
+        lengths[:len(blocks[0])], [4096, 8192, 16384, 32768], [1, 2, 4], STAGES,
+        {"gamma": gamma, "alpha": alpha, "beta": beta, "backward_multiplier": bmult, "hop_latency": 0.0},
+        mem, 165.0, 1000, 1, 0)
+    out["cost_model_fit"] = fit
+    out["tuner"] = {"memory_model": dict(zip(("base_gib", "per_chunk_token_gib", "per_context_token_gib",
+                                              "gqa_ratio"), mem)),
+                    "budget_gib": 165.0, "best_chunk_size": bc, "best_k": bk, "evaluations": ev,
+                    "report": report}
     out["tokens_global"] = int(lengths.sum())
     print(json.dumps(out), flush=True)
 
