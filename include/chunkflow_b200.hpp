@@ -263,6 +263,130 @@ inline PipelineTrace simulate_1f1b(const std::vector<int64_t>& lengths, int num_
 // bubble_ratio (pipeline.hpp:325): recompute forwards count as bubble.
 inline double bubble_ratio(const PipelineTrace& t) { return t.bubble; }
 
+// --- tuner.hpp / memory_model.hpp / wire formats (chunker.hpp:233-292,
+//     scheduler.hpp:300-328, dataset.hpp:112-176)
+struct MemoryModelCoefficients {  // memory_model.hpp:20-33
+  double base = 0.0, per_chunk_token = 0.0, per_context_token = 0.0, gqa_ratio = 1.0;
+};
+struct MemoryMeasurement {  // memory_model.hpp:13-18
+  int64_t chunk_size = 0, k = 1, context_len = 0;
+  double peak_gib = 0.0;
+};
+struct CalibrationResult {
+  MemoryModelCoefficients coefficients;
+  double max_residual_gib = 0.0;
+};
+inline double predict_peak(const MemoryModelCoefficients& c, int64_t chunk_size, int64_t k, int64_t context_len) {
+  const cf_mem_coeffs m{c.base, c.per_chunk_token, c.per_context_token, c.gqa_ratio};
+  double out = 0.0;
+  check(cf_mem_predict(&m, chunk_size, k, context_len, &out));
+  return out;
+}
+inline CalibrationResult calibrate(const std::vector<MemoryMeasurement>& ms, double gqa_ratio = 1.0) {
+  std::vector<int64_t> cs, k, ctx;
+  std::vector<double> pk;
+  for (const MemoryMeasurement& m : ms) {
+    cs.push_back(m.chunk_size);
+    k.push_back(m.k);
+    ctx.push_back(m.context_len);
+    pk.push_back(m.peak_gib);
+  }
+  cf_mem_coeffs c{};
+  CalibrationResult r;
+  check(cf_mem_calibrate(cs.data(), k.data(), ctx.data(), pk.data(), static_cast<int64_t>(ms.size()), gqa_ratio, &c,
+                         &r.max_residual_gib));
+  r.coefficients = {c.base_gib, c.per_chunk_token_gib, c.per_context_token_gib, c.gqa_ratio};
+  return r;
+}
+
+struct TunerCandidate {  // tuner.hpp:18-24
+  int64_t chunk_size = 0, k = 1;
+  double mean_time = 0.0, predicted_peak_gib = 0.0;
+  bool feasible = false;
+};
+struct TunerResult {  // tuner.hpp:26-32
+  bool has_best = false;
+  int64_t best_chunk_size = 0, best_k = 0, evaluations = 0;
+  std::vector<TunerCandidate> table;
+  std::string report;  // tuner_report(result)
+};
+// grid_search (tuner.hpp:39)
+inline TunerResult grid_search(const SequenceSet& set, const std::vector<int64_t>& chunk_sizes,
+                               const std::vector<int64_t>& ks, const PipelineConfig& cfg, const CostModel& cost,
+                               const MemoryModelCoefficients& mem, double budget_gib, int64_t global_batch_size,
+                               int64_t batches_to_sample, uint64_t seed) {
+  std::vector<int64_t> ids, lengths;
+  for (const SequenceRecord& r : set) {
+    ids.push_back(r.id);
+    lengths.push_back(r.length);
+  }
+  const cf_pp_cost c = detail::to_cost(cost);
+  const cf_mem_coeffs m{mem.base, mem.per_chunk_token, mem.per_context_token, mem.gqa_ratio};
+  std::vector<cf_tune_row> rows(chunk_sizes.size() * ks.size());
+  int64_t bc = -1, bk = -1, ev = 0;
+  size_t len = 0;
+  auto call = [&](char* buf, size_t cap) {
+    check(cf_tune_grid_search(ids.data(), lengths.data(), static_cast<int64_t>(ids.size()), chunk_sizes.data(),
+                              static_cast<int64_t>(chunk_sizes.size()), ks.data(), static_cast<int64_t>(ks.size()),
+                              cfg.num_stages, &c, &m, budget_gib, global_batch_size, batches_to_sample, seed,
+                              rows.data(), &bc, &bk, &ev, 0, buf, cap, &len));
+  };
+  call(nullptr, 0);
+  std::string text(len + 1, '\0');
+  call(&text[0], text.size());
+  text.resize(len);
+  TunerResult r;
+  r.has_best = bc >= 0;
+  r.best_chunk_size = r.has_best ? bc : 0;
+  r.best_k = r.has_best ? bk : 0;
+  r.evaluations = ev;
+  for (const cf_tune_row& x : rows) r.table.push_back({x.chunk_size, x.k, x.mean_time, x.predicted_peak_gib, x.feasible != 0});
+  r.report = std::move(text);
+  return r;
+}
+
+namespace detail {
+template <class F>
+inline std::string text_of(F&& f) {
+  size_t len = 0;
+  check(f(nullptr, 0, &len));
+  std::string s(len + 1, '\0');
+  check(f(&s[0], s.size(), &len));
+  s.resize(len);
+  return s;
+}
+}  // namespace detail
+
+// chunk_plan_to_json(plan).dump(2) + "\n" (chunker.hpp:233) / execution_plan_to_json (scheduler.hpp:300)
+inline std::string chunk_plan_json(const ExecutionPlan& plan) {
+  return detail::text_of([&](char* b, size_t c, size_t* l) { return cf_plan_chunk_json(plan.handle->get(), b, c, l); });
+}
+inline std::string execution_plan_json(const ExecutionPlan& plan) {
+  return detail::text_of([&](char* b, size_t c, size_t* l) { return cf_plan_exec_json(plan.handle->get(), b, c, l); });
+}
+
+// load_lengths (dataset.hpp:112): JSONL records -> SequenceSet
+inline SequenceSet load_lengths(const std::string& jsonl) {
+  int64_t n = 0, nt = 0;
+  check(cf_dataset_load_jsonl(jsonl.c_str(), &n, nullptr, nullptr, nullptr, &nt, nullptr));
+  std::vector<int64_t> ids(static_cast<size_t>(n)), lengths(static_cast<size_t>(n)), has(static_cast<size_t>(n));
+  std::vector<int32_t> tokens(static_cast<size_t>(nt) + 1);
+  check(cf_dataset_load_jsonl(jsonl.c_str(), &n, ids.data(), lengths.data(), has.data(), &nt, tokens.data()));
+  SequenceSet set;
+  int64_t off = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    SequenceRecord r;
+    r.id = ids[static_cast<size_t>(i)];
+    r.length = lengths[static_cast<size_t>(i)];
+    if (has[static_cast<size_t>(i)]) {
+      r.tokens.assign(tokens.begin() + off, tokens.begin() + off + r.length);
+      off += r.length;
+    }
+    set.push_back(std::move(r));
+  }
+  return set;
+}
+
 // RAII device context + model (ToyModelParams on the GPU).
 class Device {
  public:

@@ -20,5 +20,20 @@ int main() {
   const auto t3 = cf::simulate_state_aware_1f1b(cp, pc, cf::CostModel{});
   std::printf("makespans=%g,%g,%g bubble=%.2f stage0_ops=%zu\n", t1.makespan, t2.makespan, t3.makespan,
               100.0 * cf::bubble_ratio(t2), t2.stages[0].size());
+  // memory model (test_memory_model.cpp Table 6) and tuner (test_tuner.cpp worked batch)
+  const auto cal = cf::calibrate({{2048, 1, 32768, 41.6}, {2048, 1, 262144, 45.6}, {4096, 1, 32768, 47.5},
+                                  {4096, 1, 262144, 50.8}, {8192, 1, 32768, 59.3}, {8192, 1, 262144, 63.8}});
+  std::printf("base=%.4f resid=%.5f\n", cal.coefficients.base, cal.max_residual_gib);
+  cf::PipelineConfig tc;
+  tc.num_stages = 4;
+  const auto tr = cf::grid_search(b.sequences, {2, 4}, {1, 2}, tc, cf::CostModel{}, cf::MemoryModelCoefficients{},
+                                  1e9, 4, 1, 1);
+  std::printf("tuner best=%lld,%lld evals=%lld\n", (long long)tr.best_chunk_size, (long long)tr.best_k,
+              (long long)tr.evaluations);
+  // wire formats
+  const std::string js = cf::chunk_plan_json(ep);
+  const auto set = cf::load_lengths("{\"id\": 7, \"length\": 3, \"tokens\": [1, 2, 3]}\n{\"length\": 2}\n");
+  std::printf("json=%zu set=%zu,%lld,%zu\n", js.size() > 100 ? (size_t)1 : (size_t)0, set.size(),
+              (long long)set[0].id, set[0].tokens.size());
   return 0;
 }

@@ -17,3 +17,6 @@ def test_cpp_facade_builds_and_plans(tmp_path):
     assert "chunks=4 events=9 peak=2 recompute=2 groups=1" in out
     assert "ValidationError: chunk_size must be at least 1" in out
     assert "makespans=56,54,46 bubble=55.56 stage0_ops=9" in out
+    assert "base=34.8714 resid=0.59524" in out  # test_memory_model.cpp: 34.8717 +- 1e-3
+    assert "tuner best=2,2 evals=4" in out
+    assert "json=1 set=2,7,3" in out
