@@ -1090,6 +1090,11 @@ struct StageRunner {
       g.vc = a.take<bf16>(m->L * g.S * m->kvw);
       g.dkv = a.take<float>(m->L * g.S * 2 * m->kvw);
       CK(cudaMemsetAsync(g.dkv, 0, static_cast<size_t>(m->L * g.S * 2 * m->kvw) * 4, ex.s));
+      // K/V rows of later chunks are read (masked, P = 0) by the 128-key tiles
+      // of earlier chunks whose length is not a multiple of 128: they must be
+      // finite, since 0 * NaN garbage would poison O and dQ
+      CK(cudaMemsetAsync(g.kc, 0, static_cast<size_t>(m->L * g.S * m->kvw) * 2, ex.s));
+      CK(cudaMemsetAsync(g.vc, 0, static_cast<size_t>(m->L * g.S * m->kvw) * 2, ex.s));
       ex.kv_bytes += bytes;
       ex.kv_peak = std::max(ex.kv_peak, ex.kv_bytes);
       git = groups.emplace(cm.group, std::move(g)).first;

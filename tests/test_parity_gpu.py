@@ -43,6 +43,9 @@ CASES = [
     ("toy-dh128", 0, 96, 256, 2, 1, 2, 0, [100, 300, 77], 128, 1),
     ("llama-small", 1, 96, 128, 4, 2, 2, 256, [8, 30, 64, 150, 33], 64, 1),
     ("llama-gqa", 1, 120, 256, 2, 1, 2, 512, [200, 90, 333], 128, 2),
+    # head_dim 128 with 64-token chunks: 128-key tiles of early chunks reach
+    # KV-cache rows that later chunks have not written yet
+    ("llama-dh128-cs64", 1, 96, 256, 2, 1, 2, 512, [8, 30, 64, 150, 33, 100], 64, 1),
 ]
 
 
