@@ -46,6 +46,8 @@ CASES = [
     # head_dim 128 with 64-token chunks: 128-key tiles of early chunks reach
     # KV-cache rows that later chunks have not written yet
     ("llama-dh128-cs64", 1, 96, 256, 2, 1, 2, 512, [8, 30, 64, 150, 33, 100], 64, 1),
+    ("llama-dh128-cs96-k2", 1, 96, 256, 2, 1, 2, 512, [300, 20, 97, 5], 96, 2),
+    ("llama-dh128-mha-cs200", 1, 64, 256, 2, 2, 1, 384, [450, 64, 199], 200, 1),
 ]
 
 
