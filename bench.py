@@ -281,7 +281,7 @@ def run_b200(args):
     e1.synchronize()
     barrier()
     e2e_ms = e0.elapsed_time(e1)
-    h2d = int(step_meta_bytes(p, lengths))
+    h2d = int(step.input_bytes())  # the same per-step upload cf_run_plan performs (same plan and batch)
     d2h = 8 * (p.counts()[2] + 1)
 
     stats = torch.tensor([ms, e2e_ms, my_tokens], dtype=torch.float64, device="cuda")
@@ -344,11 +344,6 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
-
-
-def step_meta_bytes(plan, lengths):
-    # tokens/targets/positions + segment tables + tiles + embedding CSR: about 5 int32 per token
-    return 4 * 5 * int(sum(c["total_tokens"] for c in plan.export()[0]))
 
 
 def main():

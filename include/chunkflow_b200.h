@@ -374,6 +374,10 @@ int cf_step_prepare(cf_ctx* ctx, cf_model* model, const cf_plan* plan,
 int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step,
                 const cf_run_opts* opts, cf_run_result* result);
 void cf_step_destroy(cf_step* step);
+/* Bytes copied host -> device for the step's inputs (token ids, targets,
+ * positions, segment tables, attention tiles, embedding-backward CSR): what
+ * cf_step_prepare / cf_run_plan upload per step. */
+int cf_step_input_bytes(const cf_step* step, int64_t* bytes);
 /* Device time of every executed op (forward / recompute / backward, the
  * CF_PP_* kinds) of the step's last run when the context profiles
  * (cf_ctx_set_profiling): measured per-chunk costs for cf_pp_simulate.

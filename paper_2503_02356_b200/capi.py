@@ -93,7 +93,7 @@ EXPORTS = [
     "cf_model_get_grad", "cf_model_zero_grads", "cf_model_grad_buffer",
     "cf_model_num_params", "cf_run_plan", "cf_step_prepare", "cf_step_run",
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
-    "cf_pp_run_local", "cf_step_op_times", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
+    "cf_pp_run_local", "cf_step_op_times", "cf_step_input_bytes", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
 ]
@@ -566,6 +566,12 @@ class Step:
         r = RunResult()
         check(lib().cf_step_run(self.model.ctx.h, self.model.h, self.h, C.byref(o), C.byref(r)))
         return r
+
+    def input_bytes(self):
+        """Host -> device bytes of this step's inputs (cf_step_input_bytes)."""
+        n = C.c_int64()
+        check(lib().cf_step_input_bytes(self.h, C.byref(n)))
+        return n.value
 
     def op_times(self):
         """(kinds, chunk_ids, ms) of every op of the last run (profiling on)."""

@@ -276,6 +276,14 @@ int cf_step_run(cf_ctx* ctx, cf_model* model, cf_step* step, const cf_run_opts* 
 
 void cf_step_destroy(cf_step* step) { cfb::step_destroy(step); }
 
+int cf_step_input_bytes(const cf_step* step, int64_t* bytes) {
+  return cfb::guard([&] {
+    need(step, "step");
+    need(bytes, "bytes");
+    *bytes = cfb::step_input_bytes(step);
+  });
+}
+
 int cf_step_op_times(const cf_step* step, int64_t* n, int64_t* kinds, int64_t* chunk_ids, double* ms) {
   return cfb::guard([&] {
     need(step, "step");

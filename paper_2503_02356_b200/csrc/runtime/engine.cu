@@ -650,6 +650,8 @@ void step_op_times(const cf_step* st, int64_t* n, int64_t* kinds, int64_t* ids, 
   }
 }
 
+int64_t step_input_bytes(const cf_step* st) { return st->meta_len * 4; }
+
 void step_destroy(cf_step* st) {
   if (!st) return;
   cudaFree(st->meta_dev);

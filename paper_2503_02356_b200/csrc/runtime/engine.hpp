@@ -107,6 +107,7 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b);
 void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res);
 void step_destroy(cf_step* st);
 void step_op_times(const cf_step* st, int64_t* n, int64_t* kinds, int64_t* ids, double* ms);
+int64_t step_input_bytes(const cf_step* st);
 // Pipeline-parallel step of one stage on this rank (ctx has PP links): the
 // stage's chunk-aware 1F1B op stream (host/pp.hpp) with NCCL send/recv of
 // fp32 [T, d] activations and gradients.
