@@ -102,6 +102,12 @@ class GradComparison:
     max_rel_err: float
     mean_rel_err: float
 
+    def to_text(self) -> str:
+        """GradComparison::to_text (toy_model.hpp:668-678), same layout."""
+        out = "".join(f"{n} max_abs_diff={d:.6e} rel_err={r:.6e}\n" for n, d, r in self.rows)
+        return out + (f"loss_rel_err={self.loss_rel_err:.6e}\nmax_rel_err={self.max_rel_err:.6e}\n"
+                      f"mean_rel_err={self.mean_rel_err:.6e}\n")
+
 
 def compare_gradients(names, a_loss, a, b_loss, b, denom_floor=1e-12) -> GradComparison:
     """Per-tensor max|a-b| / max(max|a|, max|b|, floor) (toy_model.hpp:681-718)."""
@@ -124,6 +130,15 @@ class VerifyReport:
     instrumentation: dict
     chunk_count: int
     event_count: int
+
+    def to_text(self) -> str:
+        """VerifyReport::to_text (plan_runner.hpp:352-365), same layout."""
+        i = self.instrumentation
+        return (f"chunks: {self.chunk_count}\nevents: {self.event_count}\n" + self.comparison.to_text()
+                + f"recompute_forwards: {i['recompute_forward_count']}\n"
+                + f"recompute_loss_mismatches: {i['recompute_loss_mismatches']}\n"
+                + f"kv_completeness_violations: {i['kv_completeness_violations']}\n"
+                + f"result: {'PASS' if self.passed else 'FAIL'}\n")
 
 
 def verify_equivalence(model: Model, lengths, tokens, chunk_size, k, loss_tol=2e-3, grad_tol=3e-2,

@@ -83,6 +83,10 @@ def test_chunked_equals_unchunked_on_gpu(ctx, arch):
     model = cf.Model(ctx, gcfg)
     rep = cf.verify_equivalence(model, lengths, tokens, 16, 1, loss_tol=1e-4, grad_tol=1e-2)
     assert rep.passed, (rep.loss_rel_err, rep.max_grad_rel_err, rep.instrumentation)
+    # the `chunkflow verify` report layout (plan_runner.hpp:352-365)
+    txt = rep.to_text().splitlines()
+    assert txt[0] == f"chunks: {rep.chunk_count}" and txt[-1] == "result: PASS"
+    assert txt[2].startswith("embedding max_abs_diff=") and any(t.startswith("max_rel_err=") for t in txt)
     model.close()
 
 
