@@ -668,15 +668,15 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
          p.scale};
   const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256 * 4 + 256;
   const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // once per process, thread-safe (concurrent contexts on host threads)
+  static const cudaError_t attr = [] {
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem_dq));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dkv));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dkv));
+    return e;
+  }();
+  if (attr != cudaSuccess) return attr;
   // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
   dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   a.tiles = ktiles128;

@@ -611,12 +611,9 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   g.R = d.r;
   g.ldr = d.ldr;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per process, thread-safe (concurrent contexts on host threads)
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
+  if (attr != cudaSuccess) return attr;
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -647,12 +644,9 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.R = d.r;
   g.ldr = d.ldr;
   auto kern = pair::gemm_pair_kernel<A_MN, B_MN, EPI>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pair::kSmem));
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  // once per process, thread-safe (concurrent contexts on host threads)
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pair::kSmem));
+  if (attr != cudaSuccess) return attr;
   const int tiles = g.num_m * g.num_n;
   const int pairs = std::min(tiles, gemm_num_sms() / 2);
   kern<<<2 * pairs, 256, pair::kSmem, st>>>(ta, tb, g);

@@ -1064,6 +1064,17 @@ struct StageRunner {
     if (!opts.accumulate_grads) CK(cudaMemsetAsync(m->grads, 0, static_cast<size_t>(m->grad_numel) * 4, ex.s));
   }
 
+  // A step that throws part-way (bad plan, CUDA error) still returns its
+  // pool memory; finish() leaves nothing behind for this to release.
+  ~StageRunner() {
+    for (auto& kv : live) cudaFreeAsync(kv.second.mem, ex.s);
+    for (auto& kv : groups) cudaFreeAsync(kv.second.mem, ex.s);
+    for (auto& kv : kept_in) cudaFreeAsync(kv.second, ex.s);
+    if (ex.loss_slots) cudaFreeAsync(ex.loss_slots, ex.s);
+  }
+  StageRunner(const StageRunner&) = delete;
+  StageRunner& operator=(const StageRunner&) = delete;
+
   const ChunkMeta& chunk(int64_t id) const {
     auto it = st->pos_of.find(id);
     if (it == st->pos_of.end()) throw ValidationError("plan references unknown chunk " + std::to_string(id));
