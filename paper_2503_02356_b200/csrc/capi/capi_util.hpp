@@ -14,8 +14,11 @@ namespace cfb {
 extern thread_local std::string g_last_error;
 
 // Relative cost of one attention (query, key) pair vs one token of GEMM work
-// for the DP partition: 12*L*H*dh / (6*N) for Llama-7B-GQA8.
-constexpr double kPairWeight = 4.4e-5;
+// for the DP partition.  FLOP ratio 12*L*H*dh / (6*N) = 4.4e-5 for
+// Llama-7B-GQA8; the attention kernels run at about half the
+// GEMM rate, and the per-op times of a measured C2 step fit 8.4e-5
+// (profiles/round1_step_breakdown.json).
+constexpr double kPairWeight = 8.4e-5;
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;

@@ -399,7 +399,7 @@ std::vector<Unit> plan_units(const Plan& plan, double alpha, double beta) {
       const double L = static_cast<double>(s.len), P = static_cast<double>(s.start);
       const double c1 = alpha * L + beta * (L * P + L * (L + 1) / 2);
       u.cost += c1;
-      if (n > plan.k && i < n - plan.k) u.cost += c1 / 3.0;  // recompute forward
+      if (n > plan.k && i < n - plan.k) u.cost += 0.29 * c1;  // recompute forward (measured F/(F+B))
       u.tokens += m.total;
       u.chunk_pos.push_back(pos);
     }
