@@ -638,7 +638,10 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.num_m = static_cast<int>((d.M + 255) / 256);
   g.num_n = static_cast<int>((d.N + 255) / 256);
   g.num_k = static_cast<int>((d.K + BK - 1) / BK);
-  g.group_m = raster_group(g.num_m, 8);
+  // Short-K, wide-N shapes (qkv / gate|up forward, down dgrad) reuse the A
+  // panels best with 16 M-blocks per group (DRAM/algorithmic bytes 1.3-1.6
+  // vs 1.6-2.2 at 8, tools/gemm_group_traffic.sh); long-K shapes prefer 8.
+  g.group_m = raster_group(g.num_m, g.num_k <= 64 && g.num_n >= 24 ? 16 : 8);
   g.C = d.c;
   g.ldc = d.ldc;
   g.R = d.r;
