@@ -433,6 +433,79 @@ __global__ void ce_kernel(const float* logits, int64_t V, int64_t ld, const int3
   }
 }
 
+// Register-resident form: one 1024-thread block per row holds the whole row
+// (NV float4 per thread, V <= 4096*NV), so the logits are read from HBM once
+// (the strided kernel above reads them twice) with 16-byte loads and the
+// bf16 gradient is written with 8-byte stores.
+template <int NV>
+__global__ void __launch_bounds__(1024, 1)
+    ce_rows_kernel(const float* __restrict__ logits, int64_t V, int64_t ld, const int32_t* __restrict__ targets,
+                   float inv_norm, float* __restrict__ row_loss, bf16* __restrict__ dlogits) {
+  const int64_t row = blockIdx.x;
+  const int32_t tgt = targets[row];
+  const float4* l = reinterpret_cast<const float4*>(logits + row * ld);
+  const int64_t nv = V / 4;
+  __shared__ float red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (tgt < 0) {
+    if (threadIdx.x == 0) row_loss[row] = 0.f;
+    if (dlogits) {
+      uint2* o = reinterpret_cast<uint2*>(dlogits + row * ld);
+      for (int64_t c = threadIdx.x; c < nv; c += blockDim.x) o[c] = make_uint2(0u, 0u);
+    }
+    return;
+  }
+  float4 x[NV];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int64_t c = threadIdx.x + static_cast<int64_t>(i) * blockDim.x;
+    x[i] = c < nv ? l[c] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+    m = fmaxf(m, fmaxf(fmaxf(x[i].x, x[i].y), fmaxf(x[i].z, x[i].w)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  float M = red[0];
+  for (int w = 1; w < 32; ++w) M = fmaxf(M, red[w]);
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    x[i].x = __expf(x[i].x - M);
+    x[i].y = __expf(x[i].y - M);
+    x[i].z = __expf(x[i].z - M);
+    x[i].w = __expf(x[i].w - M);
+    s += (x[i].x + x[i].y) + (x[i].z + x[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  float S = 0.f;
+  for (int w = 0; w < 32; ++w) S += red[w];
+  if (threadIdx.x == 0) row_loss[row] = M + logf(S) - logits[row * ld + tgt];
+  if (dlogits) {
+    const float scale = inv_norm / S;
+    uint2* o = reinterpret_cast<uint2*>(dlogits + row * ld);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int64_t c = threadIdx.x + static_cast<int64_t>(i) * blockDim.x;
+      if (c >= nv) break;
+      float4 p = make_float4(x[i].x * scale, x[i].y * scale, x[i].z * scale, x[i].w * scale);
+      if (tgt >> 2 == c) {
+        const int j = tgt & 3;
+        if (j == 0) p.x -= inv_norm;
+        if (j == 1) p.y -= inv_norm;
+        if (j == 2) p.z -= inv_norm;
+        if (j == 3) p.w -= inv_norm;
+      }
+      o[c] = make_uint2(pack_bf16(p.x, p.y), pack_bf16(p.z, p.w));
+    }
+  }
+}
+
 __global__ void sum_f64_kernel(const float* v, int64_t n, double* out) {
   __shared__ double red[1024];
   double s = 0.0;
@@ -726,7 +799,17 @@ cudaError_t swiglu_bwd(const bf16* gu, const bf16* dh, int64_t T, int64_t ffn, b
 cudaError_t ce_fwd_bwd(const float* logits, int64_t T, int64_t V, int64_t ld, const int32_t* targets, float inv_norm,
                        float* row_loss, bf16* dlogits, cudaStream_t st) {
   if (T == 0) return cudaSuccess;
-  ce_kernel<<<static_cast<unsigned>(T), 256, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  const bool vec = V % 4 == 0 && ld % 4 == 0 && V <= 4096 * 8 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dlogits) & 7) == 0;
+  if (!vec) {
+    ce_kernel<<<static_cast<unsigned>(T), 256, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  } else if (V <= 4096 * 2) {
+    ce_rows_kernel<2><<<static_cast<unsigned>(T), 1024, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  } else if (V <= 4096 * 4) {
+    ce_rows_kernel<4><<<static_cast<unsigned>(T), 1024, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  } else {
+    ce_rows_kernel<8><<<static_cast<unsigned>(T), 1024, 0, st>>>(logits, V, ld, targets, inv_norm, row_loss, dlogits);
+  }
   return cudaGetLastError();
 }
 cudaError_t sum_f64(const float* v, int64_t n, double* out, cudaStream_t st) {

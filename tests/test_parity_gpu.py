@@ -48,6 +48,11 @@ CASES = [
     ("llama-dh128-cs64", 1, 96, 256, 2, 1, 2, 512, [8, 30, 64, 150, 33, 100], 64, 1),
     ("llama-dh128-cs96-k2", 1, 96, 256, 2, 1, 2, 512, [300, 20, 97, 5], 96, 2),
     ("llama-dh128-mha-cs200", 1, 64, 256, 2, 2, 1, 384, [450, 64, 199], 200, 1),
+    # cross-entropy forms: register-resident rows (V % 4 == 0, V <= 32768,
+    # incl. the C2 vocabulary) and the strided kernel (odd V)
+    ("toy-v32000", 0, 32000, 64, 4, 2, 1, 0, [40, 70, 20], 64, 1),
+    ("toy-v9000", 0, 9000, 64, 4, 2, 1, 0, [33, 64], 64, 1),
+    ("toy-v97", 0, 97, 64, 4, 2, 1, 0, [40, 70, 20], 64, 1),
 ]
 
 
