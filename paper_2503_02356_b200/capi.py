@@ -31,7 +31,7 @@ PP_OP_DT = np.dtype([("kind", np.int64), ("chunk_id", np.int64), ("start", np.fl
 PP_FORWARD, PP_RECOMPUTE, PP_BACKWARD = 0, 1, 2
 
 ARCH_TOY, ARCH_LLAMA = 0, 1
-EPI_BF16, EPI_F32, EPI_F32_ACC, EPI_F32_RES, EPI_BF16_TANH, EPI_BF16_TANHGRAD = range(6)
+EPI_BF16, EPI_F32, EPI_F32_ACC, EPI_F32_RES, EPI_BF16_TANH, EPI_BF16_TANHGRAD, EPI_BF16_SWIGLU = range(7)
 
 
 class ModelCfg(C.Structure):

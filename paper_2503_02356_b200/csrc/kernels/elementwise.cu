@@ -155,7 +155,6 @@ __global__ void kv_store_kernel(const bf16* qkv, int64_t ld, int64_t T, int64_t 
   }
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + __expf(-x)); }
 
 // 8 elements (16 bytes) per thread; ffn % 8 == 0 is validated at model creation.
 __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {

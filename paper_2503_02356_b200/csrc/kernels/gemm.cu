@@ -48,6 +48,7 @@ struct Args {
   const void* R;  // fp32 residual (EPI_F32_RES) or bf16 aux (EPI_BF16_TANHGRAD)
   int64_t ldr;
   int group_m;  // raster: tiles walk group_m M-blocks x all N-blocks, M fastest
+  int split_n;  // EPI_BF16_SWIGLU: F (the up half starts at column F)
 };
 
 // Grouped raster.  Persistent CTAs take consecutive tile indices, so one wave
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       int mb, nb;
-        tile_coords(g, tile, mb, nb);
+      tile_coords(g, tile, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
@@ -332,6 +333,31 @@ __global__ void __launch_bounds__(256, 1)
 // the shared-memory bytes written by TMA and read by the tensor core per FLOP
 // (64 + 64 B/clk instead of 96 + 96 B/clk at full MMA rate), which is what
 // caps the single-CTA kernel at ~2/3 of the per-clock tensor peak.
+// EPI_BF16_SWIGLU store of 32 columns: gate and up (bf16) to C at col0 and
+// F + col0, h = silu(g) * u of the rounded values to H (= R) at col0.
+__device__ __forceinline__ void swiglu_store_row32(const Args& g, int row, int col0, const uint32_t (&rg)[32],
+                                                   const uint32_t (&ru)[32]) {
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+  __nv_bfloat16* h = const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(g.R)) +
+                     static_cast<int64_t>(row) * g.ldr + col0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t pg[4], pu[4], ph[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = 8 * q + 2 * e;
+      pg[e] = pack_bf16(__uint_as_float(rg[j]), __uint_as_float(rg[j + 1]));
+      pu[e] = pack_bf16(__uint_as_float(ru[j]), __uint_as_float(ru[j + 1]));
+      const float g0 = __uint_as_float(pg[e] << 16), g1 = __uint_as_float(pg[e] & 0xFFFF0000u);
+      const float u0 = __uint_as_float(pu[e] << 16), u1 = __uint_as_float(pu[e] & 0xFFFF0000u);
+      ph[e] = pack_bf16(g0 * sigmoidf_(g0) * u0, g1 * sigmoidf_(g1) * u1);
+    }
+    reinterpret_cast<uint4*>(c)[q] = make_uint4(pg[0], pg[1], pg[2], pg[3]);
+    reinterpret_cast<uint4*>(c + g.split_n)[q] = make_uint4(pu[0], pu[1], pu[2], pu[3]);
+    reinterpret_cast<uint4*>(h)[q] = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+  }
+}
+
 namespace pair {
 
 constexpr int kStages = 6;
@@ -433,7 +459,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         int mb, nb;
         tile_coords(g, tile, mb, nb);
         const int m0 = mb * 256 + static_cast<int>(rank) * 128;
-        const int n0 = nb * 256 + static_cast<int>(rank) * 128;
+        const int n0 = EPI == EPI_BF16_SWIGLU ? (rank == 0 ? nb * 128 : g.split_n + nb * 128)
+                                              : nb * 256 + static_cast<int>(rank) * 128;
         for (int kb = 0; kb < g.num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * kABytes;
@@ -503,32 +530,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const uint32_t tempty_leader0 = leader_addr(smem_u32(&tempty[0]));
     for (int tile = pair; tile < num_tiles; tile += npairs) {
       int mb, nb;
-        tile_coords(g, tile, mb, nb);
+      tile_coords(g, tile, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * 256);
-      float4 pre[8];
-      if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * 256, pre);
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c * 32, r);
-        tmem_ld_wait();
-        if (c == 7) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+      if constexpr (EPI == EPI_BF16_SWIGLU) {
+        // accumulator columns [0,128) = gate, [128,256) = up of the same F columns
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t rg[32], ru[32];
+          tmem_ld32(tbase + c * 32, rg);
+          tmem_ld32(tbase + 128 + c * 32, ru);
+          tmem_ld_wait();
+          if (c == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+          }
+          if (row < g.M) swiglu_store_row32(g, row, nb * 128 + c * 32, rg, ru);
         }
-        const int col0 = nb * 256 + c * 32;
-        if constexpr (kEpiReads<EPI>) {
-          float4 nxt[8];
-          if (c + 1 < 8) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
-          if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+      } else {
+        float4 pre[8];
+        if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * 256, pre);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
-        } else {
-          if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        for (int c = 0; c < 8; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          if (c == 7) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+          }
+          const int col0 = nb * 256 + c * 32;
+          if constexpr (kEpiReads<EPI>) {
+            float4 nxt[8];
+            if (c + 1 < 8) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
+            if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
+          } else {
+            if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+          }
         }
       }
       if (++acc == 2) {
@@ -642,6 +686,7 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   // panels best with 16 M-blocks per group (DRAM/algorithmic bytes 1.3-1.6
   // vs 1.6-2.2 at 8, tools/gemm_group_traffic.sh); long-K shapes prefer 8.
   g.group_m = raster_group(g.num_m, g.num_k <= 64 && g.num_n >= 24 ? 16 : 8);
+  g.split_n = static_cast<int>(d.N / 2);
   g.C = d.c;
   g.ldc = d.ldc;
   g.R = d.r;
@@ -665,6 +710,7 @@ cudaError_t pair_by_epi(const GemmDesc& d, cudaStream_t st) {
     case EPI_F32_RES: return launch_pair<A_MN, B_MN, EPI_F32_RES>(d, st);
     case EPI_BF16_TANH: return launch_pair<A_MN, B_MN, EPI_BF16_TANH>(d, st);
     case EPI_BF16_TANHGRAD: return launch_pair<A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
+    case EPI_BF16_SWIGLU: return launch_pair<A_MN, B_MN, EPI_BF16_SWIGLU>(d, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -716,6 +762,11 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
     return cudaErrorMisalignedAddress;
   const int64_t sms = gemm_num_sms();
   const int mode = gemm_mode();
+  if (d.epi == EPI_BF16_SWIGLU) {
+    if (!gemm_swiglu_ok(d.M, d.N, d.K) || (reinterpret_cast<uintptr_t>(d.r) & 15) || (d.ldr % 8))
+      return cudaErrorInvalidValue;
+    return pair_by_major(d, st);
+  }
   // CTA pairs for the large GEMMs (the step's hot path); single-CTA tiles for
   // narrow / short problems where a 256 x 256 pair tile would idle.
   const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
@@ -723,6 +774,12 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
   const int64_t tiles256 = ((d.M + BM - 1) / BM) * ((d.N + 255) / 256);
   const bool wide = d.N > 128 && tiles256 >= sms;
   return wide ? by_major<256>(d, st) : by_major<128>(d, st);
+}
+
+bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K) {
+  const int64_t pair_tiles = ((M + 255) / 256) * (N / 256);
+  const int mode = gemm_mode();
+  return mode != 1 && N % 256 == 0 && M > 128 && K > 0 && (mode == 2 || pair_tiles >= gemm_num_sms() / 4);
 }
 
 // 0 = auto (CTA pairs when large), 1 = single-CTA only, 2 = CTA pairs whenever M, N > 128 (tests).

@@ -12,7 +12,13 @@ enum GemmEpi : int {
   EPI_F32_ACC = 2,       // C(fp32) += acc              (weight-gradient accumulation)
   EPI_F32_RES = 3,       // C(fp32)  = acc + R(fp32)    (residual; R may alias C)
   EPI_BF16_TANH = 4,     // C(bf16)  = tanh(acc)        (toy FFN)
-  EPI_BF16_TANHGRAD = 5  // C(bf16)  = acc * (1 - R^2)  (toy FFN backward, R = h bf16)
+  EPI_BF16_TANHGRAD = 5, // C(bf16)  = acc * (1 - R^2)  (toy FFN backward, R = h bf16)
+  // C(bf16) = acc over [gate | up] (N = 2F columns) and, in the same
+  // epilogue, H(bf16)[M, F] = silu(gate) * up from the bf16-rounded values
+  // (H is passed as r / ldr).  Each CTA-pair tile pairs gate columns
+  // [128j, 128j+128) with up columns F + [128j, 128j+128).  CTA-pair kernel,
+  // F % 128 == 0 only (gemm_swiglu_ok).
+  EPI_BF16_SWIGLU = 6
 };
 
 struct GemmDesc {
@@ -31,6 +37,9 @@ struct GemmDesc {
 };
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
+// Whether EPI_BF16_SWIGLU is available for this problem (else run EPI_BF16
+// and the elementwise swiglu_fwd).
+bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K);
 int gemm_num_sms();
 // 0 = auto (CTA-pair kernel for large GEMMs), 1 = single-CTA kernel only.
 int gemm_mode();

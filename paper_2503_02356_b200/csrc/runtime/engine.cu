@@ -838,9 +838,13 @@ struct Exec {
       if (m->llama) {
         bf16* xn2 = t.xn2 ? t.xn2 + l * T * d : A;
         L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), xn2, s), "rmsnorm");
-        gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
         bf16* hl = t.h ? t.h + l * T * m->ffn : A;
-        L(cfk::swiglu_fwd(act, T, m->ffn, hl, s), "swiglu");
+        if (cfk::gemm_swiglu_ok(T, m->gu_w, d)) {  // h written by the gate|up GEMM's epilogue
+          gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16_SWIGLU, hl, m->ffn);
+        } else {
+          gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
+          L(cfk::swiglu_fwd(act, T, m->ffn, hl, s), "swiglu");
+        }
         gemm(hl, 1, m->ffn, ly.w2, 0, d, xn, d, T, d, m->ffn, cfk::EPI_F32_RES, xm, d);
       } else {
         L(cfk::to_bf16(xm, A, T * d, s), "to_bf16");

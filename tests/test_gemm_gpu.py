@@ -76,3 +76,31 @@ def test_gemm_residual_aliases_output(ctx, gemm_mode):
     ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, X.data_ptr(), N, M, N, K, capi.EPI_F32_RES, X.data_ptr(), N)
     ctx.synchronize()
     assert (X - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("shape,mode", [((384, 512, 320), 2), ((2048, 2048, 512), 0), ((8192, 22016, 4096), 0)],
+                         ids=["small-forced-pair", "auto", "c2-gate-up"])
+def test_gemm_swiglu_epilogue(ctx, shape, mode):
+    """EPI_BF16_SWIGLU: gate|up written exactly as EPI_BF16 writes them, plus
+    h = silu(gate) * up of the rounded values in the same epilogue."""
+    M, N, K = shape
+    F = N // 2
+    capi.check(capi.lib().cf_debug_set_gemm_mode(mode))
+    try:
+        A = _mk(M, K, 7)
+        B = _mk(K, N, 8)
+        C0 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        C1 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        H = torch.zeros(M, F, device="cuda", dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, C0.data_ptr(), N, M, N, K, capi.EPI_BF16)
+        ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, C1.data_ptr(), N, M, N, K, capi.EPI_BF16_SWIGLU,
+                 H.data_ptr(), F)
+        ctx.synchronize()
+    finally:
+        capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+    assert torch.equal(C0, C1)
+    g, u = C0[:, :F].float(), C0[:, F:].float()
+    ref = g * torch.sigmoid(g) * u
+    err = (H.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err

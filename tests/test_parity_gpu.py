@@ -11,6 +11,7 @@ import numpy as np
 import pytest
 
 import paper_2503_02356_b200 as cf
+from paper_2503_02356_b200 import capi
 from oracle.oracle import model_cfg as ocfg
 
 pytestmark = pytest.mark.gpu
@@ -75,6 +76,30 @@ def test_run_plan_matches_oracle(ctx, oracle, case):
     assert abs(r.loss - ol) / abs(ol) <= LOSS_TOL, (r.loss, ol)
     errs = _per_tensor_err(model, grads, og)
     worst = max(errs, key=lambda e: e[1])
+    assert worst[1] <= GRAD_TOL, worst
+    model.close()
+
+
+def test_run_plan_matches_oracle_forced_pair_gemms(ctx, oracle):
+    """CTA-pair GEMMs at toy sizes (cf_debug_set_gemm_mode(2)), so the fused
+    gate|up + SwiGLU epilogue and the pair epilogues run under the oracle,
+    including a recomputed forward (sequence of 3 chunks, K = 1)."""
+    gcfg, c = _cfgs(1, 96, 256, 2, 1, 2, 384)
+    lengths = np.array([700, 130, 301, 64], np.int64)
+    tokens = cf.gen_tokens(lengths, 96, 13)
+    capi.check(capi.lib().cf_debug_set_gemm_mode(2))
+    try:
+        model = cf.Model(ctx, gcfg)
+        plan = cf.Plan.build(lengths, 256, 1)
+        r = model.run_plan(plan, lengths, tokens)
+        params, grads = model.params_flat(), model.grads_flat()
+    finally:
+        capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+    ol, og, oi = oracle.run_plan(c, lengths, tokens, 256, 1, params=params)
+    assert r.recompute_forward_count == oi[1] and oi[1] > 0
+    assert r.recompute_loss_mismatches == 0
+    assert abs(r.loss - ol) / abs(ol) <= LOSS_TOL, (r.loss, ol)
+    worst = max(_per_tensor_err(model, grads, og), key=lambda e: e[1])
     assert worst[1] <= GRAD_TOL, worst
     model.close()
 
