@@ -7,8 +7,8 @@ import json
 import sys
 
 T, d, kvw, ffn, V = 8192, 4096, 1024, 11008, 32000
-BF16, F32, ACC, RES = "bf16", "f32", "f32_acc", "f32_res"
-FWD = [("qkv fwd", T, d + 2 * kvw, d, BF16), ("o fwd +res", T, d, d, RES), ("gate|up fwd", T, 2 * ffn, d, BF16),
+BF16, F32, ACC, RES, SWIGLU = "bf16", "f32", "f32_acc", "f32_res", "bf16_swiglu"
+FWD = [("qkv fwd", T, d + 2 * kvw, d, BF16), ("o fwd +res", T, d, d, RES), ("gate|up fwd", T, 2 * ffn, d, SWIGLU),
        ("down fwd +res", T, d, ffn, RES)] * 2
 BWD = [("head wgrad", d, V, T, ACC), ("head dgrad", T, d, V, F32), ("down dgrad", T, ffn, d, BF16),
        ("down wgrad", ffn, d, T, ACC), ("gate|up wgrad", d, 2 * ffn, T, ACC), ("gate|up dgrad", T, d, 2 * ffn, F32),
@@ -16,7 +16,7 @@ BWD = [("head wgrad", d, V, T, ACC), ("head dgrad", T, d, V, F32), ("down dgrad"
 
 
 def algorithmic(M, N, K, epi):
-    c = {BF16: 2, F32: 4, ACC: 8, RES: 8}[epi]
+    c = {BF16: 2, F32: 4, ACC: 8, RES: 8, SWIGLU: 3}[epi]  # SWIGLU: gate|up + h (N/2 columns) in bf16
     return 2 * (M * K + N * K) + c * M * N
 
 
