@@ -388,6 +388,37 @@ int cf_step_op_times(const cf_step* step, int64_t* n, int64_t* kinds,
 int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids,
                      const int64_t* lengths, const int32_t* tokens, int64_t n,
                      double normalizer_override, cf_run_result* result);
+
+/* Operator level: detail::segment_forward (toy_model.hpp:206-334) and
+ * detail::segment_backward (toy_model.hpp:341-520) on the GPU.  One
+ * contiguous segment of one sequence at positions [prefix_len,
+ * prefix_len + len).  Host buffers, fp64, per layer in layer order:
+ *   prefix_k / prefix_v   [L][prefix_len][kv_width] (NULL when prefix_len = 0)
+ *   saved_k / saved_v     [L][len][kv_width], the segment's own key/value rows
+ *                         (SegmentTape::saved_k/v; may be NULL)
+ *   incoming_dk / _dv     [L][len][kv_width], gradients of those rows from
+ *                         later chunks (NULL = absent)
+ *   d_prefix_k / _v       [L][prefix_len][kv_width], accumulated (+=)
+ * targets[t] = -1 marks a position without a prediction target.  loss_sum
+ * is the unnormalized cross-entropy over target positions
+ * (SegmentTape::loss_sum).  keep_tape = 0 returns *tape = NULL (a
+ * discarded forward); otherwise the retained activations stay on the device
+ * until cf_segment_destroy.  cf_segment_backward accumulates the parameter
+ * gradients into the model's gradient buffer (the reference's GradientSet&;
+ * cf_model_zero_grads clears it) with the normalizer given here.  Keys are
+ * post-RoPE for the Llama arch (what the executor caches).  A tape without
+ * retained activations is CF_EVALIDATION, like the reference's
+ * "segment backward requires a retained tape". */
+typedef struct cf_segment cf_segment;
+int cf_segment_forward(cf_ctx* ctx, cf_model* model, const int32_t* tokens, int64_t len,
+                       const int64_t* targets, const double* prefix_k, const double* prefix_v,
+                       int64_t prefix_len, int keep_tape, double* loss_sum, double* saved_k,
+                       double* saved_v, cf_segment** tape);
+int cf_segment_backward(cf_ctx* ctx, cf_model* model, const cf_segment* tape,
+                        const double* prefix_k, const double* prefix_v, double* d_prefix_k,
+                        double* d_prefix_v, const double* incoming_dk, const double* incoming_dv,
+                        double normalizer);
+void cf_segment_destroy(cf_segment* tape);
 int cf_ctx_synchronize(cf_ctx* ctx);
 
 /* ---- pipeline-parallel execution (config C5; the reference only simulates

@@ -441,4 +441,90 @@ inline cf_run_result run_plan(const Model& model, const ChunkPlan& /*chunk_plan*
   return r;
 }
 
+namespace detail {
+
+// SegmentTape (toy_model.hpp:155-165) for the device operators: the saved
+// key/value rows and loss come back to the host; the retained activations
+// stay on the device behind `handle` (null for a discarding forward).
+struct SegmentTape {
+  int64_t len = 0;
+  int64_t prefix_len = 0;
+  std::vector<std::vector<double>> saved_k;  // per layer, len x kv_width
+  std::vector<std::vector<double>> saved_v;
+  double loss_sum = 0.0;
+  std::shared_ptr<cf_segment> handle;
+};
+
+inline std::vector<double> flatten_kv(const std::vector<std::vector<double>>& per_layer, size_t layers, size_t n,
+                                      const char* what) {
+  std::vector<double> flat;
+  if (per_layer.empty()) return flat;
+  if (per_layer.size() != layers) throw ValidationError(std::string(what) + ": one entry per layer required");
+  for (const auto& v : per_layer) {
+    if (v.size() != n) throw ValidationError(std::string(what) + ": wrong row count");
+    flat.insert(flat.end(), v.begin(), v.end());
+  }
+  return flat;
+}
+
+// segment_forward (toy_model.hpp:206): prefix_k / prefix_v per layer,
+// prefix_len x kv_width (empty when prefix_len is 0).
+inline SegmentTape segment_forward(const Model& model, const cf_model_cfg& cfg, const int32_t* tokens, int64_t len,
+                                   const int64_t* targets, const std::vector<std::vector<double>>& prefix_k,
+                                   const std::vector<std::vector<double>>& prefix_v, int64_t prefix_len,
+                                   bool keep_tape) {
+  const size_t L = static_cast<size_t>(cfg.num_layers);
+  const size_t kvw = static_cast<size_t>(cfg.num_kv_heads * (cfg.d_model / cfg.num_heads));
+  const std::vector<double> pk = flatten_kv(prefix_k, L, static_cast<size_t>(prefix_len) * kvw, "prefix_k");
+  const std::vector<double> pv = flatten_kv(prefix_v, L, static_cast<size_t>(prefix_len) * kvw, "prefix_v");
+  std::vector<double> sk(L * static_cast<size_t>(len) * kvw), sv(sk.size());
+  SegmentTape t;
+  t.len = len;
+  t.prefix_len = prefix_len;
+  cf_segment* h = nullptr;
+  check(cf_segment_forward(model.device().get(), model.get(), tokens, len, targets, pk.empty() ? nullptr : pk.data(),
+                           pv.empty() ? nullptr : pv.data(), prefix_len, keep_tape ? 1 : 0, &t.loss_sum, sk.data(),
+                           sv.data(), &h));
+  if (h) t.handle.reset(h, &cf_segment_destroy);
+  const size_t per = static_cast<size_t>(len) * kvw;
+  for (size_t l = 0; l < L; ++l) {
+    t.saved_k.emplace_back(sk.begin() + l * per, sk.begin() + (l + 1) * per);
+    t.saved_v.emplace_back(sv.begin() + l * per, sv.begin() + (l + 1) * per);
+  }
+  return t;
+}
+
+// segment_backward (toy_model.hpp:341): parameter gradients accumulate in
+// the model's device buffer (the GradientSet); d_prefix_k / d_prefix_v are
+// accumulated, incoming_dk / incoming_dv may be null.
+inline void segment_backward(const Model& model, const cf_model_cfg& cfg, const SegmentTape& tape,
+                             const std::vector<std::vector<double>>& prefix_k,
+                             const std::vector<std::vector<double>>& prefix_v,
+                             std::vector<std::vector<double>>* d_prefix_k, std::vector<std::vector<double>>* d_prefix_v,
+                             const std::vector<std::vector<double>>* incoming_dk,
+                             const std::vector<std::vector<double>>* incoming_dv, double normalizer) {
+  if (!tape.handle) throw ValidationError("segment backward requires a retained tape");
+  const size_t L = static_cast<size_t>(cfg.num_layers);
+  const size_t kvw = static_cast<size_t>(cfg.num_kv_heads * (cfg.d_model / cfg.num_heads));
+  const size_t np = static_cast<size_t>(tape.prefix_len) * kvw, nl = static_cast<size_t>(tape.len) * kvw;
+  const std::vector<double> pk = flatten_kv(prefix_k, L, np, "prefix_k");
+  const std::vector<double> pv = flatten_kv(prefix_v, L, np, "prefix_v");
+  const std::vector<double> ik = incoming_dk ? flatten_kv(*incoming_dk, L, nl, "incoming_dk") : std::vector<double>{};
+  const std::vector<double> iv = incoming_dv ? flatten_kv(*incoming_dv, L, nl, "incoming_dv") : std::vector<double>{};
+  std::vector<double> dk(L * np, 0.0), dv(L * np, 0.0);
+  check(cf_segment_backward(model.device().get(), model.get(), tape.handle.get(), pk.empty() ? nullptr : pk.data(),
+                            pv.empty() ? nullptr : pv.data(), dk.data(), dv.data(), ik.empty() ? nullptr : ik.data(),
+                            iv.empty() ? nullptr : iv.data(), normalizer));
+  for (int kv = 0; kv < 2; ++kv) {
+    std::vector<std::vector<double>>* out = kv ? d_prefix_v : d_prefix_k;
+    const std::vector<double>& src = kv ? dv : dk;
+    if (!out || np == 0) continue;
+    if (out->empty()) out->assign(L, std::vector<double>(np, 0.0));
+    for (size_t l = 0; l < L; ++l)
+      for (size_t i = 0; i < np; ++i) (*out)[l][i] += src[l * np + i];
+  }
+}
+
+}  // namespace detail
+
 }  // namespace chunkflow_b200

@@ -96,6 +96,7 @@ EXPORTS = [
     "cf_pp_run_local", "cf_step_op_times", "cf_step_input_bytes", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_segment_forward", "cf_segment_backward", "cf_segment_destroy",
 ]
 
 _lib = None
@@ -114,7 +115,7 @@ def lib():
         L.cf_model_num_params.restype = C.c_int64
         vp = C.c_void_p
         for name in ("cf_plan_destroy", "cf_ctx_destroy", "cf_model_destroy", "cf_step_destroy",
-                     "cf_pp_local_destroy"):
+                     "cf_pp_local_destroy", "cf_segment_destroy"):
             getattr(L, name).argtypes = [vp]
             getattr(L, name).restype = None
         L.cf_model_num_tensors.argtypes = [vp]
@@ -542,10 +543,77 @@ class Model:
                                      C.c_int64(len(lengths)), C.c_double(normalizer), C.byref(r)))
         return r
 
+    def kv_shape(self, rows):
+        c = self.cfg
+        return (int(c.num_layers), int(rows), int(c.num_kv_heads * (c.d_model // c.num_heads)))
+
+    def segment_forward(self, tokens, targets, prefix_k=None, prefix_v=None, keep_tape=True):
+        """detail::segment_forward (toy_model.hpp:206): one segment of one
+        sequence after `prefix_k/v` ([L, prefix_len, kv_width] fp64).  Returns
+        (loss_sum, saved_k, saved_v, tape); tape is None unless keep_tape."""
+        tokens = np.ascontiguousarray(tokens, np.int32)
+        targets = np.ascontiguousarray(targets, np.int64)
+        n = len(tokens)
+        if len(targets) != n:
+            raise ValueError("tokens and targets differ in length")
+        plen = 0 if prefix_k is None else int(np.shape(prefix_k)[1])
+        pk = None if prefix_k is None else np.ascontiguousarray(prefix_k, np.float64)
+        pv = None if prefix_v is None else np.ascontiguousarray(prefix_v, np.float64)
+        sk = np.zeros(self.kv_shape(n))
+        sv = np.zeros(self.kv_shape(n))
+        loss = C.c_double()
+        h = C.c_void_p()
+        check(lib().cf_segment_forward(self.ctx.h, self.h, _p(tokens), C.c_int64(n), _p(targets),
+                                       None if pk is None else _p(pk), None if pv is None else _p(pv),
+                                       C.c_int64(plen), C.c_int(int(keep_tape)), C.byref(loss), _p(sk), _p(sv),
+                                       C.byref(h)))
+        return loss.value, sk, sv, (SegmentTape(h, plen, self) if h.value else None)
+
+    def segment_backward(self, tape, normalizer, prefix_k=None, prefix_v=None, incoming_dk=None, incoming_dv=None,
+                         d_prefix_k=None, d_prefix_v=None):
+        """detail::segment_backward (toy_model.hpp:341): accumulates parameter
+        gradients (the model's buffer) and the prefix K/V gradients into
+        d_prefix_k/v (allocated as zeros when None; returned)."""
+        h = tape.h if tape is not None else C.c_void_p()
+        plen = tape.prefix_len if tape is not None else 0
+        pk = None if prefix_k is None else np.ascontiguousarray(prefix_k, np.float64)
+        pv = None if prefix_v is None else np.ascontiguousarray(prefix_v, np.float64)
+        ik = None if incoming_dk is None else np.ascontiguousarray(incoming_dk, np.float64)
+        iv = None if incoming_dv is None else np.ascontiguousarray(incoming_dv, np.float64)
+        dpk = np.zeros(self.kv_shape(plen)) if d_prefix_k is None else d_prefix_k
+        dpv = np.zeros(self.kv_shape(plen)) if d_prefix_v is None else d_prefix_v
+        opt = lambda a: None if a is None else _p(a)  # noqa: E731
+        check(lib().cf_segment_backward(self.ctx.h, self.h, h, opt(pk), opt(pv), _p(dpk), _p(dpv), opt(ik), opt(iv),
+                                        C.c_double(normalizer)))
+        return dpk, dpv
+
+    def zero_grads(self):
+        check(lib().cf_model_zero_grads(self.h))
+
     def close(self):
         if self.h and self.h.value:
             lib().cf_model_destroy(self.h)
             self.h = C.c_void_p()
+
+
+class SegmentTape:
+    """Retained activations of one segment_forward (cf_segment)."""
+
+    def __init__(self, h, prefix_len, model):
+        self.h = h
+        self.prefix_len = prefix_len
+        self.model = model  # the tape's device memory lives in the model's context
+
+    def close(self):
+        if self.h and self.h.value and self.model.h and self.model.h.value:
+            lib().cf_segment_destroy(self.h)
+        self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Step:

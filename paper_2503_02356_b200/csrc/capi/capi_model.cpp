@@ -19,6 +19,9 @@ struct cf_model {
   cfb::Model* m = nullptr;
   cf_ctx* ctx = nullptr;
 };
+struct cf_segment {
+  cfb::SegmentState* s = nullptr;
+};
 namespace {
 void need(const void* p, const char* what) {
   if (!p) throw cfb::ValidationError(std::string(what) + " is null");
@@ -320,6 +323,42 @@ int cf_backward_full(cf_ctx* ctx, cf_model* model, const int64_t* seq_ids, const
     cfb::Batch b{seq_ids, lengths, tokens, nullptr, n};
     cfb::run_plan(&ctx->c, model->m, p, b, o, result);
   });
+}
+
+int cf_segment_forward(cf_ctx* ctx, cf_model* model, const int32_t* tokens, int64_t len, const int64_t* targets,
+                       const double* prefix_k, const double* prefix_v, int64_t prefix_len, int keep_tape,
+                       double* loss_sum, double* saved_k, double* saved_v, cf_segment** tape) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    if (tape) *tape = nullptr;
+    if (keep_tape && !tape) throw cfb::ValidationError("tape out-pointer required when keep_tape is set");
+    cfb::SegmentState* s = cfb::segment_forward(&ctx->c, model->m, tokens, len, targets, prefix_k, prefix_v,
+                                                prefix_len, keep_tape != 0, loss_sum, saved_k, saved_v);
+    if (s) {
+      auto h = std::make_unique<cf_segment>();
+      h->s = s;
+      *tape = h.release();
+    }
+  });
+}
+
+int cf_segment_backward(cf_ctx* ctx, cf_model* model, const cf_segment* tape, const double* prefix_k,
+                        const double* prefix_v, double* d_prefix_k, double* d_prefix_v, const double* incoming_dk,
+                        const double* incoming_dv, double normalizer) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    need(model, "model");
+    if (!tape) throw cfb::ValidationError("segment backward requires a retained tape");
+    cfb::segment_backward(&ctx->c, model->m, tape->s, prefix_k, prefix_v, d_prefix_k, d_prefix_v, incoming_dk,
+                          incoming_dv, normalizer);
+  });
+}
+
+void cf_segment_destroy(cf_segment* tape) {
+  if (!tape) return;
+  cfb::segment_destroy(tape->s);
+  delete tape;
 }
 
 int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t q_stride, const void* k,

@@ -455,6 +455,125 @@ struct cf_step {
 
 namespace cfb {
 
+// Appends one chunk's device metadata (tokens, targets, positions, attention
+// segments and tiles, embedding-backward CSR) to `meta` and records the
+// offsets in `cm`.  seg_ls: per segment (length, start position in its
+// sequence); a dependent chunk's keys are its sequence's rows [0, start+len)
+// of the group KV cache.
+void append_chunk_meta(ChunkMeta& cm, std::vector<int32_t>& meta, const std::vector<int32_t>& tk_rows,
+                       const std::vector<int32_t>& tg, const std::vector<int32_t>& ps,
+                       const std::vector<std::pair<int64_t, int64_t>>& seg_ls) {
+  auto put = [&](int32_t v) { meta.push_back(v); };
+  auto here = [&]() { return static_cast<int64_t>(meta.size()); };
+  cm.T = static_cast<int64_t>(tk_rows.size());
+  cm.pairs = 0;
+  for (const auto& [len, start] : seg_ls) {
+    const double L_ = static_cast<double>(len), P_ = static_cast<double>(start);
+    cm.pairs += L_ * P_ + L_ * (L_ + 1) / 2;
+  }
+  cm.o_tok = here();
+  std::vector<std::pair<int32_t, int32_t>> tok_rows;
+  for (size_t r = 0; r < tk_rows.size(); ++r) {
+    put(tk_rows[r]);
+    tok_rows.emplace_back(tk_rows[r], static_cast<int32_t>(r));
+  }
+  cm.o_tgt = here();
+  for (int32_t v : tg) put(v);
+  cm.o_pos = here();
+  for (int32_t v : ps) put(v);
+  // attention segments and tiles
+  while (meta.size() % 4) put(0);
+  cm.o_segs = here();
+  std::vector<AttnSeg> segs;
+  int32_t qs = 0;
+  for (const auto& [len, start] : seg_ls) {
+    AttnSeg a;
+    a.q_start = qs;
+    a.len = static_cast<int32_t>(len);
+    a.prefix = static_cast<int32_t>(cm.dependent ? start : 0);
+    a.kv_row0 = cm.dependent ? 0 : qs;
+    segs.push_back(a);
+    qs += a.len;
+  }
+  for (const AttnSeg& a : segs) {
+    put(a.q_start);
+    put(a.len);
+    put(a.kv_row0);
+    put(a.prefix);
+  }
+  cm.nsegs = static_cast<int64_t>(segs.size());
+  cm.o_qt = here();
+  for (size_t s = 0; s < segs.size(); ++s)
+    for (int32_t f = 0; f < segs[s].len; f += 64) {
+      put(static_cast<int32_t>(s));
+      put(f);
+      put(std::min(64, segs[s].len - f));
+      put(0);
+      ++cm.nqt;
+    }
+  cm.o_kt = here();
+  for (size_t s = 0; s < segs.size(); ++s) {
+    const int32_t nk = segs[s].prefix + segs[s].len;
+    for (int32_t f = 0; f < nk; f += 64) {
+      put(static_cast<int32_t>(s));
+      put(f);
+      put(std::min(64, nk - f));
+      put(0);
+      ++cm.nkt;
+    }
+  }
+  // 128-query tiles, heaviest (most visible keys) first so the causal tail
+  // of the grid is short; 128-key tiles likewise by number of queries.
+  {
+    std::vector<std::array<int32_t, 4>> qt, kt;
+    for (size_t s = 0; s < segs.size(); ++s) {
+      for (int32_t f = 0; f < segs[s].len; f += 128)
+        qt.push_back({static_cast<int32_t>(s), f, std::min(128, segs[s].len - f), segs[s].prefix + f});
+      const int32_t nk = segs[s].prefix + segs[s].len;
+      for (int32_t f = 0; f < nk; f += 128)
+        kt.push_back({static_cast<int32_t>(s), f, std::min(128, nk - f),
+                      segs[s].len - std::max(0, f - segs[s].prefix)});
+    }
+    auto by_work = [](const std::array<int32_t, 4>& x, const std::array<int32_t, 4>& y) { return x[3] > y[3]; };
+    std::stable_sort(qt.begin(), qt.end(), by_work);
+    std::stable_sort(kt.begin(), kt.end(), by_work);
+    cm.o_qt128 = here();
+    for (auto& x : qt) {
+      put(x[0]);
+      put(x[1]);
+      put(x[2]);
+      put(0);
+    }
+    cm.nqt128 = static_cast<int64_t>(qt.size());
+    cm.o_kt128 = here();
+    for (auto& x : kt) {
+      put(x[0]);
+      put(x[1]);
+      put(x[2]);
+      put(0);
+    }
+    cm.nkt128 = static_cast<int64_t>(kt.size());
+  }
+  // embedding-backward CSR: rows grouped by token id, ascending rows
+  std::sort(tok_rows.begin(), tok_rows.end());
+  cm.o_order = here();
+  for (const auto& tr : tok_rows) put(tr.second);
+  std::vector<int32_t> uniq, uoff;
+  for (size_t i = 0; i < tok_rows.size(); ++i) {
+    if (i == 0 || tok_rows[i].first != tok_rows[i - 1].first) {
+      uniq.push_back(tok_rows[i].first);
+      uoff.push_back(static_cast<int32_t>(i));
+    }
+  }
+  uoff.push_back(static_cast<int32_t>(tok_rows.size()));
+  cm.o_uniq = here();
+  for (int32_t v : uniq) put(v);
+  cm.o_uoff = here();
+  for (int32_t v : uoff) put(v);
+  cm.nuniq = static_cast<int64_t>(uniq.size());
+  while (meta.size() % 4) put(0);
+}
+
 // Builds metadata for every chunk of the plan.
 cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
   auto st = std::make_unique<cf_step>();
@@ -483,22 +602,17 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
   const double Nhead = static_cast<double>(m->d * m->V);
   const double attn_unit = static_cast<double>(m->H * m->dh);
   std::vector<int32_t> meta;
-  auto put = [&](int32_t v) { meta.push_back(v); };
-  auto here = [&]() { return static_cast<int64_t>(meta.size()); };
   for (size_t ci = 0; ci < plan.chunks.size(); ++ci) {
     const Chunk& c = plan.chunks[ci];
     ChunkMeta cm;
     cm.id = c.id;
-    cm.T = c.total;
     cm.dependent = c.kind == kDependent;
     cm.group = c.group;
     cm.index = c.index;
     st->pos_of[c.id] = static_cast<int64_t>(ci);
     // tokens / targets / positions (plan_runner.hpp:112-122)
-    cm.o_tok = here();
-    std::vector<int32_t> tg, ps;
-    std::vector<std::pair<int32_t, int32_t>> tok_rows;
-    int32_t row = 0;
+    std::vector<int32_t> tk_rows, tg, ps;
+    std::vector<std::pair<int64_t, int64_t>> seg_ls;
     for (int64_t s = 0; s < c.seg_cnt; ++s) {
       const Segment& sg = plan.segments[static_cast<size_t>(c.seg_off + s)];
       auto it = idx_of.find(sg.seq);
@@ -509,8 +623,7 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
       const int32_t* tk = b.tokens_host + tok_off[it->second];
       for (int64_t t = 0; t < sg.len; ++t) {
         const int64_t p = sg.start + t;
-        put(tk[p]);
-        tok_rows.emplace_back(tk[p], row++);
+        tk_rows.push_back(tk[p]);
         tg.push_back(p + 1 < len ? tk[p + 1] : -1);
         ps.push_back(static_cast<int32_t>(p));
       }
@@ -520,105 +633,9 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
         cm.seq_len = len;
         st->group_len[c.group] = len;
       }
-      const double L_ = static_cast<double>(sg.len), P_ = static_cast<double>(sg.start);
-      cm.pairs += L_ * P_ + L_ * (L_ + 1) / 2;
+      seg_ls.emplace_back(sg.len, sg.start);
     }
-    cm.o_tgt = here();
-    for (int32_t v : tg) put(v);
-    cm.o_pos = here();
-    for (int32_t v : ps) put(v);
-    // attention segments and tiles
-    while (meta.size() % 4) put(0);
-    cm.o_segs = here();
-    std::vector<AttnSeg> segs;
-    int32_t qs = 0;
-    for (int64_t s = 0; s < c.seg_cnt; ++s) {
-      const Segment& sg = plan.segments[static_cast<size_t>(c.seg_off + s)];
-      AttnSeg a;
-      a.q_start = qs;
-      a.len = static_cast<int32_t>(sg.len);
-      a.prefix = static_cast<int32_t>(cm.dependent ? sg.start : 0);
-      a.kv_row0 = cm.dependent ? 0 : qs;
-      segs.push_back(a);
-      qs += a.len;
-    }
-    for (const AttnSeg& a : segs) {
-      put(a.q_start);
-      put(a.len);
-      put(a.kv_row0);
-      put(a.prefix);
-    }
-    cm.nsegs = static_cast<int64_t>(segs.size());
-    cm.o_qt = here();
-    for (size_t s = 0; s < segs.size(); ++s)
-      for (int32_t f = 0; f < segs[s].len; f += 64) {
-        put(static_cast<int32_t>(s));
-        put(f);
-        put(std::min(64, segs[s].len - f));
-        put(0);
-        ++cm.nqt;
-      }
-    cm.o_kt = here();
-    for (size_t s = 0; s < segs.size(); ++s) {
-      const int32_t nk = segs[s].prefix + segs[s].len;
-      for (int32_t f = 0; f < nk; f += 64) {
-        put(static_cast<int32_t>(s));
-        put(f);
-        put(std::min(64, nk - f));
-        put(0);
-        ++cm.nkt;
-      }
-    }
-    // 128-query tiles, heaviest (most visible keys) first so the causal tail
-    // of the grid is short; 128-key tiles likewise by number of queries.
-    {
-      std::vector<std::array<int32_t, 4>> qt, kt;
-      for (size_t s = 0; s < segs.size(); ++s) {
-        for (int32_t f = 0; f < segs[s].len; f += 128)
-          qt.push_back({static_cast<int32_t>(s), f, std::min(128, segs[s].len - f), segs[s].prefix + f});
-        const int32_t nk = segs[s].prefix + segs[s].len;
-        for (int32_t f = 0; f < nk; f += 128)
-          kt.push_back({static_cast<int32_t>(s), f, std::min(128, nk - f),
-                        segs[s].len - std::max(0, f - segs[s].prefix)});
-      }
-      auto by_work = [](const std::array<int32_t, 4>& x, const std::array<int32_t, 4>& y) { return x[3] > y[3]; };
-      std::stable_sort(qt.begin(), qt.end(), by_work);
-      std::stable_sort(kt.begin(), kt.end(), by_work);
-      cm.o_qt128 = here();
-      for (auto& x : qt) {
-        put(x[0]);
-        put(x[1]);
-        put(x[2]);
-        put(0);
-      }
-      cm.nqt128 = static_cast<int64_t>(qt.size());
-      cm.o_kt128 = here();
-      for (auto& x : kt) {
-        put(x[0]);
-        put(x[1]);
-        put(x[2]);
-        put(0);
-      }
-      cm.nkt128 = static_cast<int64_t>(kt.size());
-    }
-    // embedding-backward CSR: rows grouped by token id, ascending rows
-    std::sort(tok_rows.begin(), tok_rows.end());
-    cm.o_order = here();
-    for (const auto& tr : tok_rows) put(tr.second);
-    std::vector<int32_t> uniq, uoff;
-    for (size_t i = 0; i < tok_rows.size(); ++i) {
-      if (i == 0 || tok_rows[i].first != tok_rows[i - 1].first) {
-        uniq.push_back(tok_rows[i].first);
-        uoff.push_back(static_cast<int32_t>(i));
-      }
-    }
-    uoff.push_back(static_cast<int32_t>(tok_rows.size()));
-    cm.o_uniq = here();
-    for (int32_t v : uniq) put(v);
-    cm.o_uoff = here();
-    for (int32_t v : uoff) put(v);
-    cm.nuniq = static_cast<int64_t>(uniq.size());
-    while (meta.size() % 4) put(0);
+    append_chunk_meta(cm, meta, tk_rows, tg, ps, seg_ls);
     st->tokens += cm.T;
     st->mf_layer += 6.0 * Nlayer * static_cast<double>(cm.T) + 12.0 * attn_unit * cm.pairs;
     st->mf_head += 6.0 * Nhead * static_cast<double>(cm.T);
@@ -1650,6 +1667,215 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
     if (e) CK(cudaEventDestroy(e));
   r.finish(res, true);
 }
+
+// ------------------------------------------------------ segment operators
+// detail::segment_forward / segment_backward (toy_model.hpp:206, :341) on
+// the GPU: one contiguous segment of one sequence with its prefix K/V passed
+// in by the caller.  It runs as a one-chunk dependent step whose KV state
+// spans positions [0, prefix_len + len): the caller's prefix rows are
+// uploaded, the segment's own rows are written by the forward, and the same
+// Exec forward / backward as run_plan does the math.
+struct SegmentState {
+  Ctx* ctx = nullptr;
+  Model* m = nullptr;
+  cf_step* st = nullptr;
+  GroupState gs;
+  Tape tape;
+  bool kept = false;
+  int64_t len = 0, prefix = 0;
+  ~SegmentState() {
+    if (tape.mem) pool_free(ctx, tape.mem);
+    if (gs.mem) pool_free(ctx, gs.mem);
+    step_destroy(st);
+  }
+};
+
+namespace {
+
+// host fp64 [L][rows][kvw] -> bf16 rows [row0, row0 + rows) of a [L][S][kvw] cache
+void upload_kv_rows(Ctx* ctx, Model* m, const double* host, int64_t rows, bf16* cache, int64_t S, int64_t row0) {
+  if (rows <= 0) return;
+  const int64_t n = m->L * rows * m->kvw;
+  double* tmp = static_cast<double*>(pool_alloc(ctx, n * 8));
+  CK(cudaMemcpyAsync(tmp, host, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, ctx->stream));
+  for (int64_t l = 0; l < m->L; ++l)
+    CK(cfk::f64_to_bf16(tmp + l * rows * m->kvw, rows, m->kvw, cache + (l * S + row0) * m->kvw, m->kvw, ctx->stream));
+  pool_free(ctx, tmp);
+  CK(cudaStreamSynchronize(ctx->stream));  // the host buffer may be reused on return
+}
+
+void upload_segment_prefix(Ctx* ctx, Model* m, SegmentState& sg, const double* pk, const double* pv) {
+  if (sg.prefix == 0) return;
+  if (!pk || !pv) throw ValidationError("prefix keys/values required when prefix_len > 0");
+  upload_kv_rows(ctx, m, pk, sg.prefix, sg.gs.kc, sg.gs.S, 0);
+  upload_kv_rows(ctx, m, pv, sg.prefix, sg.gs.vc, sg.gs.S, 0);
+}
+
+}  // namespace
+
+SegmentState* segment_forward(Ctx* ctx, Model* m, const int32_t* tokens, int64_t len, const int64_t* targets,
+                              const double* prefix_k, const double* prefix_v, int64_t prefix_len, bool keep_tape,
+                              double* loss_sum, double* saved_k, double* saved_v) {
+  if (!m->has_embed || !m->has_head) throw ValidationError("segment operators need an unstaged model");
+  if (len < 1) throw ValidationError("segment length must be positive");
+  if (prefix_len < 0) throw ValidationError("prefix_len must be non-negative");
+  if (!tokens || !targets) throw ValidationError("tokens and targets are required");
+  std::vector<int32_t> tk(tokens, tokens + len), tg(static_cast<size_t>(len)), ps(static_cast<size_t>(len));
+  for (int64_t t = 0; t < len; ++t) {
+    if (tokens[t] < 0 || tokens[t] >= m->V)
+      throw ValidationError("token id " + std::to_string(tokens[t]) + " out of vocabulary range");
+    if (targets[t] < -1 || targets[t] >= m->V)
+      throw ValidationError("target id " + std::to_string(targets[t]) + " out of vocabulary range");
+    tg[static_cast<size_t>(t)] = static_cast<int32_t>(targets[t]);
+    ps[static_cast<size_t>(t)] = static_cast<int32_t>(prefix_len + t);
+  }
+  auto sg = std::make_unique<SegmentState>();
+  sg->ctx = ctx;
+  sg->m = m;
+  sg->len = len;
+  sg->prefix = prefix_len;
+  sg->st = new cf_step();
+  cf_step* st = sg->st;
+  ChunkMeta cm;
+  cm.dependent = true;
+  cm.group = 0;
+  cm.index = 0;
+  cm.seq = 0;
+  cm.start = prefix_len;
+  cm.seq_len = prefix_len + len;
+  std::vector<int32_t> meta;
+  append_chunk_meta(cm, meta, tk, tg, ps, {{len, prefix_len}});
+  st->chunks.push_back(cm);
+  st->pos_of[0] = 0;
+  st->tokens = len;
+  st->meta_len = static_cast<int64_t>(meta.size());
+  CK(cudaMalloc(&st->meta_dev, static_cast<size_t>(st->meta_len + 4) * 4));
+  CK(cudaMemcpyAsync(st->meta_dev, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+
+  GroupState& g = sg->gs;
+  g.S = prefix_len + len;
+  const int64_t cache = m->L * g.S * m->kvw;
+  g.mem = pool_alloc(ctx, 3 * 256 + cache * 2 * 2 + cache * 2 * 4);
+  Arena a{static_cast<char*>(g.mem), 0};
+  g.kc = a.take<bf16>(cache);
+  g.vc = a.take<bf16>(cache);
+  g.dkv = a.take<float>(cache * 2);
+  CK(cudaMemsetAsync(g.kc, 0, static_cast<size_t>(cache) * 2, ctx->stream));
+  CK(cudaMemsetAsync(g.vc, 0, static_cast<size_t>(cache) * 2, ctx->stream));
+  upload_segment_prefix(ctx, m, *sg, prefix_k, prefix_v);
+
+  Exec ex;
+  ex.ctx = ctx;
+  ex.m = m;
+  ex.st = st;
+  ex.s = ctx->stream;
+  ex.inv_norm = 1.0f;  // dlogits are rebuilt with the normalizer by segment_backward
+  ex.loss_slots = static_cast<double*>(pool_alloc(ctx, 8));
+  CK(cudaMemsetAsync(ex.loss_slots, 0, 8, ex.s));
+  Tape t = ex.alloc_tape(len, keep_tape);
+  ex.forward(cm, t, &g, 0, keep_tape);
+  double ls = 0;
+  CK(cudaMemcpyAsync(&ls, ex.loss_slots, 8, cudaMemcpyDeviceToHost, ex.s));
+  pool_free(ctx, ex.loss_slots);
+  // the segment's own key/value rows (what a later segment's prefix is built from)
+  const int64_t n = m->L * len * m->kvw;
+  double* tmp = (saved_k || saved_v) ? static_cast<double*>(pool_alloc(ctx, n * 8)) : nullptr;
+  for (int kv = 0; kv < 2; ++kv) {
+    double* host = kv ? saved_v : saved_k;
+    if (!host) continue;
+    const bf16* src = kv ? g.vc : g.kc;
+    for (int64_t l = 0; l < m->L; ++l)
+      CK(cfk::bf16_to_f64(src + (l * g.S + prefix_len) * m->kvw, m->kvw, len, m->kvw, tmp + l * len * m->kvw, ex.s));
+    CK(cudaMemcpyAsync(host, tmp, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ex.s));
+  }
+  if (tmp) pool_free(ctx, tmp);
+  CK(cudaStreamSynchronize(ex.s));
+  ctx->launches += ex.launches;
+  if (loss_sum) *loss_sum = ls;
+  if (!keep_tape) {
+    ex.free_tape(t);
+    return nullptr;
+  }
+  sg->tape = t;
+  sg->kept = true;
+  return sg.release();
+}
+
+void segment_backward(Ctx* ctx, Model* m, SegmentState* sg, const double* prefix_k, const double* prefix_v,
+                      double* d_prefix_k, double* d_prefix_v, const double* incoming_dk, const double* incoming_dv,
+                      double normalizer) {
+  if (!sg || !sg->kept) throw ValidationError("segment backward requires a retained tape");
+  if (sg->m != m) throw ValidationError("segment tape belongs to another model");
+  if (!(normalizer > 0)) throw ValidationError("normalizer must be positive");
+  const ChunkMeta& cm = sg->st->chunks[0];
+  GroupState& g = sg->gs;
+  Tape& t = sg->tape;
+  const int64_t T = sg->len, d = m->d, kvw = m->kvw, Vp = align_up(m->V, 8);
+  cudaStream_t s = ctx->stream;
+  upload_segment_prefix(ctx, m, *sg, prefix_k, prefix_v);
+  // dK/dV store: gradients of the segment's own rows from later chunks
+  CK(cudaMemsetAsync(g.dkv, 0, static_cast<size_t>(m->L * g.S * 2 * kvw) * 4, s));
+  for (int kv = 0; kv < 2; ++kv) {
+    const double* host = kv ? incoming_dv : incoming_dk;
+    if (!host) continue;
+    const int64_t n = m->L * T * kvw;
+    double* tmp = static_cast<double*>(pool_alloc(ctx, n * 8));
+    CK(cudaMemcpyAsync(tmp, host, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, s));
+    for (int64_t l = 0; l < m->L; ++l)
+      CK(cfk::f64_to_f32(tmp + l * T * kvw, T, kvw, g.dkv + (l * g.S + sg->prefix) * 2 * kvw + kv * kvw, 2 * kvw, s));
+    pool_free(ctx, tmp);
+    CK(cudaStreamSynchronize(s));
+  }
+  Exec ex;
+  ex.ctx = ctx;
+  ex.m = m;
+  ex.st = sg->st;
+  ex.s = s;
+  ex.inv_norm = static_cast<float>(1.0 / normalizer);
+  // output head + cross-entropy gradient with the caller's normalizer
+  {
+    bf16* xnf = t.xnf;
+    bf16* A = nullptr;
+    if (!xnf) {
+      A = static_cast<bf16*>(pool_alloc(ctx, T * d * 2));
+      const float* xL = t.x_in + m->L * T * d;
+      if (m->llama)
+        ex.L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
+      else
+        ex.L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
+      xnf = A;
+    }
+    float* logits = static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4));
+    ex.gemm(xnf, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
+    ex.L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, ex.meta<const int32_t>(cm.o_tgt), ex.inv_norm, logits + T * Vp,
+                         t.dlogits, s),
+         "ce");
+    pool_free(ctx, logits);
+    if (A) pool_free(ctx, A);
+  }
+  ex.backward(cm, t, &g, nullptr);
+  // gradients for the prefix rows
+  if (sg->prefix > 0 && (d_prefix_k || d_prefix_v)) {
+    const int64_t n = m->L * sg->prefix * kvw;
+    double* tmp = static_cast<double*>(pool_alloc(ctx, n * 8));
+    std::vector<double> host(static_cast<size_t>(n));
+    for (int kv = 0; kv < 2; ++kv) {
+      double* out = kv ? d_prefix_v : d_prefix_k;
+      if (!out) continue;
+      for (int64_t l = 0; l < m->L; ++l)
+        CK(cfk::f32_to_f64(g.dkv + l * g.S * 2 * kvw + kv * kvw, 2 * kvw, sg->prefix, kvw, tmp + l * sg->prefix * kvw,
+                           s));
+      CK(cudaMemcpyAsync(host.data(), tmp, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      for (int64_t i = 0; i < n; ++i) out[i] += host[static_cast<size_t>(i)];  // accumulated, as the reference does
+    }
+    pool_free(ctx, tmp);
+  }
+  CK(cudaStreamSynchronize(s));
+  ctx->launches += ex.launches;
+}
+
+void segment_destroy(SegmentState* sg) { delete sg; }
 
 void run_plan(Ctx* ctx, Model* m, const Plan& plan, const Batch& b, const cf_run_opts& opts, cf_run_result* res) {
   cf_step* st = step_prepare(ctx, m, plan, b);

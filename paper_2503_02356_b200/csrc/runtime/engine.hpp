@@ -106,6 +106,17 @@ void run_plan(Ctx* ctx, Model* m, const Plan& plan, const Batch& b, const cf_run
 cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b);
 void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_result* res);
 void step_destroy(cf_step* st);
+// Operator level (detail::segment_forward / segment_backward,
+// toy_model.hpp:206, :341): one segment of one sequence with a caller-held
+// prefix.  K/V and their gradients are host fp64 [L][rows][kv_width].
+struct SegmentState;
+SegmentState* segment_forward(Ctx* ctx, Model* m, const int32_t* tokens, int64_t len, const int64_t* targets,
+                              const double* prefix_k, const double* prefix_v, int64_t prefix_len, bool keep_tape,
+                              double* loss_sum, double* saved_k, double* saved_v);
+void segment_backward(Ctx* ctx, Model* m, SegmentState* sg, const double* prefix_k, const double* prefix_v,
+                      double* d_prefix_k, double* d_prefix_v, const double* incoming_dk, const double* incoming_dv,
+                      double normalizer);
+void segment_destroy(SegmentState* sg);
 void step_op_times(const cf_step* st, int64_t* n, int64_t* kinds, int64_t* ids, double* ms);
 int64_t step_input_bytes(const cf_step* st);
 // Pipeline-parallel step of one stage on this rank (ctx has PP links): the
