@@ -16,13 +16,19 @@ METRICS = {
     "launch__grid_size": "grid",
     "launch__registers_per_thread": "regs",
 }
+# reported when the capture has them (--set full does)
+OPTIONAL = {
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pct",
+    "sm__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
+    "sm__warps_active.avg.per_cycle_active": "warps_active",
+}
 SCALE = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "s": 1.0, "nsecond": 1e-9,
          "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "hz": 1.0, "Khz": 1e3, "Mhz": 1e6,
          "Ghz": 1e9, "%": 1.0, "": 1.0, "register/thread": 1.0}
 
 
 def read(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join({**METRICS, **OPTIONAL})],
                          capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     head, units = rows[0], rows[1]
@@ -32,6 +38,9 @@ def read(rep):
         rec = {"kernel": r[idx["Kernel Name"]].split("(")[0].replace("(anonymous namespace)::", "")}
         for m, key in METRICS.items():
             rec[key] = float(r[idx[m]].replace(",", "")) * SCALE.get(units[idx[m]], 1.0)
+        for m, key in OPTIONAL.items():
+            if m in idx and r[idx[m]] not in ("", "n/a"):
+                rec[key] = float(r[idx[m]].replace(",", "")) * SCALE.get(units[idx[m]], 1.0)
         rec["dram_bytes"] = rec["dram_read"] + rec["dram_write"]
         launches.append(rec)
     return launches
