@@ -482,6 +482,15 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
                const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
                int64_t m, int64_t n, int64_t k, int epi, const void* residual,
                int64_t ld_res);
+/* The q|k|v projection with RoPE (and the KV-cache copy) in its epilogue:
+ * C[m, n] = bf16(A[m, k] W[k, n]) then rotate-half RoPE on the q and k heads
+ * (head_dim 128; columns [0, col_v)) with tab = float2 (cos, sin) [m][64];
+ * kc / vc (may be NULL) receive the k columns [col_k, col_v) and the v
+ * columns [col_v, n) with row pitch cache_ld.  CF_EVALIDATION-class error
+ * (cudaErrorInvalidValue) when the shape is not eligible (tile alignment). */
+int cf_op_gemm_rope(cf_ctx* ctx, const void* a, int64_t lda, const void* w, int64_t ldw,
+                    void* c, int64_t m, int64_t n, int64_t k, const void* tab,
+                    int64_t col_k, int64_t col_v, void* kc, void* vc, int64_t cache_ld);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -454,6 +454,22 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda, const void
   });
 }
 
+int cf_op_gemm_rope(cf_ctx* ctx, const void* a, int64_t lda, const void* w, int64_t ldw, void* c, int64_t m,
+                    int64_t n, int64_t k, const void* tab, int64_t col_k, int64_t col_v, void* kc, void* vc,
+                    int64_t cache_ld) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    cfk::GemmDesc d{a, lda, 1, w, ldw, 0, c, n, tab, 64, m, n, k, cfk::EPI_BF16_ROPE};
+    d.col_k = col_k;
+    d.col_v = col_v;
+    d.kc = kc;
+    d.vc = vc;
+    d.cache_ld = cache_ld;
+    cfb::cuda_check(cfk::gemm(d, ctx->c.stream), "gemm_rope");
+    ctx->c.launches += 1;
+  });
+}
+
 }  // extern "C"
 
 extern "C" int cf_debug_set_gemm_mode(int mode) {

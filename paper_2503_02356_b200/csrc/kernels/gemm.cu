@@ -49,6 +49,10 @@ struct Args {
   int64_t ldr;
   int group_m;  // raster: tiles walk group_m M-blocks x all N-blocks, M fastest
   int split_n;  // EPI_BF16_SWIGLU: F (the up half starts at column F)
+  int col_k, col_v;  // EPI_BF16_ROPE
+  __nv_bfloat16* kc;
+  __nv_bfloat16* vc;
+  int64_t cache_ld;
 };
 
 // Grouped raster.  Persistent CTAs take consecutive tile indices, so one wave
@@ -358,6 +362,49 @@ __device__ __forceinline__ void swiglu_store_row32(const Args& g, int row, int c
   }
 }
 
+// EPI_BF16_ROPE: columns col0.. and col0+64.. of one head (rotate-half
+// partners), 32 each, rounded to bf16 first as rope_qk does, rotated when
+// the head is a q or k head, stored, and copied to the KV cache for k / v.
+__device__ __forceinline__ void rope_store_pair32(const Args& g, int row, int col0, const uint32_t (&ra)[32],
+                                                  const uint32_t (&rb)[32]) {
+  uint32_t pa[16], pb[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    pa[e] = pack_bf16(__uint_as_float(ra[2 * e]), __uint_as_float(ra[2 * e + 1]));
+    pb[e] = pack_bf16(__uint_as_float(rb[2 * e]), __uint_as_float(rb[2 * e + 1]));
+  }
+  if (col0 < g.col_v) {
+    const float4* tp = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(g.R) +
+                                                       static_cast<int64_t>(row) * g.ldr + (col0 & 63));
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {  // pairs 2e, 2e+1 of this 32-column half
+      const float4 cs = tp[e];
+      const float a0 = __uint_as_float(pa[e] << 16), a1 = __uint_as_float(pa[e] & 0xFFFF0000u);
+      const float b0 = __uint_as_float(pb[e] << 16), b1 = __uint_as_float(pb[e] & 0xFFFF0000u);
+      pa[e] = pack_bf16(a0 * cs.x - b0 * cs.y, a1 * cs.z - b1 * cs.w);
+      pb[e] = pack_bf16(b0 * cs.x + a0 * cs.y, b1 * cs.z + a1 * cs.w);
+    }
+  }
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    reinterpret_cast<uint4*>(c)[q] = make_uint4(pa[4 * q], pa[4 * q + 1], pa[4 * q + 2], pa[4 * q + 3]);
+    reinterpret_cast<uint4*>(c + 64)[q] = make_uint4(pb[4 * q], pb[4 * q + 1], pb[4 * q + 2], pb[4 * q + 3]);
+  }
+  __nv_bfloat16* cache = nullptr;
+  if (col0 >= g.col_v)
+    cache = g.vc ? g.vc + static_cast<int64_t>(row) * g.cache_ld + (col0 - g.col_v) : nullptr;
+  else if (col0 >= g.col_k)
+    cache = g.kc ? g.kc + static_cast<int64_t>(row) * g.cache_ld + (col0 - g.col_k) : nullptr;
+  if (cache) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      reinterpret_cast<uint4*>(cache)[q] = make_uint4(pa[4 * q], pa[4 * q + 1], pa[4 * q + 2], pa[4 * q + 3]);
+      reinterpret_cast<uint4*>(cache + 64)[q] = make_uint4(pb[4 * q], pb[4 * q + 1], pb[4 * q + 2], pb[4 * q + 3]);
+    }
+  }
+}
+
 namespace pair {
 
 constexpr int kStages = 6;
@@ -550,6 +597,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           }
           if (row < g.M) swiglu_store_row32(g, row, nb * 128 + c * 32, rg, ru);
         }
+      } else if constexpr (EPI == EPI_BF16_ROPE) {
+        // rotate-half partners are 64 columns apart inside a 128-column head
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          const int ca = (c >> 1) * 4 + (c & 1);  // chunks 0,1,4,5 pair with 2,3,6,7
+          uint32_t ra[32], rb[32];
+          tmem_ld32(tbase + ca * 32, ra);
+          tmem_ld32(tbase + (ca + 2) * 32, rb);
+          tmem_ld_wait();
+          if (c == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+          }
+          if (row < g.M) rope_store_pair32(g, row, nb * 256 + ca * 32, ra, rb);
+        }
       } else {
         float4 pre[8];
         if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * 256, pre);
@@ -687,6 +750,11 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   // vs 1.6-2.2 at 8, tools/gemm_group_traffic.sh); long-K shapes prefer 8.
   g.group_m = raster_group(g.num_m, g.num_k <= 64 && g.num_n >= 24 ? 16 : 8);
   g.split_n = static_cast<int>(d.N / 2);
+  g.col_k = static_cast<int>(d.col_k);
+  g.col_v = static_cast<int>(d.col_v);
+  g.kc = static_cast<__nv_bfloat16*>(d.kc);
+  g.vc = static_cast<__nv_bfloat16*>(d.vc);
+  g.cache_ld = d.cache_ld;
   g.C = d.c;
   g.ldc = d.ldc;
   g.R = d.r;
@@ -711,6 +779,7 @@ cudaError_t pair_by_epi(const GemmDesc& d, cudaStream_t st) {
     case EPI_BF16_TANH: return launch_pair<A_MN, B_MN, EPI_BF16_TANH>(d, st);
     case EPI_BF16_TANHGRAD: return launch_pair<A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
     case EPI_BF16_SWIGLU: return launch_pair<A_MN, B_MN, EPI_BF16_SWIGLU>(d, st);
+    case EPI_BF16_ROPE: return launch_pair<A_MN, B_MN, EPI_BF16_ROPE>(d, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -762,6 +831,12 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
     return cudaErrorMisalignedAddress;
   const int64_t sms = gemm_num_sms();
   const int mode = gemm_mode();
+  if (d.epi == EPI_BF16_ROPE) {
+    if (!gemm_rope_ok(d.M, d.N, d.K, 128, d.col_k, d.col_v) || (reinterpret_cast<uintptr_t>(d.r) & 15) ||
+        d.ldr != 64 || ((d.kc || d.vc) && (d.cache_ld % 8)))
+      return cudaErrorInvalidValue;
+    return pair_by_major(d, st);
+  }
   if (d.epi == EPI_BF16_SWIGLU) {
     if (!gemm_swiglu_ok(d.M, d.N, d.K) || (reinterpret_cast<uintptr_t>(d.r) & 15) || (d.ldr % 8))
       return cudaErrorInvalidValue;
@@ -780,6 +855,13 @@ bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K) {
   const int64_t pair_tiles = ((M + 255) / 256) * (N / 256);
   const int mode = gemm_mode();
   return mode != 1 && N % 256 == 0 && M > 128 && K > 0 && (mode == 2 || pair_tiles >= gemm_num_sms() / 4);
+}
+
+bool gemm_rope_ok(int64_t M, int64_t N, int64_t K, int64_t dh, int64_t col_k, int64_t col_v) {
+  const int64_t pair_tiles = ((M + 255) / 256) * (N / 256);
+  const int mode = gemm_mode();
+  return mode != 1 && dh == 128 && N % 256 == 0 && col_k % 256 == 0 && col_v % 256 == 0 && col_k <= col_v &&
+         col_v <= N && M > 128 && K > 0 && (mode == 2 || pair_tiles >= gemm_num_sms() / 4);
 }
 
 // 0 = auto (CTA pairs when large), 1 = single-CTA only, 2 = CTA pairs whenever M, N > 128 (tests).

@@ -18,7 +18,13 @@ enum GemmEpi : int {
   // (H is passed as r / ldr).  Each CTA-pair tile pairs gate columns
   // [128j, 128j+128) with up columns F + [128j, 128j+128).  CTA-pair kernel,
   // F % 128 == 0 only (gemm_swiglu_ok).
-  EPI_BF16_SWIGLU = 6
+  EPI_BF16_SWIGLU = 6,
+  // C(bf16) = acc over [q | k | v] with rotate-half RoPE applied to the q and
+  // k columns (head_dim 128, R = float2 (cos, sin) table [M][64], ldr = 64,
+  // from the bf16-rounded values as rope_qk does), and the k / v columns
+  // also written to kc / vc (the KV cache rows of these tokens) when set.
+  // CTA-pair kernel only (gemm_rope_ok).
+  EPI_BF16_ROPE = 7
 };
 
 struct GemmDesc {
@@ -34,12 +40,20 @@ struct GemmDesc {
   int64_t ldr;
   int64_t M, N, K;
   int epi;
+  // EPI_BF16_ROPE: column where k starts / v starts, KV-cache copies
+  int64_t col_k = 0, col_v = 0;
+  void* kc = nullptr;
+  void* vc = nullptr;
+  int64_t cache_ld = 0;
 };
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
 // Whether EPI_BF16_SWIGLU is available for this problem (else run EPI_BF16
 // and the elementwise swiglu_fwd).
 bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K);
+// Whether EPI_BF16_ROPE is available ([q | k | v] of width N, head_dim dh,
+// k at col_k, v at col_v; else run EPI_BF16 + rope_qk + kv_store).
+bool gemm_rope_ok(int64_t M, int64_t N, int64_t K, int64_t dh, int64_t col_k, int64_t col_v);
 int gemm_num_sms();
 // 0 = auto (CTA-pair kernel for large GEMMs), 1 = single-CTA kernel only.
 int gemm_mode();

@@ -828,15 +828,29 @@ struct Exec {
         L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), xn1, s), "rmsnorm");
       else
         L(cfk::to_bf16(x, xn1, T * d, s), "to_bf16");
-      gemm(xn1, 1, d, ly.wqkv, 0, m->qkv_w, qkv, m->qkv_w, T, m->qkv_w, d, cfk::EPI_BF16);
-      if (m->llama)
-        L(cfk::rope_qk(qkv, m->qkv_w, T, static_cast<int>(m->H), static_cast<int>(m->KVH), static_cast<int>(m->dh),
-                       d, t.tab, s),
-          "rope");
-      if (cm.dependent)
-        L(cfk::kv_store(qkv, m->qkv_w, T, m->kvw, d, d + m->kvw, gs->kc + l * gs->S * m->kvw + cm.start * m->kvw,
-                        gs->vc + l * gs->S * m->kvw + cm.start * m->kvw, m->kvw, s),
-          "kv_store");
+      bf16* kc_rows = cm.dependent ? gs->kc + l * gs->S * m->kvw + cm.start * m->kvw : nullptr;
+      bf16* vc_rows = cm.dependent ? gs->vc + l * gs->S * m->kvw + cm.start * m->kvw : nullptr;
+      if (m->llama && cfk::gemm_rope_ok(T, m->qkv_w, d, m->dh, d, d + m->kvw)) {
+        // RoPE and the KV-cache copy in the q|k|v GEMM's epilogue
+        cfk::GemmDesc g{xn1, d, 1, ly.wqkv, m->qkv_w, 0, qkv, m->qkv_w, t.tab, m->dh / 2, T, m->qkv_w, d,
+                        cfk::EPI_BF16_ROPE};
+        g.col_k = d;
+        g.col_v = d + m->kvw;
+        g.kc = kc_rows;
+        g.vc = vc_rows;
+        g.cache_ld = m->kvw;
+        cudaEvent_t g0 = mark();
+        L(cfk::gemm(g, s), "gemm_rope");
+        close(g0, 0, 2.0 * static_cast<double>(T) * static_cast<double>(m->qkv_w) * static_cast<double>(d), 1);
+      } else {
+        gemm(xn1, 1, d, ly.wqkv, 0, m->qkv_w, qkv, m->qkv_w, T, m->qkv_w, d, cfk::EPI_BF16);
+        if (m->llama)
+          L(cfk::rope_qk(qkv, m->qkv_w, T, static_cast<int>(m->H), static_cast<int>(m->KVH),
+                         static_cast<int>(m->dh), d, t.tab, s),
+            "rope");
+        if (cm.dependent)
+          L(cfk::kv_store(qkv, m->qkv_w, T, m->kvw, d, d + m->kvw, kc_rows, vc_rows, m->kvw, s), "kv_store");
+      }
       AttnParams p = attn_params(cm, t, l, gs);
       cudaEvent_t t0 = mark();
       if (cfk::attn_fwd_pp_supported(p))

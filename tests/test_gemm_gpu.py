@@ -104,3 +104,47 @@ def test_gemm_swiglu_epilogue(ctx, shape, mode):
     ref = g * torch.sigmoid(g) * u
     err = (H.float() - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("shape,mode", [((384, 768, 256), 2), ((8192, 6144, 4096), 0)], ids=["forced-pair", "c2-qkv"])
+def test_gemm_rope_epilogue(ctx, shape, mode):
+    """EPI_BF16_ROPE: rotate-half RoPE on the q and k heads of the bf16-rounded
+    q|k|v GEMM output, v untouched, k / v copied to the KV-cache rows."""
+    M, N, K = shape
+    col_k, col_v = (256, 512) if N == 768 else (4096, 5120)
+    kvw = N - col_v
+    capi.check(capi.lib().cf_debug_set_gemm_mode(mode))
+    try:
+        A = _mk(M, K, 12)
+        B = _mk(K, N, 13)
+        pos = torch.arange(M, device="cuda", dtype=torch.float64) + 7
+        f = 10000.0 ** (-2.0 * torch.arange(64, device="cuda", dtype=torch.float64) / 128)
+        ang = pos[:, None] * f[None, :]
+        tab = torch.stack([torch.cos(ang), torch.sin(ang)], -1).float().contiguous()  # [M][64] (cos, sin)
+        C0 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        C1 = torch.zeros_like(C0)
+        kc = torch.zeros(M, kvw, device="cuda", dtype=torch.bfloat16)
+        vc = torch.zeros_like(kc)
+        torch.cuda.synchronize()
+        ctx.gemm(A.data_ptr(), 1, K, B.data_ptr(), 0, N, C0.data_ptr(), N, M, N, K, capi.EPI_BF16)
+        capi.check(capi.lib().cf_op_gemm_rope(ctx.h, capi.C.c_void_p(A.data_ptr()), capi.C.c_int64(K),
+                                              capi.C.c_void_p(B.data_ptr()), capi.C.c_int64(N),
+                                              capi.C.c_void_p(C1.data_ptr()), capi.C.c_int64(M), capi.C.c_int64(N),
+                                              capi.C.c_int64(K), capi.C.c_void_p(tab.data_ptr()),
+                                              capi.C.c_int64(col_k), capi.C.c_int64(col_v),
+                                              capi.C.c_void_p(kc.data_ptr()), capi.C.c_void_p(vc.data_ptr()),
+                                              capi.C.c_int64(kvw)))
+        ctx.synchronize()
+    finally:
+        capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+    x = C0.float()
+    ref = x.clone()
+    cs, sn = tab[..., 0], tab[..., 1]
+    for h0 in range(0, col_v, 128):
+        a, b = x[:, h0:h0 + 64], x[:, h0 + 64:h0 + 128]
+        ref[:, h0:h0 + 64] = a * cs - b * sn
+        ref[:, h0 + 64:h0 + 128] = b * cs + a * sn
+    err = (C1.float() - ref).abs().max().item() / ref.abs().max().item()
+    assert err < 1e-2, err
+    assert torch.equal(C1[:, col_v:], C0[:, col_v:])
+    assert torch.equal(kc, C1[:, col_k:col_v]) and torch.equal(vc, C1[:, col_v:])

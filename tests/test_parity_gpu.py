@@ -80,11 +80,13 @@ def test_run_plan_matches_oracle(ctx, oracle, case):
     model.close()
 
 
-def test_run_plan_matches_oracle_forced_pair_gemms(ctx, oracle):
+@pytest.mark.parametrize("kvh", [1, 2], ids=["gqa", "mha-rope-epilogue"])
+def test_run_plan_matches_oracle_forced_pair_gemms(ctx, oracle, kvh):
     """CTA-pair GEMMs at toy sizes (cf_debug_set_gemm_mode(2)), so the fused
     gate|up + SwiGLU epilogue and the pair epilogues run under the oracle,
-    including a recomputed forward (sequence of 3 chunks, K = 1)."""
-    gcfg, c = _cfgs(1, 96, 256, 2, 1, 2, 384)
+    including a recomputed forward (sequence of 3 chunks, K = 1).  With
+    kv_width 256 the q|k|v GEMM also carries RoPE and the KV-cache copy."""
+    gcfg, c = _cfgs(1, 96, 256, 2, kvh, 2, 384)
     lengths = np.array([700, 130, 301, 64], np.int64)
     tokens = cf.gen_tokens(lengths, 96, 13)
     capi.check(capi.lib().cf_debug_set_gemm_mode(2))
