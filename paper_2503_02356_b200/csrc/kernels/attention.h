@@ -42,6 +42,17 @@ struct AttnParams {
   int32_t num_tiles;
   int32_t T, H, KVH, dh;
   float scale;  // 1/sqrt(dh)
+  // tcgen05 backward only (attention_tc_bwd.cu), optional:
+  //   rope_tab: float2 (cos, sin) [T][dh/2]: dQ leaves the kernel with the
+  //             inverse rotation applied (RoPE backward) — and so does dK
+  //             when dkv_out is set
+  //   dkv_out:  bf16 dK / dV written directly at dkv_out + row*dkv_out_ld +
+  //             {col_k, col_v} + g*dh instead of being added into
+  //             dk_acc / dv_acc (standalone chunks: every key row is owned by
+  //             one CTA and nothing else accumulates into it)
+  const float2* rope_tab = nullptr;
+  __nv_bfloat16* dkv_out = nullptr;
+  int64_t dkv_out_ld = 0, col_k = 0, col_v = 0;
 };
 
 cudaError_t attn_forward(const AttnParams& p, cudaStream_t st);

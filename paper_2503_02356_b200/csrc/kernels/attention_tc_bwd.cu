@@ -52,7 +52,35 @@ struct Args {
   int64_t acc_stride;
   int32_t T, H, KVH;
   float sl2, scale;
+  const float2* rope_tab;   // RoPE backward on dQ (and dK with dkv_out)
+  __nv_bfloat16* dkv_out;   // direct bf16 dK / dV (standalone chunks)
+  int64_t dkv_out_ld, col_k, col_v;
 };
+
+// Inverse rotate-half of 32 (a, b) pairs (a = columns c0.., b = c0+64..)
+// with (cos, sin) pairs tab[c0 .. c0+32): the RoPE backward rope_qk applies.
+__device__ __forceinline__ void rope_inverse32(const float2* tab, float (&a)[32], float (&b)[32]) {
+  const float4* tp = reinterpret_cast<const float4*>(tab);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const float4 cs = tp[e];
+    const float s0 = -cs.y, s1 = -cs.w;
+    const float a0 = a[2 * e], b0 = b[2 * e], a1 = a[2 * e + 1], b1 = b[2 * e + 1];
+    a[2 * e] = a0 * cs.x - b0 * s0;
+    b[2 * e] = b0 * cs.x + a0 * s0;
+    a[2 * e + 1] = a1 * cs.z - b1 * s1;
+    b[2 * e + 1] = b1 * cs.z + a1 * s1;
+  }
+}
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32]) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    d4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+// bf16 round trip (the unfused path rotates the stored bf16 dQ)
+__device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -349,6 +377,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(&ds_free[last & 1], (last >> 1) & 1);
     tc_fence_after();
     __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+    if (a.rope_tab) {  // this half takes rotate-half partners: chunks (half, half + 2)
+      uint32_t ra[32], rb[32];
+      tmem_ld32(tQ + lane_off + half * 32, ra);
+      tmem_ld32(tQ + lane_off + (half + 2) * 32, rb);
+      tmem_ld_wait();
+      if (ok) {
+        float fa[32], fb[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          fa[e] = bf16_round(__uint_as_float(ra[e]) * a.scale);
+          fb[e] = bf16_round(__uint_as_float(rb[e]) * a.scale);
+        }
+        rope_inverse32(a.rope_tab + static_cast<int64_t>(q_row0 + row) * (DH / 2) + half * 32, fa, fb);
+        store_bf16x32(out + half * 32, fa);
+        store_bf16x32(out + (half + 2) * 32, fb);
+      }
+    } else {
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
       const int c = half * 2 + cc;  // 32-column chunk of dQ
@@ -365,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                              pack_bf16(__uint_as_float(r[8 * q + 4]) * sc, __uint_as_float(r[8 * q + 5]) * sc),
                              pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
       }
+    }
     }
   }
   tc_fence_before();
@@ -593,6 +639,30 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     const int last = iters - 1;
     mbar_wait(&pds_free[last & 1], (last >> 1) & 1);
     tc_fence_after();
+    if (a.dkv_out) {
+      // parts 0, 1: dK chunks (part, part + 2), rotated back; parts 2, 3: dV
+      // chunks (part - 2, part); bf16 straight into dq|dk|dv
+      const bool is_k = part < 2;
+      const int c0 = part & 1;
+      uint32_t ra[32], rb[32];
+      tmem_ld32((is_k ? tdK : tdV) + lane_off + c0 * 32, ra);
+      tmem_ld32((is_k ? tdK : tdV) + lane_off + (c0 + 2) * 32, rb);
+      tmem_ld_wait();
+      if (kok) {
+        const int64_t r = sg.kv_row0 + key;
+        float fa[32], fb[32];
+        const float sc = is_k ? a.scale : 1.f;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          fa[e] = __uint_as_float(ra[e]) * sc;
+          fb[e] = __uint_as_float(rb[e]) * sc;
+        }
+        if (is_k && a.rope_tab) rope_inverse32(a.rope_tab + r * (DH / 2) + c0 * 32, fa, fb);
+        __nv_bfloat16* dst = a.dkv_out + r * a.dkv_out_ld + (is_k ? a.col_k : a.col_v) + g * DH;
+        store_bf16x32(dst + c0 * 32, fa);
+        store_bf16x32(dst + (c0 + 2) * 32, fb);
+      }
+    } else {
     float* dkr = a.dk_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
     float* dvr = a.dv_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH;
     {
@@ -618,6 +688,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           reinterpret_cast<float4*>(dvr + c * 32)[q] = v4;
         }
       }
+    }
     }
   }
   tc_fence_before();
@@ -665,7 +736,7 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
     return cudaErrorInvalidValue;
   Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.o,
          p.o_stride, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e,
-         p.scale};
+         p.scale, p.rope_tab, p.dkv_out, p.dkv_out_ld, p.col_k, p.col_v};
   const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256 * 4 + 256;
   const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
   // once per process, thread-safe (concurrent contexts on host threads)

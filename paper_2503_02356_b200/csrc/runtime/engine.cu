@@ -996,11 +996,21 @@ struct Exec {
       p.dsum = dsum;
       p.dq = dqkv;
       p.dq_stride = qw;
-      const float* own_dk;
+      const float* own_dk = nullptr;
+      const bool tc = cfk::attn_tc_supported(p);
+      // tcgen05 path: RoPE backward of dQ in the dQ kernel; a standalone
+      // chunk's dK (rotated back) / dV go straight to dqkv in bf16
+      if (tc && m->llama) p.rope_tab = t.tab;
+      const bool direct = tc && !cm.dependent;
       if (cm.dependent) {
         float* own = p.dk_acc + cm.start * 2 * kvw;
         if (corrupt) L(cfk::scale_rows_f32(own, T, 2 * kvw, 2 * kvw, 1.0000001f, s), "corrupt");
         own_dk = own;
+      } else if (direct) {
+        p.dkv_out = dqkv;
+        p.dkv_out_ld = qw;
+        p.col_k = d;
+        p.col_v = d + kvw;
       } else {
         CK(cudaMemsetAsync(dkv_local, 0, static_cast<size_t>(T * 2 * kvw) * 4, s));
         p.dk_acc = dkv_local;
@@ -1008,7 +1018,7 @@ struct Exec {
         own_dk = dkv_local;
       }
       cudaEvent_t t0 = mark();
-      if (cfk::attn_tc_supported(p))
+      if (tc)
         L(cfk::attn_backward_tc(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
                                 meta<const AttnTile>(cm.o_kt128), static_cast<int32_t>(cm.nkt128),
                                 cm.dependent ? gs->S : T, s),
@@ -1016,10 +1026,11 @@ struct Exec {
       else
         L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
       close(t0, 2, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
-      L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
-                         m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
-        "dkv_to_dqkv");
-      if (m->llama)
+      if (!direct)
+        L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
+                           m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
+          "dkv_to_dqkv");
+      if (m->llama && !p.rope_tab)
         L(cfk::rope_bwd_q(dqkv, qw, T, static_cast<int>(m->H), static_cast<int>(m->dh), t.tab, s), "rope_bwd");
       // Projections (toy_model.hpp:497-511)
       const bf16* xn1 = t.xn1 ? t.xn1 + l * T * d : A;
