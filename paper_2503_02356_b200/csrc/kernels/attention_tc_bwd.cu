@@ -24,8 +24,17 @@ namespace {
 
 constexpr int DH = 128;
 constexpr int SUB = 64;                     // streamed sub-tile (keys for dQ, queries for dK/dV)
-constexpr int KS = 6, VS = 4;               // dQ kernel: K / V ring depths
-constexpr int QS = 4;                       // dK/dV kernel: Q/dO ring depth
+#ifndef CF_DQ_KS
+#define CF_DQ_KS 4
+#endif
+#ifndef CF_DQ_VS
+#define CF_DQ_VS 4
+#endif
+#ifndef CF_DKV_QS
+#define CF_DKV_QS 3
+#endif
+constexpr int KS = CF_DQ_KS, VS = CF_DQ_VS;  // dQ kernel: K / V ring depths
+constexpr int QS = CF_DKV_QS;                // dK/dV kernel: Q/dO ring depth
 constexpr uint32_t kBox128 = 128 * 64 * 2;  // [128 rows][64 cols] bf16
 constexpr uint32_t kBox64 = 64 * 64 * 2;    // [64 rows][64 cols]
 constexpr float kLog2e = 1.4426950408889634f;
