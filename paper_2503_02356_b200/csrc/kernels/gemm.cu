@@ -407,7 +407,10 @@ __device__ __forceinline__ void rope_store_pair32(const Args& g, int row, int co
 
 namespace pair {
 
-constexpr int kStages = 6;
+#ifndef CF_PAIR_STAGES
+#define CF_PAIR_STAGES 6
+#endif
+constexpr int kStages = CF_PAIR_STAGES;
 constexpr uint32_t kABytes = 128 * BK * 2;  // this CTA's half of A
 constexpr uint32_t kBBytes = 128 * BK * 2;  // this CTA's half of B
 constexpr size_t kSmem = 1024 + kStages * (kABytes + kBBytes) + 256;
