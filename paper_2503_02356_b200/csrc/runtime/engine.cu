@@ -811,6 +811,7 @@ struct Exec {
     const int32_t* tok = meta<const int32_t>(cm.o_tok);
     const int32_t* tgt = meta<const int32_t>(cm.o_tgt);
     bf16* A = static_cast<bf16*>(pool_alloc(ctx, T * std::max(d, m->ffn) * 2));
+    bf16* hscr = nullptr;  // SwiGLU output of a discard forward (fused epilogue)
     float* logits = m->has_head ? static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4)) : nullptr;
     float* row_loss = m->has_head ? logits + T * Vp : nullptr;
     if (m->has_embed) L(cfk::embed_fwd(tok, m->emb, d, T, t.x_in, s), "embed");
@@ -871,6 +872,12 @@ struct Exec {
         L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), xn2, s), "rmsnorm");
         bf16* hl = t.h ? t.h + l * T * m->ffn : A;
         if (cfk::gemm_swiglu_ok(T, m->gu_w, d)) {  // h written by the gate|up GEMM's epilogue
+          // the epilogue writes h while later tiles still load xn2: on a
+          // discard forward both would live in A, so h gets its own scratch
+          if (!t.h) {
+            if (!hscr) hscr = static_cast<bf16*>(pool_alloc(ctx, T * m->ffn * 2));
+            hl = hscr;
+          }
           gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16_SWIGLU, hl, m->ffn);
         } else {
           gemm(xn2, 1, d, ly.w1, 0, m->gu_w, act, m->gu_w, T, m->gu_w, d, cfk::EPI_BF16);
@@ -895,6 +902,7 @@ struct Exec {
       L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
       pool_free(ctx, logits);
     }
+    if (hscr) pool_free(ctx, hscr);
     pool_free(ctx, A);
   }
 

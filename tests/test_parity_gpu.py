@@ -209,3 +209,35 @@ def test_random_plans_instrumentation_matches_static(ctx):
         assert r.recompute_loss_mismatches == 0 and r.kv_completeness_violations == 0, trial
         assert np.isfinite(r.loss)
     model.close()
+
+
+def test_fused_epilogues_multi_wave_discard_forward(ctx):
+    """Regression: with more output tiles than CTA pairs, a fused epilogue
+    must not write into a buffer its own GEMM is still reading.  A discard
+    forward keeps neither the normed input nor the SwiGLU output, so both used
+    to share one scratch; the recomputed forward then disagreed with the first
+    pass.  Forced CTA-pair GEMMs; ffn = 4 d, so SwiGLU rows written by the
+    first wave of gate|up tiles (16 M-blocks x 32 N-tiles, every wave spans
+    all M-blocks) land on normed-input rows later waves still read."""
+    gcfg, _ = _cfgs(1, 64, 1024, 8, 8, 1, 4096)
+    lengths = np.array([10000, 300, 77], np.int64)
+    tokens = cf.gen_tokens(lengths, 64, 19)
+    capi.check(capi.lib().cf_debug_set_gemm_mode(2))
+    try:
+        model = cf.Model(ctx, gcfg)
+        r = model.run_plan(cf.Plan.build(lengths, 4096, 1), lengths, tokens)
+        g_chunked = model.grads_flat()
+        f = model.backward_full(lengths, tokens)
+        g_full = model.grads_flat()
+    finally:
+        capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+    assert r.recompute_forward_count >= 1
+    assert r.recompute_loss_mismatches == 0
+    assert abs(r.loss - f.loss) / abs(f.loss) < 1e-4, (r.loss, f.loss)
+    off = 0
+    for i in range(model.num_tensors()):
+        _, rr, cc = model.tensor_info(i)
+        a, b = g_chunked[off:off + rr * cc], g_full[off:off + rr * cc]
+        off += rr * cc
+        assert np.abs(a - b).max() / max(np.abs(a).max(), np.abs(b).max(), 1e-12) < 1e-2, model.tensor_info(i)[0]
+    model.close()
