@@ -337,6 +337,11 @@ def run_b200(args):
         "gpu_launches": int(sum(r.gpu_launches for r in res)),
         "clocks": clk.summary(),
         "loss": r0.loss,
+        # run_plan's own instrumentation on the measured step (plan_runner.hpp:36-60)
+        "checks": {"recompute_forwards": int(r0.recompute_forward_count),
+                   "recompute_loss_mismatches": int(r0.recompute_loss_mismatches),
+                   "kv_completeness_violations": int(r0.kv_completeness_violations),
+                   "peak_retained_tokens": int(r0.peak_retained_tokens)},
     }
     if cpu:
         line["cpu_baseline"] = {"value": cpu["tokens_per_s"], "unit": "tokens/s", "cores": cpu["cores"],
