@@ -38,6 +38,21 @@ def _params_by_name(model):
 
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_pp_local_bitwise_equals_unsplit(ctx, case):
+    _pp_bitwise(ctx, case)
+
+
+def test_pp_local_bitwise_fused_epilogues_multiwave(ctx):
+    """The same with every GEMM on the CTA-pair kernel at a size where the
+    SwiGLU / RoPE + KV-copy epilogues run over several waves (d 1024,
+    ffn 4096, 4096-token chunks, a 3-chunk dependent group with recompute)."""
+    capi.check(capi.lib().cf_debug_set_gemm_mode(2))
+    try:
+        _pp_bitwise(ctx, ("llama-p2-fused", 1, 64, 1024, 8, 8, 2, 4096, [10000, 300, 77], 4096, 1, 2))
+    finally:
+        capi.check(capi.lib().cf_debug_set_gemm_mode(0))
+
+
+def _pp_bitwise(ctx, case):
     _, arch, V, d, H, KVH, L, ffn, lengths, cs, k, P = case
     cfg = cf.model_cfg(arch=arch, vocab=V, d=d, heads=H, kv_heads=KVH, layers=L, ffn=ffn, seed=7)
     lengths = np.array(lengths, np.int64)
