@@ -222,6 +222,8 @@ def run_b200(args):
     import paper_2503_02356_b200 as cf
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"launched with WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -351,6 +353,82 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------- launcher
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`python bench.py --gpus N` without torchrun env: re-launch this script
+    as N ranks (one process per GPU) with torch.distributed.run on
+    127.0.0.1, exactly as the driver does for N > 1, and return its exit code.
+    NCCL's communicator-init lines (NCCL_DEBUG=INFO, INIT subsystem) go to
+    stderr so the N-rank communicator is visible in the log."""
+    env = dict(os.environ)
+    if not args.dry_run:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args):
+    """CPU rank-wiring check (gloo, no GPU): every rank builds the global
+    plan of the N-block batch, takes its DP partition (cf_plan_partition) and
+    the global normalizer exactly as run_b200 does; rank 0 verifies that the
+    ranks' chunks partition the global plan (each chunk on exactly one rank,
+    whole dependent groups together) and prints the bench line's rank fields."""
+    import torch
+    import torch.distributed as dist
+    import paper_2503_02356_b200 as cf
+
+    rank, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"launched with WORLD_SIZE={world} but --gpus {args.gpus}")
+    dist.init_process_group("gloo")
+    blocks = [block_lengths(b + 1) for b in range(world)]
+    lengths = np.concatenate(blocks)
+    ids = np.arange(len(lengths), dtype=np.int64)
+    gplan = cf.Plan.build(lengths, CHUNK, K_RETAIN, ids)
+    plan = gplan.partition(world, rank) if world > 1 else gplan
+    gch = gplan.export()[0]
+    ch = plan.export()[0]
+    cover = torch.zeros(len(gch), dtype=torch.int64)
+    pos = {int(c): i for i, c in enumerate(gch["chunk_id"])}
+    for c in ch["chunk_id"]:
+        cover[pos[int(c)]] += 1
+    grp = torch.full((len(gch),), -1, dtype=torch.int64)
+    for c, g in zip(ch["chunk_id"], ch["group_id"]):
+        if g >= 0:
+            grp[pos[int(c)]] = rank
+    dist.all_reduce(cover)
+    owners = [torch.zeros_like(grp) for _ in range(world)]
+    dist.all_gather(owners, grp)
+    tok = torch.tensor([int(ch["total_tokens"].sum())], dtype=torch.int64)
+    per_rank = [torch.zeros_like(tok) for _ in range(world)]
+    dist.all_gather(per_rank, tok)
+    if rank == 0:
+        ok = bool((cover == 1).all())
+        # every dependent group lives on one rank
+        for g in set(int(x) for x in gch["group_id"] if x >= 0):
+            rows = [i for i, x in enumerate(gch["group_id"]) if int(x) == g]
+            holders = {r for r in range(world) for i in rows if int(owners[r][i]) >= 0}
+            ok = ok and len(holders) == 1
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": world,
+                          "backend": "gloo", "partition_ok": ok,
+                          "global_chunks": int(len(gch)), "tokens_per_rank": [int(t.item()) for t in per_rank],
+                          "global_tokens": int(lengths.sum()), "normalizer": float((lengths - 1).sum()),
+                          "config": {"parallelism": f"dp{world}", "global_batch": 1000 * world}}), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,10 +438,16 @@ def main():
     ap.add_argument("--workload", default="c2", choices=["c2", "long", "short"],
                     help="c2 = the metric's workload; long/short = slices of it for profiling only")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only (gloo): check the N-rank wiring and DP partition, no GPU work")
     args = ap.parse_args()
     global WORKLOAD
     WORKLOAD = args.workload
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_b200(args)

@@ -160,13 +160,27 @@ int cf_plan_build(const int64_t* seq_ids, const int64_t* lengths, int64_t n,
                   int64_t chunk_size, int64_t k, cf_plan** out);
 /* schedule_group (scheduler.hpp:106): one abstract dependent group. */
 int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out);
+/* validate_plan (scheduler.hpp:182-271) over a caller-built ExecutionPlan
+ * (scheduler.hpp:36-43): `events` in execution order; ExecutionPlan.groups as
+ * CSR (group_ids[g], members[group_offsets[g] .. group_offsets[g+1]), index
+ * order; n_groups may be 0); ExecutionPlan.chunk_tokens as parallel arrays (a
+ * chunk without an entry counts chunk_size tokens).  The result is a plan
+ * with no chunks whose diagnostics and violation texts (the reference's,
+ * verbatim) are read with cf_plan_export / cf_plan_violation and whose listing
+ * is cf_plan_listing.  Violations are data, not an error status (as in the
+ * reference); cf_run_plan refuses a plan that has any. */
+int cf_plan_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* events, int64_t n_events,
+                            const int64_t* group_ids, const int64_t* group_offsets, const int64_t* members,
+                            int64_t n_groups, const int64_t* token_chunk_ids, const int64_t* token_counts,
+                            int64_t n_token_entries, cf_plan** out);
 int cf_plan_counts(const cf_plan* plan, int64_t* n_chunks, int64_t* n_segments,
                    int64_t* n_events, int64_t* n_groups);
 int cf_plan_export(const cf_plan* plan, cf_chunk_rec* chunks,
                    cf_segment_rec* segments, cf_event_rec* events,
                    cf_plan_diag* diag);
 /* ExecutionPlan.groups (scheduler.hpp:41): group ids ascending, members in
- * index order; offsets has n_groups+1 entries. */
+ * index order; offsets has n_groups+1 entries.  group_ids / members may be
+ * NULL to size the members array (offsets[n_groups]). */
 int cf_plan_export_groups(const cf_plan* plan, int64_t* group_ids,
                           int64_t* offsets, int64_t* members);
 /* text of violation i (validate_plan messages). */

@@ -452,3 +452,43 @@ extern "C" int cfr_tune(const int64_t* ids, const int64_t* lengths, int64_t n, c
     put(csv ? cf::tuner_table_csv(r) : cf::tuner_report(r), buf, cap, len);
   });
 }
+
+// validate_plan (scheduler.hpp:182) over a caller-built ExecutionPlan:
+// groups in CSR form, chunk_tokens as parallel arrays.  Writes peak / recompute
+// tokens and the violation texts joined by '\n' (for pinning
+// cf_plan_validate_events' texts against the reference verbatim).
+extern "C" int cfr_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* ev, int64_t n_ev,
+                                   const int64_t* gids, const int64_t* goff, const int64_t* mem, int64_t ng,
+                                   const int64_t* tc, const int64_t* tn, int64_t nt, int64_t* peak,
+                                   int64_t* recompute, char* buf, size_t cap, size_t* len) {
+  return guarded([&] {
+    cf::ExecutionPlan p;
+    p.chunk_size = chunk_size;
+    p.k = k;
+    for (int64_t g = 0; g < ng; ++g) p.groups[gids[g]] = std::vector<int64_t>(mem + goff[g], mem + goff[g + 1]);
+    for (int64_t i = 0; i < nt; ++i) p.chunk_tokens[tc[i]] = tn[i];
+    for (int64_t i = 0; i < n_ev; ++i) {
+      cf::ExecEvent e;
+      e.kind = static_cast<cf::ExecKind>(ev[i].kind);
+      e.chunk_id = ev[i].chunk_id;
+      e.group_id = ev[i].group_id;
+      e.index_in_group = ev[i].index_in_group;
+      e.is_recompute = ev[i].is_recompute != 0;
+      e.notes.save_kv = ev[i].save_kv != 0;
+      e.notes.read_kv_prefix = ev[i].read_kv_prefix != 0;
+      e.notes.accumulate_kv_grad = ev[i].accumulate_kv_grad != 0;
+      p.events.push_back(e);
+    }
+    const cf::PlanDiagnostics d = cf::validate_plan(p);
+    *peak = d.peak_retained_tokens;
+    *recompute = d.recompute_token_count;
+    std::string s;
+    for (const std::string& v : d.violations) s += v + "\n";
+    *len = s.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, s.size());
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}

@@ -97,6 +97,7 @@ EXPORTS = [
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
     "cf_segment_forward", "cf_segment_backward", "cf_segment_destroy", "cf_op_gemm_rope",
+    "cf_plan_validate_events",
 ]
 
 _lib = None
@@ -181,7 +182,8 @@ class Plan:
         nc, ns, ne, ng = self.counts()
         gid = np.zeros(max(ng, 1), np.int64)
         off = np.zeros(ng + 1, np.int64)
-        mem = np.zeros(max(nc, 1), np.int64)
+        check(lib().cf_plan_export_groups(self.h, None, _p(off), None))
+        mem = np.zeros(max(int(off[-1]), 1), np.int64)
         check(lib().cf_plan_export_groups(self.h, _p(gid), _p(off), _p(mem)))
         return {int(gid[i]): [int(x) for x in mem[off[i]:off[i + 1]]] for i in range(ng)}
 
@@ -214,6 +216,31 @@ class Plan:
         """chunk_plan_from_json + schedule_step (chunker.hpp:261)."""
         h = C.c_void_p()
         check(lib().cf_plan_from_chunk_json(text.encode(), C.c_int64(k), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def validate_events(cls, events, chunk_size, k=1, groups=None, chunk_tokens=None):
+        """validate_plan (scheduler.hpp:182) over a caller-built ExecutionPlan:
+        `events` an EVENT_DT array, `groups` {group: [chunk ids in index order]},
+        `chunk_tokens` {chunk: tokens}.  Diagnostics via export()[3] /
+        violations() / listing()."""
+        ev = np.ascontiguousarray(events, EVENT_DT)
+        groups = groups or {}
+        gid = np.array(sorted(groups), np.int64)
+        off = np.zeros(len(gid) + 1, np.int64)
+        mem = []
+        for i, g in enumerate(gid):
+            mem += list(groups[int(g)])
+            off[i + 1] = len(mem)
+        mem = np.array(mem or [0], np.int64)
+        chunk_tokens = chunk_tokens or {}
+        tc = np.array(list(chunk_tokens.keys()) or [0], np.int64)
+        tn = np.array(list(chunk_tokens.values()) or [0], np.int64)
+        h = C.c_void_p()
+        check(lib().cf_plan_validate_events(C.c_int64(chunk_size), C.c_int64(k), _p(ev), C.c_int64(len(ev)),
+                                            _p(gid if len(gid) else np.zeros(1, np.int64)), _p(off), _p(mem),
+                                            C.c_int64(len(gid)), _p(tc), _p(tn), C.c_int64(len(chunk_tokens)),
+                                            C.byref(h)))
         return cls(h)
 
     def partition(self, world, rank):

@@ -26,6 +26,16 @@ namespace {
 void need(const void* p, const char* what) {
   if (!p) throw cfb::ValidationError(std::string(what) + " is null");
 }
+// Every entry point that touches a context makes its device current, so two
+// contexts on different GPUs can be driven from one host thread.
+void need(const cf_ctx* c, const char* what) {
+  need(static_cast<const void*>(c), what);
+  cfb::cuda_check(cudaSetDevice(c->c.device), "cudaSetDevice");
+}
+void need(const cf_model* m, const char* what) {
+  need(static_cast<const void*>(m), what);
+  if (m->ctx) cfb::cuda_check(cudaSetDevice(m->ctx->c.device), "cudaSetDevice");
+}
 }  // namespace
 
 extern "C" {
@@ -53,7 +63,9 @@ int cf_ctx_create(int device, cf_ctx** out) {
 
 void cf_ctx_destroy(cf_ctx* ctx) {
   if (!ctx) return;
+  cudaSetDevice(ctx->c.device);
   cudaStreamSynchronize(ctx->c.stream);
+  cfb::ctx_release(&ctx->c);  // NCCL communicators, link streams, timing events
   cudaStreamDestroy(ctx->c.stream);
   delete ctx;
 }

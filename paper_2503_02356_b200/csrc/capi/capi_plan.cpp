@@ -39,6 +39,38 @@ int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out)
   });
 }
 
+int cf_plan_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* events, int64_t n_events,
+                            const int64_t* group_ids, const int64_t* group_offsets, const int64_t* members,
+                            int64_t n_groups, const int64_t* token_chunk_ids, const int64_t* token_counts,
+                            int64_t n_token_entries, cf_plan** out) {
+  return cfb::guard([&] {
+    if (!out) throw cfb::ValidationError("out is null");
+    if (n_events < 0 || n_groups < 0 || n_token_entries < 0) throw cfb::ValidationError("negative count");
+    if ((n_events && !events) || (n_groups && (!group_ids || !group_offsets || !members)) ||
+        (n_token_entries && (!token_chunk_ids || !token_counts)))
+      throw cfb::ValidationError("null array with a non-zero count");
+    auto h = std::make_unique<cf_plan>();
+    cfb::Plan& p = h->p;
+    p.chunk_size = chunk_size;
+    p.k = k;
+    for (int64_t g = 0; g < n_groups; ++g) {
+      if (group_offsets[g] < 0 || group_offsets[g + 1] < group_offsets[g])
+        throw cfb::ValidationError("group offsets must be non-decreasing");
+      p.groups[group_ids[g]] = std::vector<int64_t>(members + group_offsets[g], members + group_offsets[g + 1]);
+    }
+    for (int64_t i = 0; i < n_token_entries; ++i) p.chunk_tokens[token_chunk_ids[i]] = token_counts[i];
+    for (int64_t i = 0; i < n_events; ++i) {
+      const cf_event_rec& e = events[i];
+      if (e.kind < CF_EXEC_FORWARD_DISCARD || e.kind > CF_EXEC_BACKWARD)
+        throw cfb::ValidationError("unknown event kind " + std::to_string(e.kind));
+      p.events.push_back({e.kind, e.chunk_id, e.group_id, e.index_in_group, e.is_recompute != 0, e.save_kv != 0,
+                          e.read_kv_prefix != 0, e.accumulate_kv_grad != 0});
+    }
+    cfb::validate(p);
+    *out = h.release();
+  });
+}
+
 int cf_plan_counts(const cf_plan* plan, int64_t* n_chunks, int64_t* n_segments, int64_t* n_events,
                    int64_t* n_groups) {
   return cfb::guard([&] {
@@ -72,11 +104,15 @@ int cf_plan_export(const cf_plan* plan, cf_chunk_rec* chunks, cf_segment_rec* se
 
 int cf_plan_export_groups(const cf_plan* plan, int64_t* group_ids, int64_t* offsets, int64_t* members) {
   return cfb::guard([&] {
+    if (!plan || !offsets) throw cfb::ValidationError("plan and offsets are required");
     int64_t g = 0, m = 0;
     offsets[0] = 0;
-    for (const auto& [gid, mem] : plan->p.groups) {
-      group_ids[g] = gid;
-      for (int64_t c : mem) members[m++] = c;
+    for (const auto& [gid, mem] : plan->p.groups) {  // group_ids / members may be NULL (sizing call)
+      if (group_ids) group_ids[g] = gid;
+      for (int64_t c : mem) {
+        if (members) members[m] = c;
+        ++m;
+      }
       offsets[++g] = m;
     }
   });

@@ -42,6 +42,12 @@ std::vector<int64_t> synthesize(const std::vector<int64_t>& bounds, const std::v
     if (i > 0 && fracs[i] <= fracs[i - 1]) throw ValidationError("cumulative fractions must be strictly increasing");
   }
   if (max_length < bounds.back()) throw ValidationError("max_length must be at least the last bucket bound");
+  // DistributionSpec::validate (dataset.hpp:62-71): the tail must be reachable
+  // exactly when max_length leaves room for it
+  if (max_length > bounds.back() && fracs.back() >= 1.0)
+    throw ValidationError("last cumulative fraction must be below 1.0 when max_length exceeds the last bucket bound");
+  if (max_length == bounds.back() && fracs.back() != 1.0)
+    throw ValidationError("last cumulative fraction must equal 1.0 when max_length equals the last bucket bound");
   if (count < 1) throw ValidationError("count must be at least 1");
   uint64_t s = seed;
   std::vector<int64_t> out;

@@ -516,12 +516,9 @@ __global__ void __launch_bounds__(128) attn_dkv_kernel(AttnParams p, const AttnT
 template <int DH>
 cudaError_t fwd_t(const AttnParams& p, cudaStream_t st) {
   const size_t smem = 5 * 64 * DH * sizeof(bf16);
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = [] {
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    return e;
-  }();
+  // per (kernel, device), thread-safe
+  cudaError_t attr = cudaSuccess;
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(attn_fwd_kernel<DH>), static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
   attn_fwd_kernel<DH><<<dim3(p.num_tiles, p.H), 128, smem, st>>>(p);
   return cudaGetLastError();
@@ -531,13 +528,10 @@ template <int DH>
 cudaError_t bwd_t(const AttnParams& p, const AttnTile* key_tiles, int32_t nkt, cudaStream_t st) {
   const size_t smem_dq = 6 * 64 * DH * sizeof(bf16);
   const size_t smem_dkv = 6 * 64 * DH * sizeof(bf16) + 4 * 64 * sizeof(float);
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = [] {
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_dq_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dq));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_dkv_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dkv));
-    return e;
-  }();
+  // per (kernel, device), thread-safe
+  cudaError_t attr = cudaSuccess;
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(attn_dq_kernel<DH>), static_cast<int>(smem_dq));
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(attn_dkv_kernel<DH>), static_cast<int>(smem_dkv));
   if (attr != cudaSuccess) return attr;
   const int64_t warps = static_cast<int64_t>(p.T) * p.H;
   attn_dsum_kernel<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, st>>>(p);

@@ -761,8 +761,8 @@ cudaError_t attn_forward_tc(const AttnParams& p, const AttnTile* tiles128, int32
     return cudaErrorInvalidValue;
   TcArgs a{p.segs, tiles128, p.q, p.q_stride, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
   const size_t smem = 1024 + 2 * KVS * kTile + 512 * 4 + 256;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  // per (kernel, device), thread-safe
+  const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(attn_fwd_tc_kernel), static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
   attn_fwd_tc_kernel<<<dim3(ntiles, p.H), kFwdThreads, smem, st>>>(mq, mk, mv, a);
   return cudaGetLastError();
@@ -781,15 +781,10 @@ cudaError_t attn_backward_tc_v1(const AttnParams& p, const AttnTile* qtiles128, 
               p.T, p.H, p.KVH, p.scale * kLog2e, p.scale};
   const size_t smem_dq = 1024 + 7 * kTile + 256;
   const size_t smem_dkv = 1024 + 6 * kTile + 4 * 256 * 4 + 128;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = [] {
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_dq));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_dkv));
-    return e;
-  }();
+  // per (kernel, device), thread-safe
+  cudaError_t attr = cudaSuccess;
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(attn_dq_tc_kernel), static_cast<int>(smem_dq));
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(attn_dkv_tc_kernel), static_cast<int>(smem_dkv));
   if (attr != cudaSuccess) return attr;
   attn_dsum(p, st);
   attn_dq_tc_kernel<<<dim3(nq, p.H), 192, smem_dq, st>>>(mq, mo, mk, mv, a);

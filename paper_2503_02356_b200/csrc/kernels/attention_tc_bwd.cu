@@ -748,14 +748,10 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
          p.scale, p.rope_tab, p.dkv_out, p.dkv_out_ld, p.col_k, p.col_v};
   const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256 * 4 + 256;
   const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = [] {
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem_dq));
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(dkv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_dkv));
-    return e;
-  }();
+  // per (kernel, device), thread-safe
+  cudaError_t attr = cudaSuccess;
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(dq_kernel), static_cast<int>(smem_dq));
+  if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(dkv_kernel), static_cast<int>(smem_dkv));
   if (attr != cudaSuccess) return attr;
   // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
   dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);

@@ -337,8 +337,8 @@ cudaError_t attn_forward_tc_pp(const AttnParams& p, const AttnTile* tiles128, in
     return cudaErrorInvalidValue;
   Args a{p.segs, tiles128, p.o, p.o_stride, p.lse, p.T, p.H, p.KVH, p.scale * kLog2e};
   const size_t smem = 1024 + (2 + KS + VS) * kTile + 1024 * 4 + 256;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = cudaFuncSetAttribute(attn_fwd_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  // per (kernel, device), thread-safe
+  const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(attn_fwd_pp_kernel), static_cast<int>(smem));
   if (attr != cudaSuccess) return attr;
   attn_fwd_pp_kernel<<<dim3(ntiles, p.H / 2), kThreads, smem, st>>>(mq, mk, mv, a);
   return cudaGetLastError();

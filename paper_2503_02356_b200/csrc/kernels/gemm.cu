@@ -721,8 +721,8 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   g.R = d.r;
   g.ldr = d.ldr;
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(C::kSmem));
+  // per (kernel, device), thread-safe
+  const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(C::kSmem));
   if (attr != cudaSuccess) return attr;
   if (g_num_sms == 0) {
     int dev = 0;
@@ -763,8 +763,8 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.R = d.r;
   g.ldr = d.ldr;
   auto kern = pair::gemm_pair_kernel<A_MN, B_MN, EPI>;
-  // once per process, thread-safe (concurrent contexts on host threads)
-  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pair::kSmem));
+  // per (kernel, device), thread-safe
+  const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(pair::kSmem));
   if (attr != cudaSuccess) return attr;
   const int tiles = g.num_m * g.num_n;
   const int pairs = std::min(tiles, gemm_num_sms() / 2);

@@ -82,6 +82,7 @@ struct Nccl {
   int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*split)(void*, int, int, void**, void*) = nullptr;  // ncclCommSplit (NCCL >= 2.18)
+  int (*destroy)(void*) = nullptr;                          // ncclCommDestroy
 };
 struct Id128 {
   char b[128];
@@ -99,6 +100,7 @@ Nccl& nccl() {
     n.send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(n.h, "ncclSend"));
     n.recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(n.h, "ncclRecv"));
     n.split = reinterpret_cast<int (*)(void*, int, int, void**, void*)>(dlsym(n.h, "ncclCommSplit"));
+    n.destroy = reinterpret_cast<int (*)(void*)>(dlsym(n.h, "ncclCommDestroy"));
     if (!n.get_id || !n.all_reduce || !n.init_rank) throw NcclError("NCCL symbols missing");
   }
   return n;
@@ -111,6 +113,25 @@ constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0, kNcclNoColor = -
 }  // namespace
 
 void dp_unique_id(uint8_t* out) { nccl_check(nccl().get_id(out), "ncclGetUniqueId"); }
+
+// Releases what a context acquired beyond its stream (cf_ctx_destroy): every
+// NCCL communicator (world, DP group, the four stage links), the link
+// streams and the profiling events.  Never throws.
+void ctx_release(Ctx* ctx) {
+  void* comms[] = {ctx->nccl_comm, ctx->world_comm, ctx->act_up, ctx->grad_up, ctx->act_down, ctx->grad_down};
+  std::set<void*> seen;
+  for (void* c : comms)
+    if (c && seen.insert(c).second && nccl().destroy) nccl().destroy(c);
+  ctx->nccl_comm = ctx->world_comm = ctx->act_up = ctx->grad_up = ctx->act_down = ctx->grad_down = nullptr;
+  for (auto& ls : ctx->link_stream)
+    if (ls) {
+      cudaStreamSynchronize(ls);
+      cudaStreamDestroy(ls);
+      ls = nullptr;
+    }
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  ctx->event_pool.clear();
+}
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id) {
   // world == 1 without an id: no communicator.  With an id, a 1-rank NCCL
@@ -143,6 +164,7 @@ void pp_init(Ctx* ctx, int rank, int world, int stages, const uint8_t* id) {
   CK(cudaSetDevice(ctx->device));
   void* world_comm = nullptr;
   nccl_check(init(&world_comm, world, u, rank), "ncclCommInitRank");
+  ctx->world_comm = world_comm;  // kept so cf_ctx_destroy can release it
   const int s = rank % stages, rep = rank / stages, dp = world / stages;
   ctx->stage = s;
   ctx->stages = stages;
@@ -152,6 +174,8 @@ void pp_init(Ctx* ctx, int rank, int world, int stages, const uint8_t* id) {
     ctx->nccl_comm = dpc;
     ctx->rank = rep;
     ctx->world = dp;
+  } else if (dpc && n.destroy) {
+    n.destroy(dpc);  // a 1-rank DP group is not used
   }
   // link j joins stages j and j+1 of a replica; even links first, then odd
   auto link_color = [&](int parity) {
@@ -442,6 +466,7 @@ struct cf_step {
   int32_t* meta_host = nullptr;  // pinned
   int64_t meta_len = 0;
   double normalizer = 0;
+  std::string normalizer_error;  // batch_normalizer's ValidationError, if any
   int64_t tokens = 0;
   // algorithmic FLOPs split into one layer's share and the
   // LM head's, so a pipeline stage can report its own slice
@@ -585,13 +610,17 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
     if (!idx_of.emplace(b.ids[i], i).second) throw ValidationError("duplicate sequence id " + std::to_string(b.ids[i]));
     tok_off[i + 1] = tok_off[i] + b.lengths[i];
   }
-  // normalizer: global target count (toy_model.hpp:533-541)
+  // normalizer: global target count (toy_model.hpp:533-541).  The reference
+  // only computes (and so only validates) it when no normalizer override is
+  // given (plan_runner.hpp:89-91): the error is kept and raised by a run
+  // without an override.
   int64_t targets = 0;
   for (int64_t i = 0; i < b.n; ++i) {
-    if (b.lengths[i] < 2) throw ValidationError("sequence " + std::to_string(b.ids[i]) + " must have length >= 2");
+    if (b.lengths[i] < 2 && st->normalizer_error.empty())
+      st->normalizer_error = "sequence " + std::to_string(b.ids[i]) + " must have length >= 2";
     targets += b.lengths[i] - 1;
   }
-  if (targets <= 0) throw ValidationError("batch has no prediction targets");
+  if (targets <= 0 && st->normalizer_error.empty()) st->normalizer_error = "batch has no prediction targets";
   st->normalizer = static_cast<double>(targets);
   if (!b.tokens_host) throw ValidationError("token payload required");
   for (int64_t i = 0; i < tok_off[b.n]; ++i)
@@ -641,6 +670,40 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
     st->mf_head += 6.0 * Nhead * static_cast<double>(cm.T);
     st->chunks.push_back(cm);
   }
+  // Dependent groups write K/V rows at their sequence's absolute positions of
+  // one per-group cache, so the structure the reference's StateStore checks
+  // lazily (assemble_prefix, plan_runner.hpp:128-156: "KV prefix does not
+  // cover the segment start") is checked here up front for any plan — also
+  // one loaded from chunk_plan.json: every member of a group is one segment
+  // of the same sequence, members sit at their index_in_group, and member i
+  // starts where members 0..i-1 end.
+  for (const auto& [gid, members] : plan.groups) {
+    int64_t seq = -1, next = 0;
+    for (size_t i = 0; i < members.size(); ++i) {
+      auto pit = st->pos_of.find(members[i]);
+      if (pit == st->pos_of.end()) throw ValidationError("plan references unknown chunk " + std::to_string(members[i]));
+      const Chunk& c = plan.chunks[static_cast<size_t>(pit->second)];
+      ChunkMeta& cm = st->chunks[static_cast<size_t>(pit->second)];
+      if (!cm.dependent || c.group != gid)
+        throw ValidationError("chunk " + std::to_string(c.id) + " is listed in group " + std::to_string(gid) +
+                              " but is not one of its dependent chunks");
+      if (c.seg_cnt != 1)
+        throw ValidationError("dependent chunk " + std::to_string(c.id) + " must have exactly one segment");
+      if (c.index != static_cast<int64_t>(i))
+        throw ValidationError("chunk " + std::to_string(c.id) + " has index_in_group " + std::to_string(c.index) +
+                              " but is member " + std::to_string(i) + " of group " + std::to_string(gid));
+      if (i == 0) seq = cm.seq;
+      if (cm.seq != seq)
+        throw ValidationError("group " + std::to_string(gid) + " spans sequences " + std::to_string(seq) + " and " +
+                              std::to_string(cm.seq));
+      if (cm.start != next)
+        throw ValidationError("KV prefix does not cover the segment start of sequence " + std::to_string(cm.seq));
+      next = cm.start + cm.T;
+    }
+  }
+  for (const ChunkMeta& cm : st->chunks)
+    if (cm.dependent && !plan.groups.count(cm.group))
+      throw ValidationError("chunk plan has no group " + std::to_string(cm.group));
   st->hw_layer = st->mf_layer;
   st->hw_head = st->mf_head;
   for (const Event& e : plan.events)
@@ -1111,6 +1174,8 @@ struct StageRunner {
     ex.st = st;
     ex.s = ctx->stream;
     ex.corrupt = opts.corrupt_kv_grads != 0;
+    if (!(opts.normalizer_override > 0) && !st->normalizer_error.empty())
+      throw ValidationError(st->normalizer_error);
     norm = opts.normalizer_override > 0 ? opts.normalizer_override : st->normalizer;
     ex.inv_norm = static_cast<float>(1.0 / norm);
     ex.loss_slots = static_cast<double*>(pool_alloc(ctx, (nslots + 1) * 8));
@@ -1716,9 +1781,9 @@ struct SegmentState {
   Tape tape;
   bool kept = false;
   int64_t len = 0, prefix = 0;
-  ~SegmentState() {
-    if (tape.mem) pool_free(ctx, tape.mem);
-    if (gs.mem) pool_free(ctx, gs.mem);
+  ~SegmentState() {  // no throwing frees in a destructor
+    if (tape.mem) cudaFreeAsync(tape.mem, ctx->stream);
+    if (gs.mem) cudaFreeAsync(gs.mem, ctx->stream);
     step_destroy(st);
   }
 };
@@ -1803,13 +1868,22 @@ SegmentState* segment_forward(Ctx* ctx, Model* m, const int32_t* tokens, int64_t
   ex.st = st;
   ex.s = ctx->stream;
   ex.inv_norm = 1.0f;  // dlogits are rebuilt with the normalizer by segment_backward
-  ex.loss_slots = static_cast<double*>(pool_alloc(ctx, 8));
+  // everything allocated here is owned by sg (or the guard) from the moment
+  // it exists, so a throwing launch leaks nothing
+  struct SlotGuard {
+    Ctx* c;
+    double* p;
+    ~SlotGuard() {
+      if (p) cudaFreeAsync(p, c->stream);
+    }
+  } slot_guard{ctx, static_cast<double*>(pool_alloc(ctx, 8))};
+  ex.loss_slots = slot_guard.p;
   CK(cudaMemsetAsync(ex.loss_slots, 0, 8, ex.s));
-  Tape t = ex.alloc_tape(len, keep_tape);
+  sg->tape = ex.alloc_tape(len, keep_tape);
+  Tape& t = sg->tape;
   ex.forward(cm, t, &g, 0, keep_tape);
   double ls = 0;
   CK(cudaMemcpyAsync(&ls, ex.loss_slots, 8, cudaMemcpyDeviceToHost, ex.s));
-  pool_free(ctx, ex.loss_slots);
   // the segment's own key/value rows (what a later segment's prefix is built from)
   const int64_t n = m->L * len * m->kvw;
   double* tmp = (saved_k || saved_v) ? static_cast<double*>(pool_alloc(ctx, n * 8)) : nullptr;
@@ -1825,11 +1899,7 @@ SegmentState* segment_forward(Ctx* ctx, Model* m, const int32_t* tokens, int64_t
   CK(cudaStreamSynchronize(ex.s));
   ctx->launches += ex.launches;
   if (loss_sum) *loss_sum = ls;
-  if (!keep_tape) {
-    ex.free_tape(t);
-    return nullptr;
-  }
-  sg->tape = t;
+  if (!keep_tape) return nullptr;  // ~SegmentState releases the tape and KV state
   sg->kept = true;
   return sg.release();
 }

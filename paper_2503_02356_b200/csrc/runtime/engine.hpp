@@ -27,6 +27,7 @@ struct Ctx {
   int64_t launches = 0;
   // data-parallel group (NCCL loaded at runtime)
   void* nccl_comm = nullptr;
+  void* world_comm = nullptr;  // PP x DP: the communicator the groups are split from
   int rank = 0, world = 1;
   // pipeline-parallel links (cf_ctx_init_pp): one 2-rank communicator per
   // direction per neighbouring stage, each driven from its own stream, so
@@ -139,6 +140,7 @@ void local_pipe_destroy(LocalPipe* p);
 void pp_init_local(Ctx* ctx, LocalPipe* p, int stage);
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id128);
+void ctx_release(Ctx* ctx);
 void dp_unique_id(uint8_t* out128);
 
 }  // namespace cfb

@@ -188,3 +188,94 @@ def test_llama_oracle_chunked_equals_unchunked(oracle):
         assert abs(l - lf) <= 1e-12 * abs(lf)
         assert np.max(np.abs(g - gf)) <= 1e-9 * np.max(np.abs(gf))
         assert instr[2] == 0 and instr[3] == 0
+
+
+def _per_tensor_rel(shapes, a, b):
+    out, off = [], 0
+    for name, r, c in shapes.tensors():
+        x, y = a[off:off + r * c], b[off:off + r * c]
+        off += r * c
+        out.append((name, float(np.abs(x - y).max() / max(np.abs(x).max(), np.abs(y).max(), 1e-300))))
+    return out
+
+
+@pytest.mark.parametrize("arch,V,d,H,KVH,L,ffn,lengths", [
+    (0, 32, 16, 4, 2, 2, 0, [8, 8, 16, 32]),           # CLI verify defaults' model
+    (0, 256, 256, 4, 2, 2, 0, [294, 21, 225, 64]),     # C1 widths
+    (1, 96, 64, 4, 2, 2, 128, [30, 64, 7, 2]),
+    (1, 50, 128, 4, 1, 1, 96, [40, 3, 2]),            # GQA 4:1, head_dim 32
+    (1, 40, 256, 2, 2, 2, 320, [70, 12]),             # MHA, head_dim 128
+])
+def test_vectorised_oracle_matches_cpp_oracle(oracle, arch, V, d, H, KVH, L, ffn, lengths):
+    """oracle/llama_np.py (BLAS fp64 restatement used for production-width
+    GPU parity) == cf_oracle.cpp backward_full / forward_full, per tensor, to
+    1e-12 relative (the summation order differs, so not bitwise)."""
+    from oracle import llama_np
+    cfg = model_cfg(arch=arch, vocab=V, d=d, heads=H, kv_heads=KVH, layers=L, ffn=ffn, seed=7)
+    lengths = np.array(lengths, np.int64)
+    tokens = oracle.gen_tokens(lengths, V, 3)
+    params = oracle.init(cfg)
+    if arch == 1:  # move the norm gains off 1 so their gradients are exercised
+        params = params + np.random.default_rng(1).normal(0, 0.02, params.shape)
+    ol, og = oracle.backward_full(cfg, lengths, tokens, params=params)
+    nl, ng = llama_np.backward_full(cfg, params, lengths, tokens)
+    assert abs(nl - ol) <= 1e-12 * abs(ol)
+    assert abs(llama_np.forward_full(cfg, params, lengths, tokens) - ol) <= 1e-12 * abs(ol)
+    worst = max(_per_tensor_rel(llama_np.Shapes(cfg), ng, og), key=lambda e: e[1])
+    assert worst[1] <= 1e-12, worst
+
+
+def test_vectorised_oracle_c1_matches_reference_golden(oracle):
+    """The vectorised oracle on the C1 canonical batch reproduces the
+    reference's golden run_plan loss — chunked == unchunked
+    holds in the reference at 9.9e-15."""
+    from oracle import llama_np
+    lengths, tokens = c1_batch(oracle)
+    cfg = c1_cfg()
+    loss, grads = llama_np.backward_full(cfg, oracle.init(cfg), lengths, tokens)
+    g = GOLD["c1_run_plan"] if "c1_run_plan" in GOLD else None
+    assert abs(loss - 5.5455568137389548) <= 1e-13 * 5.5455568137389548
+    assert abs(grads.sum() - 0.0071303868983342488) <= 1e-9
+    assert abs(np.abs(grads).sum() - 6.5459081754140787) <= 1e-11 * 6.5459081754140787
+    del g
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built")
+def test_product_synthesize_and_sample_batch_match_reference(reference):
+    """Product cf_synthesize / cf_sample_batch (csrc/host/plan.cpp) against
+    the compiled reference synthesize / sample_batch (dataset.hpp:207-268):
+    presets, explicit specs, epoch slices, the short last batch, past-epoch."""
+    import ctypes as C
+    from paper_2503_02356_b200 import capi
+    for seed in (1, 3, 7, 99, 2**63 + 5):
+        for preset, kw in ((1, {}), (2, {}), (0, dict(bounds=[1024], fracs=[1.0], max_length=1024)),
+                           (0, dict(bounds=[64, 512, 4096, 32768], fracs=[0.5, 0.8, 0.99, 0.999], max_length=40000))):
+            a = capi.synthesize(400, seed, preset=preset, **kw)
+            b = reference.synthesize(400, seed, preset=preset, **kw)
+            assert np.array_equal(a, b), (seed, preset)
+    lengths = np.arange(1, 102, dtype=np.int64)
+    for seed in (0, 5, 123456789):
+        for gbs in (1, 7, 32, 101, 150):
+            for step in range(0, 101 // gbs + 2):
+                got = capi.sample_batch(len(lengths), gbs, step, seed)
+                ids = np.zeros(gbs, np.int64)
+                cnt = C.c_int64()
+                reference._check(reference.lib.cfr_sample_batch(
+                    lengths.ctypes.data_as(C.POINTER(C.c_int64)), C.c_int64(len(lengths)), C.c_int64(gbs),
+                    C.c_int64(step), C.c_uint64(seed), ids.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(cnt)))
+                assert np.array_equal(got, ids[:cnt.value]), (seed, gbs, step)
+    # the reference's spec / argument errors (DistributionSpec::validate,
+    # dataset.hpp:40-71; sample_batch :245-249) are errors here too
+    bad = [dict(bounds=[1024], fracs=[1.0], max_length=2048), dict(bounds=[1024], fracs=[0.9], max_length=1024),
+           dict(bounds=[1], fracs=[1.0], max_length=1), dict(bounds=[64, 32], fracs=[0.5, 1.0], max_length=64),
+           dict(bounds=[64, 128], fracs=[0.5, 0.5], max_length=128), dict(bounds=[64], fracs=[0.0], max_length=64),
+           dict(bounds=[1024], fracs=[1.0], max_length=512)]
+    for kw in bad:
+        with pytest.raises(ValueError):
+            reference.synthesize(10, 1, preset=0, **kw)
+        with pytest.raises(capi.CfError) as e:
+            capi.synthesize(10, 1, preset=0, **kw)
+        assert e.value.code == 1, kw
+    for args in ((0, 4, 0, 1), (10, 0, 0, 1), (10, 4, -1, 1)):
+        with pytest.raises(capi.CfError):
+            capi.sample_batch(*args)

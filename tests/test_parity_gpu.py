@@ -241,3 +241,96 @@ def test_fused_epilogues_multi_wave_discard_forward(ctx):
         off += rr * cc
         assert np.abs(a - b).max() / max(np.abs(a).max(), np.abs(b).max(), 1e-12) < 1e-2, model.tensor_info(i)[0]
     model.close()
+
+
+def _report(tag, rows):
+    import json
+    import os
+    out = os.environ.get("CF_PARITY_REPORT")
+    if out:
+        with open(out, "a") as f:
+            f.write(json.dumps({"case": tag, **rows}) + "\n")
+
+
+def test_c1_exact_config_matches_oracle(ctx, oracle):
+    """BASELINE config 1 exactly: toy arch, vocab 256, d 256,
+    4 heads / 2 KV heads (head_dim 64), 2 layers, model seed 1, the C1
+    canonical batch (synthesize(eval_table5, 32, seed 3) + a 2,048-token
+    sequence, tokens SplitMix64(5)), chunk 512, K = 2: 26 chunks, 54 events,
+    peak retained 1024, recompute 1024 tokens (plan_runner.hpp:368-395 run
+    on the GPU against the fp64 oracle on the GPU's bf16-rounded weights).
+    K = 1 must give bitwise the same gradients."""
+    from oracle.oracle import c1_batch, c1_cfg
+    lengths, tokens = c1_batch(oracle)
+    oc = c1_cfg()
+    gcfg = cf.model_cfg(arch=0, vocab=256, d=256, heads=4, kv_heads=2, layers=2, seed=1)
+    model = cf.Model(ctx, gcfg)
+    plan = cf.Plan.build(lengths, 512, 2)
+    ch, _, ev, diag = plan.export()
+    assert (len(ch), len(ev), diag["peak_retained_tokens"], diag["recompute_token_count"]) == (26, 54, 1024, 1024)
+    r = model.run_plan(plan, lengths, tokens)
+    params, grads = model.params_flat(), model.grads_flat()
+    ol, og, oi = oracle.run_plan(oc, lengths, tokens, 512, 2, params=params)
+    assert r.peak_retained_tokens == oi[0] == 1024
+    assert r.recompute_forward_count == oi[1] == 2
+    assert r.recompute_loss_mismatches == 0 and r.kv_completeness_violations == 0
+    rel = abs(r.loss - ol) / abs(ol)
+    errs = _per_tensor_err(model, grads, og)
+    worst = max(errs, key=lambda e: e[1])
+    _report("c1_exact", {"loss_gpu": r.loss, "loss_oracle": ol, "loss_rel": rel, "golden_loss_unrounded": 5.5455568137389548,
+                         "per_tensor": errs})
+    assert rel <= LOSS_TOL, (r.loss, ol)
+    assert worst[1] <= GRAD_TOL, worst
+    # K-independence (test_plan_runner.cpp:98-115) on the C1 workload
+    r1 = model.run_plan(cf.Plan.build(lengths, 512, 1), lengths, tokens)
+    assert r1.loss == r.loss and r1.recompute_loss_mismatches == 0
+    assert np.array_equal(model.grads_flat(), grads)
+    model.close()
+
+
+def test_production_width_llama_slice_matches_oracle(ctx):
+    """Production widths against the fp64 oracle (VERDICT r1 'what's weak'
+    #1): the C2 layer shape — d 4096, 32 heads / 8 KV heads (GQA 4), SwiGLU
+    ffn 11008, vocab 32000, RMSNorm, RoPE — with 2 layers.  A 3,400-token
+    sequence split into a 4-chunk dependent group at chunk 1024 (K = 1: three
+    recomputed forwards, prefix K/V reads, dK/dV accumulation) plus four
+    short sequences packed into one chunk.  Default GEMM mode, so the CTA-pair
+    kernel with the fused RoPE + KV-copy and SwiGLU epilogues runs multi-wave
+    (e.g. gate|up 1024 x 22016: 344 tiles over 74 CTA pairs).  Compared with
+    the vectorised fp64 oracle (oracle/llama_np.py, pinned to cf_oracle.cpp)
+    of the unchunked batch — the verify_equivalence comparison
+    (plan_runner.hpp:368-395) — on the GPU's bf16-rounded weights."""
+    from oracle import llama_np
+    from oracle.oracle import model_cfg as mcfg
+    dims = dict(vocab=32000, d=4096, heads=32, kv_heads=8, layers=2, ffn=11008, seed=1)
+    gcfg = cf.model_cfg(arch=1, **dims)
+    lengths = np.array([3400, 600, 250, 120, 40], np.int64)
+    tokens = cf.gen_tokens(lengths, dims["vocab"], 23)
+    model = cf.Model(ctx, gcfg)
+    plan = cf.Plan.build(lengths, 1024, 1)
+    ch, _, _, _ = plan.export()
+    assert [int(x) for x in ch["kind"]].count(1) == 4
+    r = model.run_plan(plan, lengths, tokens)
+    assert r.recompute_forward_count == 3 and r.recompute_loss_mismatches == 0
+    assert r.kv_completeness_violations == 0
+    grads = model.grads_flat()
+    # K = 2 retains one more chunk: bitwise identical gradients
+    r2 = model.run_plan(cf.Plan.build(lengths, 1024, 2), lengths, tokens)
+    assert r2.loss == r.loss and r2.recompute_forward_count == 2
+    assert np.array_equal(model.grads_flat(), grads)
+    params = model.params_flat()
+    model.close()
+    ol, og = llama_np.backward_full(mcfg(arch=1, **dims), params, lengths, tokens)
+    del params
+    rel = abs(r.loss - ol) / abs(ol)
+    shapes = llama_np.Shapes(mcfg(arch=1, **dims))
+    errs, off = [], 0
+    for name, rr, cc in shapes.tensors():
+        a, b = grads[off:off + rr * cc], og[off:off + rr * cc]
+        off += rr * cc
+        errs.append((name, float(np.abs(a - b).max() / max(np.abs(a).max(), np.abs(b).max(), 1e-12))))
+    worst = max(errs, key=lambda e: e[1])
+    _report("production_width_llama_2layer", {"loss_gpu": r.loss, "loss_oracle": ol, "loss_rel": rel,
+                                              "per_tensor": errs})
+    assert rel <= LOSS_TOL, (r.loss, ol)
+    assert worst[1] <= GRAD_TOL, worst
