@@ -136,50 +136,111 @@ def toy_flops(lengths, cfg, cs):
     return 6.0 * N * float(sum(lengths)) + 12.0 * L * d * pairs
 
 
-def cpu_reference_sample(target_s=15.0, procs=1):
-    """Times the UNMODIFIED reference run_plan (oracle/_ref/libcfref.so,
-    compiled from /root/reference in the build container) on a bounded slice
-    of the C1 toy batch on `procs` host processes (disjoint sequences), and
-    extrapolates to the C2 workload by algorithmic FLOPs/token."""
-    from oracle.oracle import Oracle, Reference, c1_batch, c1_cfg
-    try:
-        lib, kind = Reference(), "reference"
-    except FileNotFoundError:
-        lib, kind = Oracle(), "port"
+def _c1_workload():
+    from oracle.oracle import Oracle, c1_batch, c1_cfg
     o = Oracle()
     lengths, tokens = c1_batch(o)
-    cfg = c1_cfg()
-    # bounded sample: leading short sequences of the C1 batch (~1/3 of it)
+    return lengths, tokens, c1_cfg()
+
+
+def _disjoint_slices(lengths, parts):
+    """LPT split of the batch's sequences into `parts` disjoint subsets by
+    attention-weighted work (whole sequences, so a dependent group stays in
+    one process, as on the GPU)."""
+    order = np.argsort(-lengths, kind="stable")
+    load = np.zeros(parts)
+    out = [[] for _ in range(parts)]
+    for i in order:
+        w = float(lengths[i]) * (1.0 + lengths[i] / 2048.0)
+        r = int(np.argmin(load))
+        load[r] += w
+        out[r].append(int(i))
+    return [sorted(x) for x in out if x]
+
+
+def cpu_reference_sample(procs=1):
+    """Times the UNMODIFIED reference run_plan (oracle/_ref/libcfref.so,
+    compiled from /root/reference in the build container; the oracle port
+    when it is absent) on the C1 workload — toy model V256/d256/H4/KVH2/L2,
+    the canonical 33-sequence C1 batch incl. its 2,048-token sequence (a
+    4-chunk dependent group: prefix K/V reads, dK/dV scatter, recompute),
+    chunk 512, K = 2.
+      procs == 1: a bounded sample — the 2,048-token group plus the leading
+                  short sequences up to ~4,000 tokens — on one core;
+      procs  > 1: the FULL C1 batch split into `procs` disjoint subsets of
+                  whole sequences, one process each, wall-clock over all.
+    Returns C1 tokens/s and the same throughput converted to C2 tokens/s by
+    algorithmic FLOPs/token (the reference cannot run a Llama-shaped model)."""
+    from oracle.oracle import Oracle, Reference
+    try:
+        Reference()
+        kind = "reference"
+    except FileNotFoundError:
+        kind = "port"
+    lengths, tokens, cfg = _c1_workload()
     offs = np.concatenate([[0], np.cumsum(lengths)])
-    take = 11
-    sl, st = lengths[:take], tokens[:offs[take]]
-    flops = toy_flops(sl, cfg, 512)
-    t0 = time.perf_counter()
     if procs == 1:
-        lib.run_plan(cfg, sl, st, 512, 2)
+        pick, tot = [len(lengths) - 1], int(lengths[-1])
+        for i in range(len(lengths) - 1):
+            if tot + lengths[i] > 4000:
+                break
+            pick.append(i)
+            tot += int(lengths[i])
+        slices = [sorted(pick)]
+    else:
+        slices = _disjoint_slices(lengths, procs)
+    jobs = [(kind, lengths[s].tolist(), np.concatenate([tokens[offs[i]:offs[i + 1]] for i in s]).tolist(),
+             [int(i) for i in s]) for s in slices]
+    flops = sum(toy_flops(lengths[s], cfg, 512) for s in slices)
+    ntok = int(sum(lengths[s].sum() for s in slices))
+    if len(jobs) == 1:
+        t0 = time.perf_counter()
+        _ref_worker(*jobs[0])
         dt = time.perf_counter() - t0
-        agg_flops = flops
     else:
         import multiprocessing as mp
-        ctx = mp.get_context("fork")
-        with ctx.Pool(procs) as pool:
+        with mp.get_context("fork").Pool(len(jobs)) as pool:
             t0 = time.perf_counter()
-            pool.starmap(_ref_worker, [(kind, sl.tolist(), st.tolist()) for _ in range(procs)])
+            pool.starmap(_ref_worker, jobs)
             dt = time.perf_counter() - t0
-        agg_flops = flops * procs
-    fps = agg_flops / dt
+    fps = flops / dt
     c2_flops_per_token = c2_flops_per_token_est()
-    return {"kind": kind, "cpu_flops_per_s": fps, "seconds": dt, "sample_tokens": int(sl.sum()),
-            "sample": f"reference run_plan (toy C1 model, chunk 512, K=2) on the first {take} C1 sequences "
-                      f"({int(sl.sum())} tokens) x {procs} process(es); tokens/s extrapolated to C2 by "
-                      f"algorithmic FLOPs ({c2_flops_per_token / 1e9:.1f} GFLOP/token)",
-            "tokens_per_s": fps / c2_flops_per_token, "cores": procs}
+    what = (f"bounded C1 sample: the 2,048-token group + {len(slices[0]) - 1} short sequences ({ntok} tokens), 1 core"
+            if procs == 1 else f"full C1 batch ({ntok} tokens, 33 sequences) in {len(jobs)} disjoint processes")
+    return {"kind": kind, "cpu_flops_per_s": fps, "seconds": dt, "sample_tokens": ntok,
+            "c1_tokens_per_s": ntok / dt,
+            "sample": f"reference run_plan, toy C1 model (V256 d256 H4 KVH2 L2), chunk 512, K=2 — {what}; "
+                      f"tokens/s converted to C2 by algorithmic FLOPs ({c2_flops_per_token / 1e9:.1f} GFLOP/token)",
+            "tokens_per_s": fps / c2_flops_per_token, "cores": len(jobs)}
 
 
-def _ref_worker(kind, sl, st):
+def _ref_worker(kind, sl, st, ids):
     from oracle.oracle import Oracle, Reference, c1_cfg
     lib = Reference() if kind == "reference" else Oracle()
-    lib.run_plan(c1_cfg(), np.array(sl), np.array(st, np.int32), 512, 2)
+    lib.run_plan(c1_cfg(), np.array(sl), np.array(st, np.int32), 512, 2, ids=np.array(ids, np.int64))
+
+
+def gpu_c1_side_by_side(ctx, steps=3):
+    """The GPU on the same C1 workload (toy model, C1 batch, chunk 512, K=2)
+    through the public call (plan build + cf_run_plan with host buffers),
+    device-timed: the like-for-like counterpart of the CPU baseline."""
+    import torch
+    import paper_2503_02356_b200 as cf
+    lengths, tokens, _ = _c1_workload()
+    model = cf.Model(ctx, cf.model_cfg(arch=0, vocab=256, d=256, heads=4, kv_heads=2, layers=2, seed=1))
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    for _ in range(2):
+        model.run_plan(cf.Plan.build(lengths, 512, 2), lengths, tokens)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        r = model.run_plan(cf.Plan.build(lengths, 512, 2), lengths, tokens)
+    e1.record(stream)
+    e1.synchronize()
+    model.close()
+    return {"tokens_per_s": float(lengths.sum()) * steps / (e0.elapsed_time(e1) / 1e3), "loss": r.loss,
+            "tokens": int(lengths.sum())}
 
 
 def c2_flops_per_token_est():
@@ -310,7 +371,11 @@ def run_b200(args):
     step_ms = ms_max / args.steps
     value = tokens_all / (step_ms / 1e3)  # tokens of one step over all ranks / slowest rank's step time
     mfu = r0.model_flops * world / (step_ms / 1e3) / 1e12
-    cpu = cpu_reference_sample() if (world == 1 and not args.no_cpu_baseline) else None
+    cpu = cpu_nproc = c1_gpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(procs=1)
+        cpu_nproc = cpu_reference_sample(procs=os.cpu_count() or 1)
+        c1_gpu = gpu_c1_side_by_side(ctx)
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -348,6 +413,14 @@ def run_b200(args):
     if cpu:
         line["cpu_baseline"] = {"value": cpu["tokens_per_s"], "unit": "tokens/s", "cores": cpu["cores"],
                                 "kind": cpu["kind"], "sample": cpu["sample"]}
+        # like-for-like on the C1 workload itself (no FLOP conversion): the
+        # reference on 1 core (bounded sample) and on every host core (full
+        # batch, disjoint processes) beside the GPU on the full C1 batch
+        line["c1_side_by_side"] = {
+            "unit": "C1 tokens/s", "workload": "toy V256 d256 H4 KVH2 L2, C1 batch (10,266 tokens), chunk 512, K=2",
+            "cpu_reference_1core": cpu["c1_tokens_per_s"], "cpu_reference_all_cores": cpu_nproc["c1_tokens_per_s"],
+            "cpu_cores": cpu_nproc["cores"], "gpu_b200": c1_gpu["tokens_per_s"],
+            "gpu_note": "plan build + cf_run_plan with host buffers per step; the toy model is launch-bound on a B200"}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

@@ -164,15 +164,18 @@ int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out)
  * (scheduler.hpp:36-43): `events` in execution order; ExecutionPlan.groups as
  * CSR (group_ids[g], members[group_offsets[g] .. group_offsets[g+1]), index
  * order; n_groups may be 0); ExecutionPlan.chunk_tokens as parallel arrays (a
- * chunk without an entry counts chunk_size tokens).  The result is a plan
- * with no chunks whose diagnostics and violation texts (the reference's,
- * verbatim) are read with cf_plan_export / cf_plan_violation and whose listing
- * is cf_plan_listing.  Violations are data, not an error status (as in the
- * reference); cf_run_plan refuses a plan that has any. */
+ * chunk without an entry counts chunk_size tokens).  The result's
+ * diagnostics and violation texts (the reference's, verbatim) are read with
+ * cf_plan_export / cf_plan_violation, its listing with cf_plan_listing.
+ * chunk_plan (may be NULL) supplies the chunks the events refer to (e.g. the
+ * plan of cf_plan_build): the result then carries them and can be executed by
+ * cf_run_plan / cf_step_prepare — a caller-reordered schedule.  Violations are
+ * data, not an error status (as in the reference); cf_run_plan refuses a plan
+ * that has any ("execution plan is invalid: ...", plan_runner.hpp:80). */
 int cf_plan_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* events, int64_t n_events,
                             const int64_t* group_ids, const int64_t* group_offsets, const int64_t* members,
                             int64_t n_groups, const int64_t* token_chunk_ids, const int64_t* token_counts,
-                            int64_t n_token_entries, cf_plan** out);
+                            int64_t n_token_entries, const cf_plan* chunk_plan, cf_plan** out);
 int cf_plan_counts(const cf_plan* plan, int64_t* n_chunks, int64_t* n_segments,
                    int64_t* n_events, int64_t* n_groups);
 int cf_plan_export(const cf_plan* plan, cf_chunk_rec* chunks,

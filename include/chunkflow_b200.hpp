@@ -8,7 +8,10 @@
 // std::runtime_error.
 #pragma once
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -96,11 +99,12 @@ struct ChunkPlan {
   std::map<int64_t, std::vector<int64_t>> groups;
   std::vector<int64_t> ids, lengths;  // the batch it was built from
 };
-struct ExecutionPlan {
+struct ExecutionPlan {  // scheduler.hpp:35-43
   std::vector<ExecEvent> events;
   int64_t k = 1, chunk_size = 0;
   std::map<int64_t, std::vector<int64_t>> groups;
-  std::shared_ptr<PlanHandle> handle;
+  std::map<int64_t, int64_t> chunk_tokens;
+  std::shared_ptr<PlanHandle> handle;  // the library plan of the chunks (set by schedule_step)
 };
 
 namespace detail {
@@ -113,8 +117,9 @@ inline std::shared_ptr<PlanHandle> build(const std::vector<int64_t>& ids, const 
 inline std::map<int64_t, std::vector<int64_t>> groups_of(cf_plan* p) {
   int64_t nc = 0, ns = 0, ne = 0, ng = 0;
   check(cf_plan_counts(p, &nc, &ns, &ne, &ng));
-  std::vector<int64_t> gid(static_cast<size_t>(ng) + 1), off(static_cast<size_t>(ng) + 1),
-      mem(static_cast<size_t>(nc) + 1);
+  std::vector<int64_t> gid(static_cast<size_t>(ng) + 1), off(static_cast<size_t>(ng) + 1);
+  check(cf_plan_export_groups(p, nullptr, off.data(), nullptr));  // sizes the member list
+  std::vector<int64_t> mem(static_cast<size_t>(off[static_cast<size_t>(ng)]) + 1);
   check(cf_plan_export_groups(p, gid.data(), off.data(), mem.data()));
   std::map<int64_t, std::vector<int64_t>> out;
   for (int64_t g = 0; g < ng; ++g) out[gid[g]] = std::vector<int64_t>(mem.begin() + off[g], mem.begin() + off[g + 1]);
@@ -174,21 +179,50 @@ inline ExecutionPlan schedule_step(const ChunkPlan& chunk_plan, int64_t k) {
     plan.events.push_back(x);
   }
   plan.groups = chunk_plan.groups;
+  for (const Chunk& c : chunk_plan.chunks) plan.chunk_tokens[c.chunk_id] = c.total_tokens;
   return plan;
 }
 
-// validate_plan (scheduler.hpp:182)
-inline PlanDiagnostics validate_plan(const ExecutionPlan& plan) {
+namespace detail {
+// The plan as the caller holds it (events possibly edited or built by hand),
+// replayed by the library; carries the chunks of `plan.handle` when present.
+inline std::shared_ptr<PlanHandle> replay(const ExecutionPlan& plan) {
+  std::vector<cf_event_rec> ev;
+  for (const ExecEvent& e : plan.events)
+    ev.push_back({static_cast<int64_t>(e.kind), e.chunk_id, e.group_id, e.index_in_group, e.is_recompute ? 1 : 0,
+                  e.notes.save_kv ? 1 : 0, e.notes.read_kv_prefix ? 1 : 0, e.notes.accumulate_kv_grad ? 1 : 0});
+  std::vector<int64_t> gid, off{0}, mem, tc, tn;
+  for (const auto& [g, members] : plan.groups) {
+    gid.push_back(g);
+    mem.insert(mem.end(), members.begin(), members.end());
+    off.push_back(static_cast<int64_t>(mem.size()));
+  }
+  for (const auto& [c, t] : plan.chunk_tokens) {
+    tc.push_back(c);
+    tn.push_back(t);
+  }
+  cf_plan* p = nullptr;
+  check(cf_plan_validate_events(plan.chunk_size, plan.k, ev.data(), static_cast<int64_t>(ev.size()), gid.data(),
+                                off.data(), mem.data(), static_cast<int64_t>(gid.size()), tc.data(), tn.data(),
+                                static_cast<int64_t>(tc.size()), plan.handle ? plan.handle->get() : nullptr, &p));
+  return std::make_shared<PlanHandle>(p);
+}
+inline PlanDiagnostics diagnostics(cf_plan* p) {
   cf_plan_diag d{};
-  check(cf_plan_export(plan.handle->get(), nullptr, nullptr, nullptr, &d));
+  check(cf_plan_export(p, nullptr, nullptr, nullptr, &d));
   PlanDiagnostics out{d.peak_retained_tokens, d.recompute_token_count, {}};
   for (int64_t i = 0; i < d.num_violations; ++i) {
     char buf[256];
-    check(cf_plan_violation(plan.handle->get(), i, buf, sizeof(buf)));
+    check(cf_plan_violation(p, i, buf, sizeof(buf)));
     out.violations.emplace_back(buf);
   }
   return out;
 }
+}  // namespace detail
+
+// validate_plan (scheduler.hpp:182): replays plan.events as the caller holds
+// them (so hand-built or edited plans get the reference's violation texts).
+inline PlanDiagnostics validate_plan(const ExecutionPlan& plan) { return detail::diagnostics(detail::replay(plan)->get()); }
 
 // --- pipeline.hpp:24-72 types and the simulator entry points
 struct CostModel {  // pipeline.hpp:24-47
@@ -434,11 +468,183 @@ inline cf_run_result run_plan(const Model& model, const ChunkPlan& /*chunk_plan*
       throw ValidationError("sequence " + std::to_string(s.id) + " has no token payload");
     tokens.insert(tokens.end(), s.tokens.begin(), s.tokens.end());
   }
+  if (!exec_plan.handle) throw ValidationError("execution plan has no chunk plan (build it with schedule_step)");
+  // run_plan validates the plan it is given (plan_runner.hpp:78-81): the
+  // caller's events are replayed, and an edited but valid schedule runs as is
+  const auto plan = detail::replay(exec_plan);
+  const PlanDiagnostics diag = detail::diagnostics(plan->get());
+  if (!diag.violations.empty()) throw ValidationError("execution plan is invalid: " + diag.violations.front());
   cf_run_opts o{options.corrupt_kv_grads ? 1 : 0, 0, options.normalizer_override};
   cf_run_result r{};
-  check(cf_run_plan(model.device().get(), model.get(), exec_plan.handle->get(), ids.data(), lengths.data(),
-                    tokens.data(), static_cast<int64_t>(ids.size()), &o, &r));
+  check(cf_run_plan(model.device().get(), model.get(), plan->get(), ids.data(), lengths.data(), tokens.data(),
+                    static_cast<int64_t>(ids.size()), &o, &r));
   return r;
+}
+
+// --- GradientSet / compare_gradients / backward_full / verify_equivalence
+//     (toy_model.hpp:88-108, :575-596, :654-718; plan_runner.hpp:343-395).
+// The GPU keeps gradients in the model's device buffer; read_gradients()
+// copies them out in the reference tensor order as fp64.
+struct Tensor {  // toy_model.hpp:48-56
+  std::string name;
+  int64_t rows = 0, cols = 0;
+  std::vector<double> data;
+  size_t size() const { return data.size(); }
+};
+struct GradientSet {  // toy_model.hpp:88-93
+  std::vector<Tensor> tensors;
+  double loss = 0.0;
+};
+
+inline GradientSet read_gradients(const Model& model, double loss) {
+  GradientSet g;
+  g.loss = loss;
+  const int64_t n = cf_model_num_tensors(model.get());
+  for (int64_t i = 0; i < n; ++i) {
+    Tensor t;
+    char name[128];
+    check(cf_model_tensor_info(model.get(), i, name, sizeof(name), &t.rows, &t.cols));
+    t.name = name;
+    t.data.resize(static_cast<size_t>(t.rows * t.cols));
+    check(cf_model_get_grad(model.get(), i, t.data.data()));
+    g.tensors.push_back(std::move(t));
+  }
+  return g;
+}
+
+inline std::string format_scientific(double value) {  // common.hpp:81-85
+  char buf[64];
+  std::snprintf(buf, sizeof(buf), "%.6e", value);
+  return std::string(buf);
+}
+
+struct GradComparisonRow {  // toy_model.hpp:656-660
+  std::string name;
+  double max_abs_diff = 0.0;
+  double rel_err = 0.0;
+};
+struct GradComparison {  // toy_model.hpp:662-679
+  std::vector<GradComparisonRow> rows;
+  double loss_a = 0.0, loss_b = 0.0, loss_rel_err = 0.0, max_rel_err = 0.0, mean_rel_err = 0.0;
+  std::string to_text() const {
+    std::string out;
+    for (const GradComparisonRow& row : rows)
+      out += row.name + " max_abs_diff=" + format_scientific(row.max_abs_diff) +
+             " rel_err=" + format_scientific(row.rel_err) + "\n";
+    out += "loss_rel_err=" + format_scientific(loss_rel_err) + "\n";
+    out += "max_rel_err=" + format_scientific(max_rel_err) + "\n";
+    out += "mean_rel_err=" + format_scientific(mean_rel_err) + "\n";
+    return out;
+  }
+};
+
+// compare_gradients (toy_model.hpp:681-718): per-tensor max-norm relative
+// error, optionally restricted to masked entries.
+inline GradComparison compare_gradients(const GradientSet& a, const GradientSet& b,
+                                        const std::vector<std::vector<uint8_t>>* mask = nullptr,
+                                        double denom_floor = 1e-12) {
+  if (a.tensors.size() != b.tensors.size()) throw ValidationError("gradient sets have different tensor counts");
+  GradComparison cmp;
+  cmp.loss_a = a.loss;
+  cmp.loss_b = b.loss;
+  cmp.loss_rel_err = std::abs(a.loss - b.loss) / std::max({std::abs(a.loss), std::abs(b.loss), denom_floor});
+  double rel_sum = 0.0;
+  for (size_t ti = 0; ti < a.tensors.size(); ++ti) {
+    const Tensor& ta = a.tensors[ti];
+    const Tensor& tb = b.tensors[ti];
+    if (ta.size() != tb.size()) throw ValidationError("gradient tensor shape mismatch for " + ta.name);
+    double max_diff = 0.0, max_mag = 0.0;
+    for (size_t i = 0; i < ta.data.size(); ++i) {
+      if (mask && !(*mask)[ti][i]) continue;
+      max_diff = std::max(max_diff, std::abs(ta.data[i] - tb.data[i]));
+      max_mag = std::max({max_mag, std::abs(ta.data[i]), std::abs(tb.data[i])});
+    }
+    GradComparisonRow row{ta.name, max_diff, max_diff / std::max(max_mag, denom_floor)};
+    cmp.max_rel_err = std::max(cmp.max_rel_err, row.rel_err);
+    rel_sum += row.rel_err;
+    cmp.rows.push_back(std::move(row));
+  }
+  cmp.mean_rel_err = cmp.rows.empty() ? 0.0 : rel_sum / static_cast<double>(cmp.rows.size());
+  return cmp;
+}
+
+namespace detail {
+inline void flatten(const SequenceSet& batch, std::vector<int64_t>& ids, std::vector<int64_t>& lengths,
+                    std::vector<int32_t>& tokens) {
+  for (const SequenceRecord& s : batch) {
+    if (static_cast<int64_t>(s.tokens.size()) != s.length)
+      throw ValidationError("sequence " + std::to_string(s.id) + " has no token payload");
+    ids.push_back(s.id);
+    lengths.push_back(s.length);
+    tokens.insert(tokens.end(), s.tokens.begin(), s.tokens.end());
+  }
+}
+}  // namespace detail
+
+// backward_full (toy_model.hpp:575-596): every sequence alone, unchunked;
+// the model's gradient buffer is overwritten and returned.
+inline GradientSet backward_full(const Model& model, const SequenceSet& batch, double normalizer_override = 0.0) {
+  std::vector<int64_t> ids, lengths;
+  std::vector<int32_t> tokens;
+  detail::flatten(batch, ids, lengths, tokens);
+  cf_run_result r{};
+  check(cf_backward_full(model.device().get(), model.get(), ids.data(), lengths.data(), tokens.data(),
+                         static_cast<int64_t>(ids.size()), normalizer_override, &r));
+  return read_gradients(model, r.loss);
+}
+
+struct RunInstrumentation {  // plan_runner.hpp:36-47
+  int64_t peak_retained_tokens = 0, recompute_forward_count = 0, recompute_loss_mismatches = 0,
+          kv_completeness_violations = 0;
+};
+
+struct VerifyReport {  // plan_runner.hpp:343-366
+  bool pass = false;
+  double loss_rel_err = 0.0;
+  double max_grad_rel_err = 0.0;
+  GradComparison comparison;
+  RunInstrumentation instrumentation;
+  int64_t chunk_count = 0;
+  int64_t event_count = 0;
+  std::string to_text() const {
+    std::string out;
+    out += "chunks: " + std::to_string(chunk_count) + "\n";
+    out += "events: " + std::to_string(event_count) + "\n";
+    out += comparison.to_text();
+    out += "recompute_forwards: " + std::to_string(instrumentation.recompute_forward_count) + "\n";
+    out += "recompute_loss_mismatches: " + std::to_string(instrumentation.recompute_loss_mismatches) + "\n";
+    out += "kv_completeness_violations: " + std::to_string(instrumentation.kv_completeness_violations) + "\n";
+    out += std::string("result: ") + (pass ? "PASS" : "FAIL") + "\n";
+    return out;
+  }
+};
+
+// verify_equivalence (plan_runner.hpp:368-395) on the GPU: chunk, schedule
+// and run the batch, then compare with backward_full.  The reference's
+// defaults (1e-12 / 1e-9) are fp64 tolerances; a bf16/fp32 B200 model needs
+// the tolerances of DESIGN.md §4 (e.g. 1e-4 / 1e-2 chunked vs unchunked).
+inline VerifyReport verify_equivalence(const Model& model, const SequenceSet& batch, int64_t chunk_size, int64_t k,
+                                       double loss_tol = 1e-12, double grad_tol = 1e-9,
+                                       const RunPlanOptions& options = {}) {
+  Batch wrapped;
+  wrapped.sequences = batch;
+  wrapped.global_batch_size = static_cast<int64_t>(batch.size());
+  const ChunkPlan chunk_plan = construct_chunks(wrapped, chunk_size);
+  const ExecutionPlan exec_plan = schedule_step(chunk_plan, k);
+  const cf_run_result run = run_plan(model, chunk_plan, exec_plan, batch, options);
+  const GradientSet chunked = read_gradients(model, run.loss);
+  const GradientSet full = backward_full(model, batch, options.normalizer_override);
+  VerifyReport report;
+  report.chunk_count = static_cast<int64_t>(chunk_plan.chunks.size());
+  report.event_count = static_cast<int64_t>(exec_plan.events.size());
+  report.comparison = compare_gradients(chunked, full);
+  report.loss_rel_err = report.comparison.loss_rel_err;
+  report.max_grad_rel_err = report.comparison.max_rel_err;
+  report.instrumentation = {run.peak_retained_tokens, run.recompute_forward_count, run.recompute_loss_mismatches,
+                            run.kv_completeness_violations};
+  report.pass = report.loss_rel_err <= loss_tol && report.max_grad_rel_err <= grad_tol &&
+                run.recompute_loss_mismatches == 0 && run.kv_completeness_violations == 0;
+  return report;
 }
 
 namespace detail {

@@ -219,11 +219,12 @@ class Plan:
         return cls(h)
 
     @classmethod
-    def validate_events(cls, events, chunk_size, k=1, groups=None, chunk_tokens=None):
+    def validate_events(cls, events, chunk_size, k=1, groups=None, chunk_tokens=None, chunk_plan=None):
         """validate_plan (scheduler.hpp:182) over a caller-built ExecutionPlan:
         `events` an EVENT_DT array, `groups` {group: [chunk ids in index order]},
         `chunk_tokens` {chunk: tokens}.  Diagnostics via export()[3] /
-        violations() / listing()."""
+        violations() / listing().  With `chunk_plan` (a Plan.build result) the
+        returned plan carries its chunks and can be run."""
         ev = np.ascontiguousarray(events, EVENT_DT)
         groups = groups or {}
         gid = np.array(sorted(groups), np.int64)
@@ -240,7 +241,7 @@ class Plan:
         check(lib().cf_plan_validate_events(C.c_int64(chunk_size), C.c_int64(k), _p(ev), C.c_int64(len(ev)),
                                             _p(gid if len(gid) else np.zeros(1, np.int64)), _p(off), _p(mem),
                                             C.c_int64(len(gid)), _p(tc), _p(tn), C.c_int64(len(chunk_tokens)),
-                                            C.byref(h)))
+                                            chunk_plan.h if chunk_plan is not None else None, C.byref(h)))
         return cls(h)
 
     def partition(self, world, rank):

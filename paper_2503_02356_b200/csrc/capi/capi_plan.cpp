@@ -42,7 +42,7 @@ int cf_plan_build_group(int64_t n, int64_t k, int64_t chunk_size, cf_plan** out)
 int cf_plan_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* events, int64_t n_events,
                             const int64_t* group_ids, const int64_t* group_offsets, const int64_t* members,
                             int64_t n_groups, const int64_t* token_chunk_ids, const int64_t* token_counts,
-                            int64_t n_token_entries, cf_plan** out) {
+                            int64_t n_token_entries, const cf_plan* chunk_plan, cf_plan** out) {
   return cfb::guard([&] {
     if (!out) throw cfb::ValidationError("out is null");
     if (n_events < 0 || n_groups < 0 || n_token_entries < 0) throw cfb::ValidationError("negative count");
@@ -51,6 +51,12 @@ int cf_plan_validate_events(int64_t chunk_size, int64_t k, const cf_event_rec* e
       throw cfb::ValidationError("null array with a non-zero count");
     auto h = std::make_unique<cf_plan>();
     cfb::Plan& p = h->p;
+    if (chunk_plan) {  // the chunks the events refer to, so the result can be executed
+      p.chunks = chunk_plan->p.chunks;
+      p.segments = chunk_plan->p.segments;
+      p.index_of = chunk_plan->p.index_of;
+      p.chunk_tokens = chunk_plan->p.chunk_tokens;
+    }
     p.chunk_size = chunk_size;
     p.k = k;
     for (int64_t g = 0; g < n_groups; ++g) {

@@ -10,6 +10,18 @@ int main() {
   auto d = cf::validate_plan(ep);
   std::printf("chunks=%zu events=%zu peak=%lld recompute=%lld groups=%zu\n", cp.chunks.size(), ep.events.size(),
               (long long)d.peak_retained_tokens, (long long)d.recompute_token_count, cp.groups.size());
+  // validate_plan replays the plan as held: edits are seen (test_scheduler.cpp:165-221)
+  auto edited = ep;
+  std::swap(edited.events[5], edited.events[6]);  // F+ chunk3 <-> B chunk3: backward without retain
+  const auto de = cf::validate_plan(edited);
+  std::printf("edited_violations=%zu first=%s\n", de.violations.size(),
+              de.violations.empty() ? "-" : de.violations[0].c_str());
+  cf::ExecutionPlan hand;  // hand-built: one backward, nothing retained
+  hand.chunk_size = 4;
+  cf::ExecEvent bw;
+  bw.kind = cf::ExecKind::kBackward;
+  hand.events.push_back(bw);
+  std::printf("hand=%s\n", cf::validate_plan(hand).violations.at(0).c_str());
   try { cf::construct_chunks(b, 0); } catch (const cf::ValidationError& e) { std::printf("ValidationError: %s\n", e.what()); }
   // pipeline.hpp worked example (test_pipeline.cpp:141-211): 56 / 54 / 46 / 60 units
   cf::PipelineConfig pc;

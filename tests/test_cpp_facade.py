@@ -15,6 +15,8 @@ def test_cpp_facade_builds_and_plans(tmp_path):
                     f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
     assert "chunks=4 events=9 peak=2 recompute=2 groups=1" in out
+    assert "edited_violations=" in out and "without a live retain-forward" in out
+    assert "hand=backward of chunk 0 without a live retain-forward" in out
     assert "ValidationError: chunk_size must be at least 1" in out
     assert "makespans=56,54,46 bubble=55.56 stage0_ops=9" in out
     assert "base=34.8714 resid=0.59524" in out  # test_memory_model.cpp: 34.8717 +- 1e-3
