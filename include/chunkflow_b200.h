@@ -111,6 +111,15 @@ typedef struct cf_run_opts {
   int32_t corrupt_kv_grads;   /* fault-injection hook: scale incoming dK/dV */
   int32_t accumulate_grads;   /* 0: zero grads first (reference semantics) */
   double normalizer_override; /* > 0 replaces the global target count */
+  /* at most this many full activation tapes resident per stage / runner
+   * (0 = no limit; meant for pipeline stages, cf_pp_step_run /
+   * cf_pp_run_local, whose 1F1B warm-up keeps min(P - s, M) chunks in
+   * flight).  A first-pass retain-forward that would leave no free slot keeps
+   * only its stage input ([T, d] fp32; nothing on stage 0, which re-embeds its
+   * tokens) and is recomputed just before its backward (stage-input
+   * checkpointing); the free slot holds that just-in-time tape.  Results are
+   * bitwise those without a budget. */
+  int64_t stage_tape_budget;
 } cf_run_opts;
 
 /* RunPlanResult + RunInstrumentation (plan_runner.hpp:36-60), plus the
@@ -141,6 +150,10 @@ typedef struct cf_run_result {
   double attn_bwd_ms, attn_bwd_flops; /* attention backward (algorithmic FLOPs) */
   int64_t attn_bwd_launches;
   int64_t other_launches;
+  /* stage-input checkpointing (cf_run_opts.stage_tape_budget): high-water of
+   * full tapes resident on one stage, and the extra forwards it cost */
+  int64_t peak_live_tapes;
+  int64_t checkpoint_recomputes;
 } cf_run_result;
 
 typedef struct cf_ctx cf_ctx;
@@ -290,6 +303,13 @@ int cf_pp_simulate(const cf_plan* plan, int64_t num_stages, int64_t k,
                    const double* fwd_cost, const double* bwd_cost,
                    cf_pp_op* ops, double* busy, double* busy_total,
                    cf_pp_result* result);
+/* cf_pp_simulate for the executor under a per-stage tape budget
+ * (cf_run_opts.stage_tape_budget): each stage's checkpointed chunks (its op
+ * stream replayed as cf_pp_stage_memory does) pay their forward again inside
+ * their backward.  tape_budget = 0 is exactly cf_pp_simulate. */
+int cf_pp_simulate_budget(const cf_plan* plan, int64_t num_stages, int64_t k, const cf_pp_cost* cost,
+                          int backward_first, const double* fwd_cost, const double* bwd_cost, int64_t tape_budget,
+                          cf_pp_op* ops, double* busy, double* busy_total, cf_pp_result* result);
 /* simulate_1f1b (pipeline.hpp:218-242): whole sequences as microbatches. */
 int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages,
                         const cf_pp_cost* cost, cf_pp_op* ops, double* busy,
@@ -321,6 +341,30 @@ int cf_tune_grid_search(const int64_t* ids, const int64_t* lengths, int64_t n,
                         uint64_t seed, cf_tune_row* table, int64_t* best_chunk_size,
                         int64_t* best_k, int64_t* evaluations, int csv, char* buf,
                         size_t cap, size_t* len);
+/* Pipeline-aware grid_search (new; the reference's tuner.hpp:39-112 sizes
+ * memory as k * chunk_size retained tokens, but a 1F1B stage holds min(P - s,
+ * M) chunks in flight): every sampled batch's stage op streams are replayed
+ * under the executor's rules with `tape_budget` (cf_run_opts.
+ * stage_tape_budget; 0 = none); a candidate is feasible when every stage's
+ * base + per_chunk_token_gib * peak tape tokens + kept_token_gib * peak
+ * kept-input tokens + per_context_token_gib * gqa * longest sequence fits
+ * budget_gib (table rows report the worst stage).  Timing adds each stage's
+ * checkpoint recomputes to its backwards.  Other arguments and outputs as
+ * cf_tune_grid_search. */
+int cf_tune_grid_search_pp(const int64_t* ids, const int64_t* lengths, int64_t n, const int64_t* chunk_sizes,
+                           int64_t ncs, const int64_t* ks, int64_t nk, int64_t num_stages, const cf_pp_cost* cost,
+                           const cf_mem_coeffs* mem, double kept_token_gib, int64_t tape_budget, double budget_gib,
+                           int64_t global_batch_size, int64_t batches_to_sample, uint64_t seed,
+                           cf_tune_row* table, int64_t* best_chunk_size, int64_t* best_k, int64_t* evaluations,
+                           int csv, char* buf, size_t cap, size_t* len);
+/* Activation memory of each stage of the chunk-aware 1F1B (retention budget
+ * k) under a per-stage tape budget, replayed with the executor's rules:
+ * peak resident tapes and their tokens, peak tokens of kept stage inputs
+ * ([T, d] fp32 each), and how many first-pass forwards were checkpointed.
+ * Arrays (may be NULL) have num_stages entries. */
+int cf_pp_stage_memory(const cf_plan* plan, int64_t num_stages, int64_t k, int64_t tape_budget,
+                       int64_t* peak_tapes, int64_t* peak_tape_tokens, int64_t* peak_kept_tokens,
+                       int64_t* checkpointed);
 /* Layer range [begin, end) that stage `stage` of `num_stages` executes. */
 int cf_pp_stage_layers(int64_t num_layers, int64_t stage, int64_t num_stages,
                        int64_t* begin, int64_t* end);
@@ -505,6 +549,15 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
  * kc / vc (may be NULL) receive the k columns [col_k, col_v) and the v
  * columns [col_v, n) with row pitch cache_ld.  CF_EVALIDATION-class error
  * (cudaErrorInvalidValue) when the shape is not eligible (tile alignment). */
+/* Fused LM head + cross-entropy (the path run_plan uses): x bf16 [T, d]
+ * (row pitch d), head bf16 [d, ldh] ([in, out], columns >= V ignored),
+ * targets int32 [T] (-1 = no target).  Writes lse [T] and row_loss [T]
+ * (lse - logit[target], 0 without a target) from the head GEMM's epilogue
+ * partials; when dlogits != NULL also the bf16 [T, ldh] gradient
+ * (softmax - onehot) * inv_norm recomputed by a second head GEMM.  All
+ * pointers are device pointers. */
+int cf_op_lm_head_ce(cf_ctx* ctx, const void* x, const void* head, int64_t ldh, int64_t T, int64_t V, int64_t d,
+                     const int32_t* targets, float inv_norm, float* lse, float* row_loss, void* dlogits);
 int cf_op_gemm_rope(cf_ctx* ctx, const void* a, int64_t lda, const void* w, int64_t ldw,
                     void* c, int64_t m, int64_t n, int64_t k, const void* tab,
                     int64_t col_k, int64_t col_v, void* kc, void* vc, int64_t cache_ld);

@@ -45,7 +45,7 @@ class ModelCfg(C.Structure):
 
 class RunOpts(C.Structure):
     _fields_ = [("corrupt_kv_grads", C.c_int32), ("accumulate_grads", C.c_int32),
-                ("normalizer_override", C.c_double)]
+                ("normalizer_override", C.c_double), ("stage_tape_budget", C.c_int64)]
 
 
 class PpCost(C.Structure):
@@ -74,7 +74,8 @@ class RunResult(C.Structure):
                 ("hw_flops", C.c_double), ("gemm_ms", C.c_double), ("gemm_flops", C.c_double),
                 ("gemm_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
                 ("attn_launches", C.c_int64), ("attn_bwd_ms", C.c_double), ("attn_bwd_flops", C.c_double),
-                ("attn_bwd_launches", C.c_int64), ("other_launches", C.c_int64)]
+                ("attn_bwd_launches", C.c_int64), ("other_launches", C.c_int64),
+                ("peak_live_tapes", C.c_int64), ("checkpoint_recomputes", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -97,7 +98,8 @@ EXPORTS = [
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
     "cf_segment_forward", "cf_segment_backward", "cf_segment_destroy", "cf_op_gemm_rope",
-    "cf_plan_validate_events",
+    "cf_plan_validate_events", "cf_op_lm_head_ce", "cf_pp_stage_memory", "cf_tune_grid_search_pp",
+    "cf_pp_simulate_budget",
 ]
 
 _lib = None
@@ -124,6 +126,8 @@ def lib():
         L.cf_ctx_stream.argtypes = [vp]
         L.cf_op_gemm.argtypes = [vp, vp, C.c_int, C.c_int64, vp, C.c_int, C.c_int64, vp, C.c_int64,
                                  C.c_int64, C.c_int64, C.c_int64, C.c_int, vp, C.c_int64]
+        L.cf_op_lm_head_ce.argtypes = [vp, vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, vp, C.c_float, vp,
+                                       vp, vp]
         _lib = L
     return _lib
 
@@ -268,20 +272,28 @@ def _pp_cost(cost):
     return PpCost(**c)
 
 
-def pp_simulate(plan: "Plan", stages, k, cost=None, backward_first=True, fwd_cost=None, bwd_cost=None):
-    """simulate_state_aware_1f1b + bubble_ratio (pipeline.hpp:250-331).
-    Returns (ops[stages, per] of PP_OP_DT, busy, busy_total, PpResult)."""
+def pp_simulate(plan: "Plan", stages, k, cost=None, backward_first=True, fwd_cost=None, bwd_cost=None,
+                tape_budget=0):
+    """simulate_state_aware_1f1b + bubble_ratio (pipeline.hpp:250-331);
+    tape_budget > 0 times the executor's stage-input checkpointing
+    (cf_pp_simulate_budget).  Returns (ops[stages, per] of PP_OP_DT, busy,
+    busy_total, PpResult)."""
     c = _pp_cost(cost)
     r = PpResult()
     fw = None if fwd_cost is None else np.ascontiguousarray(fwd_cost, np.float64)
     bw = None if bwd_cost is None else np.ascontiguousarray(bwd_cost, np.float64)
     args = (plan.h, C.c_int64(stages), C.c_int64(k), C.byref(c), C.c_int(int(backward_first)),
             None if fw is None else _p(fw), None if bw is None else _p(bw))
-    check(lib().cf_pp_simulate(*args, None, None, None, C.byref(r)))
+    if tape_budget:
+        args = args + (C.c_int64(tape_budget),)
+        fn = lib().cf_pp_simulate_budget
+    else:
+        fn = lib().cf_pp_simulate
+    check(fn(*args, None, None, None, C.byref(r)))
     ops = np.zeros((stages, r.ops_per_stage), PP_OP_DT)
     busy = np.zeros(stages, np.float64)
     busy_t = np.zeros(stages, np.float64)
-    check(lib().cf_pp_simulate(*args, _p(ops), _p(busy), _p(busy_t), C.byref(r)))
+    check(fn(*args, _p(ops), _p(busy), _p(busy_t), C.byref(r)))
     return ops, busy, busy_t, r
 
 
@@ -331,6 +343,41 @@ def tune_grid_search(lengths, chunk_sizes, ks, stages, cost=None, mem=None, budg
                                          C.byref(bk), C.byref(ev), C.c_int(int(text == "csv")), buf, cap, n)
     txt = _text(call)
     return table, bc.value, bk.value, ev.value, txt
+
+
+def tune_grid_search_pp(lengths, chunk_sizes, ks, stages, cost=None, mem=None, kept_token_gib=0.0, tape_budget=0,
+                        budget_gib=80.0, global_batch_size=256, batches_to_sample=4, seed=0, ids=None,
+                        text="report"):
+    """Pipeline-aware grid_search (cf_tune_grid_search_pp): per-stage in-flight
+    tapes under `tape_budget` decide feasibility.  Returns as tune_grid_search."""
+    lengths = np.ascontiguousarray(lengths, np.int64)
+    ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
+    css = np.ascontiguousarray(chunk_sizes, np.int64)
+    kk = np.ascontiguousarray(ks, np.int64)
+    c = _pp_cost(cost)
+    m = mem if isinstance(mem, MemCoeffs) else MemCoeffs(*(mem or (0.0, 0.0, 0.0, 1.0)))
+    table = np.zeros(len(css) * len(kk), TUNE_ROW_DT)
+    bc, bk, ev = C.c_int64(), C.c_int64(), C.c_int64()
+
+    def call(buf, cap, n):
+        return lib().cf_tune_grid_search_pp(
+            _p(ids), _p(lengths), C.c_int64(len(lengths)), _p(css), C.c_int64(len(css)), _p(kk), C.c_int64(len(kk)),
+            C.c_int64(stages), C.byref(c), C.byref(m), C.c_double(kept_token_gib), C.c_int64(tape_budget),
+            C.c_double(budget_gib), C.c_int64(global_batch_size), C.c_int64(batches_to_sample), C.c_uint64(seed),
+            _p(table), C.byref(bc), C.byref(bk), C.byref(ev), C.c_int(int(text == "csv")), buf, cap, n)
+    txt = _text(call)
+    return table, bc.value, bk.value, ev.value, txt
+
+
+def pp_stage_memory(plan: "Plan", stages, k, tape_budget=0):
+    """cf_pp_stage_memory: per-stage dict of peak tapes / tape tokens / kept
+    input tokens / checkpointed forwards."""
+    out = {f: np.zeros(stages, np.int64) for f in ("peak_tapes", "peak_tape_tokens", "peak_kept_tokens",
+                                                  "checkpointed")}
+    check(lib().cf_pp_stage_memory(plan.h, C.c_int64(stages), C.c_int64(k), C.c_int64(tape_budget),
+                                   _p(out["peak_tapes"]), _p(out["peak_tape_tokens"]), _p(out["peak_kept_tokens"]),
+                                   _p(out["checkpointed"])))
+    return out
 
 
 def pp_stage_layers(layers, stage, stages):
@@ -443,6 +490,11 @@ class Context:
 
     def set_profiling(self, on: bool):
         check(lib().cf_ctx_set_profiling(self.h, C.c_int(int(on))))
+
+    def lm_head_ce(self, x, head, ldh, T, V, d, targets, inv_norm, lse, row_loss, dlogits=0):
+        """cf_op_lm_head_ce on device pointers (ints)."""
+        check(lib().cf_op_lm_head_ce(self.h, x, head, ldh, T, V, d, targets, inv_norm, lse, row_loss,
+                                     dlogits or None))
 
     def init_dp(self, rank, world, uid: bytes | None):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid else None
@@ -679,17 +731,18 @@ class Step:
         check(lib().cf_step_op_times(self.h, C.byref(n), _p(kinds), _p(ids), _p(ms)))
         return kinds, ids, ms
 
-    def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
-        """This rank's pipeline stage (cf_pp_step_run; needs Context.init_pp)."""
-        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+    def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0) -> RunResult:
+        """This rank's pipeline stage (cf_pp_step_run; needs Context.init_pp).
+        tape_budget > 0: stage-input checkpointing beyond that many tapes."""
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget))
         r = RunResult()
         check(lib().cf_pp_step_run(self.model.ctx.h, self.model.h, self.h, C.c_int64(k), C.byref(o), C.byref(r)))
         return r
 
-    def run_pp_local(self, models, k, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
+    def run_pp_local(self, models, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0) -> RunResult:
         """All pipeline stages on this device (cf_pp_run_local)."""
         arr = (C.c_void_p * len(models))(*[m.h.value for m in models])
-        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget))
         r = RunResult()
         check(lib().cf_pp_run_local(self.model.ctx.h, arr, C.c_int64(len(models)), self.h, C.c_int64(k),
                                     C.byref(o), C.byref(r)))

@@ -466,6 +466,35 @@ int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda, const void
   });
 }
 
+int cf_op_lm_head_ce(cf_ctx* ctx, const void* x, const void* head, int64_t ldh, int64_t T, int64_t V, int64_t d,
+                     const int32_t* targets, float inv_norm, float* lse, float* row_loss, void* dlogits) {
+  return cfb::guard([&] {
+    need(ctx, "ctx");
+    if (!x || !head || !targets || !lse || !row_loss) throw cfb::ValidationError("null operand");
+    cudaStream_t st = ctx->c.stream;
+    const int64_t np = cfk::ce_nparts(V);
+    float* buf = nullptr;
+    cfb::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&buf), static_cast<size_t>(T * np * 8 + T * 4 + 256), st),
+                    "cudaMallocAsync");
+    cfk::GemmDesc g{x, d, 1, head, ldh, 0, nullptr, 0, nullptr, 0, T, V, d, cfk::EPI_CE_STATS};
+    g.ce_tgt = targets;
+    g.ce_part = buf;
+    g.ce_tlogit = buf + T * np * 2;
+    cudaError_t e = cfk::gemm(g, st);
+    if (e == cudaSuccess) e = cfk::ce_finish(buf, np, buf + T * np * 2, targets, T, lse, row_loss, st);
+    if (e == cudaSuccess && dlogits) {
+      cfk::GemmDesc b{x, d, 1, head, ldh, 0, dlogits, ldh, nullptr, 0, T, V, d, cfk::EPI_CE_GRAD};
+      b.ce_tgt = targets;
+      b.ce_lse = lse;
+      b.ce_scale = inv_norm;
+      e = cfk::gemm(b, st);
+    }
+    cudaFreeAsync(buf, st);
+    cfb::cuda_check(e, "lm_head_ce");
+    ctx->c.launches += dlogits ? 3 : 2;
+  });
+}
+
 int cf_op_gemm_rope(cf_ctx* ctx, const void* a, int64_t lda, const void* w, int64_t ldw, void* c, int64_t m,
                     int64_t n, int64_t k, const void* tab, int64_t col_k, int64_t col_v, void* kc, void* vc,
                     int64_t cache_ld) {

@@ -282,6 +282,35 @@ int cf_pp_simulate(const cf_plan* plan, int64_t num_stages, int64_t k, const cf_
   });
 }
 
+int cf_pp_simulate_budget(const cf_plan* plan, int64_t num_stages, int64_t k, const cf_pp_cost* cost,
+                          int backward_first, const double* fwd_cost, const double* bwd_cost, int64_t tape_budget,
+                          cf_pp_op* ops, double* busy, double* busy_total, cf_pp_result* result) {
+  return cfb::guard([&] {
+    if (num_stages < 1) throw cfb::ValidationError("num_stages must be at least 1");
+    if (tape_budget < 0) throw cfb::ValidationError("tape budget must be non-negative");
+    cfb::PpChunks info = cfb::pp_chunks(plan->p, k, to_cost(cost));
+    for (size_t i = 0; i < info.fwd.size(); ++i) {
+      if (fwd_cost) info.fwd[i] = fwd_cost[i];
+      if (bwd_cost) info.bwd[i] = bwd_cost[i];
+      if (info.fwd[i] < 0 || info.bwd[i] < 0) throw cfb::ValidationError("measured costs must be non-negative");
+    }
+    std::vector<int64_t> tok;
+    for (const cfb::Chunk& c : plan->p.chunks) tok.push_back(c.total);
+    std::vector<std::vector<cfb::PpOp>> orders;
+    std::vector<std::vector<double>> extra;
+    for (int64_t s = 0; s < num_stages; ++s) {
+      orders.push_back(cfb::pp_stage_order(info, s, num_stages, backward_first != 0));
+      const cfb::PpStageMem m = cfb::pp_stage_memory(info, orders.back(), tok, tape_budget, s == 0);
+      std::vector<double> e(info.fwd.size(), 0.0);
+      for (size_t p = 0; p < e.size(); ++p)
+        if (m.ckpt[p]) e[p] = info.fwd[p];
+      extra.push_back(std::move(e));
+    }
+    emit(info, cfb::pp_dispatch(orders, info.fwd, info.bwd, to_cost(cost).hop, &extra), ops, busy, busy_total,
+         result);
+  });
+}
+
 int cf_pp_simulate_1f1b(const int64_t* lengths, int64_t n, int64_t num_stages, const cf_pp_cost* cost,
                         cf_pp_op* ops, double* busy, double* busy_total, cf_pp_result* result) {
   return cfb::guard([&] {
@@ -416,6 +445,50 @@ extern "C" int cf_pp_export_trace(const cf_pp_op* ops, int64_t num_stages, int64
         st[static_cast<size_t>(s)].push_back({o.kind, o.chunk_id, o.start, o.end});
       }
     put_text(cfb::export_trace(st, format == 0), buf, cap, len);
+  });
+}
+
+extern "C" int cf_pp_stage_memory(const cf_plan* plan, int64_t num_stages, int64_t k, int64_t tape_budget,
+                                  int64_t* peak_tapes, int64_t* peak_tape_tokens, int64_t* peak_kept_tokens,
+                                  int64_t* checkpointed) {
+  return cfb::guard([&] {
+    if (!plan) throw cfb::ValidationError("plan is null");
+    if (num_stages < 1 || k < 1 || tape_budget < 0) throw cfb::ValidationError("bad pipeline arguments");
+    const cfb::PpChunks info = cfb::pp_chunks(plan->p, k, cfb::PpCost{});
+    std::vector<int64_t> tok;
+    for (const cfb::Chunk& c : plan->p.chunks) tok.push_back(c.total);
+    for (int64_t s = 0; s < num_stages; ++s) {
+      const auto order = cfb::pp_stage_order(info, s, num_stages, true);
+      const cfb::PpStageMem m = cfb::pp_stage_memory(info, order, tok, tape_budget, s == 0);
+      if (peak_tapes) peak_tapes[s] = m.peak_tapes;
+      if (peak_tape_tokens) peak_tape_tokens[s] = m.peak_tape_tokens;
+      if (peak_kept_tokens) peak_kept_tokens[s] = m.peak_kept_tokens;
+      if (checkpointed) checkpointed[s] = m.checkpointed;
+    }
+  });
+}
+
+extern "C" int cf_tune_grid_search_pp(const int64_t* ids, const int64_t* lengths, int64_t n,
+                                      const int64_t* chunk_sizes, int64_t ncs, const int64_t* ks, int64_t nk,
+                                      int64_t num_stages, const cf_pp_cost* cost, const cf_mem_coeffs* mem,
+                                      double kept_token_gib, int64_t tape_budget, double budget_gib,
+                                      int64_t global_batch_size, int64_t batches_to_sample, uint64_t seed,
+                                      cf_tune_row* table, int64_t* best_chunk_size, int64_t* best_k,
+                                      int64_t* evaluations, int csv, char* buf, size_t cap, size_t* len) {
+  return cfb::guard([&] {
+    if (n < 0 || ncs < 0 || nk < 0 || !mem) throw cfb::ValidationError("bad tuner arguments");
+    const cfb::TuneResult r = cfb::grid_search_pp(
+        std::vector<int64_t>(ids, ids + n), std::vector<int64_t>(lengths, lengths + n),
+        std::vector<int64_t>(chunk_sizes, chunk_sizes + ncs), std::vector<int64_t>(ks, ks + nk), num_stages,
+        to_cost(cost), from_c(mem), kept_token_gib, tape_budget, budget_gib, global_batch_size, batches_to_sample,
+        seed);
+    for (size_t i = 0; table && i < r.table.size(); ++i)
+      table[i] = {r.table[i].chunk_size, r.table[i].k, r.table[i].mean_time, r.table[i].predicted_peak_gib,
+                  r.table[i].feasible ? 1 : 0};
+    if (best_chunk_size) *best_chunk_size = r.has_best ? r.best_chunk_size : -1;
+    if (best_k) *best_k = r.has_best ? r.best_k : -1;
+    if (evaluations) *evaluations = r.evaluations;
+    if (buf || len) put_text(csv ? cfb::tuner_table_csv(r) : cfb::tuner_report(r), buf, cap, len);
   });
 }
 

@@ -97,7 +97,7 @@ std::vector<PpOp> pp_stage_order(const PpChunks& c, int64_t stage, int64_t stage
 }
 
 PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vector<double>& fwd,
-                    const std::vector<double>& bwd, double hop) {
+                    const std::vector<double>& bwd, double hop, const std::vector<std::vector<double>>* bwd_extra) {
   const int64_t P = static_cast<int64_t>(orders.size());
   const size_t m = fwd.size();
   PpTrace t;
@@ -132,7 +132,8 @@ PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vec
           if (e == kUnset) break;
           ready = e + hop;
         }
-        const double dur = op.kind == kPpBackward ? bwd[p] : fwd[p];
+        double dur = op.kind == kPpBackward ? bwd[p] : fwd[p];
+        if (bwd_extra && op.kind == kPpBackward) dur += (*bwd_extra)[static_cast<size_t>(s)][p];
         const double start = std::max(free_at[static_cast<size_t>(s)], ready);
         const double end = start + dur;
         t.stages[static_cast<size_t>(s)].push_back({op.kind, op.pos, start, end});
@@ -149,6 +150,62 @@ PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vec
     if (!moved) throw std::logic_error("pipeline dispatch reached a dependency deadlock");
   }
   return t;
+}
+
+PpStageMem pp_stage_memory(const PpChunks& c, const std::vector<PpOp>& order, const std::vector<int64_t>& tokens,
+                           int64_t tape_budget, bool first_stage) {
+  PpStageMem r;
+  const size_t m = c.fwd.size();
+  r.ckpt.assign(m, 0);
+  std::vector<uint8_t> live(m, 0), kept(m, 0), seen(m, 0);
+  int64_t tapes = 0, tape_tok = 0, kept_tok = 0;
+  auto take_tape = [&](size_t p) {
+    live[p] = 1;
+    ++tapes;
+    tape_tok += tokens[p];
+    r.peak_tapes = std::max(r.peak_tapes, tapes);
+    r.peak_tape_tokens = std::max(r.peak_tape_tokens, tape_tok);
+  };
+  auto keep = [&](size_t p) {
+    if (first_stage) return;  // the first stage re-embeds its tokens
+    kept[p] = 1;
+    kept_tok += tokens[p];
+    r.peak_kept_tokens = std::max(r.peak_kept_tokens, kept_tok);
+  };
+  auto unkeep = [&](size_t p) {
+    if (!kept[p]) return;
+    kept[p] = 0;
+    kept_tok -= tokens[p];
+  };
+  for (const PpOp& op : order) {
+    const size_t p = static_cast<size_t>(op.pos);
+    if (op.kind == kPpForward) {
+      seen[p] = 1;
+      if (c.discarded[p]) {
+        keep(p);
+      } else if (tape_budget > 0 && tapes + 1 >= tape_budget) {
+        r.ckpt[p] = 1;
+        ++r.checkpointed;
+        keep(p);
+      } else {
+        take_tape(p);
+      }
+    } else if (op.kind == kPpRecompute) {
+      unkeep(p);
+      take_tape(p);
+    } else {
+      if (r.ckpt[p] && !live[p]) {  // just-in-time restore
+        unkeep(p);
+        take_tape(p);
+      }
+      if (live[p]) {
+        live[p] = 0;
+        --tapes;
+        tape_tok -= tokens[p];
+      }
+    }
+  }
+  return r;
 }
 
 double pp_bubble(const PpTrace& t) {
@@ -243,6 +300,84 @@ std::string fixed(double v, int prec) {
   return buf;
 }
 }  // namespace
+
+TuneResult grid_search_pp(const std::vector<int64_t>& ids, const std::vector<int64_t>& lengths,
+                          const std::vector<int64_t>& chunk_sizes, const std::vector<int64_t>& ks, int64_t stages,
+                          const PpCost& cost, const MemCoeffs& mem, double kept_token_gib, int64_t tape_budget,
+                          double budget_gib, int64_t global_batch_size, int64_t batches_to_sample, uint64_t seed) {
+  if (chunk_sizes.empty() || ks.empty()) throw ValidationError("tuner grid must not be empty");
+  if (budget_gib <= 0) throw ValidationError("memory budget must be positive");
+  if (batches_to_sample < 1) throw ValidationError("batches_to_sample must be at least 1");
+  if (lengths.empty()) throw ValidationError("cannot tune on an empty sequence set");
+  if (global_batch_size < 1) throw ValidationError("global batch size must be at least 1");
+  if (tape_budget < 0 || kept_token_gib < 0) throw ValidationError("tape budget and kept-token size must be non-negative");
+  cost.validate();
+  if (mem.base < 0 || mem.per_chunk_token < 0 || mem.per_context_token < 0 || mem.gqa_ratio < 0)
+    throw ValidationError("memory-model coefficients must be non-negative");
+  if (stages < 1) throw ValidationError("num_stages must be at least 1");
+  const int64_t n = static_cast<int64_t>(lengths.size());
+  const int64_t steps = (n + global_batch_size - 1) / global_batch_size;
+  std::vector<std::pair<std::vector<int64_t>, std::vector<int64_t>>> batches;
+  int64_t max_len = 0;
+  for (int64_t t = 0; t < batches_to_sample; ++t) {
+    const std::vector<int64_t> idx = sample_batch(n, global_batch_size, t % steps, seed);
+    if (idx.empty()) break;
+    std::vector<int64_t> bi, bl;
+    for (int64_t i : idx) {
+      bi.push_back(ids[static_cast<size_t>(i)]);
+      bl.push_back(lengths[static_cast<size_t>(i)]);
+      max_len = std::max(max_len, lengths[static_cast<size_t>(i)]);
+    }
+    batches.emplace_back(std::move(bi), std::move(bl));
+  }
+  TuneResult r;
+  for (int64_t cs : chunk_sizes)
+    for (int64_t k : ks) {
+      TuneRow row;
+      row.chunk_size = cs;
+      row.k = k;
+      double total = 0.0, peak = 0.0;
+      for (const auto& [bi, bl] : batches) {
+        const Plan plan = construct_chunks(bi.data(), bl.data(), static_cast<int64_t>(bi.size()), cs);
+        const PpChunks info = pp_chunks(plan, k, cost);
+        std::vector<int64_t> tok;
+        for (const Chunk& ch : plan.chunks) tok.push_back(ch.total);
+        std::vector<std::vector<PpOp>> orders;
+        std::vector<std::vector<double>> extra;
+        for (int64_t s = 0; s < stages; ++s) {
+          orders.push_back(pp_stage_order(info, s, stages, true));
+          const PpStageMem sm = pp_stage_memory(info, orders.back(), tok, tape_budget, s == 0);
+          peak = std::max(peak, mem.base + mem.per_chunk_token * static_cast<double>(sm.peak_tape_tokens) +
+                                    kept_token_gib * static_cast<double>(sm.peak_kept_tokens) +
+                                    mem.per_context_token * mem.gqa_ratio * static_cast<double>(max_len));
+          std::vector<double> e(info.fwd.size(), 0.0);
+          for (size_t p = 0; p < e.size(); ++p)
+            if (sm.ckpt[p]) e[p] = info.fwd[p];
+          extra.push_back(std::move(e));
+        }
+        total += pp_dispatch(orders, info.fwd, info.bwd, cost.hop, &extra).makespan;
+        ++r.evaluations;
+      }
+      row.predicted_peak_gib = peak;
+      row.feasible = peak <= budget_gib;
+      row.mean_time = total / static_cast<double>(batches.size());
+      r.table.push_back(row);
+    }
+  const TuneRow* best = nullptr;
+  for (const TuneRow& c : r.table) {
+    if (!c.feasible) continue;
+    if (!best || c.mean_time < best->mean_time ||
+        (c.mean_time == best->mean_time &&
+         (c.chunk_size > best->chunk_size || (c.chunk_size == best->chunk_size && c.k < best->k))))
+      best = &c;
+  }
+  if (best) {
+    r.has_best = true;
+    r.best_chunk_size = best->chunk_size;
+    r.best_k = best->k;
+  }
+  return r;
+}
 
 std::string tuner_table_csv(const TuneResult& r) {
   std::string out = "chunk_size,k,mean_time,predicted_peak_gib,feasible\n";

@@ -66,8 +66,25 @@ struct PpTrace {
 
 // Earliest-feasible list scheduling over fixed stage orders (run_dispatch,
 // pipeline.hpp:98-162).  Throws std::logic_error on a dependency deadlock.
+// bwd_extra (optional, [stage][position]): time added to that stage's
+// backward of that chunk — the just-in-time recompute of a chunk the stage
+// checkpointed under a tape budget (zero / absent: the reference timing).
 PpTrace pp_dispatch(const std::vector<std::vector<PpOp>>& orders, const std::vector<double>& fwd,
-                    const std::vector<double>& bwd, double hop);
+                    const std::vector<double>& bwd, double hop,
+                    const std::vector<std::vector<double>>* bwd_extra = nullptr);
+
+// Activation memory of one stage's op stream, replayed with the executor's
+// rules (runtime/engine.cu StageRunner): a first-pass retain-forward keeps a
+// tape unless that would leave no free slot under `tape_budget` (> 0), in
+// which case it keeps only its stage input (nothing on the first stage) and
+// is recomputed just before its backward; a K-plan discarded forward keeps
+// its stage input until its F'.  Peaks are over the whole stream.
+struct PpStageMem {
+  int64_t peak_tapes = 0, peak_tape_tokens = 0, peak_kept_tokens = 0, checkpointed = 0;
+  std::vector<uint8_t> ckpt;  // per position: checkpointed on this stage
+};
+PpStageMem pp_stage_memory(const PpChunks& c, const std::vector<PpOp>& order, const std::vector<int64_t>& tokens,
+                           int64_t tape_budget, bool first_stage);
 // bubble_ratio (pipeline.hpp:325-331): recompute counts as bubble.
 double pp_bubble(const PpTrace& t);
 
@@ -100,6 +117,18 @@ TuneResult grid_search(const std::vector<int64_t>& ids, const std::vector<int64_
                        const std::vector<int64_t>& chunk_sizes, const std::vector<int64_t>& ks, int64_t stages,
                        const PpCost& cost, const MemCoeffs& mem, double budget_gib, int64_t global_batch_size,
                        int64_t batches_to_sample, uint64_t seed);
+// grid_search for a pipeline (new; the reference's memory feasibility counts
+// k * chunk_size retained tokens, which a 1F1B stage exceeds: its warm-up
+// keeps min(P - s, M) chunks in flight).  Per sampled batch and stage the
+// op stream is replayed (pp_stage_memory) under `tape_budget`; a candidate is
+// feasible when every stage's base + per_chunk_token * peak tape tokens +
+// kept_token_gib * peak kept-input tokens + per_context_token * gqa *
+// max_len fits the budget; the reported peak is the worst stage's.  Timing
+// adds each stage's checkpoint recomputes to its backwards.
+TuneResult grid_search_pp(const std::vector<int64_t>& ids, const std::vector<int64_t>& lengths,
+                          const std::vector<int64_t>& chunk_sizes, const std::vector<int64_t>& ks, int64_t stages,
+                          const PpCost& cost, const MemCoeffs& mem, double kept_token_gib, int64_t tape_budget,
+                          double budget_gib, int64_t global_batch_size, int64_t batches_to_sample, uint64_t seed);
 std::string tuner_table_csv(const TuneResult& r);  // tuner.hpp:114-124
 std::string tuner_report(const TuneResult& r);     // tuner.hpp:126-150
 

@@ -53,6 +53,13 @@ struct Args {
   __nv_bfloat16* kc;
   __nv_bfloat16* vc;
   int64_t cache_ld;
+  // EPI_CE_STATS / EPI_CE_GRAD
+  const int32_t* ce_tgt;
+  float2* ce_part;
+  float* ce_tlogit;
+  const float* ce_lse;
+  float ce_scale;
+  int ce_nparts;
 };
 
 // Grouped raster.  Persistent CTAs take consecutive tile indices, so one wave
@@ -133,6 +140,55 @@ __device__ __forceinline__ void store_row32(const Args& g, int row, int col0, co
     }
   }
 }
+
+// EPI_CE_STATS: fold 32 logits of one row into the running (max, sum exp) of
+// the tile's 256-column slab; the target column's logit is written once.
+__device__ __forceinline__ void ce_stats_row32(const Args& g, int row, int col0, const uint32_t (&r)[32], int tgt,
+                                               float& m, float& s) {
+  float cm = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (col0 + j < g.N) cm = fmaxf(cm, __uint_as_float(r[j]));
+  if (tgt >= col0 && tgt < col0 + 32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j == tgt) g.ce_tlogit[row] = __uint_as_float(r[j]);
+  }
+  if (cm == -INFINITY) return;
+  const float nm = fmaxf(m, cm);
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (col0 + j < g.N) acc += __expf(__uint_as_float(r[j]) - nm);
+  s = s * __expf(m - nm) + acc;
+  m = nm;
+}
+
+// EPI_CE_GRAD: dlogits of 32 columns of one row from the saved LSE.
+__device__ __forceinline__ void ce_grad_row32(const Args& g, int row, int col0, const uint32_t (&r)[32], int tgt,
+                                              float lse) {
+  __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(g.C) + static_cast<int64_t>(row) * g.ldc + col0;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float p = __expf(__uint_as_float(r[j]) - lse) - (col0 + j == tgt ? 1.f : 0.f);
+    v[j] = tgt >= 0 ? p * g.ce_scale : 0.f;
+  }
+  if (col0 + 32 <= g.N) {
+    uint4* dst = reinterpret_cast<uint4*>(c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      dst[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                          pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < g.N) c[j] = __float2bfloat16_rn(v[j]);
+  }
+}
+
+template <int EPI>
+constexpr bool kEpiCe = EPI == EPI_CE_STATS || EPI == EPI_CE_GRAD;
 
 // Epilogues that read a fp32 row segment (residual R or the accumulated C)
 // prefetch the next 32-column chunk while the current one is stored: the
@@ -293,26 +349,52 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * BM + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BN);
-      float4 pre[8];
-      if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * BN, pre);
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tbase + c * 32, r);
-        tmem_ld_wait();
-        if (c == BN / 32 - 1) {
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+      if constexpr (kEpiCe<EPI>) {
+        static_assert(!kEpiCe<EPI> || BN == 256, "CE epilogues use 256-column slabs");
+        const int tgt = row < g.M ? g.ce_tgt[row] : -1;
+        const float lse = (EPI == EPI_CE_GRAD && row < g.M) ? g.ce_lse[row] : 0.f;
+        float m = -INFINITY, sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          const int col0 = nb * BN + c * 32;
+          if (row < g.M && col0 < g.N) {
+            if constexpr (EPI == EPI_CE_STATS)
+              ce_stats_row32(g, row, col0, r, tgt, m, sum);
+            else
+              ce_grad_row32(g, row, col0, r, tgt, lse);
+          }
         }
-        const int col0 = nb * BN + c * 32;
-        if constexpr (kEpiReads<EPI>) {
-          float4 nxt[8];
-          if (c + 1 < BN / 32) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
-          if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+        if constexpr (EPI == EPI_CE_STATS)
+          if (row < g.M) g.ce_part[static_cast<int64_t>(row) * g.ce_nparts + nb] = make_float2(m, sum);
+      } else {
+        float4 pre[8];
+        if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * BN, pre);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
-        } else {
-          if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          if (c == BN / 32 - 1) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          const int col0 = nb * BN + c * 32;
+          if constexpr (kEpiReads<EPI>) {
+            float4 nxt[8];
+            if (c + 1 < BN / 32) prefetch_row32<EPI>(g, row, col0 + 32, nxt);
+            if (col0 < g.N) store_row32_pre<EPI>(g, row, col0, r, pre);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pre[q] = nxt[q];
+          } else {
+            if (col0 < g.N) store_row32<EPI>(g, row, col0, r);
+          }
         }
       }
       if (++acc == 2) {
@@ -616,6 +698,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           }
           if (row < g.M) rope_store_pair32(g, row, nb * 256 + ca * 32, ra, rb);
         }
+      } else if constexpr (kEpiCe<EPI>) {
+        const int tgt = row < g.M ? g.ce_tgt[row] : -1;
+        const float lse = (EPI == EPI_CE_GRAD && row < g.M) ? g.ce_lse[row] : 0.f;
+        float m = -INFINITY, sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          if (c == 7) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(tempty_leader0 + acc * 8);
+          }
+          const int col0 = nb * 256 + c * 32;
+          if (row < g.M && col0 < g.N) {
+            if constexpr (EPI == EPI_CE_STATS)
+              ce_stats_row32(g, row, col0, r, tgt, m, sum);
+            else
+              ce_grad_row32(g, row, col0, r, tgt, lse);
+          }
+        }
+        if constexpr (EPI == EPI_CE_STATS)
+          if (row < g.M) g.ce_part[static_cast<int64_t>(row) * g.ce_nparts + nb] = make_float2(m, sum);
       } else {
         float4 pre[8];
         if constexpr (kEpiReads<EPI>) prefetch_row32<EPI>(g, row, nb * 256, pre);
@@ -690,6 +796,15 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_num_sms = 0;
 
+void set_ce(Args& g, const GemmDesc& d) {
+  g.ce_tgt = d.ce_tgt;
+  g.ce_part = reinterpret_cast<float2*>(d.ce_part);
+  g.ce_tlogit = d.ce_tlogit;
+  g.ce_lse = d.ce_lse;
+  g.ce_scale = d.ce_scale;
+  g.ce_nparts = static_cast<int>(ce_nparts(d.N));
+}
+
 // M-blocks per raster group (CF_GEMM_GROUP overrides; 0 = M-fastest over the
 // whole output, the pre-grouping order).
 int raster_group(int num_m, int dflt) {
@@ -720,6 +835,7 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   g.ldc = d.ldc;
   g.R = d.r;
   g.ldr = d.ldr;
+  set_ce(g, d);
   auto kern = gemm_tc_kernel<BN, A_MN, B_MN, EPI>;
   // per (kernel, device), thread-safe
   const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(C::kSmem));
@@ -762,6 +878,7 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.ldc = d.ldc;
   g.R = d.r;
   g.ldr = d.ldr;
+  set_ce(g, d);
   auto kern = pair::gemm_pair_kernel<A_MN, B_MN, EPI>;
   // per (kernel, device), thread-safe
   const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(pair::kSmem));
@@ -783,6 +900,8 @@ cudaError_t pair_by_epi(const GemmDesc& d, cudaStream_t st) {
     case EPI_BF16_TANHGRAD: return launch_pair<A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
     case EPI_BF16_SWIGLU: return launch_pair<A_MN, B_MN, EPI_BF16_SWIGLU>(d, st);
     case EPI_BF16_ROPE: return launch_pair<A_MN, B_MN, EPI_BF16_ROPE>(d, st);
+    case EPI_CE_STATS: return launch_pair<A_MN, B_MN, EPI_CE_STATS>(d, st);
+    case EPI_CE_GRAD: return launch_pair<A_MN, B_MN, EPI_CE_GRAD>(d, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -803,6 +922,12 @@ cudaError_t by_epi(const GemmDesc& d, cudaStream_t st) {
     case EPI_F32_RES: return launch_t<BN, A_MN, B_MN, EPI_F32_RES>(d, st);
     case EPI_BF16_TANH: return launch_t<BN, A_MN, B_MN, EPI_BF16_TANH>(d, st);
     case EPI_BF16_TANHGRAD: return launch_t<BN, A_MN, B_MN, EPI_BF16_TANHGRAD>(d, st);
+    case EPI_CE_STATS:
+      if constexpr (BN == 256) return launch_t<BN, A_MN, B_MN, EPI_CE_STATS>(d, st);
+      break;
+    case EPI_CE_GRAD:
+      if constexpr (BN == 256) return launch_t<BN, A_MN, B_MN, EPI_CE_GRAD>(d, st);
+      break;
   }
   return cudaErrorInvalidValue;
 }
@@ -828,12 +953,20 @@ int gemm_num_sms() {
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
   if (d.M <= 0 || d.N <= 0 || d.K <= 0) return cudaSuccess;
-  // TMA: 16-byte aligned bases and row pitches.
+  // TMA: 16-byte aligned bases and row pitches (EPI_CE_STATS stores no C).
+  const bool stores_c = d.epi != EPI_CE_STATS;
   if ((reinterpret_cast<uintptr_t>(d.a) & 15) || (reinterpret_cast<uintptr_t>(d.b) & 15) || (d.lda % 8) ||
-      (d.ldb % 8) || (reinterpret_cast<uintptr_t>(d.c) & 15) || (d.ldc % 8))
+      (d.ldb % 8) || (stores_c && ((reinterpret_cast<uintptr_t>(d.c) & 15) || (d.ldc % 8))))
     return cudaErrorMisalignedAddress;
   const int64_t sms = gemm_num_sms();
   const int mode = gemm_mode();
+  if (d.epi == EPI_CE_STATS || d.epi == EPI_CE_GRAD) {
+    if (!d.ce_tgt || (d.epi == EPI_CE_STATS ? (!d.ce_part || !d.ce_tlogit) : !d.ce_lse)) return cudaErrorInvalidValue;
+    // 256-column slabs in both kernels: the partial index is the slab
+    const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
+    if (mode != 1 && d.M > 128 && d.N > 128 && (pair_tiles >= sms / 4 || mode == 2)) return pair_by_major(d, st);
+    return by_major<256>(d, st);
+  }
   if (d.epi == EPI_BF16_ROPE) {
     if (!gemm_rope_ok(d.M, d.N, d.K, 128, d.col_k, d.col_v) || (reinterpret_cast<uintptr_t>(d.r) & 15) ||
         d.ldr != 64 || ((d.kc || d.vc) && (d.cache_ld % 8)))
@@ -852,6 +985,48 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
   const int64_t tiles256 = ((d.M + BM - 1) / BM) * ((d.N + 255) / 256);
   const bool wide = d.N > 128 && tiles256 >= sms;
   return wide ? by_major<256>(d, st) : by_major<128>(d, st);
+}
+
+namespace {
+// One warp per row: combine the row's (max, sum exp) slab partials in a
+// fixed order (lane-strided, then a butterfly), LSE and the row loss.
+__global__ void ce_finish_kernel(const float2* __restrict__ part, int64_t nparts, const float* __restrict__ tlogit,
+                                 const int32_t* __restrict__ tgt, int64_t M, float* __restrict__ lse,
+                                 float* __restrict__ row_loss) {
+  const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float2* p = part + row * nparts;
+  float m = -INFINITY, s = 0.f;
+  for (int64_t i = lane; i < nparts; i += 32) {
+    const float2 q = p[i];
+    if (q.x == -INFINITY) continue;
+    const float nm = fmaxf(m, q.x);
+    s = s * __expf(m - nm) + q.y * __expf(q.x - nm);
+    m = nm;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float nm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - nm));
+    m = nm;
+  }
+  if (lane == 0) {
+    const float l = m + logf(s);
+    if (lse) lse[row] = l;
+    const int32_t t = tgt[row];
+    row_loss[row] = t >= 0 ? l - tlogit[row] : 0.f;
+  }
+}
+}  // namespace
+
+cudaError_t ce_finish(const float* part, int64_t nparts, const float* tlogit, const int32_t* tgt, int64_t M,
+                      float* lse, float* row_loss, cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  ce_finish_kernel<<<static_cast<unsigned>((M * 32 + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const float2*>(part), nparts, tlogit, tgt, M, lse, row_loss);
+  return cudaGetLastError();
 }
 
 bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K) {

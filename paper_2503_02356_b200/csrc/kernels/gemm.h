@@ -24,7 +24,18 @@ enum GemmEpi : int {
   // from the bf16-rounded values as rope_qk does), and the k / v columns
   // also written to kc / vc (the KV cache rows of these tokens) when set.
   // CTA-pair kernel only (gemm_rope_ok).
-  EPI_BF16_ROPE = 7
+  EPI_BF16_ROPE = 7,
+  // Fused LM-head cross-entropy, forward (toy_model.hpp:320-331): nothing is
+  // stored to C.  Per row and 256-column slab the epilogue writes the online
+  // softmax partial (max, sum exp) to ce_part[row * ce_nparts + slab] and the
+  // target column's logit to ce_tlogit[row]; ce_finish() combines them into
+  // the row's log-sum-exp and loss.  No [T, V] logits ever reach HBM.
+  EPI_CE_STATS = 8,
+  // Fused LM-head cross-entropy, backward (toy_model.hpp:369-388): C(bf16) =
+  // (exp(acc - ce_lse[row]) - [col == ce_tgt[row]]) * ce_scale, 0 for rows
+  // without a target: dlogits recomputed from the saved LSE instead of being
+  // kept from the forward.
+  EPI_CE_GRAD = 9
 };
 
 struct GemmDesc {
@@ -45,7 +56,21 @@ struct GemmDesc {
   void* kc = nullptr;
   void* vc = nullptr;
   int64_t cache_ld = 0;
+  // EPI_CE_STATS / EPI_CE_GRAD
+  const int32_t* ce_tgt = nullptr;  // [M] target column or -1
+  float* ce_part = nullptr;         // [M][ce_nparts] float2 (max, sum)   STATS
+  float* ce_tlogit = nullptr;       // [M] target logit                    STATS
+  const float* ce_lse = nullptr;    // [M] log-sum-exp                      GRAD
+  float ce_scale = 0.f;             // 1 / normalizer                       GRAD
 };
+
+// Partial-slab count of EPI_CE_STATS for N columns (one per 256 columns).
+inline int64_t ce_nparts(int64_t N) { return (N + 255) / 256; }
+// lse[row] = logsumexp over the row's partials; row_loss[row] = lse -
+// tlogit[row] for rows with a target (0 otherwise).  One warp per row, fixed
+// combine order (deterministic).
+cudaError_t ce_finish(const float* part, int64_t nparts, const float* tlogit, const int32_t* tgt, int64_t M,
+                      float* lse, float* row_loss, cudaStream_t st);
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
 // Whether EPI_BF16_SWIGLU is available for this problem (else run EPI_BF16

@@ -444,7 +444,7 @@ struct Tape {
   float* lse = nullptr;   // L x H x T
   float* x_mid = nullptr; // L x T x d
   bf16* act = nullptr;    // L x T x gu_w
-  bf16* dlogits = nullptr;// T x Vp
+  float* lse_head = nullptr; // T   LM-head log-sum-exp (the backward rebuilds dlogits from it)
   float2* tab = nullptr;  // T x dh/2
   // llama, retained tapes only: the GEMM inputs the backward would
   // otherwise recompute — normed activations and the SwiGLU output
@@ -453,6 +453,17 @@ struct Tape {
   bf16* h = nullptr;      // L x T x ffn swiglu(gate, up)
   bf16* xnf = nullptr;    // T x d       final norm
   int64_t bytes = 0;
+  // A discard forward keeps nothing past its own layer, so its transient tape
+  // is one layer's working set (x_in a ring of 2, the rest 1 slot) instead of
+  // L layers' — what makes in-flight chunks cheap on a pipeline stage.
+  bool ring = false;
+  int64_t sx = 0, sq = 0, sl = 0, sa = 0;  // per-layer strides of x / qkv / lse / act
+  float* xin(int64_t l) const { return x_in + (ring ? (l & 1) : l) * sx; }
+  float* xmid(int64_t l) const { return x_mid + (ring ? 0 : l) * sx; }
+  bf16* qkvl(int64_t l) const { return qkv + (ring ? 0 : l) * sq; }
+  bf16* ol(int64_t l) const { return o + (ring ? 0 : l) * (sx); }
+  float* lsel(int64_t l) const { return lse + (ring ? 0 : l) * sl; }
+  bf16* actl(int64_t l) const { return act + (ring ? 0 : l) * sa; }
 };
 
 }  // namespace
@@ -706,6 +717,8 @@ cf_step* step_prepare(Ctx* ctx, Model* m, const Plan& plan, const Batch& b) {
       throw ValidationError("chunk plan has no group " + std::to_string(cm.group));
   st->hw_layer = st->mf_layer;
   st->hw_head = st->mf_head;
+  // every backward recomputes the head GEMM to rebuild dlogits from the LSE
+  for (const ChunkMeta& cm : st->chunks) st->hw_head += 2.0 * Nhead * static_cast<double>(cm.T);
   for (const Event& e : plan.events)
     if (e.recompute) {
       const ChunkMeta& cm = st->chunks[static_cast<size_t>(st->pos_of.at(e.chunk))];
@@ -797,19 +810,75 @@ struct Exec {
     close(t0, 0, 2.0 * static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K), 1);
   }
 
+  void gemm_desc(const cfk::GemmDesc& d) {
+    cudaEvent_t t0 = mark();
+    L(cfk::gemm(d, s), "gemm");
+    close(t0, 0, 2.0 * static_cast<double>(d.M) * static_cast<double>(d.N) * static_cast<double>(d.K), 1);
+  }
+
+  // LM head + cross-entropy forward (toy_model.hpp:320-331) fused into the
+  // head GEMM: the epilogue reduces each row's 256-column slabs to (max, sum
+  // exp) partials and picks the target logit, ce_finish() combines them into
+  // the LSE (kept in the tape for the backward) and the row losses — the
+  // [T, V] logits never reach HBM.
+  void head_forward(const bf16* xnf, int64_t T, const int32_t* tgt, float* lse_out, double* loss_slot) {
+    const int64_t Vp = align_up(m->V, 8), np = cfk::ce_nparts(m->V);
+    float* buf = static_cast<float*>(pool_alloc(ctx, T * np * 8 + 2 * T * 4 + 256));
+    float* part = buf;
+    float* tlogit = buf + T * np * 2;
+    float* row_loss = tlogit + T;
+    cfk::GemmDesc g{xnf, m->d, 1, m->head, Vp, 0, nullptr, 0, nullptr, 0, T, m->V, m->d, cfk::EPI_CE_STATS};
+    g.ce_tgt = tgt;
+    g.ce_part = part;
+    g.ce_tlogit = tlogit;
+    gemm_desc(g);
+    L(cfk::ce_finish(part, np, tlogit, tgt, T, lse_out, row_loss, s), "ce_finish");
+    L(cfk::sum_f64(row_loss, T, loss_slot, s), "loss_sum");
+    pool_free(ctx, buf);
+  }
+
+  // LM head backward (toy_model.hpp:369-388): dlogits are rebuilt from the
+  // saved LSE by a recompute of the head GEMM (EPI_CE_GRAD) instead of being
+  // kept from the forward, in row blocks of at most ~1 GiB of bf16 dlogits
+  // (one block at C2; C5's 152K vocabulary takes a few), each followed by
+  // its weight-gradient and input-gradient GEMMs.
+  void head_backward(const bf16* xnf, int64_t T, const int32_t* tgt, const float* lse, float* dxf) {
+    const int64_t Vp = align_up(m->V, 8), d = m->d;
+    const int64_t cap = std::max<int64_t>(256, ((int64_t{1} << 30) / (Vp * 2)) / 256 * 256);
+    const int64_t nblk = (T + cap - 1) / cap;
+    const int64_t rb = std::min<int64_t>(T, align_up((T + nblk - 1) / nblk, 128));
+    bf16* dl = static_cast<bf16*>(pool_alloc(ctx, rb * Vp * 2));
+    for (int64_t r0 = 0; r0 < T; r0 += rb) {
+      const int64_t n = std::min(rb, T - r0);
+      cfk::GemmDesc g{xnf + r0 * d, d, 1, m->head, Vp, 0, dl, Vp, nullptr, 0, n, m->V, d, cfk::EPI_CE_GRAD};
+      g.ce_tgt = tgt + r0;
+      g.ce_lse = lse + r0;
+      g.ce_scale = inv_norm;
+      gemm_desc(g);
+      gemm(xnf + r0 * d, 0, d, dl, 0, Vp, m->d_head, Vp, d, m->V, n, cfk::EPI_F32_ACC);
+      gemm(dl, 1, Vp, m->head, 1, Vp, dxf + r0 * d, d, n, d, m->V, cfk::EPI_F32);
+    }
+    pool_free(ctx, dl);
+  }
+
   Tape alloc_tape(int64_t T, bool retain) {
     Tape t;
     t.T = T;
-    const int64_t L_ = m->L, d = m->d;
-    const int64_t Vp = align_up(m->V, 8);
+    const int64_t d = m->d;
+    t.ring = !retain && m->L > 1;
+    const int64_t L_ = t.ring ? 1 : m->L;
+    t.sx = T * d;
+    t.sq = T * m->qkv_w;
+    t.sl = m->H * T;
+    t.sa = T * m->gu_w;
     auto carve = [&](Arena& a) {
-      t.x_in = a.take<float>((L_ + 1) * T * d);
+      t.x_in = a.take<float>((t.ring ? 2 : L_ + 1) * T * d);
       t.qkv = a.take<bf16>(L_ * T * m->qkv_w);
       t.o = a.take<bf16>(L_ * T * d);
       t.lse = a.take<float>(L_ * m->H * T);
       t.x_mid = a.take<float>(L_ * T * d);
       t.act = a.take<bf16>(L_ * T * m->gu_w);
-      if (retain && m->has_head) t.dlogits = a.take<bf16>(T * Vp);
+      if (retain && m->has_head) t.lse_head = a.take<float>(T);
       t.tab = a.take<float2>(T * std::max<int64_t>(1, m->dh / 2));
       if (retain && m->llama) {
         t.xn1 = a.take<bf16>(L_ * T * d);
@@ -838,7 +907,7 @@ struct Exec {
   AttnParams attn_params(const ChunkMeta& cm, const Tape& t, int64_t l, GroupState* gs) {
     AttnParams p{};
     const int64_t T = cm.T;
-    p.q = t.qkv + l * T * m->qkv_w;
+    p.q = t.qkvl(l);
     p.q_stride = m->qkv_w;
     if (cm.dependent) {
       p.k = gs->kc + l * gs->S * m->kvw;
@@ -852,9 +921,9 @@ struct Exec {
       p.kv_stride = m->qkv_w;
     }
     p.acc_stride = 2 * m->kvw;
-    p.o = t.o + l * T * m->d;
+    p.o = t.ol(l);
     p.o_stride = m->d;
-    p.lse = t.lse + l * m->H * T;
+    p.lse = t.lsel(l);
     p.segs = meta<const AttnSeg>(cm.o_segs);
     p.tiles = meta<const AttnTile>(cm.o_qt);
     p.num_tiles = static_cast<int32_t>(cm.nqt);
@@ -870,23 +939,21 @@ struct Exec {
   // A pipeline stage without the embedding finds its input already in
   // t.x_in[0]; one without the head leaves its output in t.x_in[L].
   void forward(const ChunkMeta& cm, Tape& t, GroupState* gs, int64_t slot, bool retain) {
-    const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8);
+    const int64_t T = cm.T, d = m->d;
     const int32_t* tok = meta<const int32_t>(cm.o_tok);
     const int32_t* tgt = meta<const int32_t>(cm.o_tgt);
     bf16* A = static_cast<bf16*>(pool_alloc(ctx, T * std::max(d, m->ffn) * 2));
     bf16* hscr = nullptr;  // SwiGLU output of a discard forward (fused epilogue)
-    float* logits = m->has_head ? static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4)) : nullptr;
-    float* row_loss = m->has_head ? logits + T * Vp : nullptr;
-    if (m->has_embed) L(cfk::embed_fwd(tok, m->emb, d, T, t.x_in, s), "embed");
+    if (m->has_embed) L(cfk::embed_fwd(tok, m->emb, d, T, t.xin(0), s), "embed");
     if (m->llama)
       L(cfk::rope_table(meta<const int32_t>(cm.o_pos), T, static_cast<int>(m->dh), m->cfg.rope_theta, t.tab, s),
         "rope_table");
     for (int64_t l = 0; l < m->L; ++l) {
       const Layer& ly = m->layers[static_cast<size_t>(l)];
-      float* x = t.x_in + l * T * d;
-      float* xm = t.x_mid + l * T * d;
-      bf16* qkv = t.qkv + l * T * m->qkv_w;
-      bf16* act = t.act + l * T * m->gu_w;
+      float* x = t.xin(l);
+      float* xm = t.xmid(l);
+      bf16* qkv = t.qkvl(l);
+      bf16* act = t.actl(l);
       bf16* xn1 = t.xn1 ? t.xn1 + l * T * d : A;
       if (m->llama)
         L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), xn1, s), "rmsnorm");
@@ -928,8 +995,8 @@ struct Exec {
       else
         L(cfk::attn_forward(p, s), "attn_fwd");
       close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1);
-      gemm(t.o + l * T * d, 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
-      float* xn = t.x_in + (l + 1) * T * d;
+      gemm(t.ol(l), 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
+      float* xn = t.xin(l + 1);
       if (m->llama) {
         bf16* xn2 = t.xn2 ? t.xn2 + l * T * d : A;
         L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, static_cast<float>(m->cfg.rms_eps), xn2, s), "rmsnorm");
@@ -954,16 +1021,13 @@ struct Exec {
       }
     }
     if (m->has_head) {
-      const float* xL = t.x_in + m->L * T * d;
+      const float* xL = t.xin(m->L);
       bf16* xnf = t.xnf ? t.xnf : A;
       if (m->llama)
         L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), xnf, s), "rmsnorm");
       else
         L(cfk::to_bf16(xL, xnf, T * d, s), "to_bf16");
-      gemm(xnf, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
-      L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, tgt, inv_norm, row_loss, retain ? t.dlogits : nullptr, s), "ce");
-      L(cfk::sum_f64(row_loss, T, loss_slots + slot, s), "loss_sum");
-      pool_free(ctx, logits);
+      head_forward(xnf, T, tgt, retain ? t.lse_head : nullptr, loss_slots + slot);
     }
     if (hscr) pool_free(ctx, hscr);
     pool_free(ctx, A);
@@ -973,7 +1037,7 @@ struct Exec {
   // pipeline stage without the head passes the gradient of its output in
   // dx_io; a stage without the embedding gets its input gradient back there.
   void backward(const ChunkMeta& cm, Tape& t, GroupState* gs, float* dx_io = nullptr) {
-    const int64_t T = cm.T, d = m->d, Vp = align_up(m->V, 8), qw = m->qkv_w, kvw = m->kvw;
+    const int64_t T = cm.T, d = m->d, qw = m->qkv_w, kvw = m->kvw;
     const float eps = static_cast<float>(m->cfg.rms_eps);
     float *dx, *dmid, *da, *dsum, *rstd, *dkv_local = nullptr;
     bf16 *A, *xb, *dh, *dgu, *dqkv;
@@ -1009,7 +1073,7 @@ struct Exec {
       }
     };
     if (m->has_head) {
-      const float* xL = t.x_in + m->L * T * d;
+      const float* xL = t.xin(m->L);
       const bf16* xnf = t.xnf;
       if (!xnf) {
         if (m->llama)
@@ -1018,21 +1082,21 @@ struct Exec {
           L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
         xnf = A;
       }
-      gemm(xnf, 0, d, t.dlogits, 0, Vp, m->d_head, Vp, d, m->V, T, cfk::EPI_F32_ACC);
+      const int32_t* tgt = meta<const int32_t>(cm.o_tgt);
       if (m->llama) {
-        gemm(t.dlogits, 1, Vp, m->head, 1, Vp, da, d, T, d, m->V, cfk::EPI_F32);
+        head_backward(xnf, T, tgt, t.lse_head, da);
         norm_bwd(xL, m->gf, nullptr, dx, m->d_gf);
       } else {
-        gemm(t.dlogits, 1, Vp, m->head, 1, Vp, dx, d, T, d, m->V, cfk::EPI_F32);
+        head_backward(xnf, T, tgt, t.lse_head, dx);
       }
     }
 
     for (int64_t l = m->L - 1; l >= 0; --l) {
       const Layer& ly = m->layers[static_cast<size_t>(l)];
-      const float* x = t.x_in + l * T * d;
-      const float* xm = t.x_mid + l * T * d;
-      const bf16* act = t.act + l * T * m->gu_w;
-      const bf16* O = t.o + l * T * d;
+      const float* x = t.xin(l);
+      const float* xm = t.xmid(l);
+      const bf16* act = t.actl(l);
+      const bf16* O = t.ol(l);
       // FFN (toy_model.hpp:409-425)
       // bf16(dx) is left in xb by the previous norm_bwd, except when dx came
       // from the next pipeline stage
@@ -1151,6 +1215,11 @@ struct StageRunner {
   std::vector<std::pair<int64_t, int64_t>> recompute_pairs;  // (slot, first slot)
   std::vector<int64_t> first_pass_slots;
   int64_t held = 0, peak = 0, violations = 0, recomputes = 0;
+  // stage-input checkpointing (cf_run_opts.stage_tape_budget): a first-pass
+  // retain-forward beyond `tape_budget` resident tapes keeps only its stage
+  // input and is recomputed right before its backward
+  int64_t tape_budget = 0, live_peak = 0, ckpt_recomputes = 0, next_extra_slot = 0;
+  std::set<int64_t> ckpt;
   int64_t io_bytes = 0;  // stage-boundary buffers held (kept inputs)
   struct OpMark {
     int64_t kind, id;
@@ -1166,7 +1235,12 @@ struct StageRunner {
   }
 
   StageRunner(Ctx* c, Model* mm, cf_step* s, const cf_run_opts& opts, int64_t slots)
-      : ctx(c), m(mm), st(s), nslots(slots) {
+      : ctx(c), m(mm), st(s), nslots(slots + static_cast<int64_t>(s->chunks.size())) {
+    // loss slots: one per op of the stream, then one per chunk for the
+    // checkpoint recomputes the tape budget may add
+    next_extra_slot = slots;
+    tape_budget = opts.stage_tape_budget;
+    if (tape_budget < 0) throw ValidationError("stage_tape_budget must be non-negative");
     const Plan& plan = *st->plan;
     if (!plan.violations.empty()) throw ValidationError("execution plan is invalid: " + plan.violations.front());
     ex.ctx = ctx;
@@ -1239,11 +1313,25 @@ struct StageRunner {
   // without the embedding; a recompute forward uses the input kept by the
   // chunk's first pass (keep_in).  Returns the stage output for the next
   // stage (caller-owned pool memory) or null on the last stage / for F'.
-  float* forward(int64_t id, bool retain, bool recompute, bool save_kv, int64_t slot, float* in, bool keep_in) {
+  float* forward(int64_t id, bool retain, bool recompute, bool save_kv, int64_t slot, float* in, bool keep_in,
+                 bool ckpt_recompute = false) {
     cudaEvent_t t0 = op_begin();
     const ChunkMeta& cm = chunk(id);
     GroupState* gs = group_for(cm);
     const size_t act = static_cast<size_t>(cm.T * m->d) * 4;
+    // over the tape budget: run this first-pass retain-forward as a discard
+    // forward that keeps its stage input (plan semantics unchanged: the chunk
+    // still counts as retained for the reference instrumentation).  One slot
+    // of the budget stays free for the just-in-time tape of the backward in
+    // progress (a checkpoint restore or a K-plan F'), so resident tapes never
+    // exceed the budget.
+    bool checkpoint = false;
+    if (retain && !recompute && tape_budget > 0 && static_cast<int64_t>(live.size()) + 1 >= tape_budget) {
+      checkpoint = true;
+      retain = false;
+      keep_in = true;
+      ckpt.insert(id);
+    }
     Tape t = ex.alloc_tape(cm.T, retain);
     if (!m->has_embed) {
       float* src = in;
@@ -1253,7 +1341,7 @@ struct StageRunner {
         src = k->second;
       }
       if (!src) throw ValidationError("stage input missing for chunk " + std::to_string(id));
-      CK(cudaMemcpyAsync(t.x_in, src, act, cudaMemcpyDeviceToDevice, ex.s));
+      CK(cudaMemcpyAsync(t.xin(0), src, act, cudaMemcpyDeviceToDevice, ex.s));
     }
     ex.forward(cm, t, gs, slot, retain);
     if (gs && save_kv) gs->saved[static_cast<size_t>(cm.index)] = true;
@@ -1261,22 +1349,32 @@ struct StageRunner {
       first_slot[id] = slot;
       first_pass_slots.push_back(slot);
     } else {
-      ++recomputes;
+      if (ckpt_recompute)
+        ++ckpt_recomputes;
+      else
+        ++recomputes;
       auto f = first_slot.find(id);
       recompute_pairs.emplace_back(slot, f == first_slot.end() ? -1 : f->second);
     }
     float* out = nullptr;
     if (!m->has_head && !recompute) {
       out = static_cast<float*>(pool_alloc(ctx, static_cast<int64_t>(act)));
-      CK(cudaMemcpyAsync(out, t.x_in + m->L * cm.T * m->d, act, cudaMemcpyDeviceToDevice, ex.s));
+      CK(cudaMemcpyAsync(out, t.xin(m->L), act, cudaMemcpyDeviceToDevice, ex.s));
     }
     if (retain) {
       if (live.count(id)) ex.free_tape(live[id]);
       live[id] = t;
-      held += cm.T;
-      peak = std::max(peak, held);
+      live_peak = std::max(live_peak, static_cast<int64_t>(live.size()));
+      if (!ckpt_recompute) {
+        held += cm.T;
+        peak = std::max(peak, held);
+      }
     } else {
       ex.free_tape(t);
+      if (checkpoint) {
+        held += cm.T;
+        peak = std::max(peak, held);
+      }
     }
     if (recompute) {
       auto k = kept_in.find(id);
@@ -1297,11 +1395,21 @@ struct StageRunner {
     return out;
   }
 
+  // A checkpointed chunk gets its tape back just before its backward: a
+  // retain-forward from the kept stage input (stage 0: from its tokens).
+  void restore_checkpoint(int64_t id) {
+    auto c = ckpt.find(id);
+    if (c == ckpt.end() || live.count(id)) return;
+    ckpt.erase(c);
+    forward(id, true, true, false, next_extra_slot++, nullptr, false, true);
+  }
+
   // Backward of chunk `id`.  `dy` is the gradient of the stage output (pool
   // memory, owned by the runner from here on) on stages without the head.
   // Returns the gradient of the stage input for the previous stage (caller-
   // owned) or null on the first stage.
   float* backward(int64_t id, float* dy) {
+    restore_checkpoint(id);
     cudaEvent_t t0 = op_begin();
     const ChunkMeta& cm = chunk(id);
     GroupState* gs = group_for(cm);
@@ -1429,6 +1537,8 @@ struct StageRunner {
     res->attn_bwd_flops = cls_flops[2];
     res->attn_bwd_launches = cls_n[2];
     res->other_launches = ex.launches - cls_n[0] - cls_n[1] - cls_n[2];
+    res->peak_live_tapes = live_peak;
+    res->checkpoint_recomputes = ckpt_recomputes;
   }
 };
 
@@ -1556,6 +1666,8 @@ void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t P, cf_step* st, i
     total.attn_bwd_flops += rs.attn_bwd_flops;
     total.attn_bwd_launches += rs.attn_bwd_launches;
     total.other_launches += rs.other_launches;
+    total.peak_live_tapes = std::max(total.peak_live_tapes, rs.peak_live_tapes);
+    total.checkpoint_recomputes += rs.checkpoint_recomputes;
   }
   uint64_t high = 0;
   if (ctx->pool) cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &high);
@@ -1913,7 +2025,7 @@ void segment_backward(Ctx* ctx, Model* m, SegmentState* sg, const double* prefix
   const ChunkMeta& cm = sg->st->chunks[0];
   GroupState& g = sg->gs;
   Tape& t = sg->tape;
-  const int64_t T = sg->len, d = m->d, kvw = m->kvw, Vp = align_up(m->V, 8);
+  const int64_t T = sg->len, kvw = m->kvw;
   cudaStream_t s = ctx->stream;
   upload_segment_prefix(ctx, m, *sg, prefix_k, prefix_v);
   // dK/dV store: gradients of the segment's own rows from later chunks
@@ -1935,27 +2047,8 @@ void segment_backward(Ctx* ctx, Model* m, SegmentState* sg, const double* prefix
   ex.st = sg->st;
   ex.s = s;
   ex.inv_norm = static_cast<float>(1.0 / normalizer);
-  // output head + cross-entropy gradient with the caller's normalizer
-  {
-    bf16* xnf = t.xnf;
-    bf16* A = nullptr;
-    if (!xnf) {
-      A = static_cast<bf16*>(pool_alloc(ctx, T * d * 2));
-      const float* xL = t.x_in + m->L * T * d;
-      if (m->llama)
-        ex.L(cfk::rmsnorm_fwd(xL, m->gf, T, d, static_cast<float>(m->cfg.rms_eps), A, s), "rmsnorm");
-      else
-        ex.L(cfk::to_bf16(xL, A, T * d, s), "to_bf16");
-      xnf = A;
-    }
-    float* logits = static_cast<float*>(pool_alloc(ctx, T * Vp * 4 + T * 4));
-    ex.gemm(xnf, 1, d, m->head, 0, Vp, logits, Vp, T, m->V, d, cfk::EPI_F32);
-    ex.L(cfk::ce_fwd_bwd(logits, T, m->V, Vp, ex.meta<const int32_t>(cm.o_tgt), ex.inv_norm, logits + T * Vp,
-                         t.dlogits, s),
-         "ce");
-    pool_free(ctx, logits);
-    if (A) pool_free(ctx, A);
-  }
+  // the head's dlogits are rebuilt from the forward's LSE with the caller's
+  // normalizer inside ex.backward (head_backward)
   ex.backward(cm, t, &g, nullptr);
   // gradients for the prefix rows
   if (sg->prefix > 0 && (d_prefix_k || d_prefix_v)) {

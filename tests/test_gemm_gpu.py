@@ -148,3 +148,41 @@ def test_gemm_rope_epilogue(ctx, shape, mode):
     assert err < 1e-2, err
     assert torch.equal(C1[:, col_v:], C0[:, col_v:])
     assert torch.equal(kc, C1[:, col_k:col_v]) and torch.equal(vc, C1[:, col_v:])
+
+
+@pytest.mark.parametrize("shape", [(8192, 32000, 4096), (300, 97, 64), (1000, 9000, 256), (130, 152064, 128),
+                                   (77, 520, 96)], ids=["c2", "odd-v", "v9000", "qwen-vocab", "small"])
+def test_fused_lm_head_ce(ctx, gemm_mode, shape):
+    """LM head + cross-entropy fused into the head GEMM (EPI_CE_STATS partials
+    + ce_finish, EPI_CE_GRAD dlogits from the LSE) vs torch fp32 on the same
+    bf16 operands: LSE / row loss to 1e-5 relative, dlogits to bf16 rounding
+    (toy_model.hpp:320-331, :369-388)."""
+    T, V, d = shape
+    ldh = (V + 7) // 8 * 8
+    x = _mk(T, d, 5) * 0.3
+    W = torch.zeros(d, ldh, device="cuda", dtype=torch.bfloat16)
+    W[:, :V] = _mk(d, V, 6) * 0.3
+    g = torch.Generator(device="cuda").manual_seed(7)
+    tgt = torch.randint(0, V, (T,), generator=g, device="cuda", dtype=torch.int32)
+    tgt[::5] = -1  # rows without a target
+    logits = x.float() @ W[:, :V].float()
+    lse_ref = torch.logsumexp(logits, dim=1)
+    has = tgt >= 0
+    loss_ref = torch.where(has, lse_ref - logits.gather(1, tgt.clamp(min=0).long()[:, None])[:, 0],
+                           torch.zeros_like(lse_ref))
+    inv = 1.0 / 12345.0
+    p = torch.softmax(logits, dim=1)
+    p[has, tgt[has].long()] -= 1.0
+    dl_ref = torch.where(has[:, None], p * inv, torch.zeros_like(p))
+    lse = torch.zeros(T, device="cuda")
+    loss = torch.zeros(T, device="cuda")
+    dl = torch.full((T, ldh), 7.0, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    ctx.lm_head_ce(x.data_ptr(), W.data_ptr(), ldh, T, V, d, tgt.data_ptr(), inv, lse.data_ptr(), loss.data_ptr(),
+                   dl.data_ptr())
+    ctx.synchronize()
+    assert ((lse - lse_ref).abs() / lse_ref.abs().clamp(min=1)).max().item() < 1e-5
+    assert ((loss - loss_ref).abs() / loss_ref.abs().clamp(min=1)).max().item() < 1e-5
+    err = (dl[:, :V].float() - dl_ref).abs().max().item() / dl_ref.abs().max().item()
+    assert err < 1e-2, err  # bf16 storage of the gradient
+    assert (dl[~has, :V] == 0).all()

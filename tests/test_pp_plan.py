@@ -211,3 +211,49 @@ def test_tuner_validation():
         args.update(kw)
         with pytest.raises(capi.CfError):
             capi.tune_grid_search(**args)
+
+
+def test_stage_memory_replay_budget_bounds():
+    """cf_pp_stage_memory replays each stage's 1F1B op stream with the
+    executor's tape rules: without a budget stage s of an all-standalone plan
+    holds min(P - s, M) tapes at its warm-up peak; with a budget B no stage
+    holds more than B, and the first-stage checkpoints keep no input."""
+    lengths = np.array([500, 480, 470, 450, 430, 400, 900, 1500, 40, 30], np.int64)
+    plan = cf.Plan.build(lengths, 512, 1)
+    free = capi.pp_stage_memory(plan, 4, 1, 0)
+    assert list(free["peak_tapes"]) == [4, 3, 2, 1] and free["checkpointed"].sum() == 0
+    assert free["peak_kept_tokens"][0] == 0
+    for b in (1, 2, 3):
+        m = capi.pp_stage_memory(plan, 4, 1, b)
+        assert (m["peak_tapes"] <= b).all() and m["peak_tapes"].max() == b
+        assert (m["peak_tape_tokens"] <= free["peak_tape_tokens"]).all()
+        assert m["checkpointed"][0] > 0 and m["peak_kept_tokens"][0] == 0
+    # randomized: the bound holds for every plan, stage count and budget
+    rng = np.random.default_rng(9)
+    for _ in range(100):
+        L = rng.integers(1, 400, size=int(rng.integers(1, 15))).astype(np.int64)
+        cs, k, P, b = int(rng.integers(16, 256)), int(rng.integers(1, 4)), int(rng.integers(1, 6)), int(rng.integers(0, 4))
+        m = capi.pp_stage_memory(cf.Plan.build(L, cs, k), P, k, b)
+        if b:
+            assert (m["peak_tapes"] <= b).all()
+        assert (m["peak_tape_tokens"] <= m["peak_tapes"] * cs).all()
+
+
+def test_tuner_pp_counts_in_flight_chunks():
+    """grid_search_pp: one stage with no budget predicts at least the
+    reference tuner's peak; four stages without a budget predict more (the
+    1F1B warm-up holds 4 chunks on stage 0) and a tape budget brings the
+    prediction back under the memory budget at the price of recompute time."""
+    lengths = capi.synthesize(300, 5, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
+    lengths = np.concatenate([lengths, [9000, 12000]]).astype(np.int64)
+    mem = (40.0, 0.004, 1e-4, 1.0)
+    cost = {"alpha": 1.0, "beta": 1e-4}
+    ref, _, _, _, _ = capi.tune_grid_search(lengths, [2048, 4096], [1, 2], 4, cost, mem, 1e9, 150, 2, 3)
+    free, _, _, _, _ = capi.tune_grid_search_pp(lengths, [2048, 4096], [1, 2], 4, cost, mem, 0.0, 0, 1e9, 150, 2, 3)
+    assert (free["predicted_peak_gib"] > ref["predicted_peak_gib"]).all()
+    b2, _, _, _, _ = capi.tune_grid_search_pp(lengths, [2048, 4096], [1, 2], 4, cost, mem, 1e-5, 2, 1e9, 150, 2, 3)
+    assert (b2["predicted_peak_gib"] < free["predicted_peak_gib"]).all()
+    assert (b2["mean_time"] >= free["mean_time"]).all()
+    # the reference timing when nothing is checkpointed: identical makespans
+    one, _, _, _, _ = capi.tune_grid_search_pp(lengths, [2048], [1], 4, cost, mem, 0.0, 0, 1e9, 150, 2, 3)
+    assert one["mean_time"][0] == ref["mean_time"][0]
