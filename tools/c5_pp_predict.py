@@ -18,6 +18,17 @@ chunk 16K — simulator-in-the-loop prediction from MEASURED stage costs
    Step time = slowest replica's makespan + the stage-gradient all-reduce
    estimate (2 ranks, fp32, NVLink ~ 700 GB/s bus bandwidth).
 
+4. Memory per stage (round 2): every stage's op stream is replayed under
+   the executor's rules (cf_pp_stage_memory) for tape budgets 0..4
+   (cf_run_opts.stage_tape_budget); stage peak = static (weights bf16 +
+   fp32 grads of its layers, + embedding on stage 0, + final norm / head on
+   the last) + peak tape tokens x measured tape bytes/token + kept stage-input
+   tokens x d x 4 + the dependent group's KV state + the measured transient
+   working set.  The chosen budget is the fastest (cf_pp_simulate_budget:
+   checkpointed chunks pay their forward again) whose worst stage fits
+   170 GB; the pipeline-aware tuner (cf_tune_grid_search_pp) re-picks
+   (chunk size, K) with the in-flight tapes counted.
+
 Writes one JSON object (stdout)."""
 import json
 import sys
@@ -165,7 +176,99 @@ def main():
                     "budget_gib": 165.0, "best_chunk_size": bc, "best_k": bk, "evaluations": ev,
                     "report": report}
     out["tokens_global"] = int(lengths.sum())
+    out["memory"] = stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms)
     print(json.dumps(out), flush=True)
+
+
+def tape_bytes_per_token(layers, head):
+    """alloc_tape(T, retain=true) of the executor, per token (engine.cu)."""
+    d, H, kvw, ffn = QWEN["d"], QWEN["heads"], 1024, QWEN["ffn"]
+    qkv_w, gu_w, dh = d + 2 * kvw, 2 * ffn, d // H
+    per_layer = d * 4 + qkv_w * 2 + d * 2 + H * 4 + d * 4 + gu_w * 2 + d * 2 + d * 2 + ffn * 2
+    return layers * per_layer + d * 4 + (dh // 2) * 8 + (4 + d * 2 if head else 0)
+
+
+def stage_static_bytes(stage):
+    d, kvw, ffn, V = QWEN["d"], 1024, QWEN["ffn"], QWEN["vocab"]
+    per_layer = d * (d + 2 * kvw) + d * d + d * 2 * ffn + ffn * d + 2 * d
+    n = (LAYERS // STAGES) * per_layer
+    if stage == 0:
+        n += V * d
+    if stage == STAGES - 1:
+        n += d + d * ((V + 7) // 8 * 8)
+    return 6 * n  # bf16 weights + fp32 gradients
+
+
+def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms):
+    GB = 1e9
+    # measured: one retained 16K tape of a 16-layer stage with the head, and
+    # the transient working set beyond static + tapes + KV state
+    m = cf.Model(ctx, cf.model_cfg(arch=cf.ARCH_LLAMA, layers=per_stage, **QWEN))
+    one = np.array([CHUNK], np.int64)
+    st = cf.Step(m, cf.Plan.build(one, CHUNK, 1), one, cf.gen_tokens(one, QWEN["vocab"], 9))
+    st.run()
+    r = st.run()
+    st.close()
+    m.close()
+    tape_tok_measured = r.act_hbm_bytes / CHUNK
+    transient = r.peak_hbm_bytes - r.static_hbm_bytes - r.act_hbm_bytes - r.kv_hbm_bytes
+    kv_per_ctx_token = per_stage * 1024 * (2 * 2 + 2 * 4)  # K, V bf16 + dK|dV fp32
+    out = {"tape_bytes_per_token_analytic": tape_bytes_per_token(per_stage, True),
+           "tape_bytes_per_token_measured": tape_tok_measured,
+           "transient_gb_measured": transient / GB,
+           "static_gb": [stage_static_bytes(s) / GB for s in range(STAGES)],
+           "static_gb_measured_16_layers_with_head": r.static_hbm_bytes / GB,
+           "budget_gb": 170.0, "per_budget": {}}
+    best = None
+    for budget in range(0, 5):
+        worst, spans, stages_gb = 0.0, [], []
+        for rp in replicas:
+            mem = capi.pp_stage_memory(rp, STAGES, K, budget)
+            segs = rp.export()[1]
+            chs = rp.export()[0]
+            group_len = max([int(segs[c["seg_offset"]]["start_token"] + segs[c["seg_offset"]]["length"])
+                             for c in chs if c["kind"] == 1] or [0])
+            per = []
+            for s in range(STAGES):
+                tape_tok = tape_bytes_per_token(per_stage, s == STAGES - 1)
+                b = (stage_static_bytes(s) + mem["peak_tape_tokens"][s] * tape_tok +
+                     mem["peak_kept_tokens"][s] * QWEN["d"] * 4 + group_len * kv_per_ctx_token + transient)
+                per.append(b / GB)
+            stages_gb.append(per)
+            worst = max(worst, max(per))
+            ch = rp.export()[0]
+            f = np.array([fw.get(int(c["chunk_id"]), (0, 0))[0] * per_stage + fw.get(int(c["chunk_id"]), (0, 0))[1]
+                          for c in ch])
+            b_ = np.array([bw.get(int(c["chunk_id"]), (0, 0))[0] * per_stage + bw.get(int(c["chunk_id"]), (0, 0))[1]
+                           for c in ch])
+            miss = f == 0
+            if miss.any():  # chunks only replica 1 has: cost by tokens
+                tok = ch["total_tokens"].astype(np.float64)
+                f[miss] = (f[~miss] / tok[~miss]).mean() * tok[miss]
+                b_[miss] = (b_[~miss] / tok[~miss]).mean() * tok[miss]
+            _, _, _, pr = capi.pp_simulate(rp, STAGES, K, fwd_cost=f, bwd_cost=b_, tape_budget=budget)
+            spans.append(pr.makespan)
+        step_ms = max(spans) + allreduce_ms
+        rec = {"stage_peak_gb_per_replica": stages_gb, "worst_stage_gb": worst, "makespan_ms": spans,
+               "step_ms": step_ms, "tokens_per_s_8gpu": float(lengths.sum()) / (step_ms / 1e3),
+               "fits": worst <= 170.0}
+        out["per_budget"][str(budget)] = rec
+        if rec["fits"] and (best is None or step_ms < out["per_budget"][str(best)]["step_ms"]):
+            best = budget
+    out["chosen_budget"] = best
+    # pipeline-aware tuner with the same per-stage memory model
+    lay = tape_bytes_per_token(per_stage, True) / float(1 << 30)
+    mem = (max(stage_static_bytes(s) for s in range(STAGES)) / float(1 << 30) + transient / float(1 << 30), lay,
+           kv_per_ctx_token / float(1 << 30), 1.0)
+    fit = out.get("cost_model_fit")
+    table, bc, bk, ev, report = capi.tune_grid_search_pp(
+        lengths[:1000], [4096, 8192, 16384], [1, 2], STAGES,
+        {"gamma": 30.0, "alpha": 7.0e-3, "beta": 4.2e-7, "backward_multiplier": 2.14, "hop_latency": 0.0},
+        mem, QWEN["d"] * 4 / float(1 << 30), best or 0, 170.0 / 1.073741824, 1000, 1, 0)
+    out["tuner_pp"] = {"tape_budget": best or 0, "best_chunk_size": bc, "best_k": bk, "evaluations": ev,
+                       "report": report, "memory_model": mem}
+    del fit
+    return out
 
 
 if __name__ == "__main__":
