@@ -114,6 +114,25 @@ def peaks():
 TRAFFIC_FILE = "profiles/round1_gemm_traffic.json"
 
 
+HBM_FILE = "profiles/round2_hbm_kernels.json"
+
+
+def hbm_kernels():
+    """Achieved GB/s of the non-contraction kernels at C2 widths from the
+    committed ncu capture (tools/hbm_kernels.py): algorithmic bytes per launch
+    / ncu duration, DRAM bytes, fraction of the measured copy bandwidth."""
+    try:
+        t = json.load(open(os.path.join(ROOT, HBM_FILE)))
+    except Exception:
+        return None
+    ks = {k: {f: round(v[f], 3) if isinstance(v[f], float) else v[f]
+              for f in ("median_us", "achieved_gbs", "dram_gbs", "frac_of_peak", "traffic_over_algorithmic")
+              if f in v and v[f] is not None}
+          for k, v in t["kernels"].items()}
+    return {"source": HBM_FILE, "peak_gbs": t["peak_gbs"], "peak_kind": t["peak_kind"], "workload": t["workload"],
+            "kernels": ks}
+
+
 def gemm_traffic():
     """Per-launch DRAM bytes of the GEMM from the committed ncu --set full
     capture (tools/gemm_traffic.py), with the algorithmic bytes of the same
@@ -399,6 +418,7 @@ def run_b200(args):
                      "attention_bwd": {"achieved": attnb_tf, "share_of_step": attnb_share, "unit": "TFLOP/s",
                                        "note": "algorithmic 8*H*dh FLOP/pair"},
                      "other_share_of_step": max(0.0, 1 - gemm_share - attn_share - attnb_share)},
+        "hbm_kernels": hbm_kernels(),
         "e2e": {"value": tokens_all / (e2e_max / 1e3 / max(1, args.steps)), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": int(sum(r.gpu_launches for r in res)),

@@ -120,6 +120,14 @@ typedef struct cf_run_opts {
    * checkpointing); the free slot holds that just-in-time tape.  Results are
    * bitwise those without a budget. */
   int64_t stage_tape_budget;
+  /* 1: dependent groups keep their KV state (K, V bf16 and the fp32 dK/dV
+   * accumulators, [L][S] each) in pinned host memory; the device holds two
+   * one-layer staging buffers and the rows a layer needs move on a copy
+   * stream while the neighbouring layer computes (the KV offloading the
+   * paper leaves for future work).  Device KV memory becomes
+   * 2/L of the state; results are bitwise those without offload. */
+  int32_t kv_offload;
+  int32_t reserved2;
 } cf_run_opts;
 
 /* RunPlanResult + RunInstrumentation (plan_runner.hpp:36-60), plus the
@@ -413,6 +421,30 @@ int cf_model_zero_grads(cf_model* model);
  * that reduce gradients themselves. */
 int cf_model_grad_buffer(cf_model* model, void** dev_ptr, int64_t* numel);
 int64_t cf_model_num_params(const cf_model* model);
+
+/* ---- optimizer (the reference's step ends at the
+ *      gradients, so this is new): fused AdamW over the flat fp32 gradient
+ *      buffer with fp32 master weights, torch.optim.AdamW semantics
+ *      (decoupled weight decay, bias-corrected moments) ---- */
+typedef struct cf_adamw_cfg {
+  double lr;
+  double beta1, beta2, eps;
+  double weight_decay;   /* decoupled; RMSNorm gains only with decay_gains */
+  double max_grad_norm;  /* > 0: clip the global L2 norm first (clip_grad_norm_) */
+  int32_t decay_gains;
+  int32_t reserved;
+} cf_adamw_cfg;
+/* Allocates master weights (= the current weights, fp32) and zeroed moments
+ * (3 x 4 bytes per parameter); resets the step counter.  Re-initialises when
+ * called again.  cf_model_set_param keeps the master copy in step. */
+int cf_model_adamw_init(cf_model* model);
+/* One step on the gradients currently in the model (after cf_run_plan /
+ * cf_step_run, all-reduced under DP): one fused HBM pass updates master,
+ * moments and the bf16 working weights.  grad_norm (may be NULL) receives
+ * the pre-clip global gradient norm (fp64, deterministic reduction). */
+int cf_model_adamw_step(cf_model* model, const cf_adamw_cfg* cfg, double* grad_norm);
+/* fp32 master copy of tensor idx (reference order / shape), as fp64. */
+int cf_model_get_master(cf_model* model, int64_t idx, double* host);
 
 /* ---- execution ---- */
 

@@ -474,7 +474,7 @@ inline cf_run_result run_plan(const Model& model, const ChunkPlan& /*chunk_plan*
   const auto plan = detail::replay(exec_plan);
   const PlanDiagnostics diag = detail::diagnostics(plan->get());
   if (!diag.violations.empty()) throw ValidationError("execution plan is invalid: " + diag.violations.front());
-  cf_run_opts o{options.corrupt_kv_grads ? 1 : 0, 0, options.normalizer_override, 0};
+  cf_run_opts o{options.corrupt_kv_grads ? 1 : 0, 0, options.normalizer_override, 0, 0, 0};
   cf_run_result r{};
   check(cf_run_plan(model.device().get(), model.get(), plan->get(), ids.data(), lengths.data(), tokens.data(),
                     static_cast<int64_t>(ids.size()), &o, &r));

@@ -45,7 +45,8 @@ class ModelCfg(C.Structure):
 
 class RunOpts(C.Structure):
     _fields_ = [("corrupt_kv_grads", C.c_int32), ("accumulate_grads", C.c_int32),
-                ("normalizer_override", C.c_double), ("stage_tape_budget", C.c_int64)]
+                ("normalizer_override", C.c_double), ("stage_tape_budget", C.c_int64), ("kv_offload", C.c_int32),
+                ("reserved2", C.c_int32)]
 
 
 class PpCost(C.Structure):
@@ -61,6 +62,12 @@ class PpResult(C.Structure):
 class MemCoeffs(C.Structure):
     _fields_ = [("base_gib", C.c_double), ("per_chunk_token_gib", C.c_double),
                 ("per_context_token_gib", C.c_double), ("gqa_ratio", C.c_double)]
+
+
+class AdamWCfg(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("max_grad_norm", C.c_double), ("decay_gains", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class RunResult(C.Structure):
@@ -99,7 +106,7 @@ EXPORTS = [
     "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
     "cf_segment_forward", "cf_segment_backward", "cf_segment_destroy", "cf_op_gemm_rope",
     "cf_plan_validate_events", "cf_op_lm_head_ce", "cf_pp_stage_memory", "cf_tune_grid_search_pp",
-    "cf_pp_simulate_budget",
+    "cf_pp_simulate_budget", "cf_model_adamw_init", "cf_model_adamw_step", "cf_model_get_master",
 ]
 
 _lib = None
@@ -598,17 +605,36 @@ class Model:
     def grads_flat(self):
         return np.concatenate([self.get_grad(i).ravel() for i in range(self.num_tensors())])
 
+    def adamw_init(self):
+        """fp32 master weights + zero moments (cf_model_adamw_init)."""
+        check(lib().cf_model_adamw_init(self.h))
+
+    def adamw_step(self, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, max_grad_norm=0.0,
+                   decay_gains=False):
+        """One fused AdamW step on the current gradients; returns the global
+        gradient norm (before clipping)."""
+        c = AdamWCfg(lr, beta1, beta2, eps, weight_decay, max_grad_norm, int(decay_gains), 0)
+        norm = C.c_double()
+        check(lib().cf_model_adamw_step(self.h, C.byref(c), C.byref(norm)))
+        return norm.value
+
+    def get_master(self, i):
+        _, r, c = self.tensor_info(i)
+        out = np.zeros((r, c), np.float64)
+        check(lib().cf_model_get_master(self.h, C.c_int64(i), _p(out)))
+        return out
+
     def grad_buffer(self):
         p, n = C.c_void_p(), C.c_int64()
         check(lib().cf_model_grad_buffer(self.h, C.byref(p), C.byref(n)))
         return p.value, n.value
 
     def run_plan(self, plan: Plan, lengths, tokens, ids=None, corrupt=False, normalizer=0.0,
-                 accumulate=False) -> RunResult:
+                 accumulate=False, kv_offload=False) -> RunResult:
         lengths = np.ascontiguousarray(lengths, np.int64)
         ids = np.arange(len(lengths), dtype=np.int64) if ids is None else np.ascontiguousarray(ids, np.int64)
         tokens = np.ascontiguousarray(tokens, np.int32)
-        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, 0, int(kv_offload))
         r = RunResult()
         check(lib().cf_run_plan(self.ctx.h, self.h, plan.h, _p(ids), _p(lengths), _p(tokens),
                                 C.c_int64(len(lengths)), C.byref(o), C.byref(r)))
@@ -709,8 +735,8 @@ class Step:
         check(lib().cf_step_prepare(model.ctx.h, model.h, plan.h, _p(self.ids), _p(self.lengths),
                                     _p(self.tokens), C.c_int64(len(self.lengths)), C.byref(self.h)))
 
-    def run(self, corrupt=False, normalizer=0.0, accumulate=False) -> RunResult:
-        o = RunOpts(int(corrupt), int(accumulate), normalizer)
+    def run(self, corrupt=False, normalizer=0.0, accumulate=False, kv_offload=False) -> RunResult:
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, 0, int(kv_offload))
         r = RunResult()
         check(lib().cf_step_run(self.model.ctx.h, self.model.h, self.h, C.byref(o), C.byref(r)))
         return r
@@ -731,18 +757,19 @@ class Step:
         check(lib().cf_step_op_times(self.h, C.byref(n), _p(kinds), _p(ids), _p(ms)))
         return kinds, ids, ms
 
-    def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0) -> RunResult:
+    def run_pp(self, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0, kv_offload=False) -> RunResult:
         """This rank's pipeline stage (cf_pp_step_run; needs Context.init_pp).
         tape_budget > 0: stage-input checkpointing beyond that many tapes."""
-        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget))
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget), int(kv_offload))
         r = RunResult()
         check(lib().cf_pp_step_run(self.model.ctx.h, self.model.h, self.h, C.c_int64(k), C.byref(o), C.byref(r)))
         return r
 
-    def run_pp_local(self, models, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0) -> RunResult:
+    def run_pp_local(self, models, k, corrupt=False, normalizer=0.0, accumulate=False, tape_budget=0,
+                     kv_offload=False) -> RunResult:
         """All pipeline stages on this device (cf_pp_run_local)."""
         arr = (C.c_void_p * len(models))(*[m.h.value for m in models])
-        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget))
+        o = RunOpts(int(corrupt), int(accumulate), normalizer, int(tape_budget), int(kv_offload))
         r = RunResult()
         check(lib().cf_pp_run_local(self.model.ctx.h, arr, C.c_int64(len(models)), self.h, C.c_int64(k),
                                     C.byref(o), C.byref(r)))

@@ -238,6 +238,26 @@ int cf_model_get_grad(cf_model* model, int64_t idx, double* host) {
     cfb::model_get_grad(model->m, idx, host);
   });
 }
+int cf_model_adamw_init(cf_model* model) {
+  return cfb::guard([&] {
+    need(model, "model");
+    cfb::model_adamw_init(model->m);
+  });
+}
+int cf_model_adamw_step(cf_model* model, const cf_adamw_cfg* cfg, double* grad_norm) {
+  return cfb::guard([&] {
+    need(model, "model");
+    need(cfg, "cfg");
+    cfb::model_adamw_step(model->m, *cfg, grad_norm);
+  });
+}
+int cf_model_get_master(cf_model* model, int64_t idx, double* host) {
+  return cfb::guard([&] {
+    need(model, "model");
+    need(host, "host");
+    cfb::model_get_master(model->m, idx, host);
+  });
+}
 int cf_model_zero_grads(cf_model* model) {
   return cfb::guard([&] {
     need(model, "model");

@@ -63,13 +63,49 @@ struct Arena {
   }
 };
 
+// Stream-ordered pool allocation.  The pool keeps freed blocks (release
+// threshold = max) so per-chunk scratch is a lookup; when a request does not
+// fit next to the cached blocks of other sizes, the cache is released
+// (after the stream drains) and the request retried once.
 void* pool_alloc(Ctx* c, int64_t bytes) {
   void* p = nullptr;
-  CK(cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(bytes, 256)), c->stream));
+  const size_t n = static_cast<size_t>(std::max<int64_t>(bytes, 256));
+  cudaError_t e = cudaMallocAsync(&p, n, c->stream);
+  if (e == cudaErrorMemoryAllocation && c->pool) {
+    (void)cudaGetLastError();
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemPoolTrimTo(c->pool, 0));
+    e = cudaMallocAsync(&p, n, c->stream);
+  }
+  CK(e);
   return p;
 }
 void pool_free(Ctx* c, void* p) {
   if (p) CK(cudaFreeAsync(p, c->stream));
+}
+
+// Pinned host blocks for offloaded KV state, cached on the context across
+// steps (page-locking tens of GB costs seconds; a block is reused by any
+// later group that fits).
+void* host_acquire(Ctx* c, size_t bytes) {
+  for (auto& b : c->host_blocks)
+    if (!b.busy && b.bytes >= bytes) {
+      b.busy = true;
+      return b.ptr;
+    }
+  void* p = nullptr;
+  CK(cudaMallocHost(&p, bytes));
+  c->host_blocks.push_back({p, bytes, true});
+  return p;
+}
+void host_release(Ctx* c, void* p) {
+  for (auto& b : c->host_blocks)
+    if (b.ptr == p) b.busy = false;
+}
+cudaEvent_t new_timing_free_event() {
+  cudaEvent_t e;
+  CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
 }
 
 // --------------------------------------------------------------- NCCL (dlopen)
@@ -131,6 +167,13 @@ void ctx_release(Ctx* ctx) {
     }
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   ctx->event_pool.clear();
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    ctx->copy_stream = nullptr;
+  }
+  for (auto& b : ctx->host_blocks) cudaFreeHost(b.ptr);
+  ctx->host_blocks.clear();
 }
 
 void dp_init(Ctx* ctx, int rank, int world, const uint8_t* id) {
@@ -355,6 +398,17 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage, int64_t st
                               scale, ctx->stream));
     draw += s.rows * s.cols;
   }
+  // storage pieces for the fused AdamW (weights and gradients share the
+  // element order piece by piece; RMSNorm gains are fp32 and not decayed)
+  for (size_t i = 0; i < pieces.size(); ++i) {
+    cfk::AdamPiece ap;
+    ap.goff = goff[i];
+    ap.n = pieces[i].elems;
+    ap.w = wb + woff[i];
+    ap.f32 = pieces[i].f32 ? 1 : 0;
+    ap.decay = pieces[i].f32 ? 0 : 1;
+    m->pieces.push_back(ap);
+  }
   if (m->has_head && Vp != m->V)  // zero the head's pad columns
     CK(cudaMemset2DAsync(m->head + m->V, static_cast<size_t>(Vp) * 2, 0, static_cast<size_t>(Vp - m->V) * 2,
                          static_cast<size_t>(m->d), ctx->stream));
@@ -362,17 +416,107 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage, int64_t st
   return m.release();
 }
 
-void model_destroy(Model* m) {
-  if (!m) return;
-  cudaFree(m->wbuf);
-  cudaFree(m->grads);
-  delete m;
-}
-
 static const Slot& slot_at(Model* m, int64_t idx) {
   if (idx < 0 || idx >= static_cast<int64_t>(m->slots.size())) throw ValidationError("tensor index out of range");
   return m->slots[static_cast<size_t>(idx)];
 }
+
+void model_destroy(Model* m) {
+  if (!m) return;
+  cudaFree(m->wbuf);
+  cudaFree(m->grads);
+  if (m->opt_mem) cudaFree(m->opt_mem);
+  delete m;
+}
+
+void model_adamw_init(Model* m) {
+  cudaStream_t st = m->ctx->stream;
+  if (!m->opt_mem) {
+    const int np = static_cast<int>(m->pieces.size());
+    std::vector<int64_t> bs(static_cast<size_t>(np) + 1, 0);
+    for (int i = 0; i < np; ++i) bs[static_cast<size_t>(i) + 1] = bs[static_cast<size_t>(i)] + cfk::adam_blocks(m->pieces[i].n);
+    m->opt_blocks = bs.back();
+    const int64_t nb_all = cfk::adam_blocks(m->grad_numel);
+    Arena measure{nullptr, 0};
+    auto carve = [&](Arena& a) {
+      m->master = a.take<float>(m->grad_numel);
+      m->adam_m = a.take<float>(m->grad_numel);
+      m->adam_v = a.take<float>(m->grad_numel);
+      m->opt_scratch = a.take<float>(nb_all + 1);
+      m->clip_coef = a.take<float>(1);
+      m->grad_norm = a.take<double>(1);
+      m->pieces_dev = a.take<cfk::AdamPiece>(np);
+      m->block_start_dev = a.take<int64_t>(np + 1);
+    };
+    carve(measure);
+    CK(cudaMalloc(&m->opt_mem, static_cast<size_t>(measure.off + 256)));
+    Arena a{static_cast<char*>(m->opt_mem), 0};
+    carve(a);
+    CK(cudaMemcpyAsync(m->pieces_dev, m->pieces.data(), sizeof(cfk::AdamPiece) * m->pieces.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(m->block_start_dev, bs.data(), sizeof(int64_t) * bs.size(), cudaMemcpyHostToDevice, st));
+  }
+  // padding between pieces stays 0 in every buffer
+  CK(cudaMemsetAsync(m->master, 0, static_cast<size_t>(m->grad_numel) * 4, st));
+  CK(cudaMemsetAsync(m->adam_m, 0, static_cast<size_t>(m->grad_numel) * 4, st));
+  CK(cudaMemsetAsync(m->adam_v, 0, static_cast<size_t>(m->grad_numel) * 4, st));
+  CK(cfk::master_from_weights(m->pieces_dev, static_cast<int>(m->pieces.size()), m->block_start_dev, m->opt_blocks,
+                              m->master, st));
+  m->opt_step = 0;
+  CK(cudaStreamSynchronize(st));
+}
+
+// One AdamW step (torch.optim.AdamW semantics) on the gradients of the last
+// run: optional global-norm clipping, then the fused update of master,
+// moments and working weights.
+void model_adamw_step(Model* m, const cf_adamw_cfg& c, double* grad_norm) {
+  if (!m->opt_mem) throw ValidationError("AdamW state not initialised (cf_model_adamw_init)");
+  if (!(c.lr >= 0) || !(c.beta1 >= 0 && c.beta1 < 1) || !(c.beta2 >= 0 && c.beta2 < 1) || !(c.eps > 0) ||
+      !(c.weight_decay >= 0))
+    throw ValidationError("invalid AdamW hyper-parameters");
+  cudaStream_t st = m->ctx->stream;
+  const bool clip = c.max_grad_norm > 0 || grad_norm;
+  if (clip)
+    CK(cfk::grad_clip_coef(m->grads, m->grad_numel, static_cast<float>(c.max_grad_norm), m->opt_scratch, m->clip_coef,
+                           m->grad_norm, st));
+  ++m->opt_step;
+  const double t = static_cast<double>(m->opt_step);
+  cfk::AdamHyper h;
+  h.lr = static_cast<float>(c.lr);
+  h.b1 = static_cast<float>(c.beta1);
+  h.b2 = static_cast<float>(c.beta2);
+  h.eps = static_cast<float>(c.eps);
+  h.wd = static_cast<float>(c.weight_decay);
+  h.step_size = static_cast<float>(c.lr / (1.0 - std::pow(c.beta1, t)));
+  h.sqrt_bc2 = static_cast<float>(std::sqrt(1.0 - std::pow(c.beta2, t)));
+  std::vector<cfk::AdamPiece> pcs = m->pieces;
+  if (c.decay_gains) {
+    for (auto& p : pcs) p.decay = 1;
+    CK(cudaMemcpyAsync(m->pieces_dev, pcs.data(), sizeof(cfk::AdamPiece) * pcs.size(), cudaMemcpyHostToDevice, st));
+  }
+  CK(cfk::adamw_step(m->pieces_dev, static_cast<int>(pcs.size()), m->block_start_dev, m->opt_blocks, m->grads,
+                     m->master, m->adam_m, m->adam_v, c.max_grad_norm > 0 ? m->clip_coef : nullptr, h, st));
+  if (c.decay_gains)  // restore the default table
+    CK(cudaMemcpyAsync(m->pieces_dev, m->pieces.data(), sizeof(cfk::AdamPiece) * m->pieces.size(),
+                       cudaMemcpyHostToDevice, st));
+  m->ctx->launches += clip ? 3 : 1;
+  if (grad_norm) {
+    CK(cudaMemcpyAsync(grad_norm, m->grad_norm, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+}
+
+void model_get_master(Model* m, int64_t idx, double* host) {
+  if (!m->opt_mem) throw ValidationError("AdamW state not initialised (cf_model_adamw_init)");
+  const Slot& s = slot_at(m, idx);
+  cudaStream_t st = m->ctx->stream;
+  double* tmp = static_cast<double*>(pool_alloc(m->ctx, s.rows * s.cols * 8));
+  CK(cfk::f32_to_f64(m->master + (s.g - m->grads), s.ld, s.rows, s.cols, tmp, st));
+  CK(cudaMemcpyAsync(host, tmp, static_cast<size_t>(s.rows * s.cols) * 8, cudaMemcpyDeviceToHost, st));
+  pool_free(m->ctx, tmp);
+  CK(cudaStreamSynchronize(st));
+}
+
 
 void model_get_param(Model* m, int64_t idx, double* host) {
   const Slot& s = slot_at(m, idx);
@@ -396,6 +540,9 @@ void model_set_param(Model* m, int64_t idx, const double* host) {
     CK(cfk::f64_to_f32(tmp, s.rows, s.cols, static_cast<float*>(s.w), s.ld, st));
   else
     CK(cfk::f64_to_bf16(tmp, s.rows, s.cols, static_cast<bf16*>(s.w), s.ld, st));
+  // keep the AdamW master copy in step with a caller-set weight (the fp32
+  // value the caller gave, not its bf16 rounding)
+  if (m->master) CK(cfk::f64_to_f32(tmp, s.rows, s.cols, m->master + (s.g - m->grads), s.ld, st));
   pool_free(m->ctx, tmp);
   CK(cudaStreamSynchronize(st));
 }
@@ -433,6 +580,29 @@ struct GroupState {
   void* mem = nullptr;
   std::vector<int64_t> contributions;  // per chunk index
   std::vector<bool> saved;
+  // KV offload (cf_run_opts.kv_offload; the paper's deferred "offloading
+  // optimization"): the [L][S] state lives in pinned host
+  // memory (hk / hv / hdkv) and the device holds two one-layer staging
+  // buffers (sk / sv / sdkv [S] rows, by layer parity).  Layer l's rows are
+  // loaded on the copy stream while layer l -/+ 1 computes; new K/V rows
+  // (forward) and prefix dK/dV rows (backward) are written back after the
+  // layer's attention.
+  bool offload = false;
+  bf16 *hk = nullptr, *hv = nullptr;
+  float* hdkv = nullptr;
+  void* hmem = nullptr;
+  bf16* sk[2] = {nullptr, nullptr};
+  bf16* sv[2] = {nullptr, nullptr};
+  float* sdkv[2] = {nullptr, nullptr};
+  cudaEvent_t used[2] = {nullptr, nullptr};    // compute done with staging b
+  cudaEvent_t loaded[2] = {nullptr, nullptr};  // staging b holds the layer it was loaded for
+  int64_t staged_layer[2] = {-1, -1};
+  bool staged_bwd[2] = {false, false};
+  int64_t dkv_valid = 0;                       // host dK/dV rows [0, dkv_valid) hold contributions
+  std::vector<bool> on_host;                   // chunk index -> own K/V rows written back
+  bf16* K(int64_t l, int64_t kvw) const { return offload ? sk[l & 1] : kc + l * S * kvw; }
+  bf16* V(int64_t l, int64_t kvw) const { return offload ? sv[l & 1] : vc + l * S * kvw; }
+  float* DKV(int64_t l, int64_t kvw) const { return offload ? sdkv[l & 1] : dkv + l * S * 2 * kvw; }
 };
 
 struct Tape {
@@ -861,6 +1031,63 @@ struct Exec {
     pool_free(ctx, dl);
   }
 
+  // ---- KV offload: per-layer staging of an offloaded group's state.
+  // Loads of layer l into staging buffer l & 1, on the copy stream.
+  void kv_load(const ChunkMeta& cm, GroupState* gs, int64_t l, bool bwd) {
+    const int b = static_cast<int>(l & 1);
+    if (gs->staged_layer[b] == l && gs->staged_bwd[b] == bwd) return;
+    cudaStream_t cs = ctx->copy_stream;
+    const int64_t kvw = m->kvw, S = gs->S;
+    const int64_t rows = bwd ? cm.start + cm.T : cm.start;  // backward: own rows too (incl. their incoming dK/dV)
+    CK(cudaStreamWaitEvent(cs, gs->used[b], 0));
+    if (rows > 0) {
+      CK(cudaMemcpyAsync(gs->sk[b], gs->hk + l * S * kvw, static_cast<size_t>(rows * kvw) * 2, cudaMemcpyHostToDevice, cs));
+      CK(cudaMemcpyAsync(gs->sv[b], gs->hv + l * S * kvw, static_cast<size_t>(rows * kvw) * 2, cudaMemcpyHostToDevice, cs));
+    }
+    if (bwd) {
+      const int64_t valid = std::min(rows, gs->dkv_valid);
+      if (valid > 0)
+        CK(cudaMemcpyAsync(gs->sdkv[b], gs->hdkv + l * S * 2 * kvw, static_cast<size_t>(valid * 2 * kvw) * 4,
+                           cudaMemcpyHostToDevice, cs));
+      if (rows > valid)
+        CK(cudaMemsetAsync(gs->sdkv[b] + valid * 2 * kvw, 0, static_cast<size_t>((rows - valid) * 2 * kvw) * 4, cs));
+    }
+    CK(cudaEventRecord(gs->loaded[b], cs));
+    gs->staged_layer[b] = l;
+    gs->staged_bwd[b] = bwd;
+  }
+  // Before layer l's use: its rows are staged (prefetching the next layer of
+  // the pass into the other buffer so the copy overlaps this layer's math).
+  void kv_stage(const ChunkMeta& cm, GroupState* gs, int64_t l, bool bwd) {
+    kv_load(cm, gs, l, bwd);
+    CK(cudaStreamWaitEvent(s, gs->loaded[l & 1], 0));
+    const int64_t nxt = bwd ? l - 1 : l + 1;
+    if (nxt >= 0 && nxt < m->L) kv_load(cm, gs, nxt, bwd);
+  }
+  // After layer l's attention: write back what changed, release the buffer.
+  void kv_release(const ChunkMeta& cm, GroupState* gs, int64_t l, bool bwd) {
+    const int b = static_cast<int>(l & 1);
+    cudaStream_t cs = ctx->copy_stream;
+    const int64_t kvw = m->kvw, S = gs->S;
+    CK(cudaEventRecord(gs->used[b], s));
+    CK(cudaStreamWaitEvent(cs, gs->used[b], 0));  // the copy stream now trails this layer's attention
+    if (!bwd) {
+      if (!gs->on_host[static_cast<size_t>(cm.index)]) {  // a recompute rewrites identical rows: skip
+        const size_t off = static_cast<size_t>((l * S + cm.start) * kvw);
+        CK(cudaMemcpyAsync(gs->hk + off, gs->sk[b] + cm.start * kvw, static_cast<size_t>(cm.T * kvw) * 2,
+                           cudaMemcpyDeviceToHost, cs));
+        CK(cudaMemcpyAsync(gs->hv + off, gs->sv[b] + cm.start * kvw, static_cast<size_t>(cm.T * kvw) * 2,
+                           cudaMemcpyDeviceToHost, cs));
+      }
+    } else if (cm.start > 0) {  // prefix dK/dV now include this chunk's contribution; own rows are consumed
+      CK(cudaMemcpyAsync(gs->hdkv + l * S * 2 * kvw, gs->sdkv[b], static_cast<size_t>(cm.start * 2 * kvw) * 4,
+                         cudaMemcpyDeviceToHost, cs));
+    }
+    // the staged rows no longer match the host copy for the next pass
+    gs->staged_layer[b] = -1;
+    CK(cudaEventRecord(gs->used[b], cs));  // reuse only after the write-back
+  }
+
   Tape alloc_tape(int64_t T, bool retain) {
     Tape t;
     t.T = T;
@@ -910,10 +1137,10 @@ struct Exec {
     p.q = t.qkvl(l);
     p.q_stride = m->qkv_w;
     if (cm.dependent) {
-      p.k = gs->kc + l * gs->S * m->kvw;
-      p.v = gs->vc + l * gs->S * m->kvw;
+      p.k = gs->K(l, m->kvw);
+      p.v = gs->V(l, m->kvw);
       p.kv_stride = m->kvw;
-      p.dk_acc = gs->dkv + l * gs->S * 2 * m->kvw;
+      p.dk_acc = gs->DKV(l, m->kvw);
       p.dv_acc = p.dk_acc + m->kvw;
     } else {
       p.k = p.q + m->d;
@@ -959,8 +1186,9 @@ struct Exec {
         L(cfk::rmsnorm_fwd(x, ly.g1, T, d, static_cast<float>(m->cfg.rms_eps), xn1, s), "rmsnorm");
       else
         L(cfk::to_bf16(x, xn1, T * d, s), "to_bf16");
-      bf16* kc_rows = cm.dependent ? gs->kc + l * gs->S * m->kvw + cm.start * m->kvw : nullptr;
-      bf16* vc_rows = cm.dependent ? gs->vc + l * gs->S * m->kvw + cm.start * m->kvw : nullptr;
+      if (cm.dependent && gs->offload) kv_stage(cm, gs, l, false);
+      bf16* kc_rows = cm.dependent ? gs->K(l, m->kvw) + cm.start * m->kvw : nullptr;
+      bf16* vc_rows = cm.dependent ? gs->V(l, m->kvw) + cm.start * m->kvw : nullptr;
       if (m->llama && cfk::gemm_rope_ok(T, m->qkv_w, d, m->dh, d, d + m->kvw)) {
         // RoPE and the KV-cache copy in the q|k|v GEMM's epilogue
         cfk::GemmDesc g{xn1, d, 1, ly.wqkv, m->qkv_w, 0, qkv, m->qkv_w, t.tab, m->dh / 2, T, m->qkv_w, d,
@@ -995,6 +1223,7 @@ struct Exec {
       else
         L(cfk::attn_forward(p, s), "attn_fwd");
       close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1);
+      if (cm.dependent && gs->offload) kv_release(cm, gs, l, false);
       gemm(t.ol(l), 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
       float* xn = t.xin(l + 1);
       if (m->llama) {
@@ -1125,6 +1354,7 @@ struct Exec {
       gemm(xb, 1, d, ly.wo, 1, d, dO, d, T, d, d, cfk::EPI_BF16);
       gemm(O, 0, d, xb, 0, d, ly.d_wo, d, d, d, T, cfk::EPI_F32_ACC);
       // Attention (toy_model.hpp:436-495)
+      if (cm.dependent && gs->offload) kv_stage(cm, gs, l, true);
       AttnParams p = attn_params(cm, t, l, gs);
       p.dout = dO;
       p.dout_stride = d;
@@ -1165,6 +1395,7 @@ struct Exec {
         L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
                            m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
           "dkv_to_dqkv");
+      if (cm.dependent && gs->offload) kv_release(cm, gs, l, true);
       if (m->llama && !p.rope_tab)
         L(cfk::rope_bwd_q(dqkv, qw, T, static_cast<int>(m->H), static_cast<int>(m->dh), t.tab, s), "rope_bwd");
       // Projections (toy_model.hpp:497-511)
@@ -1220,6 +1451,7 @@ struct StageRunner {
   // input and is recomputed right before its backward
   int64_t tape_budget = 0, live_peak = 0, ckpt_recomputes = 0, next_extra_slot = 0;
   std::set<int64_t> ckpt;
+  bool kv_offload = false;  // dependent groups keep their KV state in pinned host memory
   int64_t io_bytes = 0;  // stage-boundary buffers held (kept inputs)
   struct OpMark {
     int64_t kind, id;
@@ -1248,6 +1480,7 @@ struct StageRunner {
     ex.st = st;
     ex.s = ctx->stream;
     ex.corrupt = opts.corrupt_kv_grads != 0;
+    kv_offload = opts.kv_offload != 0;
     if (!(opts.normalizer_override > 0) && !st->normalizer_error.empty())
       throw ValidationError(st->normalizer_error);
     norm = opts.normalizer_override > 0 ? opts.normalizer_override : st->normalizer;
@@ -1261,7 +1494,17 @@ struct StageRunner {
   // pool memory; finish() leaves nothing behind for this to release.
   ~StageRunner() {
     for (auto& kv : live) cudaFreeAsync(kv.second.mem, ex.s);
-    for (auto& kv : groups) cudaFreeAsync(kv.second.mem, ex.s);
+    for (auto& kv : groups) {
+      if (kv.second.offload) {
+        if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);
+        host_release(ctx, kv.second.hmem);
+        for (int b = 0; b < 2; ++b) {
+          cudaEventDestroy(kv.second.used[b]);
+          cudaEventDestroy(kv.second.loaded[b]);
+        }
+      }
+      if (kv.second.mem) cudaFreeAsync(kv.second.mem, ex.s);
+    }
     for (auto& kv : kept_in) cudaFreeAsync(kv.second, ex.s);
     if (ex.loss_slots) cudaFreeAsync(ex.loss_slots, ex.s);
   }
@@ -1279,6 +1522,58 @@ struct StageRunner {
   int64_t kv_state_bytes(int64_t S) const {
     return 3 * 256 + 2 * m->L * S * m->kvw * 2 + m->L * S * 2 * m->kvw * 4;
   }
+  // offloaded group: two one-layer device staging buffers
+  int64_t staging_bytes(int64_t S) const { return 6 * 256 + 2 * (2 * S * m->kvw * 2 + S * 2 * m->kvw * 4); }
+
+  // KV offload: host state in pinned memory (from the context's cache of
+  // pinned blocks), device staging for two layers, copy-stream events.
+  void alloc_offloaded(GroupState& g) {
+    const int64_t S = g.S, kvw = m->kvw, L_ = m->L;
+    g.offload = true;
+    const size_t hbytes = static_cast<size_t>(L_ * S * kvw) * (2 + 2 + 8) + 3 * 256;
+    g.hmem = host_acquire(ctx, hbytes);
+    Arena h{static_cast<char*>(g.hmem), 0};
+    g.hk = h.take<bf16>(L_ * S * kvw);
+    g.hv = h.take<bf16>(L_ * S * kvw);
+    g.hdkv = h.take<float>(L_ * S * 2 * kvw);
+    const int64_t bytes = staging_bytes(S);
+    g.mem = pool_alloc(ctx, bytes);
+    Arena a{static_cast<char*>(g.mem), 0};
+    for (int b = 0; b < 2; ++b) {
+      g.sk[b] = a.take<bf16>(S * kvw);
+      g.sv[b] = a.take<bf16>(S * kvw);
+      g.sdkv[b] = a.take<float>(S * 2 * kvw);
+      g.used[b] = new_timing_free_event();
+      g.loaded[b] = new_timing_free_event();
+      CK(cudaEventRecord(g.used[b], ex.s));
+    }
+    // staged rows past the ones a layer loads are read (masked) by partial
+    // 128-key tiles: they must be finite
+    CK(cudaMemsetAsync(g.mem, 0, static_cast<size_t>(bytes), ex.s));
+    CK(cudaEventRecord(g.used[0], ex.s));
+    CK(cudaEventRecord(g.used[1], ex.s));
+    if (!ctx->copy_stream) CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    ex.kv_bytes += bytes;
+    ex.kv_peak = std::max(ex.kv_peak, ex.kv_bytes);
+  }
+  void free_group(GroupState& g) {
+    if (g.offload) {
+      // the copy stream's last write-backs must finish before the buffers go
+      CK(cudaEventRecord(g.used[0], ctx->copy_stream));
+      CK(cudaStreamWaitEvent(ex.s, g.used[0], 0));
+      CK(cudaStreamSynchronize(ctx->copy_stream));
+      host_release(ctx, g.hmem);
+      for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(g.used[b]);
+        cudaEventDestroy(g.loaded[b]);
+      }
+      ex.kv_bytes -= staging_bytes(g.S);
+    } else {
+      ex.kv_bytes -= kv_state_bytes(g.S);
+    }
+    pool_free(ctx, g.mem);
+    g.mem = nullptr;
+  }
 
   GroupState* group_for(const ChunkMeta& cm) {
     if (!cm.dependent) return nullptr;
@@ -1289,6 +1584,12 @@ struct StageRunner {
       const int64_t n = group_size(cm);
       g.contributions.assign(static_cast<size_t>(n), 0);
       g.saved.assign(static_cast<size_t>(n), false);
+      g.on_host.assign(static_cast<size_t>(n), false);
+      if (kv_offload) {
+        alloc_offloaded(g);
+        git = groups.emplace(cm.group, std::move(g)).first;
+        return &git->second;
+      }
       const int64_t bytes = kv_state_bytes(g.S);
       g.mem = pool_alloc(ctx, bytes);
       Arena a{static_cast<char*>(g.mem), 0};
@@ -1345,6 +1646,7 @@ struct StageRunner {
     }
     ex.forward(cm, t, gs, slot, retain);
     if (gs && save_kv) gs->saved[static_cast<size_t>(cm.index)] = true;
+    if (gs) gs->on_host[static_cast<size_t>(cm.index)] = true;
     if (!recompute) {
       first_slot[id] = slot;
       first_pass_slots.push_back(slot);
@@ -1428,9 +1730,9 @@ struct StageRunner {
     ex.backward(cm, lit->second, gs, dx);
     if (gs) {
       for (int64_t i = 0; i < cm.index; ++i) ++gs->contributions[static_cast<size_t>(i)];
+      if (gs->offload) gs->dkv_valid = std::max(gs->dkv_valid, cm.start);
       if (cm.index == 0) {  // group complete: release its KV state
-        pool_free(ctx, gs->mem);
-        ex.kv_bytes -= kv_state_bytes(gs->S);
+        free_group(*gs);
         groups.erase(cm.group);
       }
     }
@@ -1449,7 +1751,7 @@ struct StageRunner {
   void finish(cf_run_result* res, bool dp_reduce) {
     for (auto& kv : live) ex.free_tape(kv.second);
     live.clear();
-    for (auto& kv : groups) pool_free(ctx, kv.second.mem);
+    for (auto& kv : groups) free_group(kv.second);
     groups.clear();
     for (auto& kv : kept_in) pool_free(ctx, kv.second);
     kept_in.clear();

@@ -14,6 +14,7 @@
 #include "../host/plan.hpp"
 #include "../kernels/attention.h"
 #include "../kernels/ops.h"
+#include "../kernels/optim.h"
 
 namespace cfb {
 
@@ -44,6 +45,15 @@ struct Ctx {
   // per-launch CUDA-event timing (cf_ctx_set_profiling)
   bool profile = false;
   std::vector<cudaEvent_t> event_pool;
+  // KV offload: host<->device copies of offloaded group state run here, and
+  // the pinned host blocks are cached across steps
+  cudaStream_t copy_stream = nullptr;
+  struct HostBlock {
+    void* ptr;
+    size_t bytes;
+    bool busy;
+  };
+  std::vector<HostBlock> host_blocks;
 };
 
 // One reference tensor (ToyModelParams::tensors order) and where it lives on
@@ -87,6 +97,16 @@ struct Model {
   void* wbuf = nullptr;   // all weights (bf16) + gains (fp32)
   float* grads = nullptr; // all gradients, flat fp32
   int64_t grad_numel = 0, wbytes = 0, num_params = 0;
+  // AdamW state (cf_model_adamw_init): fp32 master weights and both moments in
+  // the gradient buffer's layout, the storage-piece table the fused kernel
+  // walks, and the step counter t
+  std::vector<cfk::AdamPiece> pieces;
+  void* opt_mem = nullptr;
+  float *master = nullptr, *adam_m = nullptr, *adam_v = nullptr, *opt_scratch = nullptr, *clip_coef = nullptr;
+  double* grad_norm = nullptr;
+  cfk::AdamPiece* pieces_dev = nullptr;
+  int64_t* block_start_dev = nullptr;
+  int64_t opt_blocks = 0, opt_step = 0;
 };
 
 Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage = 0, int64_t stages = 1);
@@ -94,6 +114,11 @@ void model_destroy(Model* m);
 void model_get_param(Model* m, int64_t idx, double* host);
 void model_set_param(Model* m, int64_t idx, const double* host);
 void model_get_grad(Model* m, int64_t idx, double* host);
+// AdamW (cf_model_adamw_*): state init from the current weights, one fused
+// step over the flat gradient buffer, master-weight read-back.
+void model_adamw_init(Model* m);
+void model_adamw_step(Model* m, const cf_adamw_cfg& cfg, double* grad_norm);
+void model_get_master(Model* m, int64_t idx, double* host);
 
 struct Batch {
   const int64_t* ids;

@@ -220,6 +220,10 @@ def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allredu
            "static_gb_measured_16_layers_with_head": r.static_hbm_bytes / GB,
            "budget_gb": 170.0, "per_budget": {}}
     best = None
+    ch0 = replicas[0].export()[0]
+    tok0 = {int(c["chunk_id"]): float(c["total_tokens"]) for c in ch0}
+    per_tok = (np.mean([(v[0] * per_stage + v[1]) / tok0[c] for c, v in fw.items()]),
+               np.mean([(v[0] * per_stage + v[1]) / tok0[c] for c, v in bw.items()]))
     for budget in range(0, 5):
         worst, spans, stages_gb = 0.0, [], []
         for rp in replicas:
@@ -242,10 +246,10 @@ def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allredu
             b_ = np.array([bw.get(int(c["chunk_id"]), (0, 0))[0] * per_stage + bw.get(int(c["chunk_id"]), (0, 0))[1]
                            for c in ch])
             miss = f == 0
-            if miss.any():  # chunks only replica 1 has: cost by tokens
+            if miss.any():  # chunks only replica 1 has: replica 0's mean cost per token
                 tok = ch["total_tokens"].astype(np.float64)
-                f[miss] = (f[~miss] / tok[~miss]).mean() * tok[miss]
-                b_[miss] = (b_[~miss] / tok[~miss]).mean() * tok[miss]
+                f[miss] = per_tok[0] * tok[miss]
+                b_[miss] = per_tok[1] * tok[miss]
             _, _, _, pr = capi.pp_simulate(rp, STAGES, K, fwd_cost=f, bwd_cost=b_, tape_budget=budget)
             spans.append(pr.makespan)
         step_ms = max(spans) + allreduce_ms
