@@ -36,7 +36,9 @@ def test_offload_bitwise_equals_resident(ctx, case):
         assert r.recompute_loss_mismatches == 0 and r.kv_completeness_violations == 0
         assert r.recompute_forward_count == ref.recompute_forward_count
         assert np.array_equal(model.grads_flat(), g_ref)
-        assert r.kv_hbm_bytes < ref.kv_hbm_bytes
+        # two one-layer staging buffers instead of L layers (with L = 2 the
+        # staging IS the whole state, up to allocation rounding)
+        assert r.kv_hbm_bytes <= ref.kv_hbm_bytes * min(1.0, 2.0 / L) * 1.01
     model.close()
 
 
