@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_ready, 256);
+    mbar_init(q_ready, 8);  // arrivals count softmax warps
     for (int i = 0; i < KVS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 256);
+      mbar_init(&s_free[i], 8);
     }
-    mbar_init(p_full, 256);
+    mbar_init(p_full, 8);
     mbar_init(p_free, 1);
     fence_mbar_init();
   }
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tmem_st32(tQ + lane_off + half * 32, qw);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(q_ready);
+      warp_arrive(q_ready);
     }
     float m = -FLT_MAX, l = 0.f;
     for (int j = 0; j < nkt; ++j) {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(r[e]);
       }
       tc_fence_before();
-      mbar_arrive(&s_free[st]);
+      warp_arrive(&s_free[st]);
       const int key0 = j * TK + half * 64;
       // tiles entirely below the diagonal of every row of the CTA need no mask
       const bool full = j * TK + TK - 1 <= sg.prefix + tl.first;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tmem_st32(tP + lane_off + half * 32, pk);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(p_full);
+      warp_arrive(p_full);
     }
     // combine the two half-row sums
     const uint32_t red = smem_u32(sRed) + (nkt & 1) * 1024;
@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&v_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 128);
-    mbar_init(ds_full, 128);
+    mbar_init(s_free, 4);  // arrivals count softmax warps
+    mbar_init(ds_full, 4);
     mbar_init(ds_free, 1);
     fence_mbar_init();
   }
@@ -482,9 +482,9 @@ __global__ void __launch_bounds__(192, 1)
               make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
       tc_fence_before();
-      mbar_arrive(s_free);
+      warp_arrive(s_free);
       fence_async_smem();
-      mbar_arrive(ds_full);
+      warp_arrive(ds_full);
     }
     mbar_wait(ds_free, (nkt - 1) & 1);
     tc_fence_after();
@@ -562,8 +562,8 @@ __global__ void __launch_bounds__(192, 1)
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     mbar_init(s_full, 1);
-    mbar_init(s_free, 128);
-    mbar_init(pds_full, 128);
+    mbar_init(s_free, 4);
+    mbar_init(pds_full, 4);
     mbar_init(pds_free, 1);
     fence_mbar_init();
   }
@@ -674,9 +674,9 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(s_free);
+      warp_arrive(s_free);
       fence_async_smem();
-      mbar_arrive(pds_full);
+      warp_arrive(pds_full);
     }
     mbar_wait(pds_free, (iters - 1) & 1);
     tc_fence_after();

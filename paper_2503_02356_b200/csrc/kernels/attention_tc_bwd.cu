@@ -24,6 +24,9 @@ namespace {
 
 constexpr int DH = 128;
 constexpr int SUB = 64;                     // streamed sub-tile (keys for dQ, queries for dK/dV)
+#ifndef CF_BWD_DIAG  // diagnostics only: 1 = softmax math skipped, 2 = softmax side skipped
+#define CF_BWD_DIAG 0
+#endif
 #ifndef CF_DQ_KS
 #define CF_DQ_KS 4
 #endif
@@ -32,6 +35,20 @@ constexpr int SUB = 64;                     // streamed sub-tile (keys for dQ, q
 #endif
 #ifndef CF_DKV_QS
 #define CF_DKV_QS 3
+#endif
+// diagnostics 4 / 5: no operand loads / half of them (MMAs read stale smem)
+#if CF_BWD_DIAG == 4
+#define TMA_TX(x) 0u
+#define TMA_A(...) ((void)0)
+#define TMA_B(...) ((void)0)
+#elif CF_BWD_DIAG == 5
+#define TMA_TX(x) ((x) / 2)
+#define TMA_A(...) tma_load_2d(__VA_ARGS__)
+#define TMA_B(...) ((void)0)
+#else
+#define TMA_TX(x) (x)
+#define TMA_A(...) tma_load_2d(__VA_ARGS__)
+#define TMA_B(...) tma_load_2d(__VA_ARGS__)
 #endif
 constexpr int KS = CF_DQ_KS, VS = CF_DQ_VS;  // dQ kernel: K / V ring depths
 constexpr int QS = CF_DKV_QS;                // dK/dV kernel: Q/dO ring depth
@@ -226,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch(&tmO);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
-    mbar_init(q_full, 256);  // softmax threads staging Q / dO into TMEM
+    mbar_init(q_full, 8);  // softmax warps staging Q / dO into TMEM
     for (int i = 0; i < KS; ++i) {
       mbar_init(&k_full[i], 1);
       mbar_init(&k_empty[i], 1);
@@ -237,8 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 256);
-      mbar_init(&ds_full[i], 256);
+      mbar_init(&s_free[i], 8);   // one arrive per softmax warp
+      mbar_init(&ds_full[i], 8);
       mbar_init(&ds_free[i], 1);
     }
     fence_mbar_init();
@@ -259,13 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sk = j % KS, sv = j % VS;
         const int krow = sg.kv_row0 + j * SUB;
         mbar_wait(&v_empty[sv], ((j / VS) & 1) ^ 1);
-        mbar_expect_tx(&v_full[sv], 2 * kBox64);
-        tma_load_2d(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
-        tma_load_2d(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
+        mbar_expect_tx(&v_full[sv], TMA_TX(2 * kBox64));
+        TMA_A(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
+        TMA_B(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
         mbar_wait(&k_empty[sk], ((j / KS) & 1) ^ 1);
-        mbar_expect_tx(&k_full[sk], 2 * kBox64);
-        tma_load_2d(sK + sk * 2 * kBox64, &tmK, &k_full[sk], g * DH, krow);
-        tma_load_2d(sK + sk * 2 * kBox64 + kBox64, &tmK, &k_full[sk], g * DH + 64, krow);
+        mbar_expect_tx(&k_full[sk], TMA_TX(2 * kBox64));
+        TMA_A(sK + sk * 2 * kBox64, &tmK, &k_full[sk], g * DH, krow);
+        TMA_B(sK + sk * 2 * kBox64 + kBox64, &tmK, &k_full[sk], g * DH + 64, krow);
       }
     }
   } else if (warp == 9) {
@@ -285,12 +302,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_s(bSr + b * 8, ((j >> 1) & 1) ^ 1);
       tc_fence_after();
       const uint32_t k0 = sK0 + ik * 2 * kBox64, v0 = sV0 + iv * 2 * kBox64;
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks)
-        umma_bf16_ts_w(tmem + b * 64, tAq + ks * 8, kdesc(k0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks)
-        umma_bf16_ts_w(tmem + 128 + b * 64, tAo + ks * 8, kdesc(v0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+      // K = dh in two 4-MMA chains (one 64-column box each): A columns step 8,
+      // B descriptors step 32 bytes inside a box
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq, kdesc(k0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq + 32, kdesc(k0, kBox64, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo, kdesc(v0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo + 32, kdesc(v0, kBox64, 4), idS, 1u);
       umma_commit_w(bVe + iv * 8);
       umma_commit_w(bSf + b * 8);
       if (++ik == KS) { ik = 0; pk ^= 1; }
@@ -305,9 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait_s(bDf + b * 8, (j >> 1) & 1);
       tc_fence_after();
       const uint32_t s0 = sS0 + b * kBox128, k0 = sK0 + ck * 2 * kBox64;
-#pragma unroll
-      for (int ks = 0; ks < SUB / 16; ++ks)
-        umma_bf16_w(tQ, kdesc(s0, kBox128, ks), mndesc(k0, kBox64, ks), idQ, (j > 0 || ks > 0) ? 1u : 0u);
+#if CF_BWD_DIAG < 3
+      umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 0), mndesc(k0, kBox64, 0), idQ, j > 0 ? 1u : 0u);
+#endif
       umma_commit_w(bKe + ck * 8);
       umma_commit_w(bDr + b * 8);
       if (++ck == KS) ck = 0;
@@ -330,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           a.o + r * a.o_stride + static_cast<int64_t>(h) * DH + half * 64);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(q_full);
+      warp_arrive(q_full);
       // D = rowsum(dO * O): the two half-rows meet in smem (fixed order)
       sRowD[half * 128 + row] = dpart;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
@@ -348,12 +365,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t b = j & 1;
       mbar_wait_s(bSf + b * 8, (j >> 1) & 1);
       tc_fence_after();
+#if CF_BWD_DIAG >= 2
+      warp_arrive_s(bSr + b * 8);
+      if (j >= 2) mbar_wait_s(bDr + b * 8, ((j >> 1) & 1) ^ 1);
+      warp_arrive_s(bDf + b * 8);
+      continue;
+#endif
       uint32_t rs[32], rp[32];
       tmem_ld32(tmem + b * 64 + lane_off + half * 32, rs);
       tmem_ld32(tmem + 128 + b * 64 + lane_off + half * 32, rp);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive_s(bSr + b * 8);
+      warp_arrive_s(bSr + b * 8);
       uint32_t pk[16];
       // dS = P * (dP - D); P masked only on sub-tiles that cross the causal
       // diagonal or the end of the segment (two separately compiled bodies)
@@ -370,17 +393,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
         }
       };
+#if CF_BWD_DIAG == 1
+      for (int e = 0; e < 16; ++e) pk[e] = rs[e] ^ rp[e];
+#else
       if (j * SUB + SUB - 1 <= tile_lim)  // uniform: every row of the tile sees every key
         body(std::false_type{});
       else
         body(std::true_type{});
+#endif
       if (j >= 2) mbar_wait_s(bDr + b * 8, ((j >> 1) & 1) ^ 1);
       const uint32_t dst = sS0 + b * kBox128;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         sts128(dst + dst_off[c], make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
       fence_async_smem();
-      mbar_arrive_s(bDf + b * 8);
+      warp_arrive_s(bDf + b * 8);
     }
     const int last = nkt - 1;
     mbar_wait(&ds_free[last & 1], (last >> 1) & 1);
@@ -469,15 +496,15 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmO);
-    mbar_init(kv_full, 512);
+    mbar_init(kv_full, 16);  // one arrive per softmax-side warp
     for (int i = 0; i < QS; ++i) {
       mbar_init(&q_full[i], 2);  // TMA expect_tx arrive + LSE / D staged arrive
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(s_full, 1);
-    mbar_init(s_free, 512);
+    mbar_init(s_free, 16);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&pds_full[i], 512);
+      mbar_init(&pds_full[i], 16);
       mbar_init(&pds_free[i], 1);
     }
     fence_mbar_init();
@@ -506,13 +533,13 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const int qrow = sg.q_start + qt0;
       mbar_wait_s(bQe + qs * 8, ph ^ 1);
       if (lane == 0) {
-        mbar_expect_tx(&q_full[qs], 4 * kBox64);
+        mbar_expect_tx(&q_full[qs], TMA_TX(4 * kBox64));
         uint8_t* q = sQ + qs * 2 * kBox64;
         uint8_t* o = sdO + qs * 2 * kBox64;
-        tma_load_2d(q, &tmQ, &q_full[qs], hq * DH, qrow);
-        tma_load_2d(q + kBox64, &tmQ, &q_full[qs], hq * DH + 64, qrow);
-        tma_load_2d(o, &tmO, &q_full[qs], hq * DH, qrow);
-        tma_load_2d(o + kBox64, &tmO, &q_full[qs], hq * DH + 64, qrow);
+        TMA_A(q, &tmQ, &q_full[qs], hq * DH, qrow);
+        TMA_B(q + kBox64, &tmQ, &q_full[qs], hq * DH + 64, qrow);
+        TMA_A(o, &tmO, &q_full[qs], hq * DH, qrow);
+        TMA_B(o + kBox64, &tmO, &q_full[qs], hq * DH + 64, qrow);
       }
       const int64_t base = static_cast<int64_t>(hq) * a.T + qrow;
 #pragma unroll
@@ -538,12 +565,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       mbar_wait_s(bSr, (it & 1) ^ 1);
       tc_fence_after();
       const uint32_t q0 = sQ0 + is * 2 * kBox64, o0 = sO0 + is * 2 * kBox64;
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks)
-        umma_bf16_ts_w(tS, tAk + ks * 8, kdesc(q0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
-#pragma unroll
-      for (int ks = 0; ks < DH / 16; ++ks)
-        umma_bf16_ts_w(tP, tAv + ks * 8, kdesc(o0, kBox64, ks), idS, ks > 0 ? 1u : 0u);
+      umma4_ts_w<8, 2>(tS, tAk, kdesc(q0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tS, tAk + 32, kdesc(q0, kBox64, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tP, tAv, kdesc(o0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tP, tAv + 32, kdesc(o0, kBox64, 4), idS, 1u);
       umma_commit_w(bSf);
       if (++is == QS) { is = 0; ps ^= 1; }
     };
@@ -557,12 +582,10 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       tc_fence_after();
       const uint32_t q0 = sQ0 + cs * 2 * kBox64, o0 = sO0 + cs * 2 * kBox64;
       const uint32_t p0 = sP0 + b * kBox128, s0 = sS0 + b * kBox128;
-#pragma unroll
-      for (int ks = 0; ks < SUB / 16; ++ks)
-        umma_bf16_w(tdV, kdesc(p0, kBox128, ks), mndesc(o0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
-#pragma unroll
-      for (int ks = 0; ks < SUB / 16; ++ks)
-        umma_bf16_w(tdK, kdesc(s0, kBox128, ks), mndesc(q0, kBox64, ks), idG, (it > 0 || ks > 0) ? 1u : 0u);
+#if CF_BWD_DIAG < 3
+      umma4_ss_w<2, 128>(tdV, kdesc(p0, kBox128, 0), mndesc(o0, kBox64, 0), idG, it > 0 ? 1u : 0u);
+      umma4_ss_w<2, 128>(tdK, kdesc(s0, kBox128, 0), mndesc(q0, kBox64, 0), idG, it > 0 ? 1u : 0u);
+#endif
       umma_commit_w(bQe + cs * 8);
       umma_commit_w(bPr + b * 8);
       if (++cs == QS) cs = 0;
@@ -581,7 +604,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
                        kok);
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(kv_full);
+      warp_arrive(kv_full);
     }
     // query index range this key row sees: [qlo, len) (qlo = INT_MAX: row absent)
     const int qlo = kok ? key - sg.prefix : INT_MAX;
@@ -595,12 +618,20 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const int qt0 = i0 + qi * SUB;
       mbar_wait_s(bSf, it & 1);
       tc_fence_after();
+#if CF_BWD_DIAG >= 2
+      warp_arrive_s(bSr);
+      if (it >= 2) mbar_wait_s(bPr + b * 8, ((it >> 1) & 1) ^ 1);
+      warp_arrive_s(bPf + b * 8);
+      if (++qi == nqt) qi = 0;
+      if (++qs == QS) { qs = 0; qph ^= 1; }
+      continue;
+#endif
       uint32_t rs[16], rp[16];
       tmem_ld16(tS + lane_off + part * 16, rs);
       tmem_ld16(tP + lane_off + part * 16, rp);
       tmem_ld_wait();
       tc_fence_before();
-      mbar_arrive_s(bSr);
+      warp_arrive_s(bSr);
       mbar_wait_s(bQf + qs * 8, qph);  // LSE / D of this slot (already complete: S^T waited on it)
       const uint32_t lrow = sLD0 + qs * 512 + part * 64;
       uint32_t pp[8], pd[8];
@@ -629,10 +660,14 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         }
       };
       // uniform: every key of the tile sees every query of the sub-tile
+#if CF_BWD_DIAG == 1
+      for (int e = 0; e < 8; ++e) { pp[e] = rs[e] ^ rp[e]; pd[e] = rs[e + 8] ^ rp[e + 8]; }
+#else
       if (key_first + 127 < kv_len && key_first + 127 <= sg.prefix + qt0 && qt0 + SUB <= sg.len)
         body(std::false_type{});
       else
         body(std::true_type{});
+#endif
       if (it >= 2) mbar_wait_s(bPr + b * 8, ((it >> 1) & 1) ^ 1);
       const uint32_t dP_ = sP0 + b * kBox128, dS_ = sS0 + b * kBox128;
 #pragma unroll
@@ -641,7 +676,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         sts128(dS_ + dst_off[c], make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
       }
       fence_async_smem();
-      mbar_arrive_s(bPf + b * 8);
+      warp_arrive_s(bPf + b * 8);
       if (++qi == nqt) qi = 0;
       if (++qs == QS) { qs = 0; qph ^= 1; }
     }

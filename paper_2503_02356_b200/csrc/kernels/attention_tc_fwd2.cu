@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&s_full[w], 1);
-      mbar_init(&p_full[w], 256);
+      mbar_init(&p_full[w], 8);  // one arrive per softmax warp of the head
       mbar_init(&o_done[w], 1);
     }
     fence_mbar_init();
@@ -146,48 +146,49 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 17) {
-    if (lane == 0) {
-      constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
-      const uint32_t q0 = smem_u32(sQ);
-      auto issue_s = [&](int w, int j) {
-        const uint32_t k0 = smem_u32(sK + (j % KS) * kTile);
-        const uint32_t qw = q0 + w * kTile;
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks)
-          umma_bf16(tmem + 256 * w, kdesc(qw, ks), kdesc(k0, ks), idS, ks > 0 ? 1u : 0u);
-        umma_commit(&s_full[w]);
-      };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      umma_commit(&k_empty[0]);
-      for (int j = 0; j < nkt; ++j) {
-        const int sv = j % VS;
-        const bool more = j + 1 < nkt;
-        const int sk = (j + 1) % KS;
-        const uint32_t v0 = smem_u32(sV + sv * kTile);
-        for (int w = 0; w < 2; ++w) {
-          mbar_wait(&p_full[w], j & 1);
-          if (w == 0) mbar_wait(&v_full[sv], (j / VS) & 1);
-          tc_fence_after();
-          const uint32_t tS = tmem + 256 * w, tO = tS + 128;
-#pragma unroll
-          for (int ks = 0; ks < TK / 16; ++ks)
-            umma_bf16_ts(tO, tS + ks * 8, mndesc(v0, ks), idO, (j > 0 || ks > 0) ? 1u : 0u);
-          if (w == 1) umma_commit(&v_empty[sv]);
-          if (more) {
-            if (w == 0) {
-              mbar_wait(&k_full[sk], ((j + 1) / KS) & 1);
-              tc_fence_after();
-            }
-            issue_s(w, j + 1);
-            if (w == 1) umma_commit(&k_empty[sk]);
-          } else {
-            umma_commit(&o_done[w]);
+    // whole warp, convergent (elect.sync inside the issue helpers)
+    constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idO = umma_idesc_bf16(128, 128, 0, 1);
+    const uint32_t q0 = smem_u32(sQ);
+    const uint32_t bSf = smem_u32(s_full), bPf = smem_u32(p_full), bKf = smem_u32(k_full), bKe = smem_u32(k_empty),
+                   bVf = smem_u32(v_full), bVe = smem_u32(v_empty), bOd = smem_u32(o_done);
+    // S_w = Q_w K_j^T: K = dh in two 4-MMA chains (one 64-column box each)
+    auto issue_s = [&](int w, int j) {
+      const uint32_t k0 = smem_u32(sK + (j % KS) * kTile);
+      const uint32_t qw = q0 + w * kTile;
+      umma4_ss_w<2, 2>(tmem + 256 * w, kdesc(qw, 0), kdesc(k0, 0), idS, 0u);
+      umma4_ss_w<2, 2>(tmem + 256 * w, kdesc(qw, 4), kdesc(k0, 4), idS, 1u);
+      umma_commit_w(bSf + w * 8);
+    };
+    mbar_wait(q_full, 0);
+    mbar_wait_s(bKf, 0);
+    tc_fence_after();
+    issue_s(0, 0);
+    issue_s(1, 0);
+    umma_commit_w(bKe);
+    for (int j = 0; j < nkt; ++j) {
+      const int sv = j % VS;
+      const bool more = j + 1 < nkt;
+      const int sk = (j + 1) % KS;
+      const uint32_t v0 = smem_u32(sV + sv * kTile);
+      for (int w = 0; w < 2; ++w) {
+        mbar_wait_s(bPf + w * 8, j & 1);
+        if (w == 0) mbar_wait_s(bVf + sv * 8, (j / VS) & 1);
+        tc_fence_after();
+        const uint32_t tS = tmem + 256 * w, tO = tS + 128;
+        // O_w += P_w V_j (P in TMEM over S_w), K = 128 keys in two chains
+        umma4_ts_w<8, 128>(tO, tS, mndesc(v0, 0), idO, j > 0 ? 1u : 0u);
+        umma4_ts_w<8, 128>(tO, tS + 32, mndesc(v0, 4), idO, 1u);
+        if (w == 1) umma_commit_w(bVe + sv * 8);
+        if (more) {
+          if (w == 0) {
+            mbar_wait_s(bKf + sk * 8, ((j + 1) / KS) & 1);
+            tc_fence_after();
           }
+          issue_s(w, j + 1);
+          if (w == 1) umma_commit_w(bKe + sk * 8);
+        } else {
+          umma_commit_w(bOd + w * 8);
         }
       }
     }
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&p_full[w]);
+      warp_arrive(&p_full[w]);
     }
     // combine the half-row sums (the pair re-syncs before the buffer is reused)
     sts_f32(red + (nkt & 1) * 1024 + (half * 128 + row) * 4, l);

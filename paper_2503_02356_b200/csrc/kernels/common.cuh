@@ -151,6 +151,45 @@ __device__ __forceinline__ void umma_commit_w(uint32_t bar_saddr) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar_saddr)
       : "memory");
 }
+// Four MMAs of one K-chain in a single elect.sync block: operand k uses
+// A + k*AS and B + k*BS (descriptor units of 16 bytes / TMEM columns), the
+// first accumulates per `acc`, the rest always.  Attention tiles issue many
+// short MMAs (M128 N64 K16 = 32 tensor cycles), so the per-MMA issue cost of
+// the one-at-a-time helpers (elect + uniform broadcasts, ~15 instructions)
+// would otherwise pace the tensor pipe.
+template <int AS, int BS>
+__device__ __forceinline__ void umma4_ts_w(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, %2, %6;\n\tadd.s64 b3, %2, %7;\n\t"
+      "add.u32 a1, %1, %8;\n\tadd.u32 a2, %1, %9;\n\tadd.u32 a3, %1, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%11, %11, %11, %11}, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, {%11, %11, %11, %11}, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, {%11, %11, %11, %11}, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, {%11, %11, %11, %11}, t;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc), "n"(BS), "n"(2 * BS), "n"(3 * BS), "n"(AS), "n"(2 * AS), "n"(3 * AS),
+      "r"(0u)
+      : "memory");
+}
+template <int AS, int BS>
+__device__ __forceinline__ void umma4_ss_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, %2, %6;\n\tadd.s64 b3, %2, %7;\n\t"
+      "add.s64 a1, %1, %8;\n\tadd.s64 a2, %1, %9;\n\tadd.s64 a3, %1, %10;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, t;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "n"(BS), "n"(2 * BS), "n"(3 * BS), "n"(AS), "n"(2 * AS), "n"(3 * AS)
+      : "memory");
+}
 // mbarrier wait on a shared-window address (no generic->shared conversion
 // in the loop).
 __device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t parity) {
@@ -168,6 +207,17 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive_s(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+// One arrive per warp (the barrier counts warps, not threads): many threads
+// arriving on one mbarrier serialise like same-address shared atomics (~32
+// cycles per warp-wide arrive), which sat on the attention kernels' MMA <->
+// softmax round trip.  Every lane's prior work (tcgen05.wait::ld / ::st +
+// fence::before_thread_sync, or smem stores + fence.proxy.async) is ordered
+// before the single arrive by the warp barrier.
+__device__ __forceinline__ void warp_arrive_s(uint32_t a) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_s(a);
+}
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) { warp_arrive_s(smem_u32(bar)); }
 // 1-D tiled TMA (box of `box` elements starting at element c0; out-of-range
 // elements are zero-filled).
 __device__ __forceinline__ void tma_load_1d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int32_t c0) {

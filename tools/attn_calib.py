@@ -52,6 +52,10 @@ tb = timeit(lambda: ours(1, True))
 print(f"ours   T={T}: fwd {tf*1e3:7.2f} ms {fl_f/tf/1e12:7.1f} TF | bwd {tb*1e3:7.2f} ms {fl_b/tb/1e12:7.1f} TF "
       f"(algorithmic 4/8*H*dh per pair)", flush=True)
 
+import os  # noqa: E402
+
+if os.environ.get("NO_SDPA"):
+    sys.exit(0)
 qs = q.view(1, T, H, dh).transpose(1, 2).contiguous().requires_grad_()
 ks = k.view(1, T, KVH, dh).transpose(1, 2).contiguous().requires_grad_()
 vs = v.view(1, T, KVH, dh).transpose(1, 2).contiguous().requires_grad_()
