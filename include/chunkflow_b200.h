@@ -571,6 +571,11 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q,
  * tcgen05.mma.cta_group::2 kernel for large GEMMs), 1 = single-CTA kernel
  * only, 2 = CTA pairs whenever M, N > 128. */
 int cf_debug_set_gemm_mode(int mode);
+/* Attention-backward synchronisation stress (testing): nonzero inserts
+ * pseudo-random 0-2 us delays at every mbarrier hand-off of the tcgen05
+ * dQ and dK/dV kernels (producer, MMA issuer, softmax warps); the results
+ * must not change. */
+int cf_debug_set_attn_stress(int on);
 int cf_op_gemm(cf_ctx* ctx, const void* a, int a_kmajor, int64_t lda,
                const void* b, int b_kmajor, int64_t ldb, void* c, int64_t ldc,
                int64_t m, int64_t n, int64_t k, int epi, const void* residual,

@@ -103,7 +103,7 @@ EXPORTS = [
     "cf_step_destroy", "cf_backward_full", "cf_model_create_stage", "cf_ctx_init_pp", "cf_pp_step_run",
     "cf_pp_run_local", "cf_step_op_times", "cf_step_input_bytes", "cf_pp_local_create", "cf_pp_local_destroy", "cf_ctx_init_pp_local", "cf_plan_chunk_json", "cf_plan_exec_json", "cf_plan_from_chunk_json",
     "cf_dataset_load_jsonl", "cf_dataset_write_jsonl", "cf_mem_calibrate", "cf_mem_predict", "cf_mem_parse_csv",
-    "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode",
+    "cf_mem_coeffs_json", "cf_pp_export_trace", "cf_tune_grid_search", "cf_ctx_synchronize", "cf_op_gemm", "cf_op_attention", "cf_debug_set_gemm_mode", "cf_debug_set_attn_stress",
     "cf_segment_forward", "cf_segment_backward", "cf_segment_destroy", "cf_op_gemm_rope",
     "cf_plan_validate_events", "cf_op_lm_head_ce", "cf_pp_stage_memory", "cf_tune_grid_search_pp",
     "cf_pp_simulate_budget", "cf_model_adamw_init", "cf_model_adamw_step", "cf_model_get_master",

@@ -533,6 +533,10 @@ int cf_op_gemm_rope(cf_ctx* ctx, const void* a, int64_t lda, const void* w, int6
 
 }  // extern "C"
 
+extern "C" int cf_debug_set_attn_stress(int on) {
+  return cfb::guard([&] { cfk::set_attn_stress(on); });
+}
+
 extern "C" int cf_debug_set_gemm_mode(int mode) {
   return cfb::guard([&] {
     if (mode < 0 || mode > 2) throw cfb::ValidationError("gemm mode must be 0, 1 or 2");

@@ -23,6 +23,9 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
 // kept selectable at operator level (cf_op_attention impl 2) for A/B tests.
 cudaError_t attn_backward_tc_v1(const AttnParams& p, const AttnTile* qtiles128, int32_t nq,
                                 const AttnTile* ktiles128, int32_t nk, int64_t kv_rows, cudaStream_t st);
+// Testing: pseudo-random delays in every warp role of the pipelined
+// backward kernels (cf_debug_set_attn_stress).
+void set_attn_stress(int on);
 // D = rowsum(dO * O) (shared with the warp-MMA path, attention.cu)
 cudaError_t attn_dsum(const AttnParams& p, cudaStream_t st);
 

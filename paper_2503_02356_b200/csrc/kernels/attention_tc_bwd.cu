@@ -81,7 +81,19 @@ struct Args {
   const float2* rope_tab;   // RoPE backward on dQ (and dK with dkv_out)
   __nv_bfloat16* dkv_out;   // direct bf16 dK / dV (standalone chunks)
   int64_t dkv_out_ld, col_k, col_v;
+  int32_t stress;  // cf_debug_set_attn_stress: pseudo-random delays in every warp role
 };
+
+// Synchronisation stress (testing): a pseudo-random 0-2 us sleep keyed on
+// (site, iteration, CTA, warp) so producer, MMA issuer and softmax warps
+// reach every mbarrier in perturbed orders; results must stay bitwise equal.
+__device__ __forceinline__ void stress_delay(int32_t on, uint32_t site, uint32_t it) {
+  if (on) {
+    const uint32_t h = (site * 0x9E3779B1u) ^ (it * 0x85EBCA77u) ^ (blockIdx.x * 0xC2B2AE3Du) ^
+                       (blockIdx.y * 0x27D4EB2Fu) ^ ((threadIdx.x >> 5) * 0x165667B1u);
+    __nanosleep((h >> 21) & 2047u);
+  }
+}
 
 // Inverse rotate-half of 32 (a, b) pairs (a = columns c0.., b = c0+64..)
 // with (cos, sin) pairs tab[c0 .. c0+32): the RoPE backward rope_qk applies.
@@ -275,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nkt; ++j) {
         const int sk = j % KS, sv = j % VS;
         const int krow = sg.kv_row0 + j * SUB;
+        stress_delay(a.stress, 1, j);
         mbar_wait(&v_empty[sv], ((j / VS) & 1) ^ 1);
         mbar_expect_tx(&v_full[sv], TMA_TX(2 * kBox64));
         TMA_A(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
@@ -317,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     issue_s(0);
     for (int j = 0; j < nkt; ++j) {
+      stress_delay(a.stress, 2, j);
       if (j + 1 < nkt) issue_s(j + 1);
       const uint32_t b = j & 1;
       mbar_wait_s(bDf + b * 8, (j >> 1) & 1);
@@ -401,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       else
         body(std::true_type{});
 #endif
+      stress_delay(a.stress, 3, j);
       if (j >= 2) mbar_wait_s(bDr + b * 8, ((j >> 1) & 1) ^ 1);
       const uint32_t dst = sS0 + b * kBox128;
 #pragma unroll
@@ -461,8 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // CTA = 128 keys x one kv head (sole owner of those rows); queries streamed
 // in 64-query sub-tiles over every q head of the GQA group.
 __global__ void __launch_bounds__(kDkvThreads, 1)
-    dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
-               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+    dkv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // K and V (per-CTA invariant A operands of S^T and dP^T) live in TMEM;
@@ -531,6 +545,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const int hq = g * per + hi;
       const int qt0 = i0 + qi * SUB;
       const int qrow = sg.q_start + qt0;
+      stress_delay(a.stress, 4, it);
       mbar_wait_s(bQe + qs * 8, ph ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&q_full[qs], TMA_TX(4 * kBox64));
@@ -576,6 +591,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     tc_fence_after();
     issue_s(0);
     for (int it = 0; it < iters; ++it) {
+      stress_delay(a.stress, 5, it);
       if (it + 1 < iters) issue_s(it + 1);
       const uint32_t b = it & 1;
       mbar_wait_s(bPf + b * 8, (it >> 1) & 1);
@@ -632,6 +648,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       warp_arrive_s(bSr);
+      stress_delay(a.stress, 6, it);
       mbar_wait_s(bQf + qs * 8, qph);  // LSE / D of this slot (already complete: S^T waited on it)
       const uint32_t lrow = sLD0 + qs * 512 + part * 64;
       uint32_t pp[8], pd[8];
@@ -647,11 +664,15 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           for (int u = 0; u < 4; ++u) {
             const int col = c4 * 4 + u;
             p[u] = ex2(fmaf(__uint_as_float(rs[col]), a.sl2, -l[u]));
-            if constexpr (decltype(masked)::value) {
-              const int qq = qt0 + part * 16 + col;
-              p[u] = (qq >= qlo && qq < sg.len) ? p[u] : 0.f;
-            }
             ds[u] = p[u] * (__uint_as_float(rp[col]) - d[u]);
+            if constexpr (decltype(masked)::value) {
+              // masked entries are selected away (never multiplied), so
+              // whatever LSE / D a slot holds past the segment cannot leak
+              const int qq = qt0 + part * 16 + col;
+              const bool in = qq >= qlo && qq < sg.len;
+              p[u] = in ? p[u] : 0.f;
+              ds[u] = in ? ds[u] : 0.f;
+            }
           }
           pp[2 * c4] = pack_bf16(p[0], p[1]);
           pp[2 * c4 + 1] = pack_bf16(p[2], p[3]);
@@ -668,6 +689,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       else
         body(std::true_type{});
 #endif
+      stress_delay(a.stress, 7, it);
       if (it >= 2) mbar_wait_s(bPr + b * 8, ((it >> 1) & 1) ^ 1);
       const uint32_t dP_ = sP0 + b * kBox128, dS_ = sS0 + b * kBox128;
 #pragma unroll
@@ -768,19 +790,21 @@ bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uin
 
 }  // namespace
 
+int g_attn_stress = 0;
+void set_attn_stress(int on) { g_attn_stress = on ? 1 : 0; }
+
 cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int32_t nq, const AttnTile* ktiles128,
                              int32_t nk, int64_t kv_rows, cudaStream_t st) {
   if (nq == 0) return cudaSuccess;
   const uint64_t qc = static_cast<uint64_t>(p.H) * DH, kc = static_cast<uint64_t>(p.KVH) * DH;
-  CUtensorMap q128, o128, k64, v64, q64, o64, k128, v128;
+  CUtensorMap q128, o128, k64, v64, q64, o64;
   if (!map_rows(&q128, p.q, qc, p.T, p.q_stride, 128) || !map_rows(&o128, p.dout, qc, p.T, p.dout_stride, 128) ||
       !map_rows(&k64, p.k, kc, kv_rows, p.kv_stride, 64) || !map_rows(&v64, p.v, kc, kv_rows, p.kv_stride, 64) ||
-      !map_rows(&q64, p.q, qc, p.T, p.q_stride, 64) || !map_rows(&o64, p.dout, qc, p.T, p.dout_stride, 64) ||
-      !map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
+      !map_rows(&q64, p.q, qc, p.T, p.q_stride, 64) || !map_rows(&o64, p.dout, qc, p.T, p.dout_stride, 64))
     return cudaErrorInvalidValue;
   Args a{p.segs, qtiles128, p.q, p.q_stride, p.dout, p.dout_stride, p.k, p.v, p.kv_stride, p.lse, p.dsum, p.o,
          p.o_stride, p.dq, p.dq_stride, p.dk_acc, p.dv_acc, p.acc_stride, p.T, p.H, p.KVH, p.scale * kLog2e,
-         p.scale, p.rope_tab, p.dkv_out, p.dkv_out_ld, p.col_k, p.col_v};
+         p.scale, p.rope_tab, p.dkv_out, p.dkv_out_ld, p.col_k, p.col_v, g_attn_stress};
   const size_t smem_dq = 1024 + (KS + VS) * 2 * kBox64 + 2 * kBox128 + 256 * 4 + 256;
   const size_t smem_dkv = 1024 + QS * 2 * 2 * kBox64 + 4 * kBox128 + QS * 512 + 256;
   // per (kernel, device), thread-safe
@@ -791,7 +815,7 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
   dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   a.tiles = ktiles128;
-  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, k128, v128, a);
+  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, a);
   return cudaGetLastError();
 }
 

@@ -48,6 +48,7 @@ struct Args {
   const void* R;  // fp32 residual (EPI_F32_RES) or bf16 aux (EPI_BF16_TANHGRAD)
   int64_t ldr;
   int group_m;  // raster: tiles walk group_m M-blocks x all N-blocks, M fastest
+  int serp;     // CTA-pair kernel: odd waves walk K backwards (see gemm_pair_kernel)
   int split_n;  // EPI_BF16_SWIGLU: F (the up half starts at column F)
   int col_k, col_v;  // EPI_BF16_ROPE
   __nv_bfloat16* kc;
@@ -587,13 +588,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t full_leader0 = leader_addr(smem_u32(&full[0]));
-      for (int tile = pair; tile < num_tiles; tile += npairs) {
+      // Serpentine K: consecutive waves of the grouped raster share their
+      // M-operand panels, but with long K a panel's head is evicted from L2
+      // before the next wave needs it.  Odd waves stream K from the end, so
+      // they start on the panel tail the previous wave just read.  Only the
+      // load order changes (the MMA warp consumes stages in order; the fp32
+      // summation order of a tile is fixed by its wave, so results stay
+      // deterministic).
+      int wave = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++wave) {
         int mb, nb;
         tile_coords(g, tile, mb, nb);
+        const bool rev = g.serp && (wave & 1);
         const int m0 = mb * 256 + static_cast<int>(rank) * 128;
         const int n0 = EPI == EPI_BF16_SWIGLU ? (rank == 0 ? nb * 128 : g.split_n + nb * 128)
                                               : nb * 256 + static_cast<int>(rank) * 128;
-        for (int kb = 0; kb < g.num_k; ++kb) {
+        for (int kq = 0; kq < g.num_k; ++kq) {
+          const int kb = rev ? g.num_k - 1 - kq : kq;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * kABytes;
           uint8_t* b = sB + stage * kBBytes;
@@ -796,6 +807,15 @@ bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, u
 
 int g_num_sms = 0;
 
+// CF_GEMM_SERP=0 turns the serpentine K order off (A/B traffic measurement)
+int gemm_serpentine() {
+  static const int v = [] {
+    const char* e = std::getenv("CF_GEMM_SERP");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 void set_ce(Args& g, const GemmDesc& d) {
   g.ce_tgt = d.ce_tgt;
   g.ce_part = reinterpret_cast<float2*>(d.ce_part);
@@ -823,7 +843,7 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   bool ok = A_MN ? make_map(&ta, d.a, d.M, d.K, d.lda, 64, 64) : make_map(&ta, d.a, d.K, d.M, d.lda, BK, BM);
   ok = ok && (B_MN ? make_map(&tb, d.b, d.N, d.K, d.ldb, 64, 64) : make_map(&tb, d.b, d.K, d.N, d.ldb, BK, BN));
   if (!ok) return cudaErrorInvalidValue;
-  Args g;
+  Args g{};
   g.M = static_cast<int>(d.M);
   g.N = static_cast<int>(d.N);
   g.K = static_cast<int>(d.K);
@@ -857,7 +877,7 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   bool ok = A_MN ? make_map(&ta, d.a, d.M, d.K, d.lda, 64, 64) : make_map(&ta, d.a, d.K, d.M, d.lda, BK, 128);
   ok = ok && (B_MN ? make_map(&tb, d.b, d.N, d.K, d.ldb, 64, 64) : make_map(&tb, d.b, d.K, d.N, d.ldb, BK, 128));
   if (!ok) return cudaErrorInvalidValue;
-  Args g;
+  Args g{};
   g.M = static_cast<int>(d.M);
   g.N = static_cast<int>(d.N);
   g.K = static_cast<int>(d.K);
@@ -869,6 +889,11 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   // vs 1.6-2.2 at 8, tools/gemm_group_traffic.sh); long-K shapes prefer 8.
   g.group_m = raster_group(g.num_m, g.num_k <= 64 && g.num_n >= 24 ? 16 : 8);
   g.split_n = static_cast<int>(d.N / 2);
+  // long-K shapes only (K > 4096: the dgrad / wgrad / down-projection GEMMs
+  // whose panels outgrow L2 within a wave); short-K shapes measured neutral
+  // to slightly worse, and keeping them in order keeps EPI_BF16 and
+  // EPI_BF16_SWIGLU outputs bitwise identical for the same operands
+  g.serp = gemm_serpentine() && g.num_k > 64;
   g.col_k = static_cast<int>(d.col_k);
   g.col_v = static_cast<int>(d.col_v);
   g.kc = static_cast<__nv_bfloat16*>(d.kc);

@@ -10,9 +10,11 @@ T, d, kvw, ffn, V = 8192, 4096, 1024, 11008, 32000
 BF16, F32, ACC, RES, SWIGLU = "bf16", "f32", "f32_acc", "f32_res", "bf16_swiglu"
 FWD = [("qkv fwd +rope", T, d + 2 * kvw, d, BF16), ("o fwd +res", T, d, d, RES), ("gate|up fwd", T, 2 * ffn, d, SWIGLU),
        ("down fwd +res", T, d, ffn, RES)] * 2
-BWD = [("head wgrad", d, V, T, ACC), ("head dgrad", T, d, V, F32), ("down dgrad", T, ffn, d, BF16),
-       ("down wgrad", ffn, d, T, ACC), ("gate|up wgrad", d, 2 * ffn, T, ACC), ("gate|up dgrad", T, d, 2 * ffn, F32),
-       ("o dgrad", T, d, d, BF16), ("o wgrad", d, d, T, ACC)]
+# the backward starts with the fused-CE head: dlogits rebuilt from the LSE by
+# a recompute of the head GEMM (EPI_CE_GRAD, bf16 out), then head wgrad/dgrad
+BWD = [("head ce-grad", T, V, d, BF16), ("head wgrad", d, V, T, ACC), ("head dgrad", T, d, V, F32),
+       ("down dgrad", T, ffn, d, BF16), ("down wgrad", ffn, d, T, ACC), ("gate|up wgrad", d, 2 * ffn, T, ACC),
+       ("gate|up dgrad", T, d, 2 * ffn, F32), ("o dgrad", T, d, d, BF16)]
 
 
 def algorithmic(M, N, K, epi):
