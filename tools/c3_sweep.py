@@ -18,22 +18,26 @@ MODEL = dict(vocab=32000, d=4096, heads=32, kv_heads=8, layers=32, ffn=11008, se
 ctx = cf.Context(0)
 model = cf.Model(ctx, cf.model_cfg(arch=cf.ARCH_LLAMA, **MODEL))
 short = cf.capi.synthesize(999, 1, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
-sizes = [int(x) for x in sys.argv[1:]] or [16384, 32768, 65536, 131072]
+# --offload: dependent groups keep their KV state in pinned host memory
+# (cf_run_opts.kv_offload), so the one term that grows with the sequence
+# leaves HBM too
+offload = "--offload" in sys.argv
+sizes = [int(x) for x in sys.argv[1:] if not x.startswith("--")] or [16384, 32768, 65536, 131072]
 for L in sizes:
     lengths = np.concatenate([short, [L]]).astype(np.int64)
     tokens = cf.gen_tokens(lengths, MODEL["vocab"], 1)
     plan = cf.Plan.build(lengths, 8192, 2)
     step = cf.Step(model, plan, lengths, tokens)
-    step.run()  # warm-up
+    step.run(kv_offload=offload)  # warm-up
     ctx.synchronize()
     t0 = time.perf_counter()
-    r = step.run()
+    r = step.run(kv_offload=offload)
     ctx.synchronize()
     dt = time.perf_counter() - t0
     free, total = torch.cuda.mem_get_info()
     nc, _, ne, _ = plan.counts()
     print(json.dumps({
-        "max_seq": L, "chunks": nc, "events": ne, "tokens": int(r.tokens), "step_s": dt,
+        "max_seq": L, "kv_offload": offload, "chunks": nc, "events": ne, "tokens": int(r.tokens), "step_s": dt,
         "tokens_per_s": r.tokens / dt, "loss": r.loss,
         "peak_hbm_gb": r.peak_hbm_bytes / 1e9, "static_gb": r.static_hbm_bytes / 1e9,
         "activations_gb": r.act_hbm_bytes / 1e9, "kv_state_gb": r.kv_hbm_bytes / 1e9,
