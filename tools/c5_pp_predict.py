@@ -176,8 +176,8 @@ def main():
                     "budget_gib": 165.0, "best_chunk_size": bc, "best_k": bk, "evaluations": ev,
                     "report": report}
     out["tokens_global"] = int(lengths.sum())
-    out["memory"] = stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms)
-    print(json.dumps(out), flush=True)
+    out["memory"] = stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms, fit)
+    print(json.dumps(out, default=lambda o: o.item() if hasattr(o, "item") else str(o)), flush=True)
 
 
 def tape_bytes_per_token(layers, head):
@@ -199,7 +199,7 @@ def stage_static_bytes(stage):
     return 6 * n  # bf16 weights + fp32 gradients
 
 
-def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms):
+def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allreduce_ms, fit):
     GB = 1e9
     # measured: one retained 16K tape of a 16-layer stage with the head, and
     # the transient working set beyond static + tapes + KV state
@@ -255,7 +255,7 @@ def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allredu
         step_ms = max(spans) + allreduce_ms
         rec = {"stage_peak_gb_per_replica": stages_gb, "worst_stage_gb": worst, "makespan_ms": spans,
                "step_ms": step_ms, "tokens_per_s_8gpu": float(lengths.sum()) / (step_ms / 1e3),
-               "fits": worst <= 170.0}
+               "fits": bool(worst <= 170.0)}
         out["per_budget"][str(budget)] = rec
         if rec["fits"] and (best is None or step_ms < out["per_budget"][str(best)]["step_ms"]):
             best = budget
@@ -264,14 +264,14 @@ def stage_memory(ctx, replicas, lengths, tokens, ids, fw, bw, per_stage, allredu
     lay = tape_bytes_per_token(per_stage, True) / float(1 << 30)
     mem = (max(stage_static_bytes(s) for s in range(STAGES)) / float(1 << 30) + transient / float(1 << 30), lay,
            kv_per_ctx_token / float(1 << 30), 1.0)
-    fit = out.get("cost_model_fit")
+    # the CostModel fitted to this run's measured stage costs (main())
     table, bc, bk, ev, report = capi.tune_grid_search_pp(
         lengths[:1000], [4096, 8192, 16384], [1, 2], STAGES,
-        {"gamma": 30.0, "alpha": 7.0e-3, "beta": 4.2e-7, "backward_multiplier": 2.14, "hop_latency": 0.0},
+        {"gamma": fit["gamma_ms"], "alpha": fit["alpha_ms_per_token"], "beta": fit["beta_ms_per_token2"],
+         "backward_multiplier": fit["backward_multiplier"], "hop_latency": 0.0},
         mem, QWEN["d"] * 4 / float(1 << 30), best or 0, 170.0 / 1.073741824, 1000, 1, 0)
     out["tuner_pp"] = {"tape_budget": best or 0, "best_chunk_size": bc, "best_k": bk, "evaluations": ev,
                        "report": report, "memory_model": mem}
-    del fit
     return out
 
 
