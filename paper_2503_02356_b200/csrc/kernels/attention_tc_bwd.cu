@@ -394,17 +394,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
       // dS = P * (dP - D); P masked only on sub-tiles that cross the causal
       // diagonal or the end of the segment (two separately compiled bodies)
+      // pairs in FFMA2 / FADD2 / FMUL2: x = s * sl2 - lse2, dS = P (dP - D)
+      const float2 sl2v = make_float2(a.sl2, a.sl2), nl = make_float2(-lse2, -lse2), nD = make_float2(-D, -D);
       auto body = [&](auto masked) {
         const int key0 = j * SUB + half * 32;
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          float p0 = ex2(fmaf(__uint_as_float(rs[2 * e]), a.sl2, -lse2));
-          float p1 = ex2(fmaf(__uint_as_float(rs[2 * e + 1]), a.sl2, -lse2));
+          const float2 x = ffma2(make_float2(__uint_as_float(rs[2 * e]), __uint_as_float(rs[2 * e + 1])), sl2v, nl);
+          float2 p = make_float2(ex2(x.x), ex2(x.y));
           if constexpr (decltype(masked)::value) {
-            p0 = key0 + 2 * e <= klim ? p0 : 0.f;
-            p1 = key0 + 2 * e + 1 <= klim ? p1 : 0.f;
+            p.x = key0 + 2 * e <= klim ? p.x : 0.f;
+            p.y = key0 + 2 * e + 1 <= klim ? p.y : 0.f;
           }
-          pk[e] = pack_bf16(p0 * (__uint_as_float(rp[2 * e]) - D), p1 * (__uint_as_float(rp[2 * e + 1]) - D));
+          const float2 ds =
+              fmul2(p, fadd2(make_float2(__uint_as_float(rp[2 * e]), __uint_as_float(rp[2 * e + 1])), nD));
+          pk[e] = pack_bf16(ds.x, ds.y);
         }
       };
 #if CF_BWD_DIAG == 1
@@ -653,31 +657,33 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       const uint32_t lrow = sLD0 + qs * 512 + part * 64;
       uint32_t pp[8], pd[8];
       auto body = [&](auto masked) {
+        // pairs in FFMA2 / FADD2 / FMUL2: x = s * sl2 - LSE * log2e,
+        // dS = P (dP - D), per-column LSE / D
+        const float2 sl2v = make_float2(a.sl2, a.sl2), nlg = make_float2(-kLog2e, -kLog2e),
+                     m1 = make_float2(-1.f, -1.f);
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
           const float4 L = lds_f32x4(lrow + c4 * 16);
           const float4 Dv = lds_f32x4(lrow + 256 + c4 * 16);
-          const float l[4] = {L.x * kLog2e, L.y * kLog2e, L.z * kLog2e, L.w * kLog2e};
-          const float d[4] = {Dv.x, Dv.y, Dv.z, Dv.w};
-          float p[4], ds[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int col = c4 * 4 + u;
-            p[u] = ex2(fmaf(__uint_as_float(rs[col]), a.sl2, -l[u]));
-            ds[u] = p[u] * (__uint_as_float(rp[col]) - d[u]);
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int col = c4 * 4 + 2 * h2;
+            const float2 nl = fmul2(h2 ? make_float2(L.z, L.w) : make_float2(L.x, L.y), nlg);
+            const float2 nd = fmul2(h2 ? make_float2(Dv.z, Dv.w) : make_float2(Dv.x, Dv.y), m1);
+            const float2 x = ffma2(make_float2(__uint_as_float(rs[col]), __uint_as_float(rs[col + 1])), sl2v, nl);
+            float2 p = make_float2(ex2(x.x), ex2(x.y));
+            float2 ds = fmul2(p, fadd2(make_float2(__uint_as_float(rp[col]), __uint_as_float(rp[col + 1])), nd));
             if constexpr (decltype(masked)::value) {
               // masked entries are selected away (never multiplied), so
               // whatever LSE / D a slot holds past the segment cannot leak
               const int qq = qt0 + part * 16 + col;
-              const bool in = qq >= qlo && qq < sg.len;
-              p[u] = in ? p[u] : 0.f;
-              ds[u] = in ? ds[u] : 0.f;
+              const bool in0 = qq >= qlo && qq < sg.len, in1 = qq + 1 >= qlo && qq + 1 < sg.len;
+              p = make_float2(in0 ? p.x : 0.f, in1 ? p.y : 0.f);
+              ds = make_float2(in0 ? ds.x : 0.f, in1 ? ds.y : 0.f);
             }
+            pp[2 * c4 + h2] = pack_bf16(p.x, p.y);
+            pd[2 * c4 + h2] = pack_bf16(ds.x, ds.y);
           }
-          pp[2 * c4] = pack_bf16(p[0], p[1]);
-          pp[2 * c4 + 1] = pack_bf16(p[2], p[3]);
-          pd[2 * c4] = pack_bf16(ds[0], ds[1]);
-          pd[2 * c4 + 1] = pack_bf16(ds[2], ds[3]);
         }
       };
       // uniform: every key of the tile sees every query of the sub-tile

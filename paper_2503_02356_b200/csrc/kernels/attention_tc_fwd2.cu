@@ -236,16 +236,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         rescale = j > 0;
         m = mn;
       }
-      float ps[4] = {0.f, 0.f, 0.f, 0.f};
+      // pairs of scores in FFMA2 / FADD2 (x = s * sl2 - m, running sums)
+      float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       uint32_t pk[32];
+      const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m, -m);
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        const float p0 = ex2(fmaf(__uint_as_float(r[e >> 4][(2 * e) & 31]), sl2, -m));
-        const float p1 = ex2(fmaf(__uint_as_float(r[e >> 4][(2 * e + 1) & 31]), sl2, -m));
-        ps[e & 3] += p0 + p1;
-        pk[e] = pack_bf16(p0, p1);
+        const float2 x = ffma2(make_float2(__uint_as_float(r[e >> 4][(2 * e) & 31]),
+                                           __uint_as_float(r[e >> 4][(2 * e + 1) & 31])),
+                               sl2v, nm);
+        const float2 p = make_float2(ex2(x.x), ex2(x.y));
+        ps[e & 1] = fadd2(ps[e & 1], p);
+        pk[e] = pack_bf16(p.x, p.y);
       }
-      l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
+      l = fmaf(l, alpha, (ps[0].x + ps[1].x) + (ps[0].y + ps[1].y));
       tmem_st32(tS + half * 32, pk);  // P (bf16 pairs) over S columns [0, 64)
       if (rescale) {  // after P (S registers dead); PV_w(j-1) is complete (s_full_w(j) followed it)
 #pragma unroll
@@ -254,7 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tO + half * 64 + c * 32, r);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+          for (int e = 0; e < 16; ++e) {
+            const float2 v = fmul2(make_float2(__uint_as_float(r[2 * e]), __uint_as_float(r[2 * e + 1])),
+                                   make_float2(alpha, alpha));
+            r[2 * e] = __float_as_uint(v.x);
+            r[2 * e + 1] = __float_as_uint(v.y);
+          }
           tmem_st32(tO + half * 64 + c * 32, r);
         }
       }
