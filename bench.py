@@ -111,7 +111,7 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
-TRAFFIC_FILE = "profiles/round1_gemm_traffic.json"
+TRAFFIC_FILE = "profiles/round2_gemm_traffic.json"
 
 
 HBM_FILE = "profiles/round2_hbm_kernels.json"
@@ -139,6 +139,8 @@ def gemm_traffic():
     launches for comparison; None when the capture is absent."""
     try:
         t = json.load(open(os.path.join(ROOT, TRAFFIC_FILE)))
+        if "mean_dram_bytes_per_launch" not in t:  # tools/gemm_traffic_quick.py: one entry per variant
+            t = next(v for v in t.values() if isinstance(v, dict) and "mean_dram_bytes_per_launch" in v)
         return t["mean_dram_bytes_per_launch"], t["mean_algorithmic_bytes_per_launch"]
     except Exception:
         return None, None

@@ -49,12 +49,27 @@ for name, M, N, K, ak, bk, epi in SH:
         ctx.gemm(*args)
     ctx.synchronize()
     s = torch.cuda.ExternalStream(ctx.stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n = 10
-    e0.record(s)
-    for _ in range(n):
-        ctx.gemm(*args)
-    e1.record(s)
-    e1.synchronize()
-    ms = e0.elapsed_time(e1) / n
-    print(f"{name:16s} M={M:6d} N={N:6d} K={K:6d}  {ms:7.3f} ms  {2 * M * N * K / ms / 1e9:7.1f} TFLOP/s", flush=True)
+    # SUSTAIN=seconds: back-to-back launches for that long (power-capped
+    # rate, as the sustained peak in MEASURED_PEAKS.json), else 10 launches
+    sustain = float(os.environ.get("SUSTAIN", "0"))
+    n = max(10, int(sustain * 1e3 / max(1e-3, 2 * M * N * K / 1.2e12))) if sustain else 10
+
+    def timed(fn, stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / n
+
+    ms = timed(lambda: ctx.gemm(*args), s)
+    # cuBLAS on the same operand majors (bf16 in, bf16 out), for reference
+    a_op = A if ak else A.t()
+    b_op = B.t() if bk else B
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    torch.matmul(a_op, b_op, out=out)
+    torch.cuda.synchronize()
+    ms_cb = timed(lambda: torch.matmul(a_op, b_op, out=out), torch.cuda.current_stream())
+    print(f"{name:16s} M={M:6d} N={N:6d} K={K:6d}  {ms:7.3f} ms  {2 * M * N * K / ms / 1e9:7.1f} TFLOP/s"
+          f"   cuBLAS {ms_cb:7.3f} ms {2 * M * N * K / ms_cb / 1e9:7.1f} TFLOP/s  ratio {ms_cb / ms:5.3f}", flush=True)

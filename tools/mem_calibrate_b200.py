@@ -45,9 +45,10 @@ def main():
                                   [x["context_len"] for x in rows], [x["peak_gib"] for x in rows], gqa)
     d, L, kvw, ffn, H = MODEL["d"], MODEL["layers"], 1024, MODEL["ffn"], MODEL["heads"]
     qkv = d + 2 * kvw
-    # retained tape bytes per token (engine.cu Tape): x_in (L+1) + x_mid fp32, qkv, O, gate|up, xn1, xn2, h bf16,
-    # LSE fp32 per head, dlogits bf16 (vocab padded to 8), RoPE table, final-norm copy
-    tape = (4 * d * (2 * L + 1) + 2 * L * (qkv + d + 2 * ffn + 2 * d + ffn) + 4 * L * H + 2 * MODEL["vocab"]
+    # retained tape bytes per token (engine.cu alloc_tape): x_in (L+1) + x_mid fp32, qkv, O, gate|up, xn1, xn2,
+    # h bf16, attention LSE fp32 per head, head LSE fp32 (the fused cross-entropy keeps no logits), RoPE table,
+    # final-norm copy
+    tape = (4 * d * (2 * L + 1) + 2 * L * (qkv + d + 2 * ffn + 2 * d + ffn) + 4 * L * H + 4
             + 4 * 64 * 2 + 2 * d)
     kv_state = L * kvw * (2 * 2 + 2 * 4)  # bf16 K, V + fp32 dK, dV per context token
     out = {"design": rows, "gqa_ratio": gqa,
