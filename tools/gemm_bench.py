@@ -17,6 +17,8 @@ SH = [  # name, M, N, K, a_kmajor, b_kmajor, epi
     ("gate|up fwd", T, 2 * ffn, d, 1, 0, capi.EPI_BF16),
     ("down fwd +res", T, d, ffn, 1, 0, capi.EPI_F32_RES),
     ("o fwd +res", T, d, d, 1, 0, capi.EPI_F32_RES),
+    ("o fwd bf16-out", T, d, d, 1, 0, capi.EPI_BF16),
+    ("o fwd f32-out", T, d, d, 1, 0, capi.EPI_F32),
     ("down dgrad", T, ffn, d, 1, 1, capi.EPI_BF16),
     ("gate|up dgrad", T, d, 2 * ffn, 1, 1, capi.EPI_F32),
     ("gate|up wgrad", d, 2 * ffn, T, 0, 0, capi.EPI_F32_ACC),

@@ -21,7 +21,7 @@ def capture(env, skip):
            str(skip), "--launch-count", "8", "--csv", "python", "bench.py", "--workload", "short", "--steps", "1",
            "--warmup", "1", "--no-cpu-baseline"]
     out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900).stdout
-    rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 14 and r[0] != "ID"]
+    rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 14 and r[0].isdigit()]
     per = {}
     for r in rows:
         per.setdefault(r[0], {})[r[12]] = float(r[14]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
