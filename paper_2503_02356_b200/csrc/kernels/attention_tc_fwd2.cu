@@ -236,8 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         rescale = j > 0;
         m = mn;
       }
-      // pairs of scores in FFMA2 / FADD2 (x = s * sl2 - m, running sums)
-      float2 ps[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      // pairs of scores in FFMA2 (x = s * sl2 - m); the row sum keeps the
+      // scalar order (ps[e & 3] += p0 + p1) so l stays bitwise what the
+      // operator-level segment path reproduces
+      float ps[4] = {0.f, 0.f, 0.f, 0.f};
       uint32_t pk[32];
       const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m, -m);
 #pragma unroll
@@ -246,10 +248,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                            __uint_as_float(r[e >> 4][(2 * e + 1) & 31])),
                                sl2v, nm);
         const float2 p = make_float2(ex2(x.x), ex2(x.y));
-        ps[e & 1] = fadd2(ps[e & 1], p);
+        ps[e & 3] += p.x + p.y;
         pk[e] = pack_bf16(p.x, p.y);
       }
-      l = fmaf(l, alpha, (ps[0].x + ps[1].x) + (ps[0].y + ps[1].y));
+      l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
       tmem_st32(tS + half * 32, pk);  // P (bf16 pairs) over S columns [0, 64)
       if (rescale) {  // after P (S registers dead); PV_w(j-1) is complete (s_full_w(j) followed it)
 #pragma unroll
