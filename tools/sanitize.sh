@@ -15,8 +15,8 @@ echo "memcheck tests rc=$?"
 # the fused epilogues (SwiGLU / RoPE + KV copy), cross-entropy row kernel,
 # attention backward readouts and the segment operators
 timeout 1500 $S --tool memcheck --error-exitcode 9 python -m pytest -x -q -m gpu \
-  tests/test_gemm_gpu.py tests/test_parity_gpu.py tests/test_segment_gpu.py \
-  -k "forced or v32000 or v97 or dh128 or segment or compose or single_chunk" \
+  tests/test_gemm_gpu.py tests/test_parity_gpu.py tests/test_segment_gpu.py tests/test_attention_stress_gpu.py \
+  -k "forced or v32000 or v97 or dh128 or segment or compose or single_chunk or stress" \
   > gpurun_out/sanitize_memcheck_fused.log 2>&1
 echo "memcheck fused rc=$?"
 timeout 900 $S --tool racecheck --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" \
