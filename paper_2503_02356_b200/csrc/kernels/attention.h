@@ -53,6 +53,10 @@ struct AttnParams {
   const float2* rope_tab = nullptr;
   __nv_bfloat16* dkv_out = nullptr;
   int64_t dkv_out_ld = 0, col_k = 0, col_v = 0;
+  //   keys_per_query: the launch's attention pairs / T when the caller knows
+  //             it (0 = unknown): long-context launches (>= 3072 keys per
+  //             query on average) take the 128-key-tile dQ kernel
+  double keys_per_query = 0;
 };
 
 cudaError_t attn_forward(const AttnParams& p, cudaStream_t st);

@@ -13,6 +13,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "attention.h"
@@ -476,6 +477,277 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ------------------------------------------------------------- dQ, wide
+// CTA = 128 queries x one q head, keys streamed in 128-key tiles so the S /
+// dP MMAs are N = 128 (a tcgen05.mma with N <= 64 pays a ~45-cycle floor,
+// profiles/round2_mma_probe.txt).  TMEM: S [0,128) dP [128,256) dQ
+// [256,384) Q [384,448) dO [448,512) — S / dP single-buffered; the MMA
+// issuer covers their read-out with the previous tile's dQ GEMM:
+//   S(j) dP(j) | dQ(j-1) | S(j+1) dP(j+1) | dQ(j) | ...
+// 16 softmax warps: lane quarter (warp & 3) x 32-key column quarter (warp >> 2).
+constexpr int kWKS = 3, kWVS = 2;        // K / V ring depths (128-key tiles)
+constexpr int kDqWideThreads = 576;      // 16 softmax warps + TMA + MMA
+__global__ void __launch_bounds__(kDqWideThreads, 1)
+    dq_wide_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;                            // kWKS x 2 x [128][64]
+  uint8_t* sV = sK + kWKS * 2 * kBox128;       // kWVS x 2 x [128][64]
+  uint8_t* sS = sV + kWVS * 2 * kBox128;       // 2 x 2 x [128 q][64 keys] (dS)
+  float* sRowD = reinterpret_cast<float*>(sS); // [4][128] D partials, before dS(0) exists
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 4 * kBox128);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;              // [kWKS]
+  uint64_t* k_empty = k_full + kWKS;       // [kWKS]
+  uint64_t* v_full = k_empty + kWKS;       // [kWVS]
+  uint64_t* v_empty = v_full + kWVS;       // [kWVS]
+  uint64_t* s_full = v_empty + kWVS;
+  uint64_t* s_free = s_full + 1;
+  uint64_t* ds_full = s_free + 1;          // [2]
+  uint64_t* ds_free = ds_full + 2;         // [2]
+  uint64_t* dq_done = ds_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+  const AttnTile tl = a.tiles[blockIdx.x];
+  const AttnSeg sg = a.segs[tl.seg];
+  const int h = blockIdx.y, g = h / (a.H / a.KVH);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q_row0 = sg.q_start + tl.first;
+  const int kv_len = sg.prefix + tl.first + tl.count;
+  const int nkt = (kv_len + 127) / 128;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 16);
+    for (int i = 0; i < kWKS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < kWVS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 16);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ds_full[i], 16);
+      mbar_init(&ds_free[i], 1);
+    }
+    mbar_init(dq_done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tAq = tmem + 384, tAo = tmem + 448;
+
+  if (warp == 16) {
+    if (lane == 0) {
+      for (int j = 0; j < nkt; ++j) {
+        const int sk = j % kWKS, sv = j % kWVS;
+        const int krow = sg.kv_row0 + j * 128;
+        stress_delay(a.stress, 1, j);
+        mbar_wait(&v_empty[sv], ((j / kWVS) & 1) ^ 1);
+        mbar_expect_tx(&v_full[sv], 2 * kBox128);
+        tma_load_2d(sV + sv * 2 * kBox128, &tmV, &v_full[sv], g * DH, krow);
+        tma_load_2d(sV + sv * 2 * kBox128 + kBox128, &tmV, &v_full[sv], g * DH + 64, krow);
+        mbar_wait(&k_empty[sk], ((j / kWKS) & 1) ^ 1);
+        mbar_expect_tx(&k_full[sk], 2 * kBox128);
+        tma_load_2d(sK + sk * 2 * kBox128, &tmK, &k_full[sk], g * DH, krow);
+        tma_load_2d(sK + sk * 2 * kBox128 + kBox128, &tmK, &k_full[sk], g * DH + 64, krow);
+      }
+    }
+  } else if (warp == 17) {
+    // whole warp, convergent (elect.sync inside the issue helpers)
+    constexpr uint32_t idS = umma_idesc_bf16(128, 128, 0, 0);  // S, dP: N = 128 keys
+    constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);  // dQ: N = dh, B = K (MN-major view)
+    const uint32_t sK0 = smem_u32(sK), sV0 = smem_u32(sV), sS0 = smem_u32(sS);
+    const uint32_t bKf = smem_u32(k_full), bKe = smem_u32(k_empty), bVf = smem_u32(v_full),
+                   bVe = smem_u32(v_empty), bSf = smem_u32(s_full), bSr = smem_u32(s_free),
+                   bDf = smem_u32(ds_full), bDr = smem_u32(ds_free), bQd = smem_u32(dq_done);
+    auto issue_s = [&](int j) {
+      const int sk = j % kWKS, sv = j % kWVS;
+      mbar_wait_s(bKf + sk * 8, (j / kWKS) & 1);
+      mbar_wait_s(bVf + sv * 8, (j / kWVS) & 1);
+      tc_fence_after();
+      const uint32_t k0 = sK0 + sk * 2 * kBox128, v0 = sV0 + sv * 2 * kBox128;
+      umma4_ts_w<8, 2>(tS, tAq, kdesc(k0, kBox128, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tS, tAq + 32, kdesc(k0, kBox128, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tP, tAo, kdesc(v0, kBox128, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tP, tAo + 32, kdesc(v0, kBox128, 4), idS, 1u);
+      umma_commit_w(bVe + sv * 8);
+      umma_commit_w(bSf);
+    };
+    auto issue_dq = [&](int j) {
+      const uint32_t b = j & 1;
+      mbar_wait_s(bDf + b * 8, (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t s0 = sS0 + b * 2 * kBox128, k0 = sK0 + (j % kWKS) * 2 * kBox128;
+      // dQ += dS K: K = 128 keys in two 64-key boxes of dS (4 MMAs each)
+      umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 0), mndesc(k0, kBox128, 0), idQ, j > 0 ? 1u : 0u);
+      umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 4), mndesc(k0, kBox128, 4), idQ, 1u);
+      umma_commit_w(bKe + (j % kWKS) * 8);
+      umma_commit_w(bDr + b * 8);
+    };
+    mbar_wait(q_full, 0);  // Q / dO staged into TMEM by the softmax warps
+    tc_fence_after();
+    issue_s(0);
+    for (int j = 0; j < nkt; ++j) {
+      stress_delay(a.stress, 2, j);
+      if (j >= 1) issue_dq(j - 1);
+      if (j + 1 < nkt) {
+        mbar_wait_s(bSr, j & 1);  // S(j) / dP(j) read out: the columns are free
+        tc_fence_after();
+        issue_s(j + 1);
+      }
+    }
+    issue_dq(nkt - 1);
+    umma_commit_w(bQd);
+  } else {
+    const int quarter = warp & 3, cq = warp >> 2;  // TMEM lane quarter, 32-key column quarter
+    const int row = quarter * 32 + lane;
+    const int qi = tl.first + row;
+    const bool ok = qi < sg.len && row < tl.count;
+    const int lim = sg.prefix + min(qi, sg.len - 1);
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
+    float D;
+    {
+      // this warp stages dh columns [32 cq, 32 cq + 32) of Q and dO (16 TMEM
+      // columns each) and the matching part of D = rowsum(dO * O)
+      const bool rok = row < tl.count;
+      const int64_t r = q_row0 + row;
+      stage_row_tmem16(tAq + lane_off + cq * 16, a.q + r * a.q_stride + static_cast<int64_t>(h) * DH + cq * 32, rok);
+      stage_row_tmem16(tAo + lane_off + cq * 16, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + cq * 32,
+                       ok);
+      float dpart = 0.f;
+      if (ok) {
+        const uint4* d4 = reinterpret_cast<const uint4*>(a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + cq * 32);
+        const uint4* o4 = reinterpret_cast<const uint4*>(a.o + r * a.o_stride + static_cast<int64_t>(h) * DH + cq * 32);
+        float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 dv = __ldg(d4 + c), ov = __ldg(o4 + c);
+          const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w}, ow[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&dw[e]);
+            const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+            part[e] = fmaf(__low2float(a2), __low2float(b2), part[e]);
+            part[e] = fmaf(__high2float(a2), __high2float(b2), part[e]);
+          }
+        }
+        dpart = (part[0] + part[1]) + (part[2] + part[3]);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      warp_arrive(q_full);
+      // the four column quarters of a row meet in smem (fixed order)
+      sRowD[cq * 128 + row] = dpart;
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
+      D = (sRowD[row] + sRowD[128 + row]) + (sRowD[256 + row] + sRowD[384 + row]);
+      if (ok && cq == 0) a.dsum[static_cast<int64_t>(h) * a.T + q_row0 + row] = D;
+    }
+    const uint32_t bSf = smem_u32(s_full), bSr = smem_u32(s_free), bDf = smem_u32(ds_full),
+                   bDr = smem_u32(ds_free), sS0 = smem_u32(sS);
+    const int klim = ok ? lim : -1;
+    const int tile_lim = sg.prefix + tl.first;
+    // dS row `row`, keys [32 cq, 32 cq + 32): box cq >> 1, 16-byte chunks
+    // 4 (cq & 1) .. 4 (cq & 1) + 3
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dst_off[c] = (cq >> 1) * kBox128 + sw_off(row, (cq & 1) * 4 + c);
+    const float2 sl2v = make_float2(a.sl2, a.sl2), nl = make_float2(-lse2, -lse2), nD = make_float2(-D, -D);
+    // the D exchange above used the dS buffers' memory: every softmax warp
+    // is past it before any dS store
+    asm volatile("bar.sync %0, 512;" ::"r"(5) : "memory");
+    for (int j = 0; j < nkt; ++j) {
+      const uint32_t b = j & 1;
+      mbar_wait_s(bSf, j & 1);
+      tc_fence_after();
+      uint32_t rs[32], rp[32];
+      tmem_ld32(tS + lane_off + cq * 32, rs);
+      tmem_ld32(tP + lane_off + cq * 32, rp);
+      tmem_ld_wait();
+      tc_fence_before();
+      warp_arrive_s(bSr);
+      uint32_t pk[16];
+      auto body = [&](auto masked) {
+        const int key0 = j * 128 + cq * 32;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 x = ffma2(make_float2(__uint_as_float(rs[2 * e]), __uint_as_float(rs[2 * e + 1])), sl2v, nl);
+          float2 p = make_float2(ex2(x.x), ex2(x.y));
+          if constexpr (decltype(masked)::value) {
+            p.x = key0 + 2 * e <= klim ? p.x : 0.f;
+            p.y = key0 + 2 * e + 1 <= klim ? p.y : 0.f;
+          }
+          const float2 ds =
+              fmul2(p, fadd2(make_float2(__uint_as_float(rp[2 * e]), __uint_as_float(rp[2 * e + 1])), nD));
+          pk[e] = pack_bf16(ds.x, ds.y);
+        }
+      };
+      if (j * 128 + 127 <= tile_lim)
+        body(std::false_type{});
+      else
+        body(std::true_type{});
+      stress_delay(a.stress, 3, j);
+      if (j >= 2) mbar_wait_s(bDr + b * 8, ((j >> 1) & 1) ^ 1);
+      const uint32_t dst = sS0 + b * 2 * kBox128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        sts128(dst + dst_off[c], make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+      fence_async_smem();
+      warp_arrive_s(bDf + b * 8);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+    __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+    if (a.rope_tab) {  // column quarters 0, 1 take rotate-half partner chunks (cq, cq + 2)
+      if (cq < 2) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tQ + lane_off + cq * 32, ra);
+        tmem_ld32(tQ + lane_off + (cq + 2) * 32, rb);
+        tmem_ld_wait();
+        if (ok) {
+          float fa[32], fb[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            fa[e] = bf16_round(__uint_as_float(ra[e]) * a.scale);
+            fb[e] = bf16_round(__uint_as_float(rb[e]) * a.scale);
+          }
+          rope_inverse32(a.rope_tab + static_cast<int64_t>(q_row0 + row) * (DH / 2) + cq * 32, fa, fb);
+          store_bf16x32(out + cq * 32, fa);
+          store_bf16x32(out + (cq + 2) * 32, fb);
+        }
+      }
+    } else {
+      uint32_t r[32];
+      tmem_ld32(tQ + lane_off + cq * 32, r);
+      tmem_ld_wait();
+      if (ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(out + cq * 32);
+        const float sc = a.scale;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          d4[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * sc, __uint_as_float(r[8 * q + 1]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 2]) * sc, __uint_as_float(r[8 * q + 3]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 4]) * sc, __uint_as_float(r[8 * q + 5]) * sc),
+                             pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
 // ------------------------------------------------------------- dK / dV
 // CTA = 128 keys x one kv head (sole owner of those rows); queries streamed
 // in 64-query sub-tiles over every q head of the GQA group.
@@ -796,6 +1068,18 @@ bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uin
 
 }  // namespace
 
+// dQ kernel choice: the 128-key-tile kernel (N = 128 S / dP MMAs) wins on
+// long-context launches (T = 16384 causal: -11 % dQ time) and loses a little
+// on short ones, where 64-key sub-tiles cut less into the causal diagonal
+// (T = 2048: +3 %).  CF_DQ_WIDE=1 / 0 forces it on / off (A/B, tests).
+bool dq_wide(const AttnParams& p) {
+  static const int v = [] {
+    const char* e = std::getenv("CF_DQ_WIDE");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v >= 0 ? v == 1 : p.keys_per_query >= 3072.0;
+}
+
 int g_attn_stress = 0;
 void set_attn_stress(int on) { g_attn_stress = on ? 1 : 0; }
 
@@ -819,7 +1103,17 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   if (attr == cudaSuccess) attr = smem_optin(reinterpret_cast<const void*>(dkv_kernel), static_cast<int>(smem_dkv));
   if (attr != cudaSuccess) return attr;
   // D = rowsum(dO * O) is produced by the dQ kernel (no separate dsum pass)
-  dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
+  if (dq_wide(p)) {
+    CUtensorMap k128, v128;
+    if (!map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
+      return cudaErrorInvalidValue;
+    const size_t smem_w = 1024 + (kWKS + kWVS) * 2 * kBox128 + 4 * kBox128 + 256;
+    attr = smem_optin(reinterpret_cast<const void*>(dq_wide_kernel), static_cast<int>(smem_w));
+    if (attr != cudaSuccess) return attr;
+    dq_wide_kernel<<<dim3(nq, p.H), kDqWideThreads, smem_w, st>>>(k128, v128, a);
+  } else {
+    dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
+  }
   a.tiles = ktiles128;
   if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, a);
   return cudaGetLastError();

@@ -1383,6 +1383,7 @@ struct Exec {
         own_dk = dkv_local;
       }
       cudaEvent_t t0 = mark();
+      p.keys_per_query = T > 0 ? static_cast<double>(cm.pairs) / static_cast<double>(T) : 0.0;
       if (tc)
         L(cfk::attn_backward_tc(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
                                 meta<const AttnTile>(cm.o_kt128), static_cast<int32_t>(cm.nkt128),
