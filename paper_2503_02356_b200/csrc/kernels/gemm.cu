@@ -541,9 +541,16 @@ __device__ __forceinline__ void commit2_mc(uint64_t* bar) {
       : "memory");
 }
 
+// Two problems in one persistent launch (`g2`, with its own maps and tile
+// raster; tiles [0, g.num_m * g.num_n) belong to `g`, the rest to `g2`): the
+// weight-gradient GEMMs of a layer whose tile counts fall just past a wave
+// boundary share their last wave (e.g. o 256 + q|k|v 384 tiles = 8.65 waves
+// of 74 pairs instead of 4 + 6).  Same epilogue and operand majors.
 template <bool A_MN, bool B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args g) {
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args g1,
+                     const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2, Args g2) {
+  const Args& g = g1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -558,9 +565,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
+  const int tiles1 = g.num_m * g.num_n;
+  const int num_tiles = tiles1 + g2.num_m * g2.num_n;  // g2.num_m = 0: one problem
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (g2.num_m > 0) {
+      tma_prefetch(&tmA2);
+      tma_prefetch(&tmB2);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 2);  // leader arrive.expect_tx + peer remote arrive
       mbar_init(&empty[s], 1);
@@ -580,8 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int num_tiles = g.num_m * g.num_n;  // num_m counts 256-row pair tiles
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;  // num_m counts 256-row pair tiles
 
   if (warp == 0) {
     if (lane == 0) {
@@ -597,14 +609,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       // deterministic).
       int wave = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs, ++wave) {
+        const bool second = tile >= tiles1;
+        const Args& gp = second ? g2 : g;
+        const CUtensorMap* mA = second ? &tmA2 : &tmA;
+        const CUtensorMap* mB = second ? &tmB2 : &tmB;
         int mb, nb;
-        tile_coords(g, tile, mb, nb);
-        const bool rev = g.serp && (wave & 1);
+        tile_coords(gp, second ? tile - tiles1 : tile, mb, nb);
+        const bool rev = gp.serp && (wave & 1);
         const int m0 = mb * 256 + static_cast<int>(rank) * 128;
-        const int n0 = EPI == EPI_BF16_SWIGLU ? (rank == 0 ? nb * 128 : g.split_n + nb * 128)
+        const int n0 = EPI == EPI_BF16_SWIGLU ? (rank == 0 ? nb * 128 : gp.split_n + nb * 128)
                                               : nb * 256 + static_cast<int>(rank) * 128;
-        for (int kq = 0; kq < g.num_k; ++kq) {
-          const int kb = rev ? g.num_k - 1 - kq : kq;
+        for (int kq = 0; kq < gp.num_k; ++kq) {
+          const int kb = rev ? gp.num_k - 1 - kq : kq;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* a = sA + stage * kABytes;
           uint8_t* b = sB + stage * kBBytes;
@@ -613,16 +629,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           else
             arrive_remote(full_leader0 + stage * 8);
           if constexpr (!A_MN) {
-            tma_load_2sm(a, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2sm(a, mA, &full[stage], kb * BK, m0);
           } else {
-            tma_load_2sm(a, &tmA, &full[stage], m0, kb * BK);
-            tma_load_2sm(a + kSlab, &tmA, &full[stage], m0 + 64, kb * BK);
+            tma_load_2sm(a, mA, &full[stage], m0, kb * BK);
+            tma_load_2sm(a + kSlab, mA, &full[stage], m0 + 64, kb * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2sm(b, &tmB, &full[stage], kb * BK, n0);
+            tma_load_2sm(b, mB, &full[stage], kb * BK, n0);
           } else {
-            tma_load_2sm(b, &tmB, &full[stage], n0, kb * BK);
-            tma_load_2sm(b + kSlab, &tmB, &full[stage], n0 + 64, kb * BK);
+            tma_load_2sm(b, mB, &full[stage], n0, kb * BK);
+            tma_load_2sm(b + kSlab, mB, &full[stage], n0 + 64, kb * BK);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -639,10 +655,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = pair; tile < num_tiles; tile += npairs) {
+        const int nk = tile >= tiles1 ? g2.num_k : g1.num_k;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * 256);
-        for (int kb = 0; kb < g.num_k; ++kb) {
+        for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kABytes);
@@ -672,8 +689,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader0 = leader_addr(smem_u32(&tempty[0]));
     for (int tile = pair; tile < num_tiles; tile += npairs) {
+      const bool second = tile >= tiles1;
+      const Args& g = second ? g2 : g1;  // this tile's problem
       int mb, nb;
-      tile_coords(g, tile, mb, nb);
+      tile_coords(g, second ? tile - tiles1 : tile, mb, nb);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = mb * 256 + static_cast<int>(rank) * 128 + ew * 32 + lane;
@@ -871,13 +890,13 @@ cudaError_t launch_t(const GemmDesc& d, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <bool A_MN, bool B_MN, int EPI>
-cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
-  CUtensorMap ta, tb;
+// Tensor maps and kernel arguments of one CTA-pair problem.
+template <bool A_MN, bool B_MN>
+bool pair_problem(const GemmDesc& d, CUtensorMap& ta, CUtensorMap& tb, Args& g) {
   bool ok = A_MN ? make_map(&ta, d.a, d.M, d.K, d.lda, 64, 64) : make_map(&ta, d.a, d.K, d.M, d.lda, BK, 128);
   ok = ok && (B_MN ? make_map(&tb, d.b, d.N, d.K, d.ldb, 64, 64) : make_map(&tb, d.b, d.K, d.N, d.ldb, BK, 128));
-  if (!ok) return cudaErrorInvalidValue;
-  Args g{};
+  if (!ok) return false;
+  g = Args{};
   g.M = static_cast<int>(d.M);
   g.N = static_cast<int>(d.N);
   g.K = static_cast<int>(d.K);
@@ -904,13 +923,27 @@ cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st) {
   g.R = d.r;
   g.ldr = d.ldr;
   set_ce(g, d);
+  return true;
+}
+
+// One problem, or two (d2 != nullptr: same epilogue and majors) sharing the
+// persistent grid.
+template <bool A_MN, bool B_MN, int EPI>
+cudaError_t launch_pair(const GemmDesc& d, cudaStream_t st, const GemmDesc* d2 = nullptr) {
+  CUtensorMap ta, tb, ta2, tb2;
+  Args g{}, g2{};
+  if (!pair_problem<A_MN, B_MN>(d, ta, tb, g)) return cudaErrorInvalidValue;
+  if (d2 && !pair_problem<A_MN, B_MN>(*d2, ta2, tb2, g2)) return cudaErrorInvalidValue;
   auto kern = pair::gemm_pair_kernel<A_MN, B_MN, EPI>;
   // per (kernel, device), thread-safe
   const cudaError_t attr = smem_optin(reinterpret_cast<const void*>(kern), static_cast<int>(pair::kSmem));
   if (attr != cudaSuccess) return attr;
-  const int tiles = g.num_m * g.num_n;
+  const int tiles = g.num_m * g.num_n + (d2 ? g2.num_m * g2.num_n : 0);
   const int pairs = std::min(tiles, gemm_num_sms() / 2);
-  kern<<<2 * pairs, 256, pair::kSmem, st>>>(ta, tb, g);
+  if (d2)
+    kern<<<2 * pairs, 256, pair::kSmem, st>>>(ta, tb, g, ta2, tb2, g2);
+  else
+    kern<<<2 * pairs, 256, pair::kSmem, st>>>(ta, tb, g, ta, tb, g2);  // g2.num_m = 0: one problem
   return cudaGetLastError();
 }
 
@@ -1010,6 +1043,29 @@ cudaError_t gemm(const GemmDesc& d, cudaStream_t st) {
   const int64_t tiles256 = ((d.M + BM - 1) / BM) * ((d.N + 255) / 256);
   const bool wide = d.N > 128 && tiles256 >= sms;
   return wide ? by_major<256>(d, st) : by_major<128>(d, st);
+}
+
+// Two weight-gradient GEMMs (EPI_F32_ACC, same operand majors) in one
+// CTA-pair launch when both would take the pair kernel; otherwise one after
+// the other.  Each output tile is computed exactly as in its own launch
+// (serpentine K aside, whose direction follows the shared wave index).
+cudaError_t gemm2(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t st) {
+  auto pair_ok = [](const GemmDesc& d) {
+    const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
+    const int mode = gemm_mode();
+    return mode != 1 && d.M > 128 && d.N > 128 && (pair_tiles >= gemm_num_sms() / 4 || mode >= 2) &&
+           !(reinterpret_cast<uintptr_t>(d.a) & 15) && !(reinterpret_cast<uintptr_t>(d.b) & 15) && d.lda % 8 == 0 &&
+           d.ldb % 8 == 0 && !(reinterpret_cast<uintptr_t>(d.c) & 15) && d.ldc % 8 == 0 && d.K > 0;
+  };
+  if (d0.epi != EPI_F32_ACC || d1.epi != EPI_F32_ACC || d0.a_kmajor != d1.a_kmajor || d0.b_kmajor != d1.b_kmajor ||
+      !pair_ok(d0) || !pair_ok(d1)) {
+    const cudaError_t e = gemm(d0, st);
+    return e != cudaSuccess ? e : gemm(d1, st);
+  }
+  if (d0.a_kmajor && d0.b_kmajor) return launch_pair<false, false, EPI_F32_ACC>(d0, st, &d1);
+  if (d0.a_kmajor && !d0.b_kmajor) return launch_pair<false, true, EPI_F32_ACC>(d0, st, &d1);
+  if (!d0.a_kmajor && !d0.b_kmajor) return launch_pair<true, true, EPI_F32_ACC>(d0, st, &d1);
+  return launch_pair<true, false, EPI_F32_ACC>(d0, st, &d1);
 }
 
 namespace {

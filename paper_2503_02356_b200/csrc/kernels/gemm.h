@@ -73,6 +73,10 @@ cudaError_t ce_finish(const float* part, int64_t nparts, const float* tlogit, co
                       float* lse, float* row_loss, cudaStream_t st);
 
 cudaError_t gemm(const GemmDesc& d, cudaStream_t st);
+// Two EPI_F32_ACC GEMMs with the same operand majors in one CTA-pair launch
+// (their tiles share the persistent grid's waves); falls back to two gemm()
+// calls when either would not take the pair kernel.
+cudaError_t gemm2(const GemmDesc& d0, const GemmDesc& d1, cudaStream_t st);
 // Whether EPI_BF16_SWIGLU is available for this problem (else run EPI_BF16
 // and the elementwise swiglu_fwd).
 bool gemm_swiglu_ok(int64_t M, int64_t N, int64_t K);

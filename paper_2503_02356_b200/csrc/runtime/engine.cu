@@ -980,6 +980,17 @@ struct Exec {
     close(t0, 0, 2.0 * static_cast<double>(M) * static_cast<double>(N) * static_cast<double>(K), 1);
   }
 
+  // Two weight-gradient GEMMs (EPI_F32_ACC) in one CTA-pair launch when the
+  // kernel can take both (cfk::gemm2), so their tiles share the last wave.
+  void gemm_wgrad2(const cfk::GemmDesc& d0, const cfk::GemmDesc& d1) {
+    cudaEvent_t t0 = mark();
+    L(cfk::gemm2(d0, d1, s), "gemm2");
+    close(t0, 0,
+          2.0 * (static_cast<double>(d0.M) * static_cast<double>(d0.N) * static_cast<double>(d0.K) +
+                 static_cast<double>(d1.M) * static_cast<double>(d1.N) * static_cast<double>(d1.K)),
+          1);
+  }
+
   void gemm_desc(const cfk::GemmDesc& d) {
     cudaEvent_t t0 = mark();
     L(cfk::gemm(d, s), "gemm");
@@ -1334,11 +1345,20 @@ struct Exec {
         gemm(xb, 1, d, ly.w2, 1, d, dh, m->ffn, T, m->ffn, d, cfk::EPI_BF16);
         const bf16* hl = t.h ? t.h + l * T * m->ffn : A;
         if (!t.h) L(cfk::swiglu_fwd(act, T, m->ffn, A, s), "swiglu");  // recompute h
-        gemm(hl, 0, m->ffn, xb, 0, d, ly.d_w2, d, m->ffn, d, T, cfk::EPI_F32_ACC);
+        // down and gate|up weight gradients in one launch when h and xn2 are
+        // tape-resident (xb, their shared dY operand, lives until norm_bwd)
+        const cfk::GemmDesc dw2{hl, m->ffn, 0, xb, d, 0, ly.d_w2, d, nullptr, 0, m->ffn, d, T, cfk::EPI_F32_ACC};
+        const bool group_ffn = t.h && t.xn2;
+        if (!group_ffn) gemm_desc(dw2);
         L(cfk::swiglu_bwd(act, dh, T, m->ffn, dgu, s), "swiglu_bwd");
         const bf16* xn2 = t.xn2 ? t.xn2 + l * T * d : A;
         if (!t.xn2) L(cfk::rmsnorm_fwd(xm, ly.g2, T, d, eps, A, s), "rmsnorm");  // recompute xn2
-        gemm(xn2, 0, d, dgu, 0, m->gu_w, ly.d_w1, m->gu_w, d, m->gu_w, T, cfk::EPI_F32_ACC);
+        const cfk::GemmDesc dw1{xn2, d, 0, dgu, m->gu_w, 0, ly.d_w1, m->gu_w, nullptr, 0, d, m->gu_w, T,
+                                cfk::EPI_F32_ACC};
+        if (group_ffn)
+          gemm_wgrad2(dw2, dw1);
+        else
+          gemm_desc(dw1);
         gemm(dgu, 1, m->gu_w, ly.w1, 1, m->gu_w, da, d, T, d, m->gu_w, cfk::EPI_F32);
         norm_bwd(xm, ly.g2, dx, dmid, ly.d_g2);
       } else {
@@ -1352,7 +1372,9 @@ struct Exec {
       if (!fused) L(cfk::to_bf16(dmid, xb, T * d, s), "to_bf16");
       bf16* dO = A;  // reuse
       gemm(xb, 1, d, ly.wo, 1, d, dO, d, T, d, d, cfk::EPI_BF16);
-      gemm(O, 0, d, xb, 0, d, ly.d_wo, d, d, d, T, cfk::EPI_F32_ACC);
+      // the o weight gradient joins the q|k|v one below (same launch): O is
+      // tape-resident and xb is not rewritten before norm_bwd
+      const cfk::GemmDesc dwo{O, d, 0, xb, d, 0, ly.d_wo, d, nullptr, 0, d, d, T, cfk::EPI_F32_ACC};
       // Attention (toy_model.hpp:436-495)
       if (cm.dependent && gs->offload) kv_stage(cm, gs, l, true);
       AttnParams p = attn_params(cm, t, l, gs);
@@ -1407,7 +1429,7 @@ struct Exec {
         else
           L(cfk::to_bf16(x, A, T * d, s), "to_bf16");
       }
-      gemm(xn1, 0, d, dqkv, 0, qw, ly.d_wqkv, qw, d, qw, T, cfk::EPI_F32_ACC);
+      gemm_wgrad2(dwo, cfk::GemmDesc{xn1, d, 0, dqkv, qw, 0, ly.d_wqkv, qw, nullptr, 0, d, qw, T, cfk::EPI_F32_ACC});
       if (m->llama) {
         gemm(dqkv, 1, qw, ly.wqkv, 1, qw, da, d, T, d, qw, cfk::EPI_F32);
         norm_bwd(x, ly.g1, dmid, dx, ly.d_g1);
