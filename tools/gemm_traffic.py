@@ -12,13 +12,18 @@ FWD = [("qkv fwd +rope", T, d + 2 * kvw, d, BF16), ("o fwd +res", T, d, d, RES),
        ("down fwd +res", T, d, ffn, RES)] * 2
 # the backward starts with the fused-CE head: dlogits rebuilt from the LSE by
 # a recompute of the head GEMM (EPI_CE_GRAD, bf16 out), then head wgrad/dgrad
+# (round 2: the down + gate|up and o + q|k|v weight gradients run as one
+# grouped launch each; their rows list both problems)
 BWD = [("head ce-grad", T, V, d, BF16), ("head wgrad", d, V, T, ACC), ("head dgrad", T, d, V, F32),
-       ("down dgrad", T, ffn, d, BF16), ("down wgrad", ffn, d, T, ACC), ("gate|up wgrad", d, 2 * ffn, T, ACC),
-       ("gate|up dgrad", T, d, 2 * ffn, F32), ("o dgrad", T, d, d, BF16)]
+       ("down dgrad", T, ffn, d, BF16), ("down+gate|up wgrad", [(ffn, d, T), (d, 2 * ffn, T)], None, None, ACC),
+       ("gate|up dgrad", T, d, 2 * ffn, F32), ("o dgrad", T, d, d, BF16),
+       ("o+qkv wgrad", [(d, d, T), (d, d + 2 * kvw, T)], None, None, ACC)]
 
 
 def algorithmic(M, N, K, epi):
     c = {BF16: 2, F32: 4, ACC: 8, RES: 8, SWIGLU: 3}[epi]  # SWIGLU: gate|up + h (N/2 columns) in bf16
+    if isinstance(M, list):  # grouped launch: the sum over its problems
+        return sum(algorithmic(m, n, k, epi) for m, n, k in M)
     return 2 * (M * K + N * K) + c * M * N
 
 

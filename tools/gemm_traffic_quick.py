@@ -40,7 +40,8 @@ def main():
         for (name, M, N, K, epi), l in zip(FWD + BWD, launches):
             dram = l["dram__bytes_read.sum"] + l["dram__bytes_write.sum"]
             a = algorithmic(M, N, K, epi)
-            rows.append({"shape": name, "M": M, "N": N, "K": K, "dram_bytes": dram, "algorithmic_bytes": a,
+            rows.append({"shape": name, "M": M, "N": N, "K": K if K is not None else M[0][2], "dram_bytes": dram,
+                         "algorithmic_bytes": a,
                          "ratio": dram / a, "duration_us": l["gpu__time_duration.sum"] * 1e6})
         tot_d = sum(r["dram_bytes"] for r in rows)
         tot_a = sum(r["algorithmic_bytes"] for r in rows)
