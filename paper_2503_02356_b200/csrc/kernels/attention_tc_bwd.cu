@@ -10,6 +10,7 @@
 //   softmax:      P/dS(i) from TMEM -> bf16 -> swizzled smem  |  P/dS(i+1)
 //
 // TMEM: S0 S1 dP0 dP1 (4 x 64 cols) + accumulators (dQ: 128; dV + dK: 256).
+#include <algorithm>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -467,6 +468,305 @@ __global__ void __launch_bounds__(kThreads, 1)
                              pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
       }
     }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------- dQ, persistent
+// dq_kernel's math and 64-key sub-tiles for packed short segments, with one
+// CTA per SM looping over (128-query tile, q head) items (item = blockIdx.x
+// + k * gridDim.x): TMEM and barriers are set up once, the producer streams
+// the next item's K/V while the current one drains, and the softmax warps
+// stage the next item's Q / dO into TMEM (the A operands are free once the
+// item's last MMA has completed) before reading out the current dQ, so the
+// MMA issuer starts the next item while the dQ row stores run.  Ring slots
+// and the S / dP buffer parity run on counters that continue across items.
+__device__ __forceinline__ void item_of(const Args& a, int nq, int item, AttnTile& tl, AttnSeg& sg, int& h) {
+  h = item / nq;
+  tl = a.tiles[item - h * nq];
+  sg = a.segs[tl.seg];
+}
+__global__ void __launch_bounds__(kThreads, 1)
+    dq_persist_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a,
+                      int nq) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;                    // KS stages x 2 x [64][64]
+  uint8_t* sV = sK + KS * 2 * kBox64;  // VS stages
+  uint8_t* sS = sV + VS * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
+  float* sRowD = reinterpret_cast<float*>(sS + 2 * kBox128);  // [2 half][128 rows]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRowD + 256);
+  uint64_t* q_full = bar;
+  uint64_t* k_full = bar + 1;              // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [VS]
+  uint64_t* v_empty = v_full + VS;         // [VS]
+  uint64_t* s_full = v_empty + VS;         // [2]
+  uint64_t* s_free = s_full + 2;           // [2]
+  uint64_t* ds_full = s_free + 2;          // [2]
+  uint64_t* ds_free = ds_full + 2;         // [2]
+  uint64_t* dq_done = ds_free + 2;         // MMA: the item's last MMA completed
+  uint64_t* dq_free = dq_done + 1;         // softmax: the item's dQ read out
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_free + 1);
+
+  const int items = nq * a.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = a.H / a.KVH;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(q_full, 8);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&ds_full[i], 8);
+      mbar_init(&ds_free[i], 1);
+    }
+    mbar_init(dq_done, 1);
+    mbar_init(dq_free, 8);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tQ = tmem + 256, tAq = tmem + 384, tAo = tmem + 448;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      int jj = 0;  // sub-tiles loaded so far (ring position)
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        AttnTile tl;
+        AttnSeg sg;
+        int h;
+        item_of(a, nq, item, tl, sg, h);
+        const int g = h / per;
+        const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+        for (int j = 0; j < nkt; ++j, ++jj) {
+          const int sk = jj % KS, sv = jj % VS;
+          const int krow = sg.kv_row0 + j * SUB;
+          stress_delay(a.stress, 1, jj);
+          mbar_wait(&v_empty[sv], ((jj / VS) & 1) ^ 1);
+          mbar_expect_tx(&v_full[sv], 2 * kBox64);
+          tma_load_2d(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
+          tma_load_2d(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
+          mbar_wait(&k_empty[sk], ((jj / KS) & 1) ^ 1);
+          mbar_expect_tx(&k_full[sk], 2 * kBox64);
+          tma_load_2d(sK + sk * 2 * kBox64, &tmK, &k_full[sk], g * DH, krow);
+          tma_load_2d(sK + sk * 2 * kBox64 + kBox64, &tmK, &k_full[sk], g * DH + 64, krow);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);
+    constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);
+    const uint32_t sK0 = smem_u32(sK), sV0 = smem_u32(sV), sS0 = smem_u32(sS);
+    const uint32_t bKf = smem_u32(k_full), bKe = smem_u32(k_empty), bVf = smem_u32(v_full),
+                   bVe = smem_u32(v_empty), bSf = smem_u32(s_full), bSr = smem_u32(s_free),
+                   bDf = smem_u32(ds_full), bDr = smem_u32(ds_free), bQf = smem_u32(q_full),
+                   bQd = smem_u32(dq_done), bQr = smem_u32(dq_free);
+    int ik = 0, iv = 0, ck = 0;
+    uint32_t pk = 0, pv = 0;
+    auto issue_s = [&](int J) {
+      const uint32_t b = J & 1;
+      mbar_wait_s(bKf + ik * 8, pk);
+      mbar_wait_s(bVf + iv * 8, pv);
+      mbar_wait_s(bSr + b * 8, ((J >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t k0 = sK0 + ik * 2 * kBox64, v0 = sV0 + iv * 2 * kBox64;
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq, kdesc(k0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq + 32, kdesc(k0, kBox64, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo, kdesc(v0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo + 32, kdesc(v0, kBox64, 4), idS, 1u);
+      umma_commit_w(bVe + iv * 8);
+      umma_commit_w(bSf + b * 8);
+      if (++ik == KS) { ik = 0; pk ^= 1; }
+      if (++iv == VS) { iv = 0; pv ^= 1; }
+    };
+    int J0 = 0, n = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, item, tl, sg, h);
+      const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+      mbar_wait_s(bQf, n & 1);  // this item's Q / dO staged
+      tc_fence_after();
+      issue_s(J0);
+      for (int j = 0; j < nkt; ++j) {
+        const int J = J0 + j;
+        stress_delay(a.stress, 2, J);
+        if (j + 1 < nkt) issue_s(J + 1);
+        const uint32_t b = J & 1;
+        mbar_wait_s(bDf + b * 8, (J >> 1) & 1);
+        if (j == 0 && n > 0) mbar_wait_s(bQr, (n - 1) & 1);  // previous item's dQ read out
+        tc_fence_after();
+        const uint32_t s0 = sS0 + b * kBox128, k0 = sK0 + ck * 2 * kBox64;
+        umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 0), mndesc(k0, kBox64, 0), idQ, j > 0 ? 1u : 0u);
+        umma_commit_w(bKe + ck * 8);
+        umma_commit_w(bDr + b * 8);
+        if (++ck == KS) ck = 0;
+      }
+      umma_commit_w(bQd);
+      J0 += nkt;
+    }
+  } else {
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t bSf = smem_u32(s_full), bSr = smem_u32(s_free), bDf = smem_u32(ds_full),
+                   bDr = smem_u32(ds_free), sS0 = smem_u32(sS), bQd = smem_u32(dq_done), bQr = smem_u32(dq_free);
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
+    // stage item `it`'s Q / dO rows into TMEM and return D = rowsum(dO * O)
+    auto stage = [&](int it, int rnd) -> float {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, it, tl, sg, h);
+      const int qi = tl.first + row;
+      const bool ok = qi < sg.len && row < tl.count;
+      const bool rok = row < tl.count;
+      const int64_t r = sg.q_start + tl.first + row;
+      stage_row_tmem(tAq + lane_off + half * 32, a.q + r * a.q_stride + static_cast<int64_t>(h) * DH + half * 64, rok);
+      const float dpart = stage_row_tmem(
+          tAo + lane_off + half * 32, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + half * 64, ok,
+          a.o + r * a.o_stride + static_cast<int64_t>(h) * DH + half * 64);
+      tmem_st_wait();
+      tc_fence_before();
+      warp_arrive(q_full);
+      // the two half-rows meet in smem (fixed order); rnd alternates the
+      // buffer so a fast warp pair cannot overwrite a slot still being read
+      sRowD[half * 128 + row] = dpart;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const float D = sRowD[row] + sRowD[128 + row];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      if (ok && half == 0) a.dsum[static_cast<int64_t>(h) * a.T + r] = D;
+      (void)rnd;
+      return D;
+    };
+    int J0 = 0, n = 0;
+    float D = blockIdx.x < items ? stage(blockIdx.x, 0) : 0.f;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, item, tl, sg, h);
+      const int q_row0 = sg.q_start + tl.first;
+      const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+      const int qi = tl.first + row;
+      const bool ok = qi < sg.len && row < tl.count;
+      const int lim = sg.prefix + min(qi, sg.len - 1);
+      const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
+      const int klim = ok ? lim : -1;
+      const int tile_lim = sg.prefix + tl.first;
+      const float2 sl2v = make_float2(a.sl2, a.sl2), nl = make_float2(-lse2, -lse2), nD = make_float2(-D, -D);
+      for (int j = 0; j < nkt; ++j) {
+        const int J = J0 + j;
+        const uint32_t b = J & 1;
+        mbar_wait_s(bSf + b * 8, (J >> 1) & 1);
+        tc_fence_after();
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tmem + b * 64 + lane_off + half * 32, rs);
+        tmem_ld32(tmem + 128 + b * 64 + lane_off + half * 32, rp);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bSr + b * 8);
+        uint32_t pk[16];
+        auto body = [&](auto masked) {
+          const int key0 = j * SUB + half * 32;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x = ffma2(make_float2(__uint_as_float(rs[2 * e]), __uint_as_float(rs[2 * e + 1])), sl2v, nl);
+            float2 p = make_float2(ex2(x.x), ex2(x.y));
+            if constexpr (decltype(masked)::value) {
+              p.x = key0 + 2 * e <= klim ? p.x : 0.f;
+              p.y = key0 + 2 * e + 1 <= klim ? p.y : 0.f;
+            }
+            const float2 ds =
+                fmul2(p, fadd2(make_float2(__uint_as_float(rp[2 * e]), __uint_as_float(rp[2 * e + 1])), nD));
+            pk[e] = pack_bf16(ds.x, ds.y);
+          }
+        };
+        if (j * SUB + SUB - 1 <= tile_lim)
+          body(std::false_type{});
+        else
+          body(std::true_type{});
+        stress_delay(a.stress, 3, J);
+        if (J >= 2) mbar_wait_s(bDr + b * 8, ((J >> 1) & 1) ^ 1);
+        const uint32_t dst = sS0 + b * kBox128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          sts128(dst + dst_off[c], make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+        fence_async_smem();
+        warp_arrive_s(bDf + b * 8);
+      }
+      J0 += nkt;
+      mbar_wait_s(bQd, n & 1);  // every MMA of this item done: Q / dO / dQ settled
+      tc_fence_after();
+      // the next item's Q / dO go into TMEM now, so its S / dP overlap this
+      // item's dQ read-out
+      const int next = item + gridDim.x;
+      const float Dn = next < items ? stage(next, n + 1) : 0.f;
+      __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+      if (a.rope_tab) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tQ + lane_off + half * 32, ra);
+        tmem_ld32(tQ + lane_off + (half + 2) * 32, rb);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bQr);
+        if (ok) {
+          float fa[32], fb[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            fa[e] = bf16_round(__uint_as_float(ra[e]) * a.scale);
+            fb[e] = bf16_round(__uint_as_float(rb[e]) * a.scale);
+          }
+          rope_inverse32(a.rope_tab + static_cast<int64_t>(q_row0 + row) * (DH / 2) + half * 32, fa, fb);
+          store_bf16x32(out + half * 32, fa);
+          store_bf16x32(out + (half + 2) * 32, fb);
+        }
+      } else {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tQ + lane_off + (half * 2) * 32, r0);
+        tmem_ld32(tQ + lane_off + (half * 2 + 1) * 32, r1);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bQr);
+        if (ok) {
+          const float sc = a.scale;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t* r = cc ? r1 : r0;
+            uint4* d4 = reinterpret_cast<uint4*>(out + (half * 2 + cc) * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              d4[q] = make_uint4(pack_bf16(__uint_as_float(r[8 * q]) * sc, __uint_as_float(r[8 * q + 1]) * sc),
+                                 pack_bf16(__uint_as_float(r[8 * q + 2]) * sc, __uint_as_float(r[8 * q + 3]) * sc),
+                                 pack_bf16(__uint_as_float(r[8 * q + 4]) * sc, __uint_as_float(r[8 * q + 5]) * sc),
+                                 pack_bf16(__uint_as_float(r[8 * q + 6]) * sc, __uint_as_float(r[8 * q + 7]) * sc));
+          }
+        }
+      }
+      D = Dn;
     }
   }
   tc_fence_before();
@@ -1080,6 +1380,25 @@ bool dq_wide(const AttnParams& p) {
   return v >= 0 ? v == 1 : p.keys_per_query >= 3072.0;
 }
 
+// CF_DQ_PERSIST=0 falls back to one CTA per (tile, head) for the 64-key dQ
+// kernel (A/B); default: the persistent kernel
+int dq_persist() {
+  static const int v = [] {
+    const char* e = std::getenv("CF_DQ_PERSIST");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+int attn_num_sms() {
+  static const int n = [] {
+    int dev = 0, c = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
+  }();
+  return n;
+}
+
 int g_attn_stress = 0;
 void set_attn_stress(int on) { g_attn_stress = on ? 1 : 0; }
 
@@ -1111,6 +1430,12 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
     attr = smem_optin(reinterpret_cast<const void*>(dq_wide_kernel), static_cast<int>(smem_w));
     if (attr != cudaSuccess) return attr;
     dq_wide_kernel<<<dim3(nq, p.H), kDqWideThreads, smem_w, st>>>(k128, v128, a);
+  } else if (dq_persist()) {
+    const int items = nq * p.H;
+    const int grid = std::min(items, attn_num_sms());
+    attr = smem_optin(reinterpret_cast<const void*>(dq_persist_kernel), static_cast<int>(smem_dq));
+    if (attr != cudaSuccess) return attr;
+    dq_persist_kernel<<<grid, kThreads, smem_dq, st>>>(k64, v64, a, nq);
   } else {
     dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   }

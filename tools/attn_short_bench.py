@@ -15,7 +15,7 @@ H, KVH, dh = 32, 8, 128
 short = capi.synthesize(999, 1, preset=0, bounds=[1024], fracs=[1.0], max_length=1024)
 plan = cf.Plan.build(short, 8192, 1)
 ch, sg, _, _ = plan.export()
-c0 = ch[0]
+c0 = ch[int(sys.argv[1]) if len(sys.argv) > 1 else 0]  # chunk index (FFD order: 0 holds the longest shorts)
 lens = [int(x["length"]) for x in sg[c0["seg_offset"]:c0["seg_offset"] + c0["seg_count"]]]
 segs, q0 = [], 0
 for L in lens:
