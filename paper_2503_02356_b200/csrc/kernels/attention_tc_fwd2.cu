@@ -34,6 +34,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescale = 8.0f;
 constexpr int KS = 2, VS = 2;  // K / V ring depths
+#ifndef CF_FWD_DIAG
+#define CF_FWD_DIAG 0
+#endif
 constexpr int kThreads = 576;  // 16 softmax warps + TMA + MMA
 
 struct Args {
@@ -207,6 +210,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < nkt; ++j) {
       mbar_wait(&s_full[w], j & 1);
       tc_fence_after();
+#if CF_FWD_DIAG  // diagnostics: softmax side skipped (MMA + TMA pipeline only)
+      tc_fence_before();
+      warp_arrive(&p_full[w]);
+      continue;
+#endif
       const int key0 = j * TK + half * 64;
       const bool full = j * TK + TK - 1 <= sg.prefix + tl.first;
       // this half-row of S, read from TMEM once (kept as raw bits)
