@@ -66,6 +66,14 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
       "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -248,19 +256,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       // scalar order (ps[e & 3] += p0 + p1) so l stays bitwise what the
       // operator-level segment path reproduces
       float ps[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[32];
       const float2 sl2v = make_float2(sl2, sl2), nm = make_float2(-m, -m);
+      // P (bf16 pairs) over S columns [0, 64), stored per 32-key half as soon
+      // as it is packed, so a half's S registers die early (no spills)
 #pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const float2 x = ffma2(make_float2(__uint_as_float(r[e >> 4][(2 * e) & 31]),
-                                           __uint_as_float(r[e >> 4][(2 * e + 1) & 31])),
-                               sl2v, nm);
-        const float2 p = make_float2(ex2(x.x), ex2(x.y));
-        ps[e & 3] += p.x + p.y;
-        pk[e] = pack_bf16(p.x, p.y);
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float2 x = ffma2(make_float2(__uint_as_float(r[hh][2 * e]), __uint_as_float(r[hh][2 * e + 1])),
+                                 sl2v, nm);
+          const float2 p = make_float2(ex2(x.x), ex2(x.y));
+          ps[e & 3] += p.x + p.y;
+          pk[e] = pack_bf16(p.x, p.y);
+        }
+        tmem_st16(tS + half * 32 + hh * 16, pk);
       }
       l = fmaf(l, alpha, (ps[0] + ps[1]) + (ps[2] + ps[3]));
-      tmem_st32(tS + half * 32, pk);  // P (bf16 pairs) over S columns [0, 64)
       if (rescale) {  // after P (S registers dead); PV_w(j-1) is complete (s_full_w(j) followed it)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
