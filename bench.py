@@ -241,7 +241,7 @@ def _ref_worker(kind, sl, st, ids):
     lib.run_plan(c1_cfg(), np.array(sl), np.array(st, np.int32), 512, 2, ids=np.array(ids, np.int64))
 
 
-def gpu_c1_side_by_side(ctx, steps=3):
+def gpu_c1_side_by_side(ctx, steps=10):
     """The GPU on the same C1 workload (toy model, C1 batch, chunk 512, K=2)
     through the public call (plan build + cf_run_plan with host buffers),
     device-timed: the like-for-like counterpart of the CPU baseline."""
@@ -250,7 +250,7 @@ def gpu_c1_side_by_side(ctx, steps=3):
     lengths, tokens, _ = _c1_workload()
     model = cf.Model(ctx, cf.model_cfg(arch=0, vocab=256, d=256, heads=4, kv_heads=2, layers=2, seed=1))
     stream = torch.cuda.ExternalStream(ctx.stream)
-    for _ in range(2):
+    for _ in range(3):
         model.run_plan(cf.Plan.build(lengths, 512, 2), lengths, tokens)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.synchronize()
