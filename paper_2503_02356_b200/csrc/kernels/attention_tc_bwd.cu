@@ -171,6 +171,69 @@ __device__ __forceinline__ float stage_row_tmem(uint32_t taddr, const __nv_bfloa
   return acc;
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st32w(uint32_t taddr, const uint32_t (&w)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]),
+      "r"(w[19]), "r"(w[20]), "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+      "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
+      : "memory");
+}
+// stage_row_tmem for the Q and dO half-rows of one query row together, with
+// the D = rowsum(dO * O) partial: all 24 global loads are issued before the
+// first tcgen05.st, so the three row fetches cost one memory latency instead
+// of three (short-chunk items are latency-bound).  Same values and the same
+// D arithmetic order as stage_row_tmem.
+__device__ __forceinline__ float stage_qdo_tmem(uint32_t tq, uint32_t tdo, const __nv_bfloat16* q,
+                                                const __nv_bfloat16* dout, const __nv_bfloat16* o, bool rok,
+                                                bool ok) {
+  uint32_t wq[32], wd[32];
+  uint4 ov[8];
+  const uint4* q4 = reinterpret_cast<const uint4*>(q);
+  const uint4* d4 = reinterpret_cast<const uint4*>(dout);
+  const uint4* o4 = reinterpret_cast<const uint4*>(o);
+  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 v = rok ? __ldg(q4 + c) : z;
+    wq[4 * c] = v.x;
+    wq[4 * c + 1] = v.y;
+    wq[4 * c + 2] = v.z;
+    wq[4 * c + 3] = v.w;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 v = ok ? __ldg(d4 + c) : z;
+    wd[4 * c] = v.x;
+    wd[4 * c + 1] = v.y;
+    wd[4 * c + 2] = v.z;
+    wd[4 * c + 3] = v.w;
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) ov[c] = ok ? __ldg(o4 + c) : z;
+  tmem_st32w(tq, wq);
+  tmem_st32w(tdo, wd);
+  if (!ok) return 0.f;
+  float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t ow[4] = {ov[c].x, ov[c].y, ov[c].z, ov[c].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&wd[4 * c + e]);
+      const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+      part[e] = fmaf(__low2float(a2), __low2float(b2), part[e]);
+      part[e] = fmaf(__high2float(a2), __high2float(b2), part[e]);
+    }
+  }
+  return (part[0] + part[1]) + (part[2] + part[3]);
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 constexpr int kThreads = 320;
 // dK/dV kernel: 16 softmax-side warps (4 per TMEM lane quarter, 16 query
 // columns each) + TMA + MMA; 576 threads cap registers at 96 per thread
@@ -645,10 +708,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool ok = qi < sg.len && row < tl.count;
       const bool rok = row < tl.count;
       const int64_t r = sg.q_start + tl.first + row;
-      stage_row_tmem(tAq + lane_off + half * 32, a.q + r * a.q_stride + static_cast<int64_t>(h) * DH + half * 64, rok);
-      const float dpart = stage_row_tmem(
-          tAo + lane_off + half * 32, a.dout + r * a.dout_stride + static_cast<int64_t>(h) * DH + half * 64, ok,
-          a.o + r * a.o_stride + static_cast<int64_t>(h) * DH + half * 64);
+      const int64_t hc = static_cast<int64_t>(h) * DH + half * 64;
+      const float dpart = stage_qdo_tmem(tAq + lane_off + half * 32, tAo + lane_off + half * 32,
+                                         a.q + r * a.q_stride + hc, a.dout + r * a.dout_stride + hc,
+                                         a.o + r * a.o_stride + hc, rok, ok);
       tmem_st_wait();
       tc_fence_before();
       warp_arrive(q_full);
@@ -677,6 +740,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float lse2 = ok ? a.lse[static_cast<int64_t>(h) * a.T + q_row0 + row] * kLog2e : 0.f;
       const int klim = ok ? lim : -1;
       const int tile_lim = sg.prefix + tl.first;
+      {
+        // pull the next item's Q / dO / O half-rows into L2 now, so staging
+        // them after this item's last MMA waits on L2, not HBM
+        const int nx = item + gridDim.x;
+        if (nx < items) {
+          AttnTile tn;
+          AttnSeg sn;
+          int hn;
+          item_of(a, nq, nx, tn, sn, hn);
+          if (row < tn.count) {
+            const int64_t r = sn.q_start + tn.first + row;
+            const int64_t hc = static_cast<int64_t>(hn) * DH + half * 64;
+            prefetch_l2(a.q + r * a.q_stride + hc);
+            prefetch_l2(a.dout + r * a.dout_stride + hc);
+            prefetch_l2(a.o + r * a.o_stride + hc);
+          }
+        }
+      }
       const float2 sl2v = make_float2(a.sl2, a.sl2), nl = make_float2(-lse2, -lse2), nD = make_float2(-D, -D);
       for (int j = 0; j < nkt; ++j) {
         const int J = J0 + j;
@@ -1189,11 +1270,31 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     const bool kok = row < tl.count && key < kv_len;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     {
+      // K and V quarter-rows: both fetches in flight before either tcgen05.st
       const int64_t r = sg.kv_row0 + key;
-      stage_row_tmem16(tAk + lane_off + part * 16, a.k + r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32,
-                       kok);
-      stage_row_tmem16(tAv + lane_off + part * 16, a.v + r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32,
-                       kok);
+      const int64_t off = r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32;
+      const uint4* k4 = reinterpret_cast<const uint4*>(a.k + off);
+      const uint4* v4 = reinterpret_cast<const uint4*>(a.v + off);
+      uint32_t wk[16], wv[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint4 x = kok ? __ldg(k4 + c) : make_uint4(0u, 0u, 0u, 0u);
+        const uint4 y = kok ? __ldg(v4 + c) : make_uint4(0u, 0u, 0u, 0u);
+        wk[4 * c] = x.x, wk[4 * c + 1] = x.y, wk[4 * c + 2] = x.z, wk[4 * c + 3] = x.w;
+        wv[4 * c] = y.x, wv[4 * c + 1] = y.y, wv[4 * c + 2] = y.z, wv[4 * c + 3] = y.w;
+      }
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tAk + lane_off + part * 16),
+          "r"(wk[0]), "r"(wk[1]), "r"(wk[2]), "r"(wk[3]), "r"(wk[4]), "r"(wk[5]), "r"(wk[6]), "r"(wk[7]), "r"(wk[8]),
+          "r"(wk[9]), "r"(wk[10]), "r"(wk[11]), "r"(wk[12]), "r"(wk[13]), "r"(wk[14]), "r"(wk[15])
+          : "memory");
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tAv + lane_off + part * 16),
+          "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3]), "r"(wv[4]), "r"(wv[5]), "r"(wv[6]), "r"(wv[7]), "r"(wv[8]),
+          "r"(wv[9]), "r"(wv[10]), "r"(wv[11]), "r"(wv[12]), "r"(wv[13]), "r"(wv[14]), "r"(wv[15])
+          : "memory");
       tmem_st_wait();
       tc_fence_before();
       warp_arrive(kv_full);
