@@ -347,6 +347,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 //     warps' read-out of O_w(n).
 // Per item, every value is computed in the same order as attn_fwd_pp_kernel,
 // so the two kernels' outputs are bitwise equal.
+__device__ __forceinline__ int nctaid_x() {
+  int v;
+  asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(v));
+  return v;
+}
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_pp_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                                const __grid_constant__ CUtensorMap tmV, Args a, int ntiles) {
@@ -511,22 +516,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tS = tmem + 256 * w + lane_off, tO = tS + 128;
     const uint32_t red = smem_u32(sRed) + w * 2048;  // [2 parity][2 half][128 rows] per head
     const float sl2 = a.sl2;
-    int J = 0, n = 0, x = 0;  // key tiles so far, items so far, half-row exchanges so far
-    for (int it = blockIdx.x; it < items; it += gridDim.x, ++n) {
-      AttnTile tl;
-      AttnSeg sg;
-      int h0;
-      item_of(it, tl, sg, h0);
-      const int q_row0 = sg.q_start + tl.first;
-      const int nkt = (sg.prefix + tl.first + tl.count + TK - 1) / TK;
-      const int qi = tl.first + row;
-      const int lim = sg.prefix + min(qi, sg.len - 1);
+    // key tiles so far, items so far; half-row exchanges so far = J + n (one
+    // per key tile and one per item), their parity picks the smem buffer
+    int J = 0, n = 0;
+    // the grid size is re-read from %nctaid at each step (ptxas otherwise
+    // spills it across the key loop at this warp role's 96-register budget)
+    for (int it = blockIdx.x; it < items; it += nctaid_x(), ++n) {
+      int nkt, lim, tile_lo;
+      {
+        AttnTile tl;
+        AttnSeg sg;
+        int h0;
+        item_of(it, tl, sg, h0);
+        nkt = (sg.prefix + tl.first + tl.count + TK - 1) / TK;
+        lim = sg.prefix + min(tl.first + row, sg.len - 1);
+        tile_lo = sg.prefix + tl.first;
+      }
       float m = -FLT_MAX, l = 0.f;
       for (int j = 0; j < nkt; ++j, ++J) {
         mbar_wait(&s_full[w], J & 1);
         tc_fence_after();
         const int key0 = j * TK + half * 64;
-        const bool full = j * TK + TK - 1 <= sg.prefix + tl.first;
+        const bool full = j * TK + TK - 1 <= tile_lo;
         uint32_t r[2][32];
         tmem_ld32(tS + half * 64, r[0]);
         tmem_ld32(tS + half * 64 + 32, r[1]);
@@ -540,8 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int e = 0; e < 64; ++e) pm[e & 3] = fmaxf(pm[e & 3], __uint_as_float(r[e >> 5][e & 31]));
         float tmax = fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3]));
-        const uint32_t xb = red + (x & 1) * 1024;
-        ++x;
+        const uint32_t xb = red + ((J + n) & 1) * 1024;
         sts_f32(xb + (half * 128 + row) * 4, tmax);
         asm volatile("bar.sync %0, 64;" ::"r"(1 + w * 4 + quarter) : "memory");
         tmax = fmaxf(tmax, lds_f32(xb + ((half ^ 1) * 128 + row) * 4)) * sl2;
@@ -589,15 +599,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         warp_arrive(&p_full[w]);
       }
-      const uint32_t xb = red + (x & 1) * 1024;
-      ++x;
+      const uint32_t xb = red + ((J + n) & 1) * 1024;
       sts_f32(xb + (half * 128 + row) * 4, l);
       asm volatile("bar.sync %0, 64;" ::"r"(1 + w * 4 + quarter) : "memory");
       l += lds_f32(xb + ((half ^ 1) * 128 + row) * 4);
       mbar_wait(&o_done[w], n & 1);
       tc_fence_after();
+      // the item's rows / head, re-read here so they are not live across the
+      // key loop (register budget: 96 per thread at 576 threads)
+      AttnTile tl;
+      AttnSeg sg;
+      int h0;
+      item_of(it, tl, sg, h0);
+      const int q_row0 = sg.q_start + tl.first;
       const int h = h0 + w;
-      const bool ok = qi < sg.len && row < tl.count;
+      const bool ok = tl.first + row < sg.len && row < tl.count;
       const float inv = 1.f / l;
       __nv_bfloat16* orow =
           a.o + static_cast<int64_t>(q_row0 + row) * a.o_stride + static_cast<int64_t>(h) * DH + half * 64;
