@@ -57,6 +57,26 @@ constexpr int QS = CF_DKV_QS;                // dK/dV kernel: Q/dO ring depth
 constexpr uint32_t kBox128 = 128 * 64 * 2;  // [128 rows][64 cols] bf16
 constexpr uint32_t kBox64 = 64 * 64 * 2;    // [64 rows][64 cols]
 constexpr float kLog2e = 1.4426950408889634f;
+// CF_ATTN_TRACE=1 (diagnostic builds only): CTA 0 of the persistent dQ
+// kernel stamps clock64 at its pipeline events (role 0 = MMA issuer, 1 =
+// softmax warp 0, 2 = TMA producer); the host writes them to $CF_TRACE_OUT.
+#ifndef CF_ATTN_TRACE
+#define CF_ATTN_TRACE 0
+#endif
+#if CF_ATTN_TRACE
+__device__ unsigned long long g_trace[3][8192];
+__device__ int g_trace_n[3];
+#define TR(role, ev, J)                                                                                  \
+  do {                                                                                                 \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                                                  \
+      const int i_ = g_trace_n[role]++;                                                                \
+      if (i_ < 8192)                                                                                   \
+        g_trace[role][i_] = (static_cast<unsigned long long>(clock64()) << 20) | ((ev) << 16) | ((J) & 0xffff); \
+    }                                                                                                  \
+  } while (0)
+#else
+#define TR(role, ev, J) ((void)0)
+#endif
 
 struct Args {
   const AttnSeg* segs;
@@ -230,6 +250,69 @@ __device__ __forceinline__ float stage_qdo_tmem(uint32_t tq, uint32_t tdo, const
     }
   }
   return (part[0] + part[1]) + (part[2] + part[3]);
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+// 32 rows x 64 bf16 of a row-major bf16 matrix (row i at base + i * stride;
+// rows >= valid read as zero) into registers with lane i holding row i
+// (out[c] = 16-byte chunk c).  Read coalesced -- 8 lanes per 128-byte
+// half-row, 4 rows per load -- and transposed through a 4 KB per-warp smem
+// scratch whose 16-byte chunks are XOR-swizzled by row (4 wavefronts per
+// 512-byte access, the minimum).  A lane-per-row global read instead touches
+// 32 cache lines per load instruction: staging a short-chunk dQ item that way
+// took ~7,900 cycles, 38 % of the kernel (tools/attn_trace.py).
+__device__ __forceinline__ void rows_to_lanes(uint32_t scr, const __nv_bfloat16* base, int64_t stride, int valid,
+                                              uint4 (&out)[8]) {
+  const int lane = threadIdx.x & 31, c = lane & 7;
+  uint4 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = 4 * k + (lane >> 3);
+    v[k] = i < valid ? __ldg(reinterpret_cast<const uint4*>(base + i * stride) + c) : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = 4 * k + (lane >> 3);
+    sts128(scr + i * 128 + ((c ^ (i & 7)) << 4), v[k]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < 8; ++cc) out[cc] = lds128(scr + lane * 128 + ((cc ^ (lane & 7)) << 4));
+  __syncwarp();
+}
+// rows_to_lanes for 32 bf16 (64 bytes) per row: 4 lanes per row, 8 rows per
+// load, a 2 KB scratch with chunks swizzled by (row >> 1) & 3 so the 8 lanes
+// of each read wavefront hit distinct bank groups.
+__device__ __forceinline__ void rows_to_lanes64(uint32_t scr, const __nv_bfloat16* base, int64_t stride, int valid,
+                                                uint4 (&out)[4]) {
+  const int lane = threadIdx.x & 31, c = lane & 3;
+  uint4 v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = 8 * k + (lane >> 2);
+    v[k] = i < valid ? __ldg(reinterpret_cast<const uint4*>(base + i * stride) + c) : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = 8 * k + (lane >> 2);
+    sts128(scr + i * 64 + ((c ^ ((i >> 1) & 3)) << 4), v[k]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) out[cc] = lds128(scr + lane * 64 + ((cc ^ ((lane >> 1) & 3)) << 4));
+  __syncwarp();
+}
+__device__ __forceinline__ void words_of(const uint4 (&x)[8], uint32_t (&w)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    w[4 * c] = x[c].x;
+    w[4 * c + 1] = x[c].y;
+    w[4 * c + 2] = x[c].z;
+    w[4 * c + 3] = x[c].w;
+  }
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -626,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int krow = sg.kv_row0 + j * SUB;
           stress_delay(a.stress, 1, jj);
           mbar_wait(&v_empty[sv], ((jj / VS) & 1) ^ 1);
+          TR(2, 1, jj);
           mbar_expect_tx(&v_full[sv], 2 * kBox64);
           tma_load_2d(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
           tma_load_2d(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
@@ -648,10 +732,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t pk = 0, pv = 0;
     auto issue_s = [&](int J) {
       const uint32_t b = J & 1;
+      TR(0, 1, J);
       mbar_wait_s(bKf + ik * 8, pk);
       mbar_wait_s(bVf + iv * 8, pv);
+      TR(0, 2, J);
       mbar_wait_s(bSr + b * 8, ((J >> 1) & 1) ^ 1);
       tc_fence_after();
+      TR(0, 3, J);
       const uint32_t k0 = sK0 + ik * 2 * kBox64, v0 = sV0 + iv * 2 * kBox64;
       umma4_ts_w<8, 2>(tmem + b * 64, tAq, kdesc(k0, kBox64, 0), idS, 0u);
       umma4_ts_w<8, 2>(tmem + b * 64, tAq + 32, kdesc(k0, kBox64, 4), idS, 1u);
@@ -669,8 +756,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int h;
       item_of(a, nq, item, tl, sg, h);
       const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+      TR(0, 4, J0);
       mbar_wait_s(bQf, n & 1);  // this item's Q / dO staged
       tc_fence_after();
+      TR(0, 5, J0);
       issue_s(J0);
       for (int j = 0; j < nkt; ++j) {
         const int J = J0 + j;
@@ -678,8 +767,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j + 1 < nkt) issue_s(J + 1);
         const uint32_t b = J & 1;
         mbar_wait_s(bDf + b * 8, (J >> 1) & 1);
+        TR(0, 6, J);
         if (j == 0 && n > 0) mbar_wait_s(bQr, (n - 1) & 1);  // previous item's dQ read out
         tc_fence_after();
+        TR(0, 7, J);
         const uint32_t s0 = sS0 + b * kBox128, k0 = sK0 + ck * 2 * kBox64;
         umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 0), mndesc(k0, kBox64, 0), idQ, j > 0 ? 1u : 0u);
         umma_commit_w(bKe + ck * 8);
@@ -699,6 +790,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
     // stage item `it`'s Q / dO rows into TMEM and return D = rowsum(dO * O)
+    // per-warp transpose scratch: the dS buffers, free whenever staging runs
+    // (before the first item, and after dq_done: every MMA of the previous
+    // item, the dQ GEMMs that read dS included, has completed)
+    const uint32_t scr = smem_u32(sS) + warp * 4096;
     auto stage = [&](int it, int rnd) -> float {
       AttnTile tl;
       AttnSeg sg;
@@ -706,12 +801,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       item_of(a, nq, it, tl, sg, h);
       const int qi = tl.first + row;
       const bool ok = qi < sg.len && row < tl.count;
-      const bool rok = row < tl.count;
-      const int64_t r = sg.q_start + tl.first + row;
+      const int vq = tl.count - quarter * 32;                             // rows with Q
+      const int vo = min(tl.count, sg.len - tl.first) - quarter * 32;     // rows with dO / O
+      const int64_t r0 = sg.q_start + tl.first + quarter * 32;            // this warp's first row
       const int64_t hc = static_cast<int64_t>(h) * DH + half * 64;
-      const float dpart = stage_qdo_tmem(tAq + lane_off + half * 32, tAo + lane_off + half * 32,
-                                         a.q + r * a.q_stride + hc, a.dout + r * a.dout_stride + hc,
-                                         a.o + r * a.o_stride + hc, rok, ok);
+      float dpart = 0.f;
+      {
+        uint4 x[8];
+        uint32_t w[32];
+        rows_to_lanes(scr, a.q + r0 * a.q_stride + hc, a.q_stride, vq, x);
+        words_of(x, w);
+        tmem_st32w(tAq + lane_off + half * 32, w);
+      }
+      {
+        uint4 xd[8], xo[8];
+        uint32_t w[32];
+        rows_to_lanes(scr, a.dout + r0 * a.dout_stride + hc, a.dout_stride, vo, xd);
+        words_of(xd, w);
+        tmem_st32w(tAo + lane_off + half * 32, w);
+        rows_to_lanes(scr, a.o + r0 * a.o_stride + hc, a.o_stride, vo, xo);
+        if (ok) {  // D partial: same arithmetic order as stage_row_tmem
+          float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t ow[4] = {xo[c].x, xo[c].y, xo[c].z, xo[c].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&w[4 * c + e]);
+              const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+              part[e] = fmaf(__low2float(a2), __low2float(b2), part[e]);
+              part[e] = fmaf(__high2float(a2), __high2float(b2), part[e]);
+            }
+          }
+          dpart = (part[0] + part[1]) + (part[2] + part[3]);
+        }
+      }
+      const int64_t r = sg.q_start + tl.first + row;
       tmem_st_wait();
       tc_fence_before();
       warp_arrive(q_full);
@@ -762,8 +887,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nkt; ++j) {
         const int J = J0 + j;
         const uint32_t b = J & 1;
+        if (warp == 0) TR(1, 1, J);
         mbar_wait_s(bSf + b * 8, (J >> 1) & 1);
         tc_fence_after();
+        if (warp == 0) TR(1, 2, J);
         uint32_t rs[32], rp[32];
         tmem_ld32(tmem + b * 64 + lane_off + half * 32, rs);
         tmem_ld32(tmem + 128 + b * 64 + lane_off + half * 32, rp);
@@ -791,7 +918,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           body(std::true_type{});
         stress_delay(a.stress, 3, J);
+        if (warp == 0) TR(1, 3, J);
         if (J >= 2) mbar_wait_s(bDr + b * 8, ((J >> 1) & 1) ^ 1);
+        if (warp == 0) TR(1, 4, J);
         const uint32_t dst = sS0 + b * kBox128;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -802,10 +931,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       J0 += nkt;
       mbar_wait_s(bQd, n & 1);  // every MMA of this item done: Q / dO / dQ settled
       tc_fence_after();
+      if (warp == 0) TR(1, 5, J0);
       // the next item's Q / dO go into TMEM now, so its S / dP overlap this
       // item's dQ read-out
       const int next = item + gridDim.x;
       const float Dn = next < items ? stage(next, n + 1) : 0.f;
+      if (warp == 0) TR(1, 6, J0);
       __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
       if (a.rope_tab) {
         uint32_t ra[32], rb[32];
@@ -847,6 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (warp == 0) TR(1, 7, J0);
       D = Dn;
     }
   }
@@ -1270,18 +1402,20 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
     const bool kok = row < tl.count && key < kv_len;
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     {
-      // K and V quarter-rows: both fetches in flight before either tcgen05.st
-      const int64_t r = sg.kv_row0 + key;
-      const int64_t off = r * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32;
-      const uint4* k4 = reinterpret_cast<const uint4*>(a.k + off);
-      const uint4* v4 = reinterpret_cast<const uint4*>(a.v + off);
+      // K and V quarter-rows, read coalesced through a per-warp scratch in
+      // the P / dS buffers (unused until the first S^T completes)
+      const int valid = min(tl.count, kv_len - key_first) - quarter * 32;
+      const int64_t r0 = sg.kv_row0 + key_first + quarter * 32;
+      const int64_t off = r0 * a.kv_stride + static_cast<int64_t>(g) * DH + part * 32;
+      const uint32_t scr = smem_u32(sP) + warp * 2048;
+      uint4 xk[4], xv[4];
+      rows_to_lanes64(scr, a.k + off, a.kv_stride, valid, xk);
+      rows_to_lanes64(scr, a.v + off, a.kv_stride, valid, xv);
       uint32_t wk[16], wv[16];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const uint4 x = kok ? __ldg(k4 + c) : make_uint4(0u, 0u, 0u, 0u);
-        const uint4 y = kok ? __ldg(v4 + c) : make_uint4(0u, 0u, 0u, 0u);
-        wk[4 * c] = x.x, wk[4 * c + 1] = x.y, wk[4 * c + 2] = x.z, wk[4 * c + 3] = x.w;
-        wv[4 * c] = y.x, wv[4 * c + 1] = y.y, wv[4 * c + 2] = y.z, wv[4 * c + 3] = y.w;
+        wk[4 * c] = xk[c].x, wk[4 * c + 1] = xk[c].y, wk[4 * c + 2] = xk[c].z, wk[4 * c + 3] = xk[c].w;
+        wv[4 * c] = xv[c].x, wv[4 * c + 1] = xv[c].y, wv[4 * c + 2] = xv[c].z, wv[4 * c + 3] = xv[c].w;
       }
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -1540,6 +1674,26 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   } else {
     dq_kernel<<<dim3(nq, p.H), kThreads, smem_dq, st>>>(q128, o128, k64, v64, a);
   }
+#if CF_ATTN_TRACE
+  {
+    cudaStreamSynchronize(st);
+    static unsigned long long h[3][8192];
+    int n[3] = {0, 0, 0};
+    cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+    cudaMemcpyFromSymbol(n, g_trace_n, sizeof(n));
+    if (const char* path = std::getenv("CF_TRACE_OUT")) {
+      if (FILE* f = std::fopen(path, "a")) {
+        std::fprintf(f, "# launch nq=%d H=%d\n", nq, p.H);
+        for (int r = 0; r < 3; ++r)
+          for (int i = 0; i < std::min(n[r], 8192); ++i)
+            std::fprintf(f, "%d %llu %llu %llu\n", r, h[r][i] >> 20, (h[r][i] >> 16) & 15, h[r][i] & 0xffff);
+        std::fclose(f);
+      }
+    }
+    const int z[3] = {0, 0, 0};
+    cudaMemcpyToSymbol(g_trace_n, z, sizeof(z));
+  }
+#endif
   a.tiles = ktiles128;
   if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, a);
   return cudaGetLastError();
