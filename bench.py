@@ -386,6 +386,20 @@ def run_b200(args):
     gemm_tf = sum(r.gemm_flops for r in res) / (sum(r.gemm_ms for r in res) / 1e3) / 1e12
     attn_tf = sum(r.attn_flops for r in res) / max(1e-9, sum(r.attn_ms for r in res) / 1e3) / 1e12
     attnb_tf = sum(r.attn_bwd_flops for r in res) / max(1e-9, sum(r.attn_bwd_ms for r in res) / 1e3) / 1e12
+    def _tf(f, t):
+        return f / max(1e-9, t / 1e3) / 1e12
+
+    def _split(ms_all, fl_all, ms_dep, fl_dep):
+        # the class split by chunk kind: dependent chunks (the 37,888-token
+        # sequence's pieces, with a KV prefix) vs the packed standalone chunks
+        return {"dependent_chunks": {"achieved": _tf(fl_dep, ms_dep), "share_of_step": ms_dep / ms},
+                "standalone_chunks": {"achieved": _tf(fl_all - fl_dep, ms_all - ms_dep),
+                                      "share_of_step": (ms_all - ms_dep) / ms}}
+
+    attn_split = _split(sum(r.attn_ms for r in res), sum(r.attn_flops for r in res),
+                        sum(r.attn_dep_ms for r in res), sum(r.attn_dep_flops for r in res))
+    attnb_split = _split(sum(r.attn_bwd_ms for r in res), sum(r.attn_bwd_flops for r in res),
+                         sum(r.attn_bwd_dep_ms for r in res), sum(r.attn_bwd_dep_flops for r in res))
     gemm_share = sum(r.gemm_ms for r in res) / ms
     attn_share = sum(r.attn_ms for r in res) / ms
     attnb_share = sum(r.attn_bwd_ms for r in res) / ms
@@ -416,9 +430,10 @@ def run_b200(args):
                      "frac": gemm_tf / pk["bf16_tflops_sustained"], "traffic": traffic[0],
                      "traffic_algorithmic": traffic[1], "traffic_source": TRAFFIC_FILE,
                      "share_of_step": gemm_share, "peak_kind": "measured sustained (MEASURED_PEAKS.json)",
-                     "attention_fwd": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s"},
+                     "attention_fwd": {"achieved": attn_tf, "share_of_step": attn_share, "unit": "TFLOP/s",
+                                       **attn_split},
                      "attention_bwd": {"achieved": attnb_tf, "share_of_step": attnb_share, "unit": "TFLOP/s",
-                                       "note": "algorithmic 8*H*dh FLOP/pair"},
+                                       "note": "algorithmic 8*H*dh FLOP/pair", **attnb_split},
                      "other_share_of_step": max(0.0, 1 - gemm_share - attn_share - attnb_share)},
         "hbm_kernels": hbm_kernels(),
         "e2e": {"value": tokens_all / (e2e_max / 1e3 / max(1, args.steps)), "unit": "tokens/s",

@@ -162,6 +162,10 @@ typedef struct cf_run_result {
    * full tapes resident on one stage, and the extra forwards it cost */
   int64_t peak_live_tapes;
   int64_t checkpoint_recomputes;
+  /* the attention classes restricted to dependent chunks (the pieces of
+   * split long sequences, which carry a KV prefix): forward / backward */
+  double attn_dep_ms, attn_dep_flops;
+  double attn_bwd_dep_ms, attn_bwd_dep_flops;
 } cf_run_result;
 
 typedef struct cf_ctx cf_ctx;

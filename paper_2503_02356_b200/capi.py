@@ -82,7 +82,9 @@ class RunResult(C.Structure):
                 ("gemm_launches", C.c_int64), ("attn_ms", C.c_double), ("attn_flops", C.c_double),
                 ("attn_launches", C.c_int64), ("attn_bwd_ms", C.c_double), ("attn_bwd_flops", C.c_double),
                 ("attn_bwd_launches", C.c_int64), ("other_launches", C.c_int64),
-                ("peak_live_tapes", C.c_int64), ("checkpoint_recomputes", C.c_int64)]
+                ("peak_live_tapes", C.c_int64), ("checkpoint_recomputes", C.c_int64),
+                ("attn_dep_ms", C.c_double), ("attn_dep_flops", C.c_double),
+                ("attn_bwd_dep_ms", C.c_double), ("attn_bwd_dep_flops", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -946,9 +946,10 @@ struct Exec {
   // --- optional per-launch timing (cf_ctx_set_profiling)
   struct Rec {
     cudaEvent_t a, b;
-    int cls;  // 0 gemm, 1 attention
+    int cls;  // 0 gemm, 1 attention forward, 2 attention backward
     double flops;
     int n;
+    bool dep;  // attention of a dependent (split-sequence) chunk
   };
   std::vector<Rec> recs;
   size_t ev_used = 0;
@@ -966,11 +967,11 @@ struct Exec {
     CK(cudaEventRecord(a, on ? on : s));
     return a;
   }
-  void close(cudaEvent_t a, int cls, double flops, int n, cudaStream_t on = nullptr) {
+  void close(cudaEvent_t a, int cls, double flops, int n, cudaStream_t on = nullptr, bool dep = false) {
     if (!ctx->profile) return;
     cudaEvent_t b = ev();
     CK(cudaEventRecord(b, on ? on : s));
-    recs.push_back({a, b, cls, flops, n});
+    recs.push_back({a, b, cls, flops, n, dep});
   }
   void gemm(const void* a, int a_k, int64_t lda, const void* b, int b_k, int64_t ldb, void* c, int64_t ldc, int64_t M,
             int64_t N, int64_t K, int epi, const void* r = nullptr, int64_t ldr = 0) {
@@ -1234,7 +1235,7 @@ struct Exec {
           "attn_fwd_tc");
       else
         L(cfk::attn_forward(p, s), "attn_fwd");
-      close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1);
+      close(t0, 1, 4.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 1, nullptr, cm.dependent);
       if (cm.dependent && gs->offload) kv_release(cm, gs, l, false);
       gemm(t.ol(l), 1, d, ly.wo, 0, d, xm, d, T, d, d, cfk::EPI_F32_RES, x, d);
       float* xn = t.xin(l + 1);
@@ -1414,7 +1415,7 @@ struct Exec {
           "attn_bwd_tc", 3);
       else
         L(cfk::attn_backward(p, meta<const AttnTile>(cm.o_kt), static_cast<int32_t>(cm.nkt), s), "attn_bwd", 3);
-      close(t0, 2, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3);
+      close(t0, 2, 8.0 * static_cast<double>(m->H * m->dh) * cm.pairs, 3, nullptr, cm.dependent);
       if (!direct)
         L(cfk::dkv_to_dqkv(own_dk, own_dk + kvw, 2 * kvw, T, static_cast<int>(m->KVH), static_cast<int>(m->dh),
                            m->llama ? t.tab : nullptr, dqkv, qw, d, d + kvw, s),
@@ -1810,6 +1811,31 @@ struct StageRunner {
         }
       }
     }
+    // attention launches of dependent chunks (the split long sequence), the
+    // same union rule restricted to them: [0] forward, [1] backward
+    double dep_ms[2] = {0, 0}, dep_flops[2] = {0, 0};
+    for (int c = 1; c <= 2; ++c) {
+      std::vector<std::pair<double, double>> dv;
+      for (const auto& r : ex.recs) {
+        if (r.cls != c || !r.dep) continue;
+        float t0 = 0, t1 = 0;
+        CK(cudaEventElapsedTime(&t0, ex.recs.front().a, r.a));
+        CK(cudaEventElapsedTime(&t1, ex.recs.front().a, r.b));
+        dv.emplace_back(t0, t1);
+        dep_flops[c - 1] += r.flops;
+      }
+      std::sort(dv.begin(), dv.end());
+      double end = -1e300;
+      for (const auto& [a0, a1] : dv) {
+        if (a0 >= end) {
+          dep_ms[c - 1] += a1 - a0;
+          end = a1;
+        } else if (a1 > end) {
+          dep_ms[c - 1] += a1 - end;
+          end = a1;
+        }
+      }
+    }
     for (const OpMark& mk : marks) {
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, mk.a, mk.b));
@@ -1863,6 +1889,10 @@ struct StageRunner {
     res->attn_bwd_flops = cls_flops[2];
     res->attn_bwd_launches = cls_n[2];
     res->other_launches = ex.launches - cls_n[0] - cls_n[1] - cls_n[2];
+    res->attn_dep_ms = dep_ms[0];
+    res->attn_dep_flops = dep_flops[0];
+    res->attn_bwd_dep_ms = dep_ms[1];
+    res->attn_bwd_dep_flops = dep_flops[1];
     res->peak_live_tapes = live_peak;
     res->checkpoint_recomputes = ckpt_recomputes;
   }
@@ -1992,6 +2022,10 @@ void pp_step_run_local(Ctx* ctx, Model* const* models, int64_t P, cf_step* st, i
     total.attn_bwd_flops += rs.attn_bwd_flops;
     total.attn_bwd_launches += rs.attn_bwd_launches;
     total.other_launches += rs.other_launches;
+    total.attn_dep_ms += rs.attn_dep_ms;
+    total.attn_dep_flops += rs.attn_dep_flops;
+    total.attn_bwd_dep_ms += rs.attn_bwd_dep_ms;
+    total.attn_bwd_dep_flops += rs.attn_bwd_dep_flops;
     total.peak_live_tapes = std::max(total.peak_live_tapes, rs.peak_live_tapes);
     total.checkpoint_recomputes += rs.checkpoint_recomputes;
   }
