@@ -16,8 +16,10 @@
 //  * losses are reduced on the device in a fixed order into per-event slots,
 //    read back once per step; recompute-loss equality is checked bitwise.
 #include <algorithm>
+#include <functional>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <dlfcn.h>
 #include <memory>
@@ -172,6 +174,11 @@ void ctx_release(Ctx* ctx) {
     cudaStreamDestroy(ctx->copy_stream);
     ctx->copy_stream = nullptr;
   }
+  if (ctx->dp_stream) {
+    cudaStreamSynchronize(ctx->dp_stream);
+    cudaStreamDestroy(ctx->dp_stream);
+    ctx->dp_stream = nullptr;
+  }
   for (auto& b : ctx->host_blocks) cudaFreeHost(b.ptr);
   ctx->host_blocks.clear();
 }
@@ -318,7 +325,9 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage, int64_t st
     m->d_emb = gptr(pi++);
   }
   m->layers.resize(static_cast<size_t>(m->L));
+  m->layer_goff.clear();
   for (auto& ly : m->layers) {
+    m->layer_goff.push_back(goff[pi]);
     ly.wqkv = reinterpret_cast<bf16*>(wptr(pi));
     ly.d_wqkv = gptr(pi++);
     ly.wo = reinterpret_cast<bf16*>(wptr(pi));
@@ -335,6 +344,7 @@ Model* model_create(Ctx* ctx, const cf_model_cfg& cfg, int64_t stage, int64_t st
       ly.d_g2 = gptr(pi++);
     }
   }
+  m->layer_goff.push_back(pi < goff.size() ? goff[pi] : gelems);
   if (m->has_head) {
     if (m->llama) {
       m->gf = reinterpret_cast<float*>(wptr(pi));
@@ -1278,6 +1288,9 @@ struct Exec {
   // Backward of one chunk (segment_backward, toy_model.hpp:341-520).  A
   // pipeline stage without the head passes the gradient of its output in
   // dx_io; a stage without the embedding gets its input gradient back there.
+  // Called (when set) as each gradient range becomes final in this
+  // backward: -1 final norm + head, l for layer l, -2 the embedding.
+  std::function<void(int64_t)> on_grads_final;
   void backward(const ChunkMeta& cm, Tape& t, GroupState* gs, float* dx_io = nullptr) {
     const int64_t T = cm.T, d = m->d, qw = m->qkv_w, kvw = m->kvw;
     const float eps = static_cast<float>(m->cfg.rms_eps);
@@ -1332,6 +1345,7 @@ struct Exec {
         head_backward(xnf, T, tgt, t.lse_head, dx);
       }
     }
+    if (on_grads_final) on_grads_final(-1);
 
     for (int64_t l = m->L - 1; l >= 0; --l) {
       const Layer& ly = m->layers[static_cast<size_t>(l)];
@@ -1438,12 +1452,14 @@ struct Exec {
       } else {
         gemm(dqkv, 1, qw, ly.wqkv, 1, qw, dx, d, T, d, qw, cfk::EPI_F32_RES, dmid, d);
       }
+      if (on_grads_final) on_grads_final(l);
     }
     // Embedding (toy_model.hpp:514-519), deterministic per-token sums.
     if (m->has_embed)
       L(cfk::embed_bwd(dx, d, meta<const int32_t>(cm.o_order), meta<const int32_t>(cm.o_uniq),
                        meta<const int32_t>(cm.o_uoff), cm.nuniq, m->d_emb, s),
         "embed_bwd");
+    if (on_grads_final) on_grads_final(-2);
     pool_free(ctx, scratch);
   }
 };
@@ -1752,7 +1768,15 @@ struct StageRunner {
     float* dx = dy;
     if (!m->has_head && !dy) throw ValidationError("output gradient missing for chunk " + std::to_string(id));
     if (!dx && !m->has_embed) dx = static_cast<float*>(pool_alloc(ctx, cm.T * m->d * 4));
+    // this stage's last backward: each gradient range is final as soon as
+    // the backward has enqueued it, so its DP all-reduce starts then, on
+    // the DP stream, under the rest of the backward
+    if (id == final_bwd && dp_overlap_on()) ex.on_grads_final = [this](int64_t which) { dp_allreduce(which); };
     ex.backward(cm, lit->second, gs, dx);
+    if (ex.on_grads_final) {
+      ex.on_grads_final = nullptr;
+      dp_overlapped = true;
+    }
     if (gs) {
       for (int64_t i = 0; i < cm.index; ++i) ++gs->contributions[static_cast<size_t>(i)];
       if (gs->offload) gs->dkv_valid = std::max(gs->dkv_valid, cm.start);
@@ -1770,6 +1794,45 @@ struct StageRunner {
       return nullptr;
     }
     return dx;
+  }
+
+  // ---- data-parallel gradient all-reduce
+  int64_t final_bwd = -1;  // chunk id of this stage's last backward (set by the driver)
+  bool dp_overlapped = false;
+  std::vector<cudaEvent_t> dp_events;
+  bool dp_overlap_on() const {
+    static const bool on = [] {
+      const char* e = std::getenv("CF_DP_OVERLAP");
+      return !(e && std::atoi(e) == 0);
+    }();
+    return ctx->nccl_comm && on;
+  }
+  // Sum one gradient range over the DP group on the DP stream, after
+  // everything enqueued so far on the step stream: -1 final norm + head,
+  // l layer l, -2 the embedding.  Every replica issues the same ranges in
+  // the same order (-1, L-1 .. 0, -2), which NCCL requires.
+  void dp_allreduce(int64_t which) {
+    const std::vector<int64_t>& go = m->layer_goff;
+    int64_t lo = 0, hi = 0;
+    if (which == -1) {
+      lo = go.back();
+      hi = m->grad_numel;
+    } else if (which == -2) {
+      hi = go.front();
+    } else {
+      lo = go[static_cast<size_t>(which)];
+      hi = go[static_cast<size_t>(which) + 1];
+    }
+    if (hi <= lo) return;
+    if (!ctx->dp_stream) CK(cudaStreamCreateWithFlags(&ctx->dp_stream, cudaStreamNonBlocking));
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    dp_events.push_back(e);
+    CK(cudaEventRecord(e, ex.s));
+    CK(cudaStreamWaitEvent(ctx->dp_stream, e, 0));
+    nccl_check(nccl().all_reduce(m->grads + lo, m->grads + lo, static_cast<size_t>(hi - lo), kNcclFloat32, kNcclSum,
+                                 ctx->nccl_comm, ctx->dp_stream),
+               "ncclAllReduce(grads range)");
   }
 
   // Loss read-back, recompute-loss check, DP all-reduce, result fields.
@@ -1852,12 +1915,29 @@ struct StageRunner {
       // DP: gradients and loss are sums of per-rank partials (global normalizer)
       double* dl = ex.loss_slots + nslots;
       CK(cudaMemcpyAsync(dl, &loss, 8, cudaMemcpyHostToDevice, ex.s));
-      nccl_check(nccl().all_reduce(m->grads, m->grads, static_cast<size_t>(m->grad_numel), kNcclFloat32, kNcclSum,
-                                   ctx->nccl_comm, ex.s),
-                 "ncclAllReduce(grads)");
+      if (dp_overlap_on()) {
+        if (!dp_overlapped) {  // no backward on this rank: the same ranges, now
+          dp_allreduce(-1);
+          for (int64_t l = m->L - 1; l >= 0; --l) dp_allreduce(l);
+          dp_allreduce(-2);
+        }
+        if (ctx->dp_stream) {
+          cudaEvent_t e;
+          CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          dp_events.push_back(e);
+          CK(cudaEventRecord(e, ctx->dp_stream));
+          CK(cudaStreamWaitEvent(ex.s, e, 0));
+        }
+      } else {
+        nccl_check(nccl().all_reduce(m->grads, m->grads, static_cast<size_t>(m->grad_numel), kNcclFloat32,
+                                     kNcclSum, ctx->nccl_comm, ex.s),
+                   "ncclAllReduce(grads)");
+      }
       nccl_check(nccl().all_reduce(dl, dl, 1, kNcclFloat64, kNcclSum, ctx->nccl_comm, ex.s), "ncclAllReduce(loss)");
       CK(cudaMemcpyAsync(&loss, dl, 8, cudaMemcpyDeviceToHost, ex.s));
       CK(cudaStreamSynchronize(ex.s));
+      for (cudaEvent_t e : dp_events) cudaEventDestroy(e);
+      dp_events.clear();
     }
     pool_free(ctx, ex.loss_slots);
     ex.loss_slots = nullptr;
@@ -1929,6 +2009,8 @@ void step_run(Ctx* ctx, Model* m, cf_step* st, const cf_run_opts& opts, cf_run_r
   st->op_times.clear();
   reset_pool_high(ctx);
   StageRunner r(ctx, m, st, opts, static_cast<int64_t>(plan.events.size()));
+  for (const Event& e : plan.events)
+    if (e.kind == kBackward) r.final_bwd = e.chunk;
   for (size_t ei = 0; ei < plan.events.size(); ++ei) {
     const Event& e = plan.events[ei];
     if (e.kind == kBackward)
@@ -2190,6 +2272,8 @@ void pp_step_run(Ctx* ctx, Model* m, cf_step* st, int64_t k, const cf_run_opts& 
   st->op_times.clear();
   reset_pool_high(ctx);
   StageRunner r(ctx, m, st, opts, static_cast<int64_t>(order.size()));
+  for (const PpOp& op : order)
+    if (op.kind != kPpForward && op.kind != kPpRecompute) r.final_bwd = sp.info.ids[static_cast<size_t>(op.pos)];
   std::vector<LinkOp> sends;  // output buffers in flight to a neighbour
   auto reap = [&](bool all) {
     for (size_t i = 0; i < sends.size();) {

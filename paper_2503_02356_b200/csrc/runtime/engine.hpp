@@ -48,6 +48,9 @@ struct Ctx {
   // KV offload: host<->device copies of offloaded group state run here, and
   // the pinned host blocks are cached across steps
   cudaStream_t copy_stream = nullptr;
+  // data-parallel gradient all-reduces overlapped with the last backward
+  // (created on first use, released by cf_ctx_destroy)
+  cudaStream_t dp_stream = nullptr;
   struct HostBlock {
     void* ptr;
     size_t bytes;
@@ -97,6 +100,9 @@ struct Model {
   void* wbuf = nullptr;   // all weights (bf16) + gains (fp32)
   float* grads = nullptr; // all gradients, flat fp32
   int64_t grad_numel = 0, wbytes = 0, num_params = 0;
+  // gradient element ranges: layer l is [layer_goff[l], layer_goff[l+1]),
+  // the embedding [0, layer_goff[0]), final norm + head [layer_goff[L], grad_numel)
+  std::vector<int64_t> layer_goff;
   // AdamW state (cf_model_adamw_init): fp32 master weights and both moments in
   // the gradient buffer's layout, the storage-piece table the fused kernel
   // walks, and the step counter t
