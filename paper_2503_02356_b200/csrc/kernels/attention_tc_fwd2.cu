@@ -332,10 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------- persistent
-// attn_fwd_pp_kernel's math for packed short-sequence chunks, where an item
-// (128-query tile x head pair) sees only a few key tiles and a one-CTA-per-item
-// grid spends most of each CTA in its prologue (TMEM / barrier set-up, the Q
-// fetch from HBM) and epilogue.  One CTA per SM loops over items
+// attn_fwd_pp_kernel's math with one CTA per SM looping over items.  Built
+// for packed short-sequence chunks, where an item (128-query tile x head
+// pair) sees only a few key tiles and a one-CTA-per-item grid spends most of
+// each CTA in its prologue (TMEM / barrier set-up, the Q fetch from HBM) and
+// epilogue; it also wins on long-context launches (hidden Q fetches).  One CTA per SM loops over items
 // (item = blockIdx.x + k * gridDim.x, tile-major so the heaviest tiles of
 // every head pair come first); ring positions and barrier phases run on
 // counters that continue across items:
@@ -676,15 +677,17 @@ bool map_rows(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows, uin
 
 int attn_num_sms();  // attention_tc_bwd.cu
 
-// Persistent forward for short-context launches (packed short sequences:
-// fewer than 3072 keys per query on average, the dQ kernel's criterion);
-// CF_FWD_PERSIST=1 / 0 forces it on / off (A/B, tests).
-bool fwd_persist(const AttnParams& p) {
+// The persistent forward serves every launch: packed short chunks -11..-25 %,
+// causal T = 16K -4 % (1.88 -> 1.80 ms), the C2 long group's chunks +1.8 %
+// TFLOP/s in-step (profiles/round2_ab_short_attention.txt,
+// profiles/round2_ab_fwd_persist_long.txt).  CF_FWD_PERSIST=0 selects the
+// one-CTA-per-item kernel (A/B, tests).
+bool fwd_persist(const AttnParams&) {
   static const int v = [] {
     const char* e = std::getenv("CF_FWD_PERSIST");
     return e ? std::atoi(e) : -1;
   }();
-  return v >= 0 ? v == 1 : p.keys_per_query > 0.0 && p.keys_per_query < 3072.0;
+  return v != 0;
 }
 
 bool attn_fwd_pp_supported(const AttnParams& p) {
