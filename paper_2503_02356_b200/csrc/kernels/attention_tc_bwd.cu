@@ -139,6 +139,27 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
     d4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                        pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
 }
+// rope_inverse32 / store_bf16x32 on 16 (a, b) pairs / 16 values
+__device__ __forceinline__ void rope_inverse16(const float2* tab, float (&a)[16], float (&b)[16]) {
+  const float4* tp = reinterpret_cast<const float4*>(tab);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const float4 cs = tp[e];
+    const float s0 = -cs.y, s1 = -cs.w;
+    const float a0 = a[2 * e], b0 = b[2 * e], a1 = a[2 * e + 1], b1 = b[2 * e + 1];
+    a[2 * e] = a0 * cs.x - b0 * s0;
+    b[2 * e] = b0 * cs.x + a0 * s0;
+    a[2 * e + 1] = a1 * cs.z - b1 * s1;
+    b[2 * e + 1] = b1 * cs.z + a1 * s1;
+  }
+}
+__device__ __forceinline__ void store_bf16x16(__nv_bfloat16* dst, const float (&v)[16]) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    d4[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                       pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
 // bf16 round trip (the unfused path rotates the stored bf16 dQ)
 __device__ __forceinline__ float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 
@@ -1578,6 +1599,429 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   }
 }
 
+// The item a persistent CTA takes in round r: boustrophedon order over the
+// grid (even rounds ascending, odd rounds descending), so with items sorted
+// by decreasing work each CTA's total stays close to the mean (plain
+// round-robin hands CTA 0 the heaviest item of every round).
+__device__ __forceinline__ int snake_item(int r) {
+  const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+  return r * G + ((r & 1) ? G - 1 - b : b);
+}
+// -------------------------------------------------- dK / dV, persistent
+// dkv_kernel's math with one CTA per SM looping over (128-key tile, kv head)
+// items (item = blockIdx.x + k * gridDim.x, tile-major: heaviest tiles
+// first).  Ring positions and barrier phases run on counters that continue
+// across items, and the item boundary is overlapped:
+//   * the producer TMA-loads the next item's K / V tiles into a smem buffer
+//     once it has issued this item's last Q / dO sub-tile;
+//   * the softmax warps copy them into the K / V TMEM A operands as soon as
+//     this item's last S^T / dP^T MMAs have completed (the s_full of its last
+//     sub-tile), so the MMA issuer queues the next item's first S^T / dP^T
+//     ahead of this item's last dV / dK GEMMs;
+//   * the next item's first dV / dK GEMMs overwrite the accumulators, so they
+//     wait for dkv_free: the softmax warps' read-out of this item's dK / dV,
+//     whose global stores then overlap the next item's MMAs.
+// Per item every value is computed in dkv_kernel's order (bitwise equal).
+__global__ void __launch_bounds__(kDkvThreads, 1)
+    dkv_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO,
+                       const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV, Args a,
+                       int nk) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = sm;                      // QS stages x 2 x [64][64]
+  uint8_t* sdO = sQ + QS * 2 * kBox64;   // QS stages x 2 x [64][64]
+  uint8_t* sP = sdO + QS * 2 * kBox64;   // 2 x [128 keys][64 q]
+  uint8_t* sS = sP + 2 * kBox128;        // 2 x [128 keys][64 q]
+  uint8_t* sKV = sS + 2 * kBox128;       // next item's K, V: 2 x 2 x [128 keys][64 dh]
+  uint8_t* sLD = sKV + 4 * kBox128;      // QS stages x {LSE[64], D[64]} fp32
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sLD + QS * 512);
+  uint64_t* kv_full = bar;               // K / V in TMEM (16 warp arrivals)
+  uint64_t* q_full = bar + 1;            // [QS]
+  uint64_t* q_empty = q_full + QS;       // [QS]
+  uint64_t* s_full = q_empty + QS;       // [1]
+  uint64_t* s_free = s_full + 1;         // [1]
+  uint64_t* pds_full = s_free + 1;       // [2]
+  uint64_t* pds_free = pds_full + 2;     // [2]
+  uint64_t* kv_tma = pds_free + 2;       // K / V landed in sKV (TMA)
+  uint64_t* kv_smem_free = kv_tma + 1;   // sKV copied to TMEM (16 warp arrivals)
+  uint64_t* dkv_done = kv_smem_free + 1; // the item's last dV / dK GEMMs completed
+  uint64_t* dkv_free = dkv_done + 1;     // the item's dK / dV read out (16 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_free + 1);
+
+  const int items = nk * a.KVH;
+  const int per = a.H / a.KVH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // item -> (key tile, kv head) and its loop extent
+  auto item_of = [&](int it, AttnTile& tl, AttnSeg& sg, int& g, int& i0, int& nqt) {
+    const int t = it / a.KVH;
+    g = it - t * a.KVH;
+    tl = a.tiles[t];
+    sg = a.segs[tl.seg];
+    i0 = max(0, tl.first - sg.prefix);
+    nqt = (sg.len - i0 + SUB - 1) / SUB;
+  };
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    mbar_init(kv_full, 16);
+    for (int i = 0; i < QS; ++i) {
+      mbar_init(&q_full[i], 2);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(s_free, 16);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pds_full[i], 16);
+      mbar_init(&pds_free[i], 1);
+    }
+    mbar_init(kv_tma, 1);
+    mbar_init(kv_smem_free, 16);
+    mbar_init(dkv_done, 1);
+    mbar_init(dkv_free, 16);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS = tmem, tP = tmem + 64;
+  const uint32_t tdV = tmem + 128, tdK = tmem + 256;
+  const uint32_t tAk = tmem + 384, tAv = tmem + 448;
+  const uint32_t sQ0 = smem_u32(sQ), sO0 = smem_u32(sdO), sP0 = smem_u32(sP), sS0 = smem_u32(sS),
+                 sLD0 = smem_u32(sLD), sKV0 = smem_u32(sKV);
+  const uint32_t bQf = smem_u32(q_full), bQe = smem_u32(q_empty), bSf = smem_u32(s_full),
+                 bSr = smem_u32(s_free), bPf = smem_u32(pds_full), bPr = smem_u32(pds_free);
+
+  if (warp == 16) {
+    int qs = 0, n = 0;
+    uint32_t ph = 0;
+    auto load_kv = [&](int it) {  // lane 0: the item's K / V tiles into sKV
+      AttnTile tl;
+      AttnSeg sg;
+      int g, i0, nqt;
+      item_of(it, tl, sg, g, i0, nqt);
+      const int krow = sg.kv_row0 + tl.first;
+      mbar_expect_tx(kv_tma, 4 * kBox128);
+      tma_load_2d(sKV, &tmK, kv_tma, g * DH, krow);
+      tma_load_2d(sKV + kBox128, &tmK, kv_tma, g * DH + 64, krow);
+      tma_load_2d(sKV + 2 * kBox128, &tmV, kv_tma, g * DH, krow);
+      tma_load_2d(sKV + 3 * kBox128, &tmV, kv_tma, g * DH + 64, krow);
+    };
+    if (lane == 0 && blockIdx.x < items) load_kv(blockIdx.x);
+    for (int item = snake_item(0); item < items; item = snake_item(++n)) {
+      AttnTile tl;
+      AttnSeg sg;
+      int g, i0, nqt;
+      item_of(item, tl, sg, g, i0, nqt);
+      const int iters = per * nqt;
+      int hi = 0, qi = 0;
+      for (int it = 0; it < iters; ++it) {
+        const int hq = g * per + hi;
+        const int qt0 = i0 + qi * SUB;
+        const int qrow = sg.q_start + qt0;
+        // LSE / D of the sub-tile fetched before the slot wait (their latency
+        // overlaps it)
+        const int64_t base = static_cast<int64_t>(hq) * a.T + qrow;
+        float lv[2], dv[2];
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = lane + 32 * h2;
+          const bool in = qt0 + c < sg.len;
+          lv[h2] = in ? __ldg(a.lse + base + c) : 0.f;
+          dv[h2] = in ? __ldg(a.dsum + base + c) : 0.f;
+        }
+        stress_delay(a.stress, 4, it);
+        mbar_wait_s(bQe + qs * 8, ph ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&q_full[qs], 4 * kBox64);
+          uint8_t* q = sQ + qs * 2 * kBox64;
+          uint8_t* o = sdO + qs * 2 * kBox64;
+          tma_load_2d(q, &tmQ, &q_full[qs], hq * DH, qrow);
+          tma_load_2d(q + kBox64, &tmQ, &q_full[qs], hq * DH + 64, qrow);
+          tma_load_2d(o, &tmO, &q_full[qs], hq * DH, qrow);
+          tma_load_2d(o + kBox64, &tmO, &q_full[qs], hq * DH + 64, qrow);
+        }
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = lane + 32 * h2;
+          sts_f32(sLD0 + qs * 512 + c * 4, lv[h2]);
+          sts_f32(sLD0 + qs * 512 + 256 + c * 4, dv[h2]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_s(bQf + qs * 8);
+        if (++qi == nqt) { qi = 0; ++hi; }
+        if (++qs == QS) { qs = 0; ph ^= 1; }
+      }
+      // the next item's K / V, once this item's copy has left sKV
+      if (lane == 0 && snake_item(n + 1) < items) {
+        mbar_wait(kv_smem_free, n & 1);
+        load_kv(snake_item(n + 1));
+      }
+    }
+  } else if (warp == 17) {
+    constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);
+    constexpr uint32_t idG = umma_idesc_bf16(128, 128, 0, 1);
+    int is = 0, cs = 0, J = 0, n = 0;  // ring slots, sub-tiles so far, items so far
+    uint32_t ps = 0;
+    auto issue_s = [&](int Js) {
+      mbar_wait_s(bQf + is * 8, ps);
+      mbar_wait_s(bSr, (Js & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t q0 = sQ0 + is * 2 * kBox64, o0 = sO0 + is * 2 * kBox64;
+      umma4_ts_w<8, 2>(tS, tAk, kdesc(q0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tS, tAk + 32, kdesc(q0, kBox64, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tP, tAv, kdesc(o0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tP, tAv + 32, kdesc(o0, kBox64, 4), idS, 1u);
+      umma_commit_w(bSf);
+      if (++is == QS) { is = 0; ps ^= 1; }
+    };
+    if (blockIdx.x < items) {
+      mbar_wait(kv_full, 0);
+      tc_fence_after();
+      issue_s(0);
+    }
+    for (int item = snake_item(0); item < items; item = snake_item(++n)) {
+      AttnTile tl;
+      AttnSeg sg;
+      int g, i0, nqt;
+      item_of(item, tl, sg, g, i0, nqt);
+      const int iters = per * nqt;
+      for (int it = 0; it < iters; ++it, ++J) {
+        stress_delay(a.stress, 5, J);
+        if (it + 1 < iters) {
+          issue_s(J + 1);
+        } else if (snake_item(n + 1) < items) {
+          // the next item's K / V are in TMEM: its first S^T / dP^T go ahead
+          // of this item's last dV / dK GEMMs
+          mbar_wait(kv_full, (n + 1) & 1);
+          tc_fence_after();
+          issue_s(J + 1);
+        }
+        const uint32_t b = J & 1;
+        mbar_wait_s(bPf + b * 8, (J >> 1) & 1);
+        if (it == 0 && n > 0) mbar_wait(dkv_free, (n - 1) & 1);  // previous item's dK / dV read out
+        tc_fence_after();
+        const uint32_t q0 = sQ0 + cs * 2 * kBox64, o0 = sO0 + cs * 2 * kBox64;
+        const uint32_t p0 = sP0 + b * kBox128, s0 = sS0 + b * kBox128;
+        umma4_ss_w<2, 128>(tdV, kdesc(p0, kBox128, 0), mndesc(o0, kBox64, 0), idG, it > 0 ? 1u : 0u);
+        umma4_ss_w<2, 128>(tdK, kdesc(s0, kBox128, 0), mndesc(q0, kBox64, 0), idG, it > 0 ? 1u : 0u);
+        umma_commit_w(bQe + cs * 8);
+        umma_commit_w(bPr + b * 8);
+        if (++cs == QS) cs = 0;
+      }
+      umma_commit_w(smem_u32(dkv_done));
+    }
+  } else {
+    const int quarter = warp & 3, part = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    uint32_t dst_off[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) dst_off[c] = sw_off(row, part * 2 + c);
+    // sKV -> the K / V TMEM A operands: this warp's 32 rows, dh columns
+    // [32 part, 32 part + 32) of each (16-byte chunks (part & 1) * 4 .. + 3
+    // of box part >> 1, 128B-swizzled by row)
+    auto copy_kv = [&](uint32_t phase) {
+      mbar_wait(kv_tma, phase);
+      uint32_t wk[16], wv[16];
+      const uint32_t bk = sKV0 + (part >> 1) * kBox128 + row * 128;
+      const uint32_t bv = bk + 2 * kBox128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ch = ((part & 1) * 4 + c) ^ (row & 7);
+        const uint4 x = lds128(bk + (ch << 4));
+        const uint4 y = lds128(bv + (ch << 4));
+        wk[4 * c] = x.x, wk[4 * c + 1] = x.y, wk[4 * c + 2] = x.z, wk[4 * c + 3] = x.w;
+        wv[4 * c] = y.x, wv[4 * c + 1] = y.y, wv[4 * c + 2] = y.z, wv[4 * c + 3] = y.w;
+      }
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tAk + lane_off + part * 16),
+          "r"(wk[0]), "r"(wk[1]), "r"(wk[2]), "r"(wk[3]), "r"(wk[4]), "r"(wk[5]), "r"(wk[6]), "r"(wk[7]), "r"(wk[8]),
+          "r"(wk[9]), "r"(wk[10]), "r"(wk[11]), "r"(wk[12]), "r"(wk[13]), "r"(wk[14]), "r"(wk[15])
+          : "memory");
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tAv + lane_off + part * 16),
+          "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3]), "r"(wv[4]), "r"(wv[5]), "r"(wv[6]), "r"(wv[7]), "r"(wv[8]),
+          "r"(wv[9]), "r"(wv[10]), "r"(wv[11]), "r"(wv[12]), "r"(wv[13]), "r"(wv[14]), "r"(wv[15])
+          : "memory");
+      tmem_st_wait();
+      tc_fence_before();
+      warp_arrive(kv_full);
+      warp_arrive(kv_smem_free);
+    };
+    if (blockIdx.x < items) copy_kv(0);
+    int qs = 0, J = 0, n = 0;
+    uint32_t qph = 0;
+    for (int item = snake_item(0); item < items; item = snake_item(++n)) {
+      // per-item loop state kept small (96 registers at 576 threads): the
+      // rows / head are re-read from the tile table for the epilogue
+      int iters, i0, qend, seg_len, qlo, full_lo;
+      {
+        AttnTile tl;
+        AttnSeg sg;
+        int g, nqt;
+        item_of(item, tl, sg, g, i0, nqt);
+        iters = per * nqt;
+        qend = i0 + nqt * SUB;
+        seg_len = sg.len;
+        const int kv_len = sg.prefix + sg.len;
+        const int key = tl.first + row;
+        qlo = row < tl.count && key < kv_len ? key - sg.prefix : INT_MAX;
+        // sub-tiles from query full_lo on see every key of the tile (uniform body)
+        full_lo = tl.first + 127 < kv_len ? tl.first + 127 - sg.prefix : INT_MAX;
+      }
+      const bool next = snake_item(n + 1) < items;
+      int qt0 = i0;
+      for (int it = 0; it < iters; ++it, ++J) {
+        const uint32_t b = J & 1;
+        mbar_wait_s(bSf, J & 1);
+        tc_fence_after();
+        // this s_full certifies the item's last S^T / dP^T: the K / V A
+        // operands are free for the next item's
+        if (it + 1 == iters && next) copy_kv((n + 1) & 1);
+        uint32_t rs[16], rp[16];
+        tmem_ld16(tS + lane_off + part * 16, rs);
+        tmem_ld16(tP + lane_off + part * 16, rp);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bSr);
+        stress_delay(a.stress, 6, J);
+        mbar_wait_s(bQf + qs * 8, qph);
+        const uint32_t lrow = sLD0 + qs * 512 + part * 64;
+        uint32_t pp[8], pd[8];
+        auto body = [&](auto masked) {
+          const float2 sl2v = make_float2(a.sl2, a.sl2), nlg = make_float2(-kLog2e, -kLog2e),
+                       m1 = make_float2(-1.f, -1.f);
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 L = lds_f32x4(lrow + c4 * 16);
+            const float4 Dv = lds_f32x4(lrow + 256 + c4 * 16);
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int col = c4 * 4 + 2 * h2;
+              const float2 nl = fmul2(h2 ? make_float2(L.z, L.w) : make_float2(L.x, L.y), nlg);
+              const float2 nd = fmul2(h2 ? make_float2(Dv.z, Dv.w) : make_float2(Dv.x, Dv.y), m1);
+              const float2 x = ffma2(make_float2(__uint_as_float(rs[col]), __uint_as_float(rs[col + 1])), sl2v, nl);
+              float2 p = make_float2(ex2(x.x), ex2(x.y));
+              float2 ds = fmul2(p, fadd2(make_float2(__uint_as_float(rp[col]), __uint_as_float(rp[col + 1])), nd));
+              if constexpr (decltype(masked)::value) {
+                const int qq = qt0 + part * 16 + col;
+                const bool in0 = qq >= qlo && qq < seg_len, in1 = qq + 1 >= qlo && qq + 1 < seg_len;
+                p = make_float2(in0 ? p.x : 0.f, in1 ? p.y : 0.f);
+                ds = make_float2(in0 ? ds.x : 0.f, in1 ? ds.y : 0.f);
+              }
+              pp[2 * c4 + h2] = pack_bf16(p.x, p.y);
+              pd[2 * c4 + h2] = pack_bf16(ds.x, ds.y);
+            }
+          }
+        };
+        if (full_lo <= qt0 && qt0 + SUB <= seg_len)
+          body(std::false_type{});
+        else
+          body(std::true_type{});
+        stress_delay(a.stress, 7, J);
+        if (J >= 2) mbar_wait_s(bPr + b * 8, ((J >> 1) & 1) ^ 1);
+        const uint32_t dP_ = sP0 + b * kBox128, dS_ = sS0 + b * kBox128;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          sts128(dP_ + dst_off[c], make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]));
+          sts128(dS_ + dst_off[c], make_uint4(pd[4 * c], pd[4 * c + 1], pd[4 * c + 2], pd[4 * c + 3]));
+        }
+        fence_async_smem();
+        warp_arrive_s(bPf + b * 8);
+        qt0 += SUB;
+        if (qt0 == qend) qt0 = i0;
+        if (++qs == QS) { qs = 0; qph ^= 1; }
+      }
+      AttnTile tl;
+      AttnSeg sg;
+      int g, i0_, nqt_;
+      item_of(item, tl, sg, g, i0_, nqt_);
+      const int key = tl.first + row;
+      const bool kok = row < tl.count && key < sg.prefix + sg.len;
+      mbar_wait(dkv_done, n & 1);
+      tc_fence_after();
+      // read-out in two 16-column halves (register budget); dkv_free after
+      // the last TMEM load, the global stores overlap the next item's MMAs
+      if (a.dkv_out) {
+        // parts 0, 1: dK chunks (part, part + 2), rotated back; parts 2, 3: dV
+        const bool is_k = part < 2;
+        const int c0 = part & 1;
+        const uint32_t src = (is_k ? tdK : tdV) + lane_off;
+        const int64_t r = sg.kv_row0 + key;
+        const float sc = is_k ? a.scale : 1.f;
+        __nv_bfloat16* dst = a.dkv_out + r * a.dkv_out_ld + (is_k ? a.col_k : a.col_v) + g * DH;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t ra[16], rb[16];
+          tmem_ld16(src + c0 * 32 + hh * 16, ra);
+          tmem_ld16(src + (c0 + 2) * 32 + hh * 16, rb);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            warp_arrive(dkv_free);
+          }
+          if (kok) {
+            float fa[16], fb[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              fa[e] = __uint_as_float(ra[e]) * sc;
+              fb[e] = __uint_as_float(rb[e]) * sc;
+            }
+            if (is_k && a.rope_tab) rope_inverse16(a.rope_tab + r * (DH / 2) + c0 * 32 + hh * 16, fa, fb);
+            store_bf16x16(dst + c0 * 32 + hh * 16, fa);
+            store_bf16x16(dst + (c0 + 2) * 32 + hh * 16, fb);
+          }
+        }
+      } else {
+        const int c = part;
+        float* dkr = a.dk_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH + c * 32;
+        float* dvr = a.dv_acc + static_cast<int64_t>(sg.kv_row0 + key) * a.acc_stride + g * DH + c * 32;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t rk[16], rv[16];
+          tmem_ld16(tdK + lane_off + c * 32 + hh * 16, rk);
+          tmem_ld16(tdV + lane_off + c * 32 + hh * 16, rv);
+          tmem_ld_wait();
+          if (hh == 1) {
+            tc_fence_before();
+            warp_arrive(dkv_free);
+          }
+          if (kok) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float4 k4 = reinterpret_cast<float4*>(dkr + hh * 16)[q];
+              k4.x += __uint_as_float(rk[4 * q]) * a.scale;
+              k4.y += __uint_as_float(rk[4 * q + 1]) * a.scale;
+              k4.z += __uint_as_float(rk[4 * q + 2]) * a.scale;
+              k4.w += __uint_as_float(rk[4 * q + 3]) * a.scale;
+              reinterpret_cast<float4*>(dkr + hh * 16)[q] = k4;
+              float4 v4 = reinterpret_cast<float4*>(dvr + hh * 16)[q];
+              v4.x += __uint_as_float(rv[4 * q]);
+              v4.y += __uint_as_float(rv[4 * q + 1]);
+              v4.z += __uint_as_float(rv[4 * q + 2]);
+              v4.w += __uint_as_float(rv[4 * q + 3]);
+              reinterpret_cast<float4*>(dvr + hh * 16)[q] = v4;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1623,6 +2067,19 @@ int dq_persist() {
     return e ? std::atoi(e) : 1;
   }();
   return v;
+}
+// dK/dV kernel choice: the persistent kernel for short-context launches
+// (packed short chunks: in-step attention backward 135 -> 143 TFLOP/s), the
+// one-CTA-per-(key tile, kv head) grid for long-context ones (>= 3072 keys per
+// query, the wide-dQ criterion), where hardware scheduling of the causal work
+// does as well (profiles/round2_ab_dkv_persist.txt).  CF_DKV_PERSIST=1 / 0
+// forces it on / off (A/B, tests).
+bool dkv_persist(const AttnParams& p) {
+  static const int v = [] {
+    const char* e = std::getenv("CF_DKV_PERSIST");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v >= 0 ? v == 1 : p.keys_per_query < 3072.0;
 }
 int attn_num_sms() {
   static const int n = [] {
@@ -1695,7 +2152,18 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
   }
 #endif
   a.tiles = ktiles128;
-  if (nk > 0) dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, a);
+  if (nk > 0 && dkv_persist(p)) {
+    CUtensorMap k128, v128;
+    if (!map_rows(&k128, p.k, kc, kv_rows, p.kv_stride, 128) || !map_rows(&v128, p.v, kc, kv_rows, p.kv_stride, 128))
+      return cudaErrorInvalidValue;
+    const size_t smem_p = smem_dkv + 4 * kBox128;
+    attr = smem_optin(reinterpret_cast<const void*>(dkv_persist_kernel), static_cast<int>(smem_p));
+    if (attr != cudaSuccess) return attr;
+    const int items = nk * p.KVH;
+    dkv_persist_kernel<<<std::min(items, attn_num_sms()), kDkvThreads, smem_p, st>>>(q64, o64, k128, v128, a, nk);
+  } else if (nk > 0) {
+    dkv_kernel<<<dim3(nk, p.KVH), kDkvThreads, smem_dkv, st>>>(q64, o64, a);
+  }
   return cudaGetLastError();
 }
 

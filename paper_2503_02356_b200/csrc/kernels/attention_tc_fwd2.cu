@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pair) sees only a few key tiles and a one-CTA-per-item grid spends most of
 // each CTA in its prologue (TMEM / barrier set-up, the Q fetch from HBM) and
 // epilogue; it also wins on long-context launches (hidden Q fetches).  One CTA per SM loops over items
-// (item = blockIdx.x + k * gridDim.x, tile-major so the heaviest tiles of
-// every head pair come first); ring positions and barrier phases run on
+// (snake_item order over tile-major items, the heaviest tiles of every head
+// pair first); ring positions and barrier phases run on
 // counters that continue across items:
 //   * Q(n+1) is fetched as soon as item n's last S MMAs have read Q(n)
 //     (q_empty), i.e. during item n's last softmax, PV and epilogue;
@@ -348,10 +348,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 //     warps' read-out of O_w(n).
 // Per item, every value is computed in the same order as attn_fwd_pp_kernel,
 // so the two kernels' outputs are bitwise equal.
-__device__ __forceinline__ int nctaid_x() {
-  int v;
-  asm volatile("mov.u32 %0, %%nctaid.x;" : "=r"(v));
-  return v;
+// The item a persistent CTA takes in round r: boustrophedon order over the
+// grid (even rounds ascending, odd rounds descending), so with items sorted
+// by decreasing work each CTA's total stays close to the mean (plain
+// round-robin hands CTA 0 the heaviest item of every round).
+__device__ __forceinline__ int snake_item(int r) {
+  const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+  return r * G + ((r & 1) ? G - 1 - b : b);
 }
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_pp_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 16) {
     if (lane == 0) {
       int jk = 0, jv = 0, n = 0;  // K / V ring positions, item count
-      for (int it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+      for (int it = snake_item(0); it < items; it = snake_item(++n)) {
         AttnTile tl;
         AttnSeg sg;
         int h0;
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma4_ss_w<2, 2>(tmem + 256 * w, kdesc(qw, 4), kdesc(k0, 4), idS, 1u);
       umma_commit_w(bSf + w * 8);
     };
-    for (int it = blockIdx.x; it < items; it += gridDim.x, ++n) {
+    for (int it = snake_item(0); it < items; it = snake_item(++n)) {
       AttnTile tl;
       AttnSeg sg;
       int h0;
@@ -520,9 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // key tiles so far, items so far; half-row exchanges so far = J + n (one
     // per key tile and one per item), their parity picks the smem buffer
     int J = 0, n = 0;
-    // the grid size is re-read from %nctaid at each step (ptxas otherwise
-    // spills it across the key loop at this warp role's 96-register budget)
-    for (int it = blockIdx.x; it < items; it += nctaid_x(), ++n) {
+    for (int it = snake_item(0); it < items; it = snake_item(++n)) {
       int nkt, lim, tile_lo;
       {
         AttnTile tl;
