@@ -448,14 +448,6 @@ int cf_op_attention(cf_ctx* ctx, int impl, int backward, const void* q, int64_t 
     cudaError_t e;
     if (!backward) {
       if (impl == 3) {
-        // keys per query of this launch: picks the persistent short-context
-        // forward the way the engine does
-        double pairs = 0;
-        for (int64_t s = 0; s < nseg; ++s) {
-          const double len = segs[4 * s + 1], prefix = segs[4 * s + 3];
-          pairs += len * prefix + len * (len + 1) / 2;
-        }
-        p.keys_per_query = T > 0 ? pairs / static_cast<double>(T) : 0.0;
         if (!cfk::attn_fwd_pp_supported(p))
           throw cfb::ValidationError("ping-pong attention needs head_dim 128 and an even GQA group");
         e = cfk::attn_forward_tc_pp(p, reinterpret_cast<const cfk::AttnTile*>(dmeta + q128.first),

@@ -1233,7 +1233,6 @@ struct Exec {
           L(cfk::kv_store(qkv, m->qkv_w, T, m->kvw, d, d + m->kvw, kc_rows, vc_rows, m->kvw, s), "kv_store");
       }
       AttnParams p = attn_params(cm, t, l, gs);
-      p.keys_per_query = T > 0 ? static_cast<double>(cm.pairs) / static_cast<double>(T) : 0.0;
       cudaEvent_t t0 = mark();
       if (cfk::attn_fwd_pp_supported(p))
         L(cfk::attn_forward_tc_pp(p, meta<const AttnTile>(cm.o_qt128), static_cast<int32_t>(cm.nqt128),
