@@ -1011,6 +1011,371 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// --------------------------------------------------- dQ, persistent + TMA
+// dq_persist_kernel with the per-item staging taken off the critical path:
+// the clock64 trace (profiles/round2_dq_persist_trace.txt) has the MMA issuer
+// waiting ~32 % of the time for the softmax warps to fetch the next item's
+// Q / dO / O rows from global memory.  Here
+//   * D = rowsum(dO * O) comes from dsum_rows_kernel, launched just before;
+//   * the producer TMA-loads the next item's Q and dO tiles into a 64 KB smem
+//     buffer (qo_tma) once the current item's copy has left it (qo_free);
+//   * the softmax warps copy them into the Q / dO TMEM A operands (smem ->
+//     tcgen05.st) as soon as the s_full of the item's last sub-tile certifies
+//     its last S / dP MMAs, and the MMA issuer queues the next item's first
+//     S / dP ahead of the current item's last dQ GEMM;
+//   * the next item's LSE and D are read at that point too.
+// Items and the per-item math are dq_persist_kernel's.
+__global__ void __launch_bounds__(kThreads, 1)
+    dq_persist_tma_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmO, Args a,
+                          int nq) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = sm;                    // KS stages x 2 x [64][64]
+  uint8_t* sV = sK + KS * 2 * kBox64;  // VS stages
+  uint8_t* sS = sV + VS * 2 * kBox64;  // 2 x [128 q][64 keys] (dS)
+  uint8_t* sQO = sS + 2 * kBox128;     // next item's Q, dO: 2 x 2 x [128 rows][64 dh]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sQO + 4 * kBox128);
+  uint64_t* q_full = bar;                  // Q / dO in TMEM (8 warp arrivals)
+  uint64_t* k_full = bar + 1;              // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* v_full = k_empty + KS;         // [VS]
+  uint64_t* v_empty = v_full + VS;         // [VS]
+  uint64_t* s_full = v_empty + VS;         // [2]
+  uint64_t* s_free = s_full + 2;           // [2]
+  uint64_t* ds_full = s_free + 2;          // [2]
+  uint64_t* ds_free = ds_full + 2;         // [2]
+  uint64_t* dq_done = ds_free + 2;         // the item's last MMA completed
+  uint64_t* dq_free = dq_done + 1;         // the item's dQ read out (8 warp arrivals)
+  uint64_t* qo_tma = dq_free + 1;          // Q / dO landed in sQO
+  uint64_t* qo_free = qo_tma + 1;          // sQO copied to TMEM (8 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qo_free + 1);
+
+  const int items = nq * a.H;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmO);
+    mbar_init(q_full, 8);
+    for (int i = 0; i < KS; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&ds_full[i], 8);
+      mbar_init(&ds_free[i], 1);
+    }
+    mbar_init(dq_done, 1);
+    mbar_init(dq_free, 8);
+    mbar_init(qo_tma, 1);
+    mbar_init(qo_free, 8);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tQ = tmem + 256, tAq = tmem + 384, tAo = tmem + 448;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      auto load_qo = [&](int it) {
+        AttnTile tl;
+        AttnSeg sg;
+        int h;
+        item_of(a, nq, it, tl, sg, h);
+        const int qrow = sg.q_start + tl.first;
+        mbar_expect_tx(qo_tma, 4 * kBox128);
+        tma_load_2d(sQO, &tmQ, qo_tma, h * DH, qrow);
+        tma_load_2d(sQO + kBox128, &tmQ, qo_tma, h * DH + 64, qrow);
+        tma_load_2d(sQO + 2 * kBox128, &tmO, qo_tma, h * DH, qrow);
+        tma_load_2d(sQO + 3 * kBox128, &tmO, qo_tma, h * DH + 64, qrow);
+      };
+      if (blockIdx.x < items) load_qo(blockIdx.x);
+      int jj = 0, n = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+        AttnTile tl;
+        AttnSeg sg;
+        int h;
+        item_of(a, nq, item, tl, sg, h);
+        const int g = h / (a.H / a.KVH);
+        const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+        for (int j = 0; j < nkt; ++j, ++jj) {
+          const int sk = jj % KS, sv = jj % VS;
+          const int krow = sg.kv_row0 + j * SUB;
+          stress_delay(a.stress, 1, jj);
+          mbar_wait(&v_empty[sv], ((jj / VS) & 1) ^ 1);
+          mbar_expect_tx(&v_full[sv], 2 * kBox64);
+          tma_load_2d(sV + sv * 2 * kBox64, &tmV, &v_full[sv], g * DH, krow);
+          tma_load_2d(sV + sv * 2 * kBox64 + kBox64, &tmV, &v_full[sv], g * DH + 64, krow);
+          mbar_wait(&k_empty[sk], ((jj / KS) & 1) ^ 1);
+          mbar_expect_tx(&k_full[sk], 2 * kBox64);
+          tma_load_2d(sK + sk * 2 * kBox64, &tmK, &k_full[sk], g * DH, krow);
+          tma_load_2d(sK + sk * 2 * kBox64 + kBox64, &tmK, &k_full[sk], g * DH + 64, krow);
+        }
+        // the next item's Q / dO, once this item's copy has left sQO
+        if (item + static_cast<int>(gridDim.x) < items) {
+          mbar_wait(qo_free, n & 1);
+          load_qo(item + gridDim.x);
+        }
+      }
+    }
+  } else if (warp == 9) {
+    constexpr uint32_t idS = umma_idesc_bf16(128, SUB, 0, 0);
+    constexpr uint32_t idQ = umma_idesc_bf16(128, 128, 0, 1);
+    const uint32_t sK0 = smem_u32(sK), sV0 = smem_u32(sV), sS0 = smem_u32(sS);
+    const uint32_t bKf = smem_u32(k_full), bKe = smem_u32(k_empty), bVf = smem_u32(v_full),
+                   bVe = smem_u32(v_empty), bSf = smem_u32(s_full), bSr = smem_u32(s_free),
+                   bDf = smem_u32(ds_full), bDr = smem_u32(ds_free), bQf = smem_u32(q_full),
+                   bQd = smem_u32(dq_done), bQr = smem_u32(dq_free);
+    int ik = 0, iv = 0, ck = 0;
+    uint32_t pk = 0, pv = 0;
+    auto issue_s = [&](int J) {
+      const uint32_t b = J & 1;
+      mbar_wait_s(bKf + ik * 8, pk);
+      mbar_wait_s(bVf + iv * 8, pv);
+      mbar_wait_s(bSr + b * 8, ((J >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t k0 = sK0 + ik * 2 * kBox64, v0 = sV0 + iv * 2 * kBox64;
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq, kdesc(k0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + b * 64, tAq + 32, kdesc(k0, kBox64, 4), idS, 1u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo, kdesc(v0, kBox64, 0), idS, 0u);
+      umma4_ts_w<8, 2>(tmem + 128 + b * 64, tAo + 32, kdesc(v0, kBox64, 4), idS, 1u);
+      umma_commit_w(bVe + iv * 8);
+      umma_commit_w(bSf + b * 8);
+      if (++ik == KS) { ik = 0; pk ^= 1; }
+      if (++iv == VS) { iv = 0; pv ^= 1; }
+    };
+    int J0 = 0, n = 0;
+    if (blockIdx.x < items) {
+      mbar_wait_s(bQf, 0);
+      tc_fence_after();
+      issue_s(0);
+    }
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, item, tl, sg, h);
+      const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+      for (int j = 0; j < nkt; ++j) {
+        const int J = J0 + j;
+        stress_delay(a.stress, 2, J);
+        if (j + 1 < nkt) {
+          issue_s(J + 1);
+        } else if (item + static_cast<int>(gridDim.x) < items) {
+          mbar_wait_s(bQf, (n + 1) & 1);  // the next item's Q / dO are in TMEM
+          tc_fence_after();
+          issue_s(J + 1);
+        }
+        const uint32_t b = J & 1;
+        mbar_wait_s(bDf + b * 8, (J >> 1) & 1);
+        if (j == 0 && n > 0) mbar_wait_s(bQr, (n - 1) & 1);  // previous item's dQ read out
+        tc_fence_after();
+        const uint32_t s0 = sS0 + b * kBox128, k0 = sK0 + ck * 2 * kBox64;
+        umma4_ss_w<2, 128>(tQ, kdesc(s0, kBox128, 0), mndesc(k0, kBox64, 0), idQ, j > 0 ? 1u : 0u);
+        umma_commit_w(bKe + ck * 8);
+        umma_commit_w(bDr + b * 8);
+        if (++ck == KS) ck = 0;
+      }
+      umma_commit_w(bQd);
+      J0 += nkt;
+    }
+  } else {
+    const int quarter = warp & 3, half = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t bSf = smem_u32(s_full), bSr = smem_u32(s_free), bDf = smem_u32(ds_full),
+                   bDr = smem_u32(ds_free), sS0 = smem_u32(sS), bQd = smem_u32(dq_done), bQr = smem_u32(dq_free),
+                   sQO0 = smem_u32(sQO);
+    uint32_t dst_off[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dst_off[c] = sw_off(row, half * 4 + c);
+    // sQO -> the Q / dO TMEM A operands (this warp's 32 rows, dh columns
+    // [64 half, 64 half + 64) = box `half`, 128B-swizzled by row); returns
+    // the item's LSE (log2 units) and D for this row
+    auto copy_qo = [&](int it, uint32_t phase, float& lse2, float& D) {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, it, tl, sg, h);
+      const bool ok = tl.first + row < sg.len && row < tl.count;
+      const int64_t r = static_cast<int64_t>(h) * a.T + sg.q_start + tl.first + row;
+      lse2 = ok ? __ldg(a.lse + r) * kLog2e : 0.f;
+      D = ok ? __ldg(a.dsum + r) : 0.f;
+      mbar_wait(qo_tma, phase);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const uint32_t base = sQO0 + (2 * t + half) * kBox128 + row * 128;
+        uint32_t w[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 x = lds128(base + ((c ^ (row & 7)) << 4));
+          w[4 * c] = x.x, w[4 * c + 1] = x.y, w[4 * c + 2] = x.z, w[4 * c + 3] = x.w;
+        }
+        tmem_st32w((t ? tAo : tAq) + lane_off + half * 32, w);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      warp_arrive(q_full);
+      warp_arrive(qo_free);
+    };
+    int J0 = 0, n = 0;
+    float lse2 = 0.f, D = 0.f, lse2n = 0.f, Dn = 0.f;
+    if (blockIdx.x < items) copy_qo(blockIdx.x, 0, lse2, D);
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++n) {
+      AttnTile tl;
+      AttnSeg sg;
+      int h;
+      item_of(a, nq, item, tl, sg, h);
+      const int q_row0 = sg.q_start + tl.first;
+      const int nkt = (sg.prefix + tl.first + tl.count + SUB - 1) / SUB;
+      const int qi = tl.first + row;
+      const bool ok = qi < sg.len && row < tl.count;
+      const int lim = sg.prefix + min(qi, sg.len - 1);
+      const int klim = ok ? lim : -1;
+      const int tile_lim = sg.prefix + tl.first;
+      const bool next = item + static_cast<int>(gridDim.x) < items;
+      const float2 sl2v = make_float2(a.sl2, a.sl2), nl = make_float2(-lse2, -lse2), nD = make_float2(-D, -D);
+      for (int j = 0; j < nkt; ++j) {
+        const int J = J0 + j;
+        const uint32_t b = J & 1;
+        mbar_wait_s(bSf + b * 8, (J >> 1) & 1);
+        tc_fence_after();
+        // the item's last S / dP completed: Q / dO TMEM free for the next item
+        if (j + 1 == nkt && next) copy_qo(item + gridDim.x, (n + 1) & 1, lse2n, Dn);
+        uint32_t rs[32], rp[32];
+        tmem_ld32(tmem + b * 64 + lane_off + half * 32, rs);
+        tmem_ld32(tmem + 128 + b * 64 + lane_off + half * 32, rp);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bSr + b * 8);
+        uint32_t pk[16];
+        auto body = [&](auto masked) {
+          const int key0 = j * SUB + half * 32;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float2 x = ffma2(make_float2(__uint_as_float(rs[2 * e]), __uint_as_float(rs[2 * e + 1])), sl2v, nl);
+            float2 p = make_float2(ex2(x.x), ex2(x.y));
+            if constexpr (decltype(masked)::value) {
+              p.x = key0 + 2 * e <= klim ? p.x : 0.f;
+              p.y = key0 + 2 * e + 1 <= klim ? p.y : 0.f;
+            }
+            const float2 ds =
+                fmul2(p, fadd2(make_float2(__uint_as_float(rp[2 * e]), __uint_as_float(rp[2 * e + 1])), nD));
+            pk[e] = pack_bf16(ds.x, ds.y);
+          }
+        };
+        if (j * SUB + SUB - 1 <= tile_lim)
+          body(std::false_type{});
+        else
+          body(std::true_type{});
+        stress_delay(a.stress, 3, J);
+        if (J >= 2) mbar_wait_s(bDr + b * 8, ((J >> 1) & 1) ^ 1);
+        const uint32_t dst = sS0 + b * kBox128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          sts128(dst + dst_off[c], make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+        fence_async_smem();
+        warp_arrive_s(bDf + b * 8);
+      }
+      J0 += nkt;
+      mbar_wait_s(bQd, n & 1);  // every MMA of this item done: dQ settled
+      tc_fence_after();
+      __nv_bfloat16* out = a.dq + static_cast<int64_t>(q_row0 + row) * a.dq_stride + h * DH;
+      if (a.rope_tab) {
+        uint32_t ra[32], rb[32];
+        tmem_ld32(tQ + lane_off + half * 32, ra);
+        tmem_ld32(tQ + lane_off + (half + 2) * 32, rb);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bQr);
+        if (ok) {
+          float fa[32], fb[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            fa[e] = bf16_round(__uint_as_float(ra[e]) * a.scale);
+            fb[e] = bf16_round(__uint_as_float(rb[e]) * a.scale);
+          }
+          rope_inverse32(a.rope_tab + static_cast<int64_t>(q_row0 + row) * (DH / 2) + half * 32, fa, fb);
+          store_bf16x32(out + half * 32, fa);
+          store_bf16x32(out + (half + 2) * 32, fb);
+        }
+      } else {
+        uint32_t r0[32], r1[32];
+        tmem_ld32(tQ + lane_off + (half * 2) * 32, r0);
+        tmem_ld32(tQ + lane_off + (half * 2 + 1) * 32, r1);
+        tmem_ld_wait();
+        tc_fence_before();
+        warp_arrive_s(bQr);
+        if (ok) {
+          const float sc = a.scale;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const uint32_t* rr = cc ? r1 : r0;
+            uint4* d4 = reinterpret_cast<uint4*>(out + (half * 2 + cc) * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              d4[q] = make_uint4(pack_bf16(__uint_as_float(rr[8 * q]) * sc, __uint_as_float(rr[8 * q + 1]) * sc),
+                                 pack_bf16(__uint_as_float(rr[8 * q + 2]) * sc, __uint_as_float(rr[8 * q + 3]) * sc),
+                                 pack_bf16(__uint_as_float(rr[8 * q + 4]) * sc, __uint_as_float(rr[8 * q + 5]) * sc),
+                                 pack_bf16(__uint_as_float(rr[8 * q + 6]) * sc, __uint_as_float(rr[8 * q + 7]) * sc));
+          }
+        }
+      }
+      lse2 = lse2n;
+      D = Dn;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// D = rowsum(dO * O) per (q head, row) for dq_persist_tma_kernel and the
+// dK/dV kernel: one 256-thread CTA per row, 16-byte coalesced reads, each
+// head's 16 chunks reduced across a half-warp in a fixed order.  HBM-bound:
+// 4 bytes read per element of dO and O.
+__global__ void __launch_bounds__(256) dsum_rows_kernel(Args a) {
+  const int t = blockIdx.x, lane = threadIdx.x & 31;
+  const int chunks = a.H * (DH / 8);
+  const uint4* d4 = reinterpret_cast<const uint4*>(a.dout + static_cast<int64_t>(t) * a.dout_stride);
+  const uint4* o4 = reinterpret_cast<const uint4*>(a.o + static_cast<int64_t>(t) * a.o_stride);
+  // whole warps iterate together (the shuffles need every lane)
+  for (int k0 = threadIdx.x - lane; k0 < chunks; k0 += blockDim.x) {
+    const int k = k0 + lane;
+    float acc = 0.f;
+    if (k < chunks) {
+      const uint4 dv = __ldg(d4 + k), ov = __ldg(o4 + k);
+      const uint32_t dw[4] = {dv.x, dv.y, dv.z, dv.w}, ow[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 x = *reinterpret_cast<const __nv_bfloat162*>(&dw[e]);
+        const __nv_bfloat162 y = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
+        acc = fmaf(__low2float(x), __low2float(y), acc);
+        acc = fmaf(__high2float(x), __high2float(y), acc);
+      }
+    }
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (k < chunks && (k & 15) == 0) a.dsum[static_cast<int64_t>(k >> 4) * a.T + t] = acc;
+  }
+}
+
 // ------------------------------------------------------------- dQ, wide
 // CTA = 128 queries x one q head, keys streamed in 128-key tiles so the S /
 // dP MMAs are N = 128 (a tcgen05.mma with N <= 64 pays a ~45-cycle floor,
@@ -2059,12 +2424,14 @@ bool dq_wide(const AttnParams& p) {
   return v >= 0 ? v == 1 : p.keys_per_query >= 3072.0;
 }
 
-// CF_DQ_PERSIST=0 falls back to one CTA per (tile, head) for the 64-key dQ
-// kernel (A/B); default: the persistent kernel
+// 64-key dQ kernel choice (CF_DQ_PERSIST): 2 (default) the TMA-fed
+// persistent kernel with D from dsum_rows_kernel (packed short chunks: in-step
+// attention backward +2 %, profiles/round2_ab_dq_tma.txt), 1 the persistent
+// kernel staging Q / dO / O itself, 0 one CTA per (tile, head)
 int dq_persist() {
   static const int v = [] {
     const char* e = std::getenv("CF_DQ_PERSIST");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   return v;
 }
@@ -2122,6 +2489,14 @@ cudaError_t attn_backward_tc(const AttnParams& p, const AttnTile* qtiles128, int
     attr = smem_optin(reinterpret_cast<const void*>(dq_wide_kernel), static_cast<int>(smem_w));
     if (attr != cudaSuccess) return attr;
     dq_wide_kernel<<<dim3(nq, p.H), kDqWideThreads, smem_w, st>>>(k128, v128, a);
+  } else if (dq_persist() == 2) {
+    // D first (HBM-bound pass), then the TMA-fed persistent dQ kernel
+    const size_t smem_t = 1024 + (KS + VS) * 2 * kBox64 + 6 * kBox128 + 256;
+    attr = smem_optin(reinterpret_cast<const void*>(dq_persist_tma_kernel), static_cast<int>(smem_t));
+    if (attr != cudaSuccess) return attr;
+    dsum_rows_kernel<<<p.T, 256, 0, st>>>(a);
+    const int items = nq * p.H;
+    dq_persist_tma_kernel<<<std::min(items, attn_num_sms()), kThreads, smem_t, st>>>(k64, v64, q128, o128, a, nq);
   } else if (dq_persist()) {
     const int items = nq * p.H;
     const int grid = std::min(items, attn_num_sms());
