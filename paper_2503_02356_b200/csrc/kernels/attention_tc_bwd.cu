@@ -223,55 +223,6 @@ __device__ __forceinline__ void tmem_st32w(uint32_t taddr, const uint32_t (&w)[3
       "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
       : "memory");
 }
-// stage_row_tmem for the Q and dO half-rows of one query row together, with
-// the D = rowsum(dO * O) partial: all 24 global loads are issued before the
-// first tcgen05.st, so the three row fetches cost one memory latency instead
-// of three (short-chunk items are latency-bound).  Same values and the same
-// D arithmetic order as stage_row_tmem.
-__device__ __forceinline__ float stage_qdo_tmem(uint32_t tq, uint32_t tdo, const __nv_bfloat16* q,
-                                                const __nv_bfloat16* dout, const __nv_bfloat16* o, bool rok,
-                                                bool ok) {
-  uint32_t wq[32], wd[32];
-  uint4 ov[8];
-  const uint4* q4 = reinterpret_cast<const uint4*>(q);
-  const uint4* d4 = reinterpret_cast<const uint4*>(dout);
-  const uint4* o4 = reinterpret_cast<const uint4*>(o);
-  const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 v = rok ? __ldg(q4 + c) : z;
-    wq[4 * c] = v.x;
-    wq[4 * c + 1] = v.y;
-    wq[4 * c + 2] = v.z;
-    wq[4 * c + 3] = v.w;
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint4 v = ok ? __ldg(d4 + c) : z;
-    wd[4 * c] = v.x;
-    wd[4 * c + 1] = v.y;
-    wd[4 * c + 2] = v.z;
-    wd[4 * c + 3] = v.w;
-  }
-#pragma unroll
-  for (int c = 0; c < 8; ++c) ov[c] = ok ? __ldg(o4 + c) : z;
-  tmem_st32w(tq, wq);
-  tmem_st32w(tdo, wd);
-  if (!ok) return 0.f;
-  float part[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const uint32_t ow[4] = {ov[c].x, ov[c].y, ov[c].z, ov[c].w};
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const __nv_bfloat162 a2 = *reinterpret_cast<const __nv_bfloat162*>(&wd[4 * c + e]);
-      const __nv_bfloat162 b2 = *reinterpret_cast<const __nv_bfloat162*>(&ow[e]);
-      part[e] = fmaf(__low2float(a2), __low2float(b2), part[e]);
-      part[e] = fmaf(__high2float(a2), __high2float(b2), part[e]);
-    }
-  }
-  return (part[0] + part[1]) + (part[2] + part[3]);
-}
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
